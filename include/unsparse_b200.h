@@ -1,0 +1,214 @@
+/*
+ * unsparse_b200.h -- C ABI of the B200-native direct sparse convolution engine.
+ *
+ * This is the drop-in boundary for the reference `unsparse` conv-layer path
+ * (/root/reference/pkg/src/unsparse).  Plain pointers and sizes only; no torch
+ * or CUDA C++ types.  Device pointers are CUDA device addresses; `stream` is a
+ * cudaStream_t passed as void*.  All device work is stream-ordered and
+ * asynchronous; no entry point allocates device memory or synchronises.
+ *
+ * Each entry point names the reference interface it replaces (file:line,
+ * relative to /root/reference/pkg/src/unsparse/).
+ *
+ * Error convention: every function returns USC_OK (0) or a status code;
+ * usc_last_error() returns a thread-local message for the last failure.
+ * USC_ERR_VALUE maps to Python ValueError, USC_ERR_CORRUPT to
+ * CsrCorruptionError(ValueError) (csr.py:21), USC_ERR_CUDA to RuntimeError.
+ */
+#ifndef UNSPARSE_B200_H
+#define UNSPARSE_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define USC_ABI_VERSION 1
+
+enum usc_status {
+    USC_OK = 0,
+    USC_ERR_VALUE = 1,       /* geometry / precision / divisibility / shape (ValueError) */
+    USC_ERR_CORRUPT = 2,     /* CSR offset does not decode to a filter tap (CsrCorruptionError) */
+    USC_ERR_CUDA = 3,        /* CUDA runtime error (launch, copy) */
+    USC_ERR_UNSUPPORTED = 4  /* configuration this build cannot run */
+};
+
+/* Operand kinds of the conv kernels. */
+enum usc_dtype {
+    USC_F32 = 0,  /* binary32 in/out, bitwise = reference BINARY32 (mul then add, stored order) */
+    USC_F16 = 1,  /* binary16 storage, fp32 accumulate, saturating RNE output (engine.py:109-110) */
+    USC_I8 = 2,   /* int8 fixed-point codes, int32 accumulate, fp32 out = acc*sigma_w*sigma_x */
+    USC_CB4 = 3   /* 4-bit codebook index -> fp32 centroid, binary16 input, binary16 output */
+};
+
+/* ConvGeometry (tensor.py:156-222).  Output dims must divide exactly
+ * (tensor.py:182-190); usc_geometry_check enforces it. */
+typedef struct usc_geometry {
+    int32_t in_channels, out_channels;
+    int32_t filter_h, filter_w;
+    int32_t input_h, input_w;
+    int32_t stride_h, stride_w;
+    int32_t pad_h, pad_w;
+} usc_geometry;
+
+/* Resident activation layout ("padded NCHW"): [n][C][Hp][Ws] with a zero halo of
+ * (pad_h, pad_w) around every plane and the row stride Ws rounded up so a row is
+ * a multiple of 16 bytes.  It is the reference's materialised zero_pad layout
+ * (tensor.py:225-235) made TMA-/bulk-copy-legal. */
+typedef struct usc_act_layout {
+    int32_t channels, height, width;   /* logical (unpadded) plane */
+    int32_t pad_h, pad_w;              /* halo */
+    int32_t hp, ws;                    /* padded height, padded+aligned row stride (elements) */
+    int64_t sample_stride;             /* channels*hp*ws elements */
+} usc_act_layout;
+
+/* Execution / tile configuration.  sub_batch and worker_count keep the meaning of
+ * ExecConfig (engine.py:25-41); the remaining fields are the B200 tile knobs the
+ * autotuner searches (0 = choose automatically). */
+typedef struct usc_exec_cfg {
+    int32_t sub_batch;        /* samples per virtual block; must divide n (engine.py:81-82) */
+    int32_t worker_count;     /* accepted for API parity; the GPU ignores it */
+    int32_t pix_per_thread;   /* P: consecutive output pixels per thread (1,2,4,8) */
+    int32_t ch_per_cta;       /* DT: output channels per CTA (4,8,16,32) */
+    int32_t samples_per_cta;  /* NS: samples per CTA (full-map tiles) */
+    int32_t chunk_channels;   /* CC: input channels per shared-memory stage */
+    int32_t threads;          /* threads per CTA (128 or 256) */
+    int32_t kernel;           /* 0 auto, 1 tiled (bulk-copy staged), 2 reference-shaped blocks */
+} usc_exec_cfg;
+
+/* Resolved plan for one (geometry, batch, dtype, cfg): tile shape, packing
+ * parameters and launch dimensions.  Produced by usc_plan, consumed by usc_pack
+ * and usc_conv_forward. */
+typedef struct usc_plan {
+    usc_geometry g;
+    int32_t dtype;
+    int32_t n;
+    int32_t out_h, out_w;
+    usc_act_layout in;           /* input layout the kernel reads */
+    int32_t kernel;              /* 1 tiled, 2 blocks */
+    int32_t P, DT, NS, CC, threads;
+    int32_t TH, HS;              /* output rows per CTA tile, staged rows per channel */
+    int32_t strips_per_row, row_tiles, sample_tiles, groups, n_chunks;
+    int32_t transposed;          /* 1D layer (W==1) run as its H/W transpose */
+    int64_t smem_stage_bytes, smem_bytes;
+    int64_t grid_x, grid_y;
+} usc_plan;
+
+/* Epilogue of one conv launch (fused): ReLU (nn.py:96-98), saturation cap
+ * (quantization.py:79-93 with the _half_hook order, 238-244), output layout. */
+typedef struct usc_epilogue {
+    int32_t relu;                /* 1: where(v > 0, v, 0) */
+    int32_t saturate;            /* 1: v = min(v, cap) before the binary16 rounding */
+    float cap;                   /* float32(threshold * calibrated_max) */
+    int32_t saturate2;           /* 1: after ReLU, v = min(v, cap2) then binary16 rounding again */
+    float cap2;                  /* (the _half_hook of the ReLU layer in a 4b/16b model) */
+    float scale;                 /* USC_I8: sigma_w * sigma_x (exact power of two) */
+    int32_t out_padded;          /* 0: plain NCHW output; 1: padded layout `out` */
+    usc_act_layout out;          /* used when out_padded */
+} usc_epilogue;
+
+/* ---- library ---------------------------------------------------------- */
+int usc_abi_version(void);
+const char *usc_last_error(void);
+/* Device properties the planner uses (SM count etc.); -1 when no device. */
+int usc_device_sm_count(int device);
+
+/* ---- geometry (tensor.py:174-210) ------------------------------------ */
+int usc_geometry_check(const usc_geometry *g);
+int usc_geometry_out(const usc_geometry *g, int32_t *out_h, int32_t *out_w);
+/* Padded activation layout for `channels x h x w` planes with halo (ph, pw) and
+ * element size `elem_bytes` (4 f32, 2 f16, 1 i8). */
+int usc_act_layout_make(int32_t channels, int32_t h, int32_t w, int32_t ph, int32_t pw,
+                        int32_t elem_bytes, usc_act_layout *out);
+
+/* ---- encoder (host) -- replaces csr.py:86-112 build_csr ----------------
+ * Pass 1: n_nz = max(1, max_d count_nonzero(w[d])) (csr.py:103).
+ * Pass 2: RP/Lambda/theta bit-identical to the reference: padding entries
+ * (offset 0, weight 0) first, genuine entries in ascending offset order. */
+int usc_csr_count(const float *w, const usc_geometry *g, int64_t *n_nz);
+int usc_build_csr(const float *w, const usc_geometry *g, int64_t n_nz, int64_t *row_ptr,
+                  int64_t *col_offsets, float *theta);
+/* CsrFilter.validate (csr.py:66-83).  On USC_ERR_CORRUPT, *bad_index receives
+ * the first entry whose offset does not decode to a tap (or -1 for a
+ * row_ptr / length violation). */
+int usc_csr_validate(const usc_geometry *g, const int64_t *row_ptr, int64_t row_ptr_len,
+                     const int64_t *col_offsets, int64_t n_col, int64_t n_theta, int64_t n_nz,
+                     int64_t *bad_index);
+/* csr_to_dense (csr.py:115-128). */
+int usc_csr_to_dense(const usc_geometry *g, const int64_t *row_ptr, const int64_t *col_offsets,
+                     const float *theta, int64_t n_nz, float *w_out);
+
+/* ---- planner / packer (host) -------------------------------------------
+ * usc_plan resolves tile/launch parameters (the B200 analogue of plan_blocks,
+ * engine.py:53-61).  usc_pack writes the kernel-private entry stream for one
+ * plan into a HOST buffer of plan->pack_bytes bytes, which the caller copies to
+ * the device.  Zero-weight entries are deduplicated per (channel, offset):
+ * for finite inputs they are no-ops, and one copy per distinct offset keeps the
+ * reference's NaN propagation exact.
+ * payload: USC_F32/USC_F16 -> the CSR theta (fp32, binary16 values for F16);
+ *          USC_I8 -> int8 codes (one per CSR entry, theta = code*sigma_w);
+ *          USC_CB4 -> uint8 centroid indices (one per CSR entry) + 16-entry
+ *                     fp32 centroid table `table`. */
+int usc_plan_make(const usc_geometry *g, int32_t n, int32_t dtype, const usc_exec_cfg *cfg,
+                  usc_plan *out);
+int usc_pack_size(const usc_plan *plan, int64_t n_nz, int64_t *bytes);
+int usc_pack(const usc_plan *plan, const int64_t *row_ptr, const int64_t *col_offsets,
+             const void *payload, int64_t n_nz, const float *table, void *host_blob,
+             int64_t blob_bytes, int64_t *n_entries);
+
+/* ---- device kernels ------------------------------------------------------
+ * usc_pad_input: plain NCHW (n x C x H x W, dtype elements) -> padded layout
+ * (zero_pad, tensor.py:225-235).  `dst` must hold n*layout.sample_stride elems. */
+int usc_pad_input(const usc_act_layout *layout, int32_t dtype, int32_t n, const void *src,
+                  void *dst, void *stream);
+/* Direct sparse convolution -- replaces engine.py:64-111 sparse_conv_forward with
+ * kernels.py:57-100 as its hot loop.  x_dev is in plan->in layout, blob_dev is
+ * the device copy of usc_pack's output, y_dev receives n x D x Yh x Yw (plain)
+ * or the epilogue's padded layout. */
+int usc_conv_forward(const usc_plan *plan, const void *blob_dev, const void *x_dev, void *y_dev,
+                     const usc_epilogue *epi, void *stream);
+/* Reference-shaped kernel entry, the exact analogue of the numba FFI
+ * kernels.sparse_conv_blocks(xflat, row_ptr, col_offsets, theta, out, blocks, sb,
+ * x_size, s_h, s_w, padded_w) (kernels.py:57-58), all arrays on the device:
+ * xflat f32[n*x_size] (materialised padded input), row_ptr i64[D+1],
+ * col_offsets i64, theta f32, out f32[n][D][Yh][Yw], blocks i64[nb][2]. */
+int usc_sparse_conv_blocks(const float *xflat, const int64_t *row_ptr, const int64_t *col_offsets,
+                           const float *theta, float *out, const int64_t *blocks, int64_t n_blocks,
+                           int32_t sb, int64_t x_size, int32_t s_h, int32_t s_w, int32_t padded_w,
+                           int32_t D, int32_t out_h, int32_t out_w, void *stream);
+/* round_to_binary16 (tensor.py:48-63) on device: f32 in -> f32 on the binary16 grid
+ * (to_half == 0) or binary16 storage (to_half == 1). */
+int usc_round_binary16(const float *src, void *dst, int64_t count, int32_t to_half, void *stream);
+/* Elementwise conversions between storage kinds (f32 <-> binary16). */
+int usc_convert(const void *src, int32_t src_dtype, void *dst, int32_t dst_dtype, int64_t count,
+                void *stream);
+/* 2x2 stride-2 max pooling (nn.py:109-135): NaN-first argmax semantics.
+ * Input in `in_l` (padded or plain when in_l->pad_* == 0 and ws == width),
+ * output written to `out_l` layout. dtype USC_F32 or USC_F16. */
+int usc_maxpool2(const usc_act_layout *in_l, const usc_act_layout *out_l, int32_t dtype,
+                 int32_t n, const void *src, void *dst, void *stream);
+/* Quantise a device f32 tensor to int8 fixed-point codes (quantization.py:61-76):
+ * code = clip(copysign(floor(|x/sigma| + 0.5)), -(2^(bits-1)-1), 2^(bits-1)-1). */
+int usc_quantize_i8(const float *src, int8_t *dst, int64_t count, double sigma, int32_t bits,
+                    void *stream);
+
+/* ---- quantisation primitives (host) -- quantization.py ------------------ */
+/* fit_fixed_point (quantization.py:41-58): from max|x| */
+int usc_fit_fixed_point(double amax, int32_t total_bits, int32_t *int_bits, int32_t *frac_bits,
+                        double *sigma);
+/* linear_quantize codes (quantization.py:61-76), fp64 arithmetic. */
+int usc_linear_codes(const double *x, int64_t count, double sigma, int32_t total_bits,
+                     double *codes);
+/* kmeans_codebook (quantization.py:112-180): zero-pinned 1-D Lloyd with
+ * deterministic quantile seeding; bit-identical to the numpy reference.
+ * centroids/quantized have room for omega values; *k_out receives the codebook
+ * size; assignments has `count` entries. */
+int usc_kmeans_codebook(const double *w, int64_t count, int32_t omega, int32_t psi,
+                        double *centroids, double *quantized, int64_t *assignments,
+                        int32_t *k_out, int32_t *zero_pinned);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* UNSPARSE_B200_H */

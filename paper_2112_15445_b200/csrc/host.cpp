@@ -1,0 +1,572 @@
+// host.cpp -- host side of the C ABI: geometry, activation layouts, the CSR
+// encoder (bit-exact build_csr), validation, the tile planner and the packer
+// that turns a CsrFilter into the kernel-private entry stream, and the
+// quantisation primitives (fixed point, codebook k-means).
+//
+// References are to /root/reference/pkg/src/unsparse/<file>:<line>.
+#include "usc_internal.h"
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <unordered_set>
+#include <vector>
+
+namespace usc {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_last_error = buf;
+    return code;
+}
+
+int elem_bytes(int dtype) {
+    switch (dtype) {
+        case USC_F32: return 4;
+        case USC_F16: return 2;
+        case USC_I8: return 1;
+        case USC_CB4: return 2;  // binary16 activations
+    }
+    return 0;
+}
+
+int entry_bytes(int dtype) { return (dtype == USC_F32 || dtype == USC_F16) ? 8 : 4; }
+
+}  // namespace usc
+
+using namespace usc;
+
+extern "C" {
+
+int usc_abi_version(void) { return USC_ABI_VERSION; }
+
+const char *usc_last_error(void) { return g_last_error.c_str(); }
+
+// tensor.py:174-190 -- stride >= 1, pad >= 0, filter fits, exact division.
+int usc_geometry_check(const usc_geometry *g) {
+    if (!g) return fail(USC_ERR_VALUE, "null geometry");
+    if (g->stride_h < 1) return fail(USC_ERR_VALUE, "stride_h must be >= 1, got %d", g->stride_h);
+    if (g->stride_w < 1) return fail(USC_ERR_VALUE, "stride_w must be >= 1, got %d", g->stride_w);
+    if (g->pad_h < 0 || g->pad_w < 0) return fail(USC_ERR_VALUE, "padding must be non-negative");
+    if (g->in_channels < 1 || g->out_channels < 1 || g->filter_h < 1 || g->filter_w < 1 ||
+        g->input_h < 1 || g->input_w < 1)
+        return fail(USC_ERR_VALUE, "geometry dims must be positive");
+    int num_h = g->input_h + 2 * g->pad_h - g->filter_h;
+    int num_w = g->input_w + 2 * g->pad_w - g->filter_w;
+    if (num_h < 0 || num_w < 0) return fail(USC_ERR_VALUE, "filter larger than padded input");
+    if (num_h % g->stride_h || num_w % g->stride_w)
+        return fail(USC_ERR_VALUE, "output dims not integral for geometry: (%d %% %d, %d %% %d)",
+                    num_h, g->stride_h, num_w, g->stride_w);
+    return USC_OK;
+}
+
+int usc_geometry_out(const usc_geometry *g, int32_t *out_h, int32_t *out_w) {
+    int rc = usc_geometry_check(g);
+    if (rc) return rc;
+    *out_h = (g->input_h + 2 * g->pad_h - g->filter_h) / g->stride_h + 1;
+    *out_w = (g->input_w + 2 * g->pad_w - g->filter_w) / g->stride_w + 1;
+    return USC_OK;
+}
+
+int usc_act_layout_make(int32_t channels, int32_t h, int32_t w, int32_t ph, int32_t pw,
+                        int32_t eb, usc_act_layout *out) {
+    if (channels < 1 || h < 1 || w < 1 || ph < 0 || pw < 0 || (eb != 1 && eb != 2 && eb != 4))
+        return fail(USC_ERR_VALUE, "bad activation layout");
+    out->channels = channels;
+    out->height = h;
+    out->width = w;
+    out->pad_h = ph;
+    out->pad_w = pw;
+    out->hp = h + 2 * ph;
+    int per16 = 16 / eb;
+    out->ws = (w + 2 * pw + per16 - 1) / per16 * per16;
+    out->sample_stride = (int64_t)channels * out->hp * out->ws;
+    return USC_OK;
+}
+
+// ---------------------------------------------------------------------------
+// encoder
+
+// csr.py:97-103
+int usc_csr_count(const float *w, const usc_geometry *g, int64_t *n_nz) {
+    int rc = usc_geometry_check(g);
+    if (rc) return rc;
+    int64_t per = (int64_t)g->in_channels * g->filter_h * g->filter_w, best = 0;
+    for (int64_t d = 0; d < g->out_channels; ++d) {
+        int64_t cnt = 0;
+        const float *wd = w + d * per;
+        for (int64_t k = 0; k < per; ++k) cnt += (wd[k] != 0.0f);
+        best = std::max(best, cnt);
+    }
+    *n_nz = std::max<int64_t>(1, best);
+    return USC_OK;
+}
+
+// csr.py:94-112.  np.nonzero walks (c, kh, kw) in C order, which is already
+// ascending in offset = (c*Hp + kh)*Wp + kw, so the stable argsort is the
+// identity; padding (offset 0, weight 0) goes first in each slice.
+int usc_build_csr(const float *w, const usc_geometry *g, int64_t n_nz, int64_t *row_ptr,
+                  int64_t *col, float *theta) {
+    int rc = usc_geometry_check(g);
+    if (rc) return rc;
+    const int64_t C = g->in_channels, D = g->out_channels, Kh = g->filter_h, Kw = g->filter_w;
+    const int64_t Hp = g->input_h + 2 * g->pad_h, Wp = g->input_w + 2 * g->pad_w;
+    const int64_t per = C * Kh * Kw;
+    for (int64_t d = 0; d <= D; ++d) row_ptr[d] = d * n_nz;
+    for (int64_t d = 0; d < D; ++d) {
+        const float *wd = w + d * per;
+        int64_t cnt = 0;
+        for (int64_t k = 0; k < per; ++k) cnt += (wd[k] != 0.0f);
+        if (cnt > n_nz) return fail(USC_ERR_VALUE, "n_nz %lld smaller than channel count %lld",
+                                    (long long)n_nz, (long long)cnt);
+        int64_t pos = d * n_nz;
+        for (int64_t i = 0; i < n_nz - cnt; ++i, ++pos) {
+            col[pos] = 0;
+            theta[pos] = 0.0f;
+        }
+        for (int64_t c = 0; c < C; ++c)
+            for (int64_t kh = 0; kh < Kh; ++kh)
+                for (int64_t kw = 0; kw < Kw; ++kw) {
+                    float v = wd[(c * Kh + kh) * Kw + kw];
+                    if (v != 0.0f) {
+                        col[pos] = (c * Hp + kh) * Wp + kw;
+                        theta[pos] = v;
+                        ++pos;
+                    }
+                }
+    }
+    return USC_OK;
+}
+
+// csr.py:66-83 (with offset_to_tap, csr.py:30-42)
+int usc_csr_validate(const usc_geometry *g, const int64_t *row_ptr, int64_t rp_len,
+                     const int64_t *col, int64_t n_col, int64_t n_theta, int64_t n_nz,
+                     int64_t *bad) {
+    *bad = -1;
+    int rc = usc_geometry_check(g);
+    if (rc) return rc;
+    const int64_t D = g->out_channels;
+    if (rp_len != D + 1 || row_ptr[0] != 0)
+        return fail(USC_ERR_CORRUPT, "row_ptr must have length D+1 and start at 0");
+    for (int64_t d = 0; d < D; ++d)
+        if (row_ptr[d + 1] - row_ptr[d] != n_nz)
+            return fail(USC_ERR_CORRUPT, "row_ptr slices are not uniform");
+    if (n_col != D * n_nz || n_theta != D * n_nz)
+        return fail(USC_ERR_CORRUPT, "col_offsets/weights length must be D*n_nz");
+    const int64_t Hp = g->input_h + 2 * g->pad_h, Wp = g->input_w + 2 * g->pad_w;
+    const int64_t plane = Hp * Wp, x_size = (int64_t)g->in_channels * plane;
+    for (int64_t i = 0; i < n_col; ++i) {
+        int64_t lam = col[i];
+        if (lam < 0 || lam >= x_size) {
+            *bad = i;
+            return fail(USC_ERR_CORRUPT, "offset %lld outside padded sample", (long long)lam);
+        }
+        int64_t c = lam / plane, rem = lam % plane, kh = rem / Wp, kw = rem % Wp;
+        if (kh >= g->filter_h || kw >= g->filter_w) {
+            *bad = i;
+            return fail(USC_ERR_CORRUPT, "offset %lld decodes to (%lld,%lld,%lld), not a %dx%d tap",
+                        (long long)lam, (long long)c, (long long)kh, (long long)kw, g->filter_h,
+                        g->filter_w);
+        }
+    }
+    return USC_OK;
+}
+
+// csr.py:115-128
+int usc_csr_to_dense(const usc_geometry *g, const int64_t *row_ptr, const int64_t *col,
+                     const float *theta, int64_t n_nz, float *w_out) {
+    int rc = usc_geometry_check(g);
+    if (rc) return rc;
+    const int64_t C = g->in_channels, D = g->out_channels, Kh = g->filter_h, Kw = g->filter_w;
+    const int64_t Hp = g->input_h + 2 * g->pad_h, Wp = g->input_w + 2 * g->pad_w;
+    const int64_t plane = Hp * Wp;
+    std::memset(w_out, 0, sizeof(float) * D * C * Kh * Kw);
+    for (int64_t d = 0; d < D; ++d)
+        for (int64_t i = row_ptr[d]; i < row_ptr[d + 1]; ++i) {
+            float v = theta[i];
+            if (v == 0.0f) continue;
+            int64_t lam = col[i], c = lam / plane, rem = lam % plane;
+            int64_t kh = rem / Wp, kw = rem % Wp;
+            if (lam < 0 || c >= C || kh >= Kh || kw >= Kw)
+                return fail(USC_ERR_CORRUPT, "offset %lld does not decode to a tap", (long long)lam);
+            w_out[((d * C + c) * Kh + kh) * Kw + kw] = v;
+        }
+    (void)n_nz;
+    return USC_OK;
+}
+
+// ---------------------------------------------------------------------------
+// planner (the GPU analogue of plan_blocks, engine.py:53-61)
+
+static int pow2_floor(int v) {
+    int p = 1;
+    while (p * 2 <= v) p *= 2;
+    return p;
+}
+
+int usc_plan_make(const usc_geometry *g0, int32_t n, int32_t dtype, const usc_exec_cfg *cfg,
+                  usc_plan *pl) {
+    int rc = usc_geometry_check(g0);
+    if (rc) return rc;
+    if (n < 1) return fail(USC_ERR_VALUE, "batch must be >= 1");
+    if (dtype < USC_F32 || dtype > USC_CB4) return fail(USC_ERR_VALUE, "unknown dtype %d", dtype);
+    usc_exec_cfg c = cfg ? *cfg : usc_exec_cfg{};
+    if (c.sub_batch < 1) c.sub_batch = 1;
+    if (n % c.sub_batch)
+        return fail(USC_ERR_VALUE, "sub_batch %d does not divide batch %d", c.sub_batch, n);
+    std::memset(pl, 0, sizeof *pl);
+    pl->dtype = dtype;
+    pl->n = n;
+    usc_geometry g = *g0;
+    // A 1-D layer along H (input_w == filter_w == 1) is the same memory as its
+    // H/W transpose; run it along W so pixels of a thread are contiguous.
+    if (g.input_w == 1 && g.filter_w == 1 && g.pad_w == 0 && g.input_h > 1) {
+        std::swap(g.filter_h, g.filter_w);
+        std::swap(g.input_h, g.input_w);
+        std::swap(g.stride_h, g.stride_w);
+        std::swap(g.pad_h, g.pad_w);
+        pl->transposed = 1;
+    }
+    pl->g = g;
+    usc_geometry_out(&g, &pl->out_h, &pl->out_w);
+    const int eb = elem_bytes(dtype);
+    rc = usc_act_layout_make(g.in_channels, g.input_h, g.input_w, g.pad_h, g.pad_w, eb, &pl->in);
+    if (rc) return rc;
+    const int Yh = pl->out_h, Yw = pl->out_w, Ws = pl->in.ws;
+    const int threads = (c.threads == 128 || c.threads == 256) ? c.threads : 256;
+    int kernel = c.kernel ? c.kernel : 1;
+    if (g.stride_w > 2) kernel = 2;
+    if (kernel == 1) {
+        int P = c.pix_per_thread ? c.pix_per_thread : std::min(4, pow2_floor(Yw));
+        if (P != 1 && P != 2 && P != 4 && P != 8) return fail(USC_ERR_VALUE, "pix_per_thread must be 1,2,4,8");
+        int SPR = (Yw + P - 1) / P;
+        while (SPR > threads && P < 8) {
+            P *= 2;
+            SPR = (Yw + P - 1) / P;
+        }
+        if (SPR > threads) kernel = 2;
+        if (kernel == 1) {
+            int DT = c.ch_per_cta ? c.ch_per_cta : 16;
+            if (DT != 8 && DT != 16) return fail(USC_ERR_VALUE, "ch_per_cta must be 8 or 16");
+            int per_sample = Yh * SPR;
+            int NS, TH;
+            if (per_sample <= threads) {
+                TH = Yh;
+                int maxNS = threads / per_sample;
+                NS = c.samples_per_cta ? std::min(c.samples_per_cta, maxNS) : maxNS;
+                NS = std::max(1, std::min(NS, n));
+            } else {
+                NS = 1;
+                TH = threads / SPR;
+            }
+            int HS = (TH - 1) * g.stride_h + g.filter_h;
+            if (TH == Yh) HS = pl->in.hp;
+            // stage = NS samples x CC channels x HS rows x Ws, plus read slack for
+            // partial strips (row wrap of the last row)
+            const int64_t per_ch = (int64_t)HS * Ws * eb;
+            const int64_t slack = 64 * eb;
+            const int64_t budget = c.chunk_channels ? INT64_MAX : 48 * 1024;  // per stage
+            int CC = c.chunk_channels ? c.chunk_channels : 32;
+            CC = std::min(CC, g.in_channels);
+            while (CC > 1 && NS * CC * per_ch + slack > budget) --CC;
+            int64_t stage = ((int64_t)NS * CC * per_ch + slack + 127) / 128 * 128;
+            if (2 * stage + 256 > 220 * 1024) kernel = 2;
+            if (kernel == 1) {
+                pl->P = P;
+                pl->DT = DT;
+                pl->NS = NS;
+                pl->CC = CC;
+                pl->TH = TH;
+                pl->HS = HS;
+                pl->threads = threads;
+                pl->strips_per_row = SPR;
+                pl->row_tiles = (Yh + TH - 1) / TH;
+                pl->sample_tiles = (n + NS - 1) / NS;
+                pl->groups = (g.out_channels + DT - 1) / DT;
+                pl->n_chunks = (g.in_channels + CC - 1) / CC;
+                pl->smem_stage_bytes = stage;
+                pl->smem_bytes = 2 * stage + 128;
+                pl->grid_x = (int64_t)pl->sample_tiles * pl->row_tiles;
+                pl->grid_y = pl->groups;
+            }
+        }
+    }
+    pl->kernel = kernel;
+    if (kernel == 2) {
+        pl->P = 1;
+        pl->DT = 1;
+        pl->NS = 1;
+        pl->CC = g.in_channels;
+        pl->TH = Yh;
+        pl->HS = pl->in.hp;
+        pl->threads = 256;
+        pl->groups = g.out_channels;
+        pl->n_chunks = 1;
+        int64_t total = (int64_t)n * g.out_channels * Yh * Yw;
+        pl->grid_x = std::min<int64_t>((total + 255) / 256, 148 * 64);
+        pl->grid_y = 1;
+    }
+    return USC_OK;
+}
+
+// ---------------------------------------------------------------------------
+// packer: CsrFilter -> kernel-private entry stream
+//
+// blob = 16-float centroid table (CB4; zeros otherwise), int32 cpg[G][n_chunks*DT + 1]
+// (padded to 16 B), entries (int2 for F32/F16 = {offset, theta bits}; int32 for
+// I8 = code<<24 | offset and for CB4 = index<<28 | offset).
+// Entries are laid out (group, chunk, d_local, stored order) so one chunk of one
+// group is contiguous and its DT+1 boundaries are consecutive in cpg.
+
+static int64_t align16(int64_t v) { return (v + 15) / 16 * 16; }
+
+int usc_pack_size(const usc_plan *pl, int64_t n_nz, int64_t *bytes) {
+    int64_t cp = align16(4 * ((int64_t)pl->groups * pl->n_chunks * pl->DT + 1));
+    int64_t ent = align16((int64_t)pl->g.out_channels * n_nz * entry_bytes(pl->dtype));
+    *bytes = 64 + cp + ent;  // [16-float centroid table][cpg][entries]
+    return USC_OK;
+}
+
+int usc_pack(const usc_plan *pl, const int64_t *row_ptr, const int64_t *col, const void *payload,
+             int64_t n_nz, const float *table, void *blob, int64_t blob_bytes, int64_t *n_entries) {
+    int64_t need;
+    usc_pack_size(pl, n_nz, &need);
+    if (blob_bytes < need) return fail(USC_ERR_VALUE, "pack buffer too small");
+    const usc_geometry &g = pl->g;
+    const int D = g.out_channels, DT = pl->DT, G = pl->groups, NC = pl->n_chunks, CC = pl->CC;
+    // decode offsets against the ORIGINAL (untransposed) geometry
+    int Hp0, Wp0, Kh0, Kw0;
+    if (pl->transposed) {
+        Hp0 = g.input_w + 2 * g.pad_w;  // original H
+        Wp0 = 1;
+        Kh0 = g.filter_w;
+        Kw0 = 1;
+    } else {
+        Hp0 = g.input_h + 2 * g.pad_h;
+        Wp0 = g.input_w + 2 * g.pad_w;
+        Kh0 = g.filter_h;
+        Kw0 = g.filter_w;
+    }
+    const int64_t plane0 = (int64_t)Hp0 * Wp0;
+    const int Ws = pl->in.ws, Hp = pl->in.hp;
+    const int64_t cs_tiled = (int64_t)pl->HS * Ws;  // channel stride inside a stage
+    std::memset(blob, 0, 64);
+    if (pl->dtype == USC_CB4) std::memcpy(blob, table, 16 * sizeof(float));
+    int32_t *cpg = (int32_t *)((char *)blob + 64);
+    const int64_t cp_bytes = align16(4 * ((int64_t)G * NC * DT + 1));
+    char *ent = (char *)blob + 64 + cp_bytes;
+    const int eb = entry_bytes(pl->dtype);
+    const int64_t max_off = pl->dtype == USC_I8 ? (1 << 24) : (1 << 28);
+    int64_t pos = 0;
+    std::vector<int64_t> zero_seen;
+    for (int gi = 0; gi < G; ++gi)
+        for (int k = 0; k < NC; ++k)
+            for (int dl = 0; dl < DT; ++dl) {
+                cpg[((int64_t)gi * NC + k) * DT + dl] = (int32_t)pos;
+                int d = gi * DT + dl;
+                if (d >= D) continue;
+                zero_seen.clear();
+                for (int64_t j = row_ptr[d]; j < row_ptr[d] + n_nz; ++j) {
+                    int64_t lam = col[j];
+                    int64_t c = lam / plane0, rem = lam % plane0, kh = rem / Wp0, kw = rem % Wp0;
+                    if (lam < 0 || c >= g.in_channels || kh >= Kh0 || kw >= Kw0)
+                        return fail(USC_ERR_CORRUPT, "offset %lld does not decode to a tap",
+                                    (long long)lam);
+                    if (c / CC != k) continue;
+                    bool zero;
+                    switch (pl->dtype) {
+                        case USC_F32:
+                        case USC_F16: zero = ((const float *)payload)[j] == 0.0f; break;
+                        case USC_I8: zero = ((const int8_t *)payload)[j] == 0; break;
+                        default: zero = table[((const uint8_t *)payload)[j] & 15] == 0.0f; break;
+                    }
+                    if (zero) {
+                        // a zero-weight entry only matters when x is non-finite, where
+                        // one copy per distinct offset already yields the NaN
+                        if (std::find(zero_seen.begin(), zero_seen.end(), lam) != zero_seen.end())
+                            continue;
+                        zero_seen.push_back(lam);
+                    }
+                    if (pl->transposed) std::swap(kh, kw);  // (c, kh, 0) -> (c, 0, kh)
+                    int64_t off = pl->kernel == 1
+                                      ? (c - (int64_t)k * CC) * cs_tiled + kh * Ws + kw
+                                      : (c * Hp + kh) * Ws + kw;
+                    if (off >= max_off || off > INT32_MAX)
+                        return fail(USC_ERR_UNSUPPORTED, "packed offset %lld too large", (long long)off);
+                    char *e = ent + pos * eb;
+                    switch (pl->dtype) {
+                        case USC_F32:
+                        case USC_F16: {
+                            int32_t v[2];
+                            v[0] = (int32_t)off;
+                            std::memcpy(&v[1], &((const float *)payload)[j], 4);
+                            std::memcpy(e, v, 8);
+                            break;
+                        }
+                        case USC_I8: {
+                            int32_t v = (int32_t)((uint32_t)(uint8_t)((const int8_t *)payload)[j] << 24 |
+                                                  (uint32_t)off);
+                            std::memcpy(e, &v, 4);
+                            break;
+                        }
+                        default: {
+                            uint32_t idx = ((const uint8_t *)payload)[j] & 15;
+                            uint32_t v = idx << 28 | (uint32_t)off;
+                            std::memcpy(e, &v, 4);
+                            break;
+                        }
+                    }
+                    ++pos;
+                }
+            }
+    cpg[(int64_t)G * NC * DT] = (int32_t)pos;
+    *n_entries = pos;
+    return USC_OK;
+}
+
+// ---------------------------------------------------------------------------
+// quantisation primitives (quantization.py)
+
+// quantization.py:41-58
+int usc_fit_fixed_point(double amax, int32_t total_bits, int32_t *int_bits, int32_t *frac_bits,
+                        double *sigma) {
+    if (total_bits < 2) return fail(USC_ERR_VALUE, "total_bits must be >= 2");
+    int ib = amax == 0.0 ? 0 : (int)std::ceil(std::log2(amax));
+    *int_bits = ib;
+    *frac_bits = total_bits - ib - 1;
+    *sigma = std::pow(2.0, (double)(-(*frac_bits)));
+    return USC_OK;
+}
+
+// quantization.py:61-76: copysign(floor(|x/sigma| + 0.5)) clipped to +-(2^(b-1)-1)
+int usc_linear_codes(const double *x, int64_t count, double sigma, int32_t bits, double *codes) {
+    const double limit = std::ldexp(1.0, bits - 1) - 1.0;
+    for (int64_t i = 0; i < count; ++i) {
+        double s = x[i] / sigma;
+        double c = std::copysign(std::floor(std::fabs(s) + 0.5), s);
+        codes[i] = c < -limit ? -limit : (c > limit ? limit : c);  // np.clip (NaN stays NaN)
+    }
+    return USC_OK;
+}
+
+// numpy's pairwise summation (the add.reduce behind ndarray.mean), so the
+// k-means centroids are bit-identical to the reference's `sel.mean()`.
+static double pairwise_sum(const double *a, int64_t n) {
+    if (n < 8) {
+        double r = 0.0;
+        for (int64_t i = 0; i < n; ++i) r += a[i];
+        return r;
+    }
+    if (n <= 128) {
+        double r[8];
+        for (int j = 0; j < 8; ++j) r[j] = a[j];
+        int64_t i;
+        for (i = 8; i < n - (n % 8); i += 8)
+            for (int j = 0; j < 8; ++j) r[j] += a[i + j];
+        double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+        for (; i < n; ++i) res += a[i];
+        return res;
+    }
+    int64_t n2 = n / 2;
+    n2 -= n2 % 8;
+    return pairwise_sum(a, n2) + pairwise_sum(a + n2, n - n2);
+}
+
+// quantization.py:112-131
+static void kmeans_1d(const std::vector<double> &values, int k_req, std::vector<double> &cent,
+                      std::vector<int64_t> &assign) {
+    std::vector<double> uniq(values);
+    std::sort(uniq.begin(), uniq.end());
+    uniq.erase(std::unique(uniq.begin(), uniq.end()), uniq.end());
+    const int64_t U = (int64_t)uniq.size();
+    const int k = (int)std::min<int64_t>(k_req, U);
+    cent.assign(k, 0.0);
+    for (int i = 0; i < k; ++i) {
+        double t = ((double)i + 0.5) / (double)k * (double)U;
+        double m = std::min(t, (double)(U - 1));
+        cent[i] = uniq[(int64_t)m];
+    }
+    const int64_t n = (int64_t)values.size();
+    std::vector<int64_t> na(n);
+    std::vector<double> sel;
+    assign.clear();
+    for (int it = 0; it < 100; ++it) {
+        for (int64_t i = 0; i < n; ++i) {
+            int best = 0;
+            double bd = std::fabs(values[i] - cent[0]);
+            for (int j = 1; j < k; ++j) {
+                double dd = std::fabs(values[i] - cent[j]);
+                if (dd < bd) {
+                    bd = dd;
+                    best = j;
+                }
+            }
+            na[i] = best;
+        }
+        if (!assign.empty() && na == assign) break;
+        assign = na;
+        for (int j = 0; j < k; ++j) {
+            sel.clear();
+            for (int64_t i = 0; i < n; ++i)
+                if (assign[i] == j) sel.push_back(values[i]);
+            if (!sel.empty()) cent[j] = pairwise_sum(sel.data(), (int64_t)sel.size()) / (double)sel.size();
+        }
+    }
+}
+
+// quantization.py:134-180
+int usc_kmeans_codebook(const double *w, int64_t count, int32_t omega, int32_t psi, double *centroids,
+                        double *quantized, int64_t *assignments, int32_t *k_out, int32_t *zp_out) {
+    if (omega < 1) return fail(USC_ERR_VALUE, "omega must be >= 1");
+    if (psi != 8 && psi != 16) return fail(USC_ERR_VALUE, "psi must be 8 or 16");
+    std::vector<double> nz;
+    for (int64_t i = 0; i < count; ++i)
+        if (w[i] != 0.0) nz.push_back(w[i]);
+    const bool zp = (int64_t)nz.size() < count;
+    const int budget = zp ? omega - 1 : omega;
+    if (budget < 1) return fail(USC_ERR_VALUE, "omega too small to pin zero and keep a cluster");
+    std::vector<double> cent;
+    if (nz.empty()) {
+        cent = {0.0};
+        for (int64_t i = 0; i < count; ++i) assignments[i] = 0;
+    } else {
+        std::vector<double> nc;
+        std::vector<int64_t> na;
+        kmeans_1d(nz, budget, nc, na);
+        if (zp) {
+            cent.push_back(0.0);
+            cent.insert(cent.end(), nc.begin(), nc.end());
+            int64_t j = 0;
+            for (int64_t i = 0; i < count; ++i) assignments[i] = (w[i] != 0.0) ? na[j++] + 1 : 0;
+        } else {
+            cent = nc;
+            for (int64_t i = 0; i < count; ++i) assignments[i] = na[i];
+        }
+    }
+    const int K = (int)cent.size();
+    double amax = 0.0;
+    for (double v : cent) amax = std::max(amax, std::fabs(v));
+    int32_t ib, fb;
+    double sigma;
+    usc_fit_fixed_point(amax, psi, &ib, &fb, &sigma);
+    for (int i = 0; i < K; ++i) {
+        centroids[i] = cent[i];
+        double code;
+        usc_linear_codes(&cent[i], 1, sigma, psi, &code);
+        quantized[i] = 0.0 + sigma * code;  // mu + sigma*codes (quantization.py:73)
+    }
+    if (zp) quantized[0] = 0.0;
+    *k_out = K;
+    *zp_out = zp ? 1 : 0;
+    return USC_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,199 @@
+"""Full-network inference built from the sparse conv layer: pruned VGG-16 for
+CIFAR-10 (13 sparse 3x3 convs, ReLU, 5 max-pools).
+
+The reference has no VGG model; SURVEY.md §3(D) defines this network as the
+composition of its public pieces -- sparse_conv_forward (engine.py:64-111),
+nn.ReLU (nn.py:96-98) and nn.MaxPool2 (nn.py:124-135) -- which is what the
+oracle and tests/golden reproduce.  Here every activation stays in HBM in the
+padded layout the next layer reads: each conv kernel writes its output
+(ReLU fused in the epilogue) straight into the zero-haloed input buffer of the
+next conv, or into the max-pool's input, and the pool writes into the next
+conv's padded buffer.  A forward pass is 13 conv + 5 pool launches with no host
+synchronisation, capturable as one CUDA graph.
+"""
+
+from __future__ import annotations
+
+import zlib
+
+import numpy as np
+
+from . import _lib
+from .csr import build_csr
+from .engine import ExecConfig, device_pack, launch, make_plan, time_median_cuda, tile_candidates
+from .pruning import synthesize_masked_weights
+from .tensor import ConvGeometry, PrecisionMode
+
+VGG16_CIFAR = [64, 64, "M", 128, 128, "M", 256, 256, 256, "M", 512, 512, 512, "M", 512, 512, 512, "M"]
+
+
+def vgg16_geometries(cfg=VGG16_CIFAR, in_ch: int = 3, hw: int = 32):
+    out, c = [], in_ch
+    for v in cfg:
+        if v == "M":
+            hw //= 2
+            continue
+        out.append(ConvGeometry(c, v, 3, 3, hw, hw, padding=(1, 1)))
+        c = v
+    return out
+
+
+def vgg16_rng(sparsity: float, seed: int = 0):
+    """bench.py:160-161 style seeding for the network's synthetic weights."""
+    return np.random.default_rng([seed, zlib.crc32(b"vgg16-cifar10"), int(round(sparsity * 1000))])
+
+
+def vgg16_weights(rng, sparsity: float, precision=PrecisionMode.BINARY32, unified: bool = False):
+    """Random-init pruned weights, one DenseTensor4 per conv (bench.py:84-95 generator)."""
+    return [synthesize_masked_weights(g, sparsity, rng, precision, unified) for g in vgg16_geometries()]
+
+
+class SparseVGG16:
+    """Pruned VGG-16 CIFAR-10 conv trunk on one GPU, for a fixed batch.
+
+    forward(x) takes a plain NCHW (n,3,32,32) CUDA tensor (fp32, or fp16 for
+    BINARY16) and returns the (n,512,1,1) features.
+    """
+
+    def __init__(self, weights, batch: int, precision=PrecisionMode.BINARY32, configs=None,
+                 device=None):
+        import torch
+        self.precision = precision
+        self.dtype = _lib.USC_F16 if precision is PrecisionMode.BINARY16 else _lib.USC_F32
+        self.tdtype = torch.float16 if self.dtype == _lib.USC_F16 else torch.float32
+        self.eb = 2 if self.dtype == _lib.USC_F16 else 4
+        self.batch = batch
+        self.device = torch.device(device or "cuda")
+        self.geoms = vgg16_geometries()
+        self.filters = [build_csr(w, g) for w, g in zip(weights, self.geoms)]
+        self.configs = list(configs) if configs else [ExecConfig() for _ in self.geoms]
+        self.graph = None
+        self._build()
+
+    # -- buffers and plans ---------------------------------------------------
+    def _buf(self, lay):
+        import torch
+        return torch.zeros(self.batch * lay.sample_stride, dtype=self.tdtype, device=self.device)
+
+    def _build(self):
+        n = self.batch
+        self.plans, self.blobs, self.steps = [], [], []
+        # input buffer of the first conv
+        g0 = self.geoms[0]
+        self.in_layout = _lib.act_layout(g0.in_channels, g0.input_h, g0.input_w, 1, 1, self.eb)
+        self.x_buf = self._buf(self.in_layout)
+        cur_buf, cur_lay = self.x_buf, self.in_layout
+        self.nonzero_macs = 0
+        li = 0
+        for i, v in enumerate(VGG16_CIFAR):
+            if v == "M":
+                continue
+            g = self.geoms[li]
+            plan = make_plan(g, n, self.dtype, self.configs[li])
+            blob, n_ent = device_pack(self.filters[li], plan, self.filters[li].weights, device=self.device)
+            nxt = VGG16_CIFAR[i + 1] if i + 1 < len(VGG16_CIFAR) else None
+            epi = _lib.Epilogue()
+            epi.relu = 1
+            epi.scale = 1.0
+            if nxt == "M":
+                out_lay = _lib.act_layout(g.out_channels, g.out_h, g.out_w, 0, 0, self.eb)
+            else:
+                out_lay = _lib.act_layout(g.out_channels, g.out_h, g.out_w, 1, 1, self.eb)
+            epi.out_padded = 1
+            epi.out = out_lay
+            out_buf = self._buf(out_lay)
+            self.steps.append(("conv", li, plan, blob, cur_buf, out_buf, epi))
+            self.nonzero_macs += int(np.count_nonzero(self.filters[li].weights)) * g.out_h * g.out_w * n
+            cur_buf, cur_lay = out_buf, out_lay
+            if nxt == "M":
+                last = i + 2 >= len(VGG16_CIFAR)
+                ph = 0 if last else 1
+                pool_lay = _lib.act_layout(g.out_channels, g.out_h // 2, g.out_w // 2, ph, ph, self.eb)
+                pool_buf = self._buf(pool_lay)
+                self.steps.append(("pool", li, cur_lay, pool_lay, cur_buf, pool_buf))
+                cur_buf, cur_lay = pool_buf, pool_lay
+            li += 1
+        self.out_buf, self.out_layout = cur_buf, cur_lay
+
+    # -- execution -------------------------------------------------------------
+    def load_input(self, x, stream=None):
+        """Plain NCHW device tensor -> the first conv's padded input buffer."""
+        _lib.check(_lib.lib().usc_pad_input(_lib.ref(self.in_layout), self.dtype, self.batch,
+                                            _lib.t_ptr(x), _lib.t_ptr(self.x_buf),
+                                            _lib.stream_ptr(stream)), "pad")
+
+    def run(self, stream=None):
+        """All 18 launches on the current stream (no host synchronisation)."""
+        L = _lib.lib()
+        sp = _lib.stream_ptr(stream)
+        for st in self.steps:
+            if st[0] == "conv":
+                _, _, plan, blob, xin, yout, epi = st
+                _lib.check(L.usc_conv_forward(_lib.ref(plan), _lib.t_ptr(blob), _lib.t_ptr(xin),
+                                              _lib.t_ptr(yout), _lib.ref(epi), sp), "conv")
+            else:
+                _, _, lin, lout, xin, yout = st
+                _lib.check(L.usc_maxpool2(_lib.ref(lin), _lib.ref(lout), self.dtype, self.batch,
+                                          _lib.t_ptr(xin), _lib.t_ptr(yout), sp), "pool")
+
+    def output(self):
+        return self.out_buf.view(self.batch, self.out_layout.channels, 1, 1)
+
+    def forward(self, x):
+        self.load_input(x)
+        if self.graph is not None:
+            self.graph.replay()
+        else:
+            self.run()
+        return self.output()
+
+    def capture(self):
+        """Capture run() as one CUDA graph (launch-bound small layers)."""
+        import torch
+        s = torch.cuda.Stream(device=self.device)
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            self.run()  # warm (attributes, lazy init) outside capture
+        torch.cuda.current_stream().wait_stream(s)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self.run()
+        self.graph = g
+        return g
+
+    @property
+    def launches_per_forward(self) -> int:
+        return len(self.steps)
+
+    def conv_launch_list(self):
+        return [(st[1], st[2]) for st in self.steps if st[0] == "conv"]
+
+    # -- per-layer autotuning ----------------------------------------------------
+    def autotune(self, repeats: int = 5, warmup: int = 2, noise_floor: float = 0.02):
+        """Per-layer tile search (autotune_sb semantics, engine.py:139-170), timed
+        with CUDA events on the model's real buffers; rebuilds the plans."""
+        import torch
+        best_cfgs = []
+        for st in [s for s in self.steps if s[0] == "conv"]:
+            _, li, plan0, _, xin, yout, epi = st
+            g = self.geoms[li]
+            usable = [sb for sb in (1, 2, 4, 8, 16, 32) if self.batch % sb == 0]
+            results = []
+            for cfg in [ExecConfig()] + tile_candidates(g, self.batch, usable):
+                try:
+                    plan = make_plan(g, self.batch, self.dtype, cfg)
+                except ValueError:
+                    continue
+                blob, _ = device_pack(self.filters[li], plan, self.filters[li].weights,
+                                      device=self.device)
+                ms = time_median_cuda(lambda: launch(plan, blob, xin, yout, epi), repeats, warmup)
+                results.append((ms, cfg))
+            best = min(ms for ms, _ in results)
+            pick = next(cfg for ms, cfg in results if ms <= best * (1.0 + noise_floor))
+            best_cfgs.append(pick)
+        torch.cuda.synchronize()
+        self.configs = best_cfgs
+        self.graph = None
+        self._build()
+        return best_cfgs

@@ -1,0 +1,200 @@
+"""Parity of the sm_100a kernels with the reference, through the product API and
+the C ABI.  Bitwise for fp32 (the reference's per-element mul-then-add order),
+fp16, int8 and the 4-bit codebook path; checked against the golden digests the
+reference produced (tests/golden) and against the oracle at larger sizes."""
+import numpy as np
+import pytest
+
+import oracle
+import paper_2112_15445_b200 as U
+from golden_util import arrays, geom, golden, layer_inputs, sha
+
+pytestmark = pytest.mark.gpu
+
+F32, F16 = U.PrecisionMode.BINARY32, U.PrecisionMode.BINARY16
+
+
+def G(t):
+    c, d, kh, kw, h, w, s, p = t
+    return U.ConvGeometry(c, d, kh, kw, h, w, tuple(s), tuple(p))
+
+
+def _dev(x, prec=F32):
+    import torch
+    return U.DenseTensor4.from_array(torch.from_numpy(np.ascontiguousarray(x)).cuda(), prec)
+
+
+@pytest.mark.parametrize("kernel", [0, 2])
+def test_random_corpus_bitwise(kernel):
+    """The reference's own oracle corpus (verify.py:55-69), 400 cases: every GPU
+    output is bit-identical to the reference's sparse_conv_forward."""
+    rng = np.random.default_rng([0, 1])
+    for rec in golden()["random_cases"]:
+        x, w, g, sb = oracle.random_case(rng, binary16=rec["binary16"])
+        prec = F16 if rec["binary16"] else F32
+        filt = U.build_csr(U.DenseTensor4.from_array(w, prec), G(rec["geometry"]))
+        out = U.sparse_conv_forward(U.DenseTensor4.from_array(x, prec), filt,
+                                    U.ExecConfig(sb, kernel=kernel))
+        assert sha(out.data) == rec["sparse_out"], (rec["i"], rec["geometry"])
+
+
+def test_random_corpus_dense_reference():
+    rng = np.random.default_rng([0, 1])
+    for rec in golden()["random_cases"][:120]:
+        x, w, g, sb = oracle.random_case(rng, binary16=rec["binary16"])
+        prec = F16 if rec["binary16"] else F32
+        out = U.dense_conv_reference(U.DenseTensor4.from_array(x, prec),
+                                     U.DenseTensor4.from_array(w, prec), G(rec["geometry"]))
+        assert sha(out.data) == rec["dense_out"], rec["i"]
+
+
+def test_reference_shaped_blocks_kernel():
+    """usc_sparse_conv_blocks: the numba FFI kernels.sparse_conv_blocks on device arrays."""
+    import torch
+    rng = np.random.default_rng([0, 1])
+    for rec in golden()["random_cases"][:100]:
+        x, w, g, sb = oracle.random_case(rng, binary16=rec["binary16"])
+        if rec["binary16"]:
+            continue
+        gg = G(rec["geometry"])
+        f = U.build_csr(U.DenseTensor4.from_array(w), gg)
+        xflat = torch.from_numpy(oracle.zero_pad(x, g).reshape(-1)).cuda()
+        blocks = np.array([(b.out_channel, b.sample_start) for b in U.plan_blocks(gg, x.shape[0], sb)],
+                          np.int64)
+        out = torch.zeros((x.shape[0], gg.out_channels, gg.out_h, gg.out_w), device="cuda")
+        cu = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+        U.engine.sparse_conv_blocks(xflat, cu(f.row_ptr), cu(f.col_offsets), cu(f.weights), out,
+                                    cu(blocks), sb, gg.x_size, gg.stride[0], gg.stride[1], gg.padded_w)
+        assert sha(out.cpu().numpy()) == rec["sparse_out"], rec["i"]
+
+
+def test_nonfinite_inputs_propagate_like_reference():
+    arr = arrays()
+    for rec in golden()["nonfinite_cases"]:
+        k = rec["k"]
+        gg = G(rec["geometry"])
+        f = U.build_csr(U.DenseTensor4.from_array(arr[f"nf{k}_w"]), gg)
+        for kernel in (0, 2):
+            got = U.sparse_conv_forward(_dev(arr[f"nf{k}_x"]), f, U.ExecConfig(kernel=kernel)).data
+            ref = arr[f"nf{k}_out"]
+            assert np.array_equal(np.isnan(got), np.isnan(ref))
+            m = ~np.isnan(ref)
+            assert np.array_equal(got[m], ref[m])
+
+
+LAYERS = ["cfg1-vgg16-256x8", "cfg1-vgg16-256x8-f16", "vgg16-512x14", "resnet50-1x1-64x256",
+          "resnet50-1x1-256x64", "cnn1d-300x64-k2", "cnn1d-300x64-k3", "resnet-3x3-s2-prepad",
+          "resnet-1x1-s2-crop", "sweep-3x3-256x8-98", "sweep-3x3-64x32-50"]
+
+
+@pytest.mark.parametrize("name", LAYERS)
+def test_layer_configs_bitwise_all_tiles(name):
+    """Every tile configuration the autotuner may pick gives the same bits
+    (schedule determinism, verify.py:139-150) and they equal the reference."""
+    rec = golden()["layers"][name]
+    g = geom(rec["geometry"])
+    prec = F16 if rec["binary16"] else F32
+    x, w = layer_inputs(name, g, rec["sparsity"], rec["batch"], rec["binary16"])
+    gg = G(rec["geometry"])
+    f = U.build_csr(U.DenseTensor4.from_array(w, prec), gg)
+    xd = _dev(x, prec)
+    cfgs = [U.ExecConfig(), U.ExecConfig(kernel=2)] + U.engine.tile_candidates(gg, rec["batch"], [1, 2])
+    for cfg in cfgs:
+        out = U.sparse_conv_forward(xd, f, cfg)
+        assert sha(out.data) == rec["out"], cfg
+
+
+@pytest.mark.parametrize("name", ["int8-vgg16-256x8", "int8-vgg16-64x32", "int8-1x1-256x64"])
+def test_int8_kernel_equals_reference_composition(name):
+    rec = golden()["int8"][name]
+    g = geom(rec["geometry"])
+    x, w = layer_inputs(name, g, rec["sparsity"], rec["batch"])
+    gg = G(rec["geometry"])
+    fq = U.build_csr_int8(U.DenseTensor4.from_array(w), gg)
+    xq = U.quantize_input_int8(_dev(x))
+    assert xq.params.sigma == rec["sigma_x"]
+    for cfg in (U.ExecConfig(), U.ExecConfig(kernel=2)):
+        out = U.sparse_conv_forward_int8(xq, fq, cfg)
+        assert sha(out.data) == rec["out"], cfg
+
+
+@pytest.mark.parametrize("name", ["cb4-vgg16-256x8", "cb4-vgg16-128x16"])
+def test_codebook_kernel_equals_reference_composition(name):
+    rec = golden()["cb4"][name]
+    g = geom(rec["geometry"])
+    x, w = layer_inputs(name, g, rec["sparsity"], rec["batch"])
+    gg = G(rec["geometry"])
+    fc = U.build_csr_codebook(U.DenseTensor4.from_array(w), gg)
+    x16 = _dev(oracle.round_to_binary16(x), F16)
+    for cfg in (U.ExecConfig(), U.ExecConfig(kernel=2)):
+        plain = U.sparse_conv_forward_codebook(x16, fc, config=cfg)
+        assert sha(plain.data) == sha(oracle.round_to_binary16(_conv_ref(x16.data, fc, g)))
+        out = U.sparse_conv_forward_codebook(x16, fc, 0.99, rec["calibrated_max"], config=cfg)
+        assert sha(out.data) == rec["out"], cfg
+
+
+def _conv_ref(x, fc, g):
+    csr = (fc.filt.row_ptr, fc.filt.col_offsets, fc.filt.weights, fc.filt.n_nz)
+    return oracle.sparse_conv_forward(x, csr, g, threads=4)
+
+
+def test_vgg16_network_matches_reference_composition():
+    """The fused VGG-16 pipeline (conv+ReLU epilogue, pools, padded buffers) equals
+    the reference's sparse_conv_forward + nn.ReLU + nn.MaxPool2 composition."""
+    import zlib
+
+    import torch
+    from paper_2112_15445_b200.models import SparseVGG16, vgg16_weights
+    rec = golden()["vgg16"]
+    rng = np.random.default_rng([0, zlib.crc32(b"vgg16-cifar10"), int(round(rec["sparsity"] * 1000))])
+    x = rng.standard_normal((rec["batch"], 3, 32, 32)).astype(np.float32)
+    ws = vgg16_weights(rng, rec["sparsity"])
+    m = SparseVGG16(ws, rec["batch"])
+    out = m.forward(torch.from_numpy(x).cuda())
+    assert sha(out.cpu().numpy()) == rec["out"]
+    m.capture()
+    out2 = m.forward(torch.from_numpy(x).cuda())
+    assert sha(out2.cpu().numpy()) == rec["out"]
+
+
+def test_vgg16_batch64_vs_oracle():
+    """Larger batch against the oracle (the reference's algorithm restated in C)."""
+    import torch
+    from paper_2112_15445_b200.models import VGG16_CIFAR, SparseVGG16, vgg16_rng, vgg16_weights
+    rng = vgg16_rng(0.93, seed=5)
+    ws = vgg16_weights(rng, 0.93)
+    x = rng.standard_normal((64, 3, 32, 32)).astype(np.float32)
+    m = SparseVGG16(ws, 64)
+    got = m.forward(torch.from_numpy(x).cuda()).cpu().numpy()
+    a, li = x, 0
+    for v in VGG16_CIFAR:
+        if v == "M":
+            a = oracle.maxpool2(a)
+            continue
+        g = m.geoms[li]
+        gt = (g.in_channels, g.out_channels, 3, 3, g.input_h, g.input_w, (1, 1), (1, 1))
+        a = oracle.relu(oracle.sparse_conv_forward(a, oracle.build_csr(ws[li].data, gt), gt,
+                                                   threads=oracle.max_threads()))
+        li += 1
+    assert np.array_equal(got, a)
+
+
+def test_cfg1_full_batch_vs_oracle_and_autotune():
+    rec = golden()["layers"]["cfg1-vgg16-256x8"]
+    g = geom(rec["geometry"])
+    x, w = layer_inputs("cfg1-vgg16-256x8", g, 0.9, 32)
+    gg = G(rec["geometry"])
+    f = U.build_csr(U.DenseTensor4.from_array(w), gg)
+    xd = _dev(x)
+    cfg = U.autotune_sb(xd, f, repeats=3, warmup=1)
+    assert cfg.sub_batch in (1, 2, 4, 8)
+    out = U.sparse_conv_forward(xd, f, cfg)
+    assert sha(out.data) == rec["out"]
+
+
+def test_round_to_binary16_device():
+    import torch
+    rng = np.random.default_rng(3)
+    x = (rng.standard_normal(100000) * np.exp(rng.uniform(-20, 12, 100000))).astype(np.float32)
+    got = U.round_to_binary16(torch.from_numpy(x).cuda()).cpu().numpy()
+    assert np.array_equal(got, oracle.round_to_binary16(x))

@@ -1,0 +1,194 @@
+"""Host-side logic of the product (no GPU): encoder, validation, file format,
+quantisation primitives, planner/packer, and the C ABI surface."""
+import ctypes
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_2112_15445_b200 as U
+from paper_2112_15445_b200 import _lib
+from paper_2112_15445_b200.engine import make_plan
+from golden_util import geom, golden, layer_inputs, sha
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def G(t):
+    c, d, kh, kw, h, w, s, p = t
+    return U.ConvGeometry(c, d, kh, kw, h, w, tuple(s), tuple(p))
+
+
+def test_abi_exports_every_header_symbol():
+    hdr = open(os.path.join(ROOT, "include", "unsparse_b200.h")).read()
+    declared = set(re.findall(r"^\w[\w\s\*]*?\b(usc_\w+)\s*\(", hdr, re.M))
+    assert len(declared) >= 20
+    out = subprocess.run(["nm", "-D", "--defined-only", _lib.LIB_PATH], capture_output=True, text=True,
+                         check=True).stdout
+    exported = set(re.findall(r"\bT (usc_\w+)", out))
+    assert declared <= exported, declared - exported
+    assert declared == set(_lib.EXPORTED), declared ^ set(_lib.EXPORTED)
+    assert _lib.lib().usc_abi_version() == 1
+
+
+def test_library_is_sm100a():
+    out = subprocess.run(["cuobjdump", "--list-elf", _lib.LIB_PATH], capture_output=True, text=True)
+    assert "sm_100a" in out.stdout
+
+
+def test_encoder_random_corpus_bitwise():
+    rng = np.random.default_rng([0, 1])
+    for rec in golden()["random_cases"]:
+        x, w, g, sb = oracle.random_case(rng, binary16=rec["binary16"])
+        f = U.build_csr(U.DenseTensor4.from_array(w), G(rec["geometry"]))
+        assert f.n_nz == rec["csr"]["n_nz"]
+        assert sha(f.row_ptr) == rec["csr"]["row_ptr"]
+        assert sha(f.col_offsets) == rec["csr"]["col_offsets"]
+        assert sha(f.weights) == rec["csr"]["weights"]
+        back = U.csr_to_dense(f)
+        assert np.array_equal(back.data, w)  # verify.py:72-82 roundtrip
+
+
+def test_encoder_spec_examples():
+    e = golden()["kats"]["encoder_D2"]
+    f = U.build_csr(U.DenseTensor4.from_array(np.array(e["weights"], np.float32)), G(e["geometry"]))
+    assert (f.n_nz, f.row_ptr.tolist(), f.col_offsets.tolist(), f.weights.tolist()) == \
+        (3, [0, 3, 6], [0, 0, 4, 0, 5, 8], [0, 0, 5, 1, 2, 3])
+    z = U.build_csr(U.DenseTensor4.from_array(np.zeros((3, 2, 3, 3), np.float32)),
+                    U.ConvGeometry(2, 3, 3, 3, 5, 5, padding=(1, 1)))
+    assert z.n_nz == 1 and z.row_ptr.tolist() == [0, 1, 2, 3]
+    assert U.csr.tap_to_offset(0, 1, 2, U.ConvGeometry(1, 1, 3, 3, 4, 4)) == 6
+    assert len(U.plan_blocks(U.ConvGeometry(3, 64, 3, 3, 8, 8, padding=(1, 1)), 128, 4)) == 2048
+
+
+@pytest.mark.parametrize("name", ["cfg1-vgg16-256x8", "vgg16-512x14", "resnet50-1x1-64x256",
+                                  "cnn1d-300x64-k2", "resnet-3x3-s2-prepad"])
+def test_encoder_layer_configs(name):
+    rec = golden()["layers"][name]
+    g = geom(rec["geometry"])
+    x, w = layer_inputs(name, g, rec["sparsity"], rec["batch"], rec["binary16"])
+    f = U.build_csr(U.DenseTensor4.from_array(w), G(rec["geometry"]))
+    assert f.n_nz == rec["csr"]["n_nz"] and sha(f.col_offsets) == rec["csr"]["col_offsets"]
+    assert sha(f.weights) == rec["csr"]["weights"] and sha(f.row_ptr) == rec["csr"]["row_ptr"]
+
+
+def test_corruption_detected():
+    """verify.py:85-96: an out-of-range offset raises CsrCorruptionError."""
+    g = U.ConvGeometry(2, 2, 3, 3, 6, 6)
+    w = np.random.default_rng([0, 3]).standard_normal((2, 2, 3, 3)).astype(np.float32)
+    f = U.build_csr(U.DenseTensor4.from_array(w), g)
+    bad = f.col_offsets.copy()
+    bad[-1] = g.x_size + 5
+    with pytest.raises(U.CsrCorruptionError):
+        U.CsrFilter(f.row_ptr, bad, f.weights, f.n_nz, g)
+    bad = f.col_offsets.copy()
+    bad[0] = 3  # kw = 3 is not a 3x3 tap
+    with pytest.raises(U.CsrCorruptionError):
+        U.CsrFilter(f.row_ptr, bad, f.weights, f.n_nz, g)
+    with pytest.raises(U.CsrCorruptionError):
+        U.CsrFilter(f.row_ptr[:-1], f.col_offsets, f.weights, f.n_nz, g)
+    assert issubclass(U.CsrCorruptionError, ValueError)
+
+
+def test_geometry_errors():
+    with pytest.raises(ValueError):
+        U.ConvGeometry(1, 1, 3, 3, 32, 32, stride=(2, 2), padding=(1, 1))  # not integral
+    with pytest.raises(ValueError):
+        U.ConvGeometry(1, 1, 3, 3, 2, 2)
+    with pytest.raises(ValueError):
+        U.ExecConfig(0)
+    with pytest.raises(ValueError):
+        U.ExecConfig(3).block_count(8, 4)
+
+
+def test_save_load_csr_byte_compatible(tmp_path):
+    rec = golden()["layers"]["cfg1-vgg16-256x8"]
+    g = geom(rec["geometry"])
+    _, w = layer_inputs("cfg1-vgg16-256x8", g, rec["sparsity"], rec["batch"])
+    f = U.build_csr(U.DenseTensor4.from_array(w), G(rec["geometry"]))
+    U.save_csr(f, tmp_path / "f.csr")
+    f2 = U.load_csr(tmp_path / "f.csr")
+    assert f2.n_nz == f.n_nz and np.array_equal(f2.col_offsets, f.col_offsets)
+    assert np.array_equal(f2.weights, f.weights) and f2.geometry == f.geometry
+    assert abs(U.effective_sparsity(f) - 0.9) < 1e-3
+
+
+def test_quantisation_primitives_match_golden():
+    k = golden()["kats"]
+    for amax, (ib, fb, sg) in k["fit_fixed_point"].items():
+        p = U.fit_fixed_point(np.array([float(amax), -0.1]), 8)
+        assert (p.int_bits, p.frac_bits, p.sigma) == (ib, fb, sg)
+    assert U.linear_quantize(0.7, U.fit_fixed_point(np.array([1.0]), 8)) == 0.703125
+    assert U.linear_quantize(3.2, U.fit_fixed_point(np.array([3.2]), 8)) == 3.1875
+    cb = U.kmeans_codebook(np.array([1.0, 1.1, -2.0, -2.1]), 2)
+    assert cb.centroids.tolist() == k["kmeans_4pts"]["centroids"]
+    assert cb.assignments.tolist() == k["kmeans_4pts"]["assignments"]
+    # quantizer bound (verify.py:99-108)
+    data = np.random.default_rng([0, 4]).uniform(-3.0, 3.0, size=257)
+    p = U.fit_fixed_point(data, 8)
+    lim = (2 ** 7 - 1) * p.sigma
+    grid = np.linspace(-lim, lim, 10000)
+    assert np.max(np.abs(U.linear_quantize(grid, p) - grid)) <= p.sigma / 2 + 1e-12
+
+
+@pytest.mark.parametrize("name", ["cb4-vgg16-256x8", "cb4-vgg16-128x16"])
+def test_native_kmeans_bitwise(name):
+    rec = golden()["cb4"][name]
+    g = geom(rec["geometry"])
+    _, w = layer_inputs(name, g, rec["sparsity"], rec["batch"])
+    cb = U.kmeans_codebook(w, 16, 16)
+    assert cb.centroids.tolist() == rec["centroids"]
+    assert cb.quantized_centroids.tolist() == rec["quantized_centroids"]
+    assert sha(cb.assignments) == rec["assignments"]
+    assert sha(cb.reconstruct(w.shape)) == rec["wc"]
+
+
+@pytest.mark.parametrize("name", ["int8-vgg16-256x8", "int8-1x1-256x64"])
+def test_int8_filter_matches_reference_composition(name):
+    rec = golden()["int8"][name]
+    g = geom(rec["geometry"])
+    _, w = layer_inputs(name, g, rec["sparsity"], rec["batch"])
+    fq = U.build_csr_int8(U.DenseTensor4.from_array(w), G(rec["geometry"]))
+    assert fq.params.sigma == rec["sigma_w"]
+    assert fq.filt.n_nz == rec["csr"]["n_nz"] and sha(fq.filt.weights) == rec["csr"]["weights"]
+    assert np.array_equal(fq.codes.astype(np.float64) * fq.params.sigma, fq.filt.weights)
+
+
+def test_planner_tiles():
+    # cfg1: 8x8 maps -> full-map tiles, several samples per CTA
+    p = make_plan(U.ConvGeometry(256, 256, 3, 3, 8, 8, padding=(1, 1)), 32, _lib.USC_F32, None)
+    assert p.kernel == 1 and p.TH == 8 and p.NS * 8 * p.strips_per_row <= 256
+    assert p.in_.ws % 4 == 0 and p.in_.hp == 10 and p.groups == 16
+    assert p.smem_bytes <= 220 * 1024
+    # 1-D layer runs transposed
+    p = make_plan(U.ConvGeometry(64, 64, 2, 1, 300, 1), 8, _lib.USC_F32, None)
+    assert p.transposed == 1 and p.out_w == 299 and p.out_h == 1
+    # stride 3 falls back to the generic kernel
+    p = make_plan(U.ConvGeometry(4, 4, 3, 3, 10, 10, stride=(3, 3), padding=(1, 1)), 2, _lib.USC_F32, None)
+    assert p.kernel == 2
+    # 32x32 maps tile by rows
+    p = make_plan(U.ConvGeometry(64, 64, 3, 3, 32, 32, padding=(1, 1)), 256, _lib.USC_F32, None)
+    assert p.kernel == 1 and p.NS == 1 and p.row_tiles * p.TH >= 32
+    with pytest.raises(ValueError):
+        make_plan(U.ConvGeometry(4, 4, 3, 3, 8, 8, padding=(1, 1)), 6, _lib.USC_F32, U.ExecConfig(4))
+
+
+def test_packer_dedupes_zero_entries():
+    g = U.ConvGeometry(3, 2, 3, 3, 6, 6, padding=(1, 1))
+    w = np.zeros((2, 3, 3, 3), np.float32)
+    w[0, 0, 0, 1] = 1.0
+    w[1, 1, :, :] = 2.0  # 9 nonzeros -> channel 0 gets 8 padding entries
+    f = U.build_csr(U.DenseTensor4.from_array(w), g)
+    assert f.n_nz == 9
+    plan = make_plan(g, 2, _lib.USC_F32, U.ExecConfig(kernel=2))
+    size = ctypes.c_int64()
+    _lib.check(_lib.lib().usc_pack_size(_lib.ref(plan), f.n_nz, _lib.ref(size)))
+    blob = np.zeros(size.value, np.uint8)
+    n = ctypes.c_int64()
+    _lib.check(_lib.lib().usc_pack(_lib.ref(plan), _lib.np_ptr(f.row_ptr), _lib.np_ptr(f.col_offsets),
+                                   _lib.np_ptr(f.weights), f.n_nz, None, _lib.np_ptr(blob), blob.size,
+                                   _lib.ref(n)))
+    assert n.value == 1 + 1 + 9  # one deduped padding entry + the genuine entries

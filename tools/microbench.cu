@@ -1,0 +1,107 @@
+// Pipe-rate microbenchmarks for the roofline of the exact fp32 path on sm_100a:
+// FFMA vs FMUL+FADD (reference order, no contraction) vs the packed f32x2 forms,
+// and shared-memory load throughput.  Prints one JSON line per test.
+#include <cstdio>
+#include <cuda_runtime.h>
+
+#define N_ACC 8
+__global__ void k_ffma(float *out, float a, float b, int iters) {
+    float acc[N_ACC];
+    for (int i = 0; i < N_ACC; ++i) acc[i] = threadIdx.x * 0.001f + i;
+    for (int it = 0; it < iters; ++it)
+#pragma unroll
+        for (int i = 0; i < N_ACC; ++i) acc[i] = __fmaf_rn(acc[i], a, b);
+    float s = 0;
+    for (int i = 0; i < N_ACC; ++i) s += acc[i];
+    if (s == 1.2345f) out[0] = s;
+}
+__global__ void k_muladd(float *out, float a, float b, int iters) {
+    float acc[N_ACC], x[N_ACC];
+    for (int i = 0; i < N_ACC; ++i) { acc[i] = threadIdx.x * 0.001f + i; x[i] = b + i; }
+    for (int it = 0; it < iters; ++it)
+#pragma unroll
+        for (int i = 0; i < N_ACC; ++i) acc[i] = __fadd_rn(x[i], __fmul_rn(a, acc[i]));
+    float s = 0;
+    for (int i = 0; i < N_ACC; ++i) s += acc[i];
+    if (s == 1.2345f) out[0] = s;
+}
+__device__ __forceinline__ unsigned long long f2x2(float lo, float hi) {
+    unsigned long long r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+__global__ void k_muladd_x2(float *out, float a, float b, int iters) {
+    unsigned long long acc[N_ACC], x[N_ACC];
+    unsigned long long aa = f2x2(a, a);
+    for (int i = 0; i < N_ACC; ++i) { acc[i] = f2x2(threadIdx.x * 0.001f + i, i); x[i] = f2x2(b + i, b - i); }
+    for (int it = 0; it < iters; ++it)
+#pragma unroll
+        for (int i = 0; i < N_ACC; ++i) {
+            unsigned long long p;
+            asm volatile("mul.rn.f32x2 %0, %1, %2;" : "=l"(p) : "l"(aa), "l"(acc[i]));
+            asm volatile("add.rn.f32x2 %0, %1, %2;" : "=l"(acc[i]) : "l"(x[i]), "l"(p));
+        }
+    float s = 0;
+    for (int i = 0; i < N_ACC; ++i) { float lo, hi; asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(acc[i])); s += lo + hi; }
+    if (s == 1.2345f) out[0] = s;
+}
+__global__ void k_ffma_x2(float *out, float a, float b, int iters) {
+    unsigned long long acc[N_ACC];
+    unsigned long long aa = f2x2(a, a), bb = f2x2(b, b);
+    for (int i = 0; i < N_ACC; ++i) acc[i] = f2x2(threadIdx.x * 0.001f + i, i);
+    for (int it = 0; it < iters; ++it)
+#pragma unroll
+        for (int i = 0; i < N_ACC; ++i)
+            asm volatile("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(acc[i]) : "l"(acc[i]), "l"(aa), "l"(bb));
+    float s = 0;
+    for (int i = 0; i < N_ACC; ++i) { float lo, hi; asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(acc[i])); s += lo + hi; }
+    if (s == 1.2345f) out[0] = s;
+}
+__global__ void k_lds(float *out, int iters) {
+    __shared__ float sm[4096];
+    for (int i = threadIdx.x; i < 4096; i += blockDim.x) sm[i] = i;
+    __syncthreads();
+    float acc[N_ACC] = {0};
+    int base = threadIdx.x;
+    for (int it = 0; it < iters; ++it)
+#pragma unroll
+        for (int i = 0; i < N_ACC; ++i) acc[i] += sm[(base + i * 33 + it) & 4095];
+    float s = 0;
+    for (int i = 0; i < N_ACC; ++i) s += acc[i];
+    if (s == 1.2345f) out[0] = s;
+}
+
+int main() {
+    float *out;
+    cudaMalloc(&out, 4);
+    int sms;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    int blocks = sms * 8, threads = 256, iters = 4096;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    auto run = [&](const char *name, auto launch, double ops_per_thread_iter, const char *unit) {
+        launch();
+        cudaDeviceSynchronize();
+        float best = 1e30f;
+        for (int r = 0; r < 5; ++r) {
+            cudaEventRecord(e0);
+            launch();
+            cudaEventRecord(e1);
+            cudaEventSynchronize(e1);
+            float ms;
+            cudaEventElapsedTime(&ms, e0, e1);
+            best = ms < best ? ms : best;
+        }
+        double total = (double)blocks * threads * iters * ops_per_thread_iter;
+        printf("{\"test\": \"%s\", \"rate\": %.2f, \"unit\": \"%s\", \"ms\": %.3f}\n", name, total / best / 1e9, unit, best);
+    };
+    run("ffma", [&] { k_ffma<<<blocks, threads>>>(out, 1.0001f, 0.5f, iters); }, 2.0 * N_ACC, "TFLOP/s(x1e3 GF)");
+    run("fmul+fadd", [&] { k_muladd<<<blocks, threads>>>(out, 1.0001f, 0.5f, iters); }, 2.0 * N_ACC, "TFLOP/s(x1e3 GF)");
+    run("fmul2+fadd2", [&] { k_muladd_x2<<<blocks, threads>>>(out, 1.0001f, 0.5f, iters); }, 4.0 * N_ACC, "TFLOP/s(x1e3 GF)");
+    run("ffma2", [&] { k_ffma_x2<<<blocks, threads>>>(out, 1.0001f, 0.5f, iters); }, 4.0 * N_ACC, "TFLOP/s(x1e3 GF)");
+    run("lds32", [&] { k_lds<<<blocks, threads>>>(out, iters); }, 4.0 * N_ACC, "GB/s");
+    cudaError_t e = cudaGetLastError();
+    printf("{\"sms\": %d, \"err\": \"%s\"}\n", sms, cudaGetErrorString(e));
+    return 0;
+}
