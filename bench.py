@@ -1,0 +1,429 @@
+"""Benchmark: pruned VGG-16 CIFAR-10 inference (13 sparse 3x3 convs + ReLU + 5
+max-pools, ~93% layer-global sparsity, fp32 bit-exact, batch 256 per GPU) --
+BASELINE.json configs[1] -- on N B200s, batch-sharded (weak scaling, no
+collective on the hot path).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Prints ONE JSON line (rank 0).  ``--impl reference`` times the reference's CPU
+algorithm (the oracle port in oracle/, all host threads) on a bounded sample of
+the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "sparse conv layer µs & images/sec vs cuDNN dense at 90–95% sparsity, HBM GB/s"
+SPARSITY = 0.93
+BATCH = 256
+WORKLOAD = ("pruned VGG-16 CIFAR-10 inference: 13 sparse 3x3 conv (ReLU fused) + 5 maxpool, "
+            "93% layer-global sparsity, fp32 bit-exact to the reference")
+
+
+def env_rank():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)),
+            int(os.environ.get("WORLD_SIZE", 1)))
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (NVML) -- runs during the timed region
+
+class ClockSampler:
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, index: int, period: float = 0.02):
+        self.index, self.period = index, period
+        self.samples, self.reasons = [], set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+
+    def __enter__(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+
+            def loop():
+                while not self._stop.is_set():
+                    try:
+                        self.samples.append(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
+                        r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                        for bit, name in self.REASONS.items():
+                            if r & bit and bit != 0x1:
+                                self.reasons.add(name)
+                    except Exception:
+                        pass
+                    time.sleep(self.period)
+
+            self._t = threading.Thread(target=loop, daemon=True)
+            self._t.start()
+        except Exception as exc:  # no NVML: report it instead of guessing
+            self.reasons.add(f"nvml-unavailable:{type(exc).__name__}")
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self):
+        med = float(np.median(self.samples)) if self.samples else None
+        return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+# measured peaks
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            d = json.load(fh)
+        return d.get("hbm_gbs", 6650.0), "measured"
+    return 6650.0, "fallback"
+
+
+_FP32_SRC = r"""
+extern "C" __global__ void k_mul_add(float *out, float a, float b, int iters) {
+    float acc[8], x[8];
+    for (int i = 0; i < 8; ++i) { acc[i] = threadIdx.x * 0.001f + i; x[i] = b + i; }
+    for (int it = 0; it < iters; ++it)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[i] = __fadd_rn(x[i], __fmul_rn(a, acc[i]));
+    float s = 0; for (int i = 0; i < 8; ++i) s += acc[i];
+    if (s == 1.2345f) out[0] = s;
+}
+"""
+
+
+def fp32_mul_add_peak(device):
+    """Live FMUL+FADD throughput (the exact path's instruction mix) in TFLOP/s
+    (2 flops per multiply-add pair), via torch's inline CUDA loader."""
+    import torch
+    from torch.utils.cpp_extension import load_inline  # noqa: F401
+    try:
+        import cupy  # noqa: F401
+    except Exception:
+        pass
+    return None
+
+
+# ---------------------------------------------------------------------------
+# workload
+
+def build_model(batch, device, seed=0):
+    import torch
+    from paper_2112_15445_b200.models import SparseVGG16, vgg16_rng, vgg16_weights
+    rng = vgg16_rng(SPARSITY, seed)
+    ws = vgg16_weights(rng, SPARSITY)
+    model = SparseVGG16(ws, batch, device=device)
+    return model, ws
+
+
+def layer_stats(model):
+    """Algorithmic bytes and nonzero FLOPs per conv launch."""
+    out = []
+    n = model.batch
+    for st in model.steps:
+        if st[0] != "conv":
+            continue
+        li = st[1]
+        g = model.geoms[li]
+        f = model.filters[li]
+        genuine = int(np.count_nonzero(f.weights))
+        flops = 2.0 * genuine * g.out_h * g.out_w * n
+        byts = (n * g.in_channels * g.input_h * g.input_w * 4 + n * g.out_channels * g.out_h * g.out_w * 4
+                + g.out_channels * f.n_nz * 8 + 4 * (g.out_channels + 1))
+        out.append(dict(layer=li, flops=flops, bytes=byts))
+    return out
+
+
+def time_per_launch(model, steps=20):
+    """Per-launch device time (CUDA events on the launching stream)."""
+    import torch
+    from paper_2112_15445_b200 import _lib
+    L = _lib.lib()
+    times = {}
+    sp = _lib.stream_ptr()
+    for st in model.steps:
+        evs = []
+        for _ in range(steps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            if st[0] == "conv":
+                _, li, plan, blob, xin, yout, epi = st
+                L.usc_conv_forward(_lib.ref(plan), _lib.t_ptr(blob), _lib.t_ptr(xin), _lib.t_ptr(yout),
+                                   _lib.ref(epi), sp)
+            else:
+                _, li, lin, lout, xin, yout = st
+                L.usc_maxpool2(_lib.ref(lin), _lib.ref(lout), model.dtype, model.batch, _lib.t_ptr(xin),
+                               _lib.t_ptr(yout), sp)
+            b.record()
+            evs.append((a, b))
+        torch.cuda.synchronize()
+        times[(st[0], st[1])] = float(np.mean([a.elapsed_time(b) for a, b in evs]))
+    return times
+
+
+def cudnn_reference(ws, batch, device, steps=10, tf32=False):
+    """The same network on cuDNN dense conv (torch), equal precision (TF32 off) unless tf32."""
+    import torch
+    from paper_2112_15445_b200.models import VGG16_CIFAR
+    torch.backends.cudnn.benchmark = True
+    torch.backends.cudnn.allow_tf32 = tf32
+    torch.backends.cuda.matmul.allow_tf32 = tf32
+    wd = [torch.from_numpy(np.array(w.data)).to(device) for w in ws]
+    x = torch.randn(batch, 3, 32, 32, device=device)
+
+    def fwd():
+        a, li = x, 0
+        for v in VGG16_CIFAR:
+            if v == "M":
+                a = torch.nn.functional.max_pool2d(a, 2)
+            else:
+                a = torch.relu(torch.nn.functional.conv2d(a, wd[li], padding=1))
+                li += 1
+        return a
+
+    for _ in range(3):
+        fwd()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(steps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        fwd()
+        b.record()
+        b.synchronize()
+        ts.append(a.elapsed_time(b))
+    torch.backends.cudnn.allow_tf32 = True
+    ms = float(np.median(ts))
+    return {"ms_per_step": ms, "images_per_s": batch / ms * 1e3}
+
+
+def cpu_reference_run(batch_sample, threads, ws_data, seed=1):
+    """The reference's algorithm (oracle port, C) for the same network on a sample."""
+    import oracle
+    from paper_2112_15445_b200.models import VGG16_CIFAR, vgg16_geometries
+    geoms = vgg16_geometries()
+    csrs = []
+    for w, g in zip(ws_data, geoms):
+        gt = (g.in_channels, g.out_channels, 3, 3, g.input_h, g.input_w, (1, 1), (1, 1))
+        csrs.append((gt, oracle.build_csr(w, gt)))
+    x = np.random.default_rng(seed).standard_normal((batch_sample, 3, 32, 32)).astype(np.float32)
+
+    def fwd():
+        a, li = x, 0
+        for v in VGG16_CIFAR:
+            if v == "M":
+                a = oracle.maxpool2(a)
+            else:
+                gt, csr = csrs[li]
+                a = oracle.relu(oracle.sparse_conv_forward(a, csr, gt, sb=1, threads=threads))
+                li += 1
+        return a
+
+    return fwd
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the reference CPU implementation (oracle port) on the host cores."""
+    if rank != 0:
+        return
+    import oracle
+    from paper_2112_15445_b200.models import vgg16_geometries, vgg16_rng
+    from paper_2112_15445_b200.pruning import synthesize_masked_weights
+    oracle.build()
+    rng = vgg16_rng(SPARSITY)
+    ws = [synthesize_masked_weights(g, SPARSITY, rng).data for g in vgg16_geometries()]
+    threads = oracle.max_threads()
+    sample = int(os.environ.get("REF_SAMPLE", 8))
+    fwd = cpu_reference_run(sample, threads, ws)
+    for _ in range(args.warmup):
+        fwd()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        fwd()
+    dt = time.perf_counter() - t0
+    v = sample * args.steps / dt
+    line = {"impl": "reference", "metric": METRIC, "value": round(v, 3), "unit": "images/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(dt / args.steps * 1e3, 3), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "per_step_sample": sample, "global_batch": sample},
+            "cpu_baseline": {"value": round(v, 3), "unit": "images/s", "cores": threads, "kind": "port",
+                             "sample": f"{sample} images per step through the 13-layer trunk "
+                                       f"(oracle/oracle.c, C restatement of kernels.py:57-100)"},
+            "e2e": {"value": round(v, 3), "unit": "images/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-autotune", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-cudnn", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    rank, local_rank, world = env_rank()
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+    from paper_2112_15445_b200 import _lib
+    torch.cuda.set_device(local_rank)
+    device = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=device)
+
+    model, ws = build_model(BATCH, device)
+    if not args.no_autotune:
+        model.autotune(repeats=3, warmup=1)
+    model.capture()
+    x_host = torch.from_numpy(np.random.default_rng([1, rank]).standard_normal(
+        (BATCH, 3, 32, 32)).astype(np.float32)).pin_memory()
+    x_dev = x_host.to(device)
+    out_host = torch.empty((BATCH, 512, 1, 1), dtype=torch.float32).pin_memory()
+    model.load_input(x_dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=device)  # 2x L2
+
+    for _ in range(args.warmup):
+        model.graph.replay()
+    torch.cuda.synchronize()
+
+    # ---- timed region: K steps, inputs resident, L2 flushed between steps -----
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local_rank) as clk:
+        for a, b in evs:
+            flush.zero_()
+            a.record()
+            model.graph.replay()
+            b.record()
+        torch.cuda.synchronize()
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    total_ms = float(np.sum(step_ms))
+    if world > 1:
+        t = torch.tensor([total_ms], device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+        dist.barrier()
+    ms_per_step = total_ms / args.steps
+    value = world * BATCH * args.steps / (total_ms / 1e3)
+
+    # ---- e2e through the public API with host buffers ---------------------------
+    e2e_steps = max(10, args.steps // 2)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(e2e_steps):
+        x_dev.copy_(x_host, non_blocking=True)
+        out = model.forward(x_dev)
+        out_host.copy_(out, non_blocking=True)
+    b.record()
+    b.synchronize()
+    e2e_ms = a.elapsed_time(b)
+    if world > 1:
+        t = torch.tensor([e2e_ms], device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e = {"value": round(world * BATCH * e2e_steps / (e2e_ms / 1e3), 1), "unit": "images/s",
+           "h2d_bytes_per_step": int(x_host.numel() * 4), "d2h_bytes_per_step": int(out_host.numel() * 4),
+           "path": "SparseVGG16.forward (pad + CUDA graph of 18 launches) with pinned H2D/D2H per step"}
+
+    # ---- per-launch breakdown, roofline of the dominant kernel --------------------
+    per = time_per_launch(model)
+    stats = {s["layer"]: s for s in layer_stats(model)}
+    conv_ms = {li: ms for (k, li), ms in per.items() if k == "conv"}
+    dom = max(conv_ms, key=conv_ms.get)
+    dom_ms = conv_ms[dom]
+    hbm_peak, peak_kind = measured_peaks()
+    s = stats[dom]
+    achieved_gbs = s["bytes"] / (dom_ms / 1e3) / 1e9
+    achieved_tf = s["flops"] / (dom_ms / 1e3) / 1e12
+    g = model.geoms[dom]
+    plan = next(st[2] for st in model.steps if st[0] == "conv" and st[1] == dom)
+    roofline = {"bound": "hbm", "achieved": round(achieved_gbs, 1), "peak": hbm_peak, "unit": "GB/s",
+                "frac": round(achieved_gbs / hbm_peak, 4), "traffic": None,
+                "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
+                "kernel": f"k_tiled conv layer {dom} ({g.in_channels}->{g.out_channels}, {g.input_h}x{g.input_w})",
+                "kernel_share_of_step": round(dom_ms / sum(per.values()), 3),
+                "nonzero_tflops": round(achieved_tf, 2),
+                "arith_intensity_flop_per_byte": round(s["flops"] / s["bytes"], 1),
+                "plan": plan.describe()}
+    layers = [{"layer": li, "us": round(conv_ms[li] * 1e3, 1),
+               "nonzero_tflops": round(stats[li]["flops"] / (conv_ms[li] / 1e3) / 1e12, 2),
+               "gbs": round(stats[li]["bytes"] / (conv_ms[li] / 1e3) / 1e9, 1)} for li in sorted(conv_ms)]
+
+    line = None
+    if rank == 0:
+        cudnn = None
+        if not args.no_cudnn:
+            cudnn = {"fp32_tf32_off": cudnn_reference(ws, BATCH, device),
+                     "tf32": cudnn_reference(ws, BATCH, device, tf32=True)}
+        cpu = None
+        if not args.no_cpu_baseline and world == 1:
+            import oracle
+            oracle.build()
+            threads = oracle.max_threads()
+            sample = 8
+            fwd = cpu_reference_run(sample, threads, [w.data for w in ws])
+            fwd()
+            t0 = time.perf_counter()
+            reps = 0
+            while time.perf_counter() - t0 < 10.0:
+                fwd()
+                reps += 1
+            dt = time.perf_counter() - t0
+            cpu = {"value": round(sample * reps / dt, 3), "unit": "images/s", "cores": threads,
+                   "kind": "port", "sample": f"{reps}x{sample} images through the same 13-conv trunk "
+                                             f"(oracle/oracle.c), ~10 s of host work"}
+        line = {"metric": METRIC, "value": round(value, 1), "unit": "images/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+                "data": "synthetic (seeded N(0,1) inputs, random-init pruned weights)",
+                "config": {"workload": WORKLOAD, "model": "vgg16-cifar10", "global_batch": world * BATCH,
+                           "per_gpu_batch": BATCH, "seq_len": None, "sparsity": SPARSITY,
+                           "parallelism": f"dp{world} (batch-sharded, no collective)",
+                           "l2": "flushed (256 MiB write) between timed steps",
+                           "cuda_graph": True},
+                "e2e": e2e, "gpu_launches": args.steps * model.launches_per_forward,
+                "roofline": roofline, "layers": layers, "cudnn": cudnn, "cpu_baseline": cpu,
+                "clocks": clk.summary()}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

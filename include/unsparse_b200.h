@@ -52,15 +52,22 @@ typedef struct usc_geometry {
     int32_t pad_h, pad_w;
 } usc_geometry;
 
-/* Resident activation layout ("padded NCHW"): [n][C][Hp][Ws] with a zero halo of
- * (pad_h, pad_w) around every plane and the row stride Ws rounded up so a row is
- * a multiple of 16 bytes.  It is the reference's materialised zero_pad layout
- * (tensor.py:225-235) made TMA-/bulk-copy-legal. */
+/* Resident activation layouts -- the reference's materialised zero_pad layout
+ * (tensor.py:225-235) made bulk-copy-legal:
+ *  interleave == 0  "padded NCHW": [n][C][Hp][Ws], zero halo (pad_h, pad_w), row
+ *                   stride Ws rounded up to a multiple of 16 bytes;
+ *                   element (b,c,y,x) at ((b*C + c)*Hp + y+pad_h)*Ws + x+pad_w.
+ *  interleave == 32 "batch-interleaved" (BI32): [ceil(n/32)][C][Hp][Wp][32], zero
+ *                   halo, 32 samples innermost so one warp reads one 128-byte
+ *                   line per pixel; element (b,c,y,x) at
+ *                   (((b/32*C + c)*Hp + y+pad_h)*Wp + x+pad_w)*32 + b%32.
+ * sample_stride is the stride of one sample (il 0) or one 32-sample block (il 32). */
 typedef struct usc_act_layout {
     int32_t channels, height, width;   /* logical (unpadded) plane */
     int32_t pad_h, pad_w;              /* halo */
-    int32_t hp, ws;                    /* padded height, padded+aligned row stride (elements) */
-    int64_t sample_stride;             /* channels*hp*ws elements */
+    int32_t hp, ws;                    /* padded height, padded (+aligned for il 0) row stride */
+    int32_t interleave;                /* 0 or 32 */
+    int64_t sample_stride;             /* elements per sample (il 0) / per 32-sample block (il 32) */
 } usc_act_layout;
 
 /* Execution / tile configuration.  sub_batch and worker_count keep the meaning of
@@ -74,7 +81,7 @@ typedef struct usc_exec_cfg {
     int32_t samples_per_cta;  /* NS: samples per CTA (full-map tiles) */
     int32_t chunk_channels;   /* CC: input channels per shared-memory stage */
     int32_t threads;          /* threads per CTA (128 or 256) */
-    int32_t kernel;           /* 0 auto, 1 tiled (bulk-copy staged), 2 reference-shaped blocks */
+    int32_t kernel;           /* 0 auto, 1 tiled (padded NCHW), 2 generic, 3 batch-interleaved */
 } usc_exec_cfg;
 
 /* Resolved plan for one (geometry, batch, dtype, cfg): tile shape, packing
@@ -86,10 +93,12 @@ typedef struct usc_plan {
     int32_t n;
     int32_t out_h, out_w;
     usc_act_layout in;           /* input layout the kernel reads */
-    int32_t kernel;              /* 1 tiled, 2 blocks */
+    int32_t kernel;              /* 1 tiled, 2 generic, 3 batch-interleaved */
     int32_t P, DT, NS, CC, threads;
     int32_t TH, HS;              /* output rows per CTA tile, staged rows per channel */
     int32_t strips_per_row, row_tiles, sample_tiles, groups, n_chunks;
+    int32_t WS, WC, DW;          /* BI kernel: warps over strips, warps over channels, channels/warp */
+    int32_t SPRt, col_tiles, TWs;/* BI kernel: strips per tile row, column tiles, staged row width */
     int32_t transposed;          /* 1D layer (W==1) run as its H/W transpose */
     int64_t smem_stage_bytes, smem_bytes;
     int64_t grid_x, grid_y;
@@ -120,7 +129,9 @@ int usc_geometry_out(const usc_geometry *g, int32_t *out_h, int32_t *out_w);
 /* Padded activation layout for `channels x h x w` planes with halo (ph, pw) and
  * element size `elem_bytes` (4 f32, 2 f16, 1 i8). */
 int usc_act_layout_make(int32_t channels, int32_t h, int32_t w, int32_t ph, int32_t pw,
-                        int32_t elem_bytes, usc_act_layout *out);
+                        int32_t elem_bytes, int32_t interleave, usc_act_layout *out);
+/* Elements a buffer of `n` samples in `layout` needs. */
+int64_t usc_act_layout_elems(const usc_act_layout *layout, int32_t n);
 
 /* ---- encoder (host) -- replaces csr.py:86-112 build_csr ----------------
  * Pass 1: n_nz = max(1, max_d count_nonzero(w[d])) (csr.py:103).
@@ -158,10 +169,14 @@ int usc_pack(const usc_plan *plan, const int64_t *row_ptr, const int64_t *col_of
              int64_t blob_bytes, int64_t *n_entries);
 
 /* ---- device kernels ------------------------------------------------------
- * usc_pad_input: plain NCHW (n x C x H x W, dtype elements) -> padded layout
- * (zero_pad, tensor.py:225-235).  `dst` must hold n*layout.sample_stride elems. */
+ * usc_pad_input: plain NCHW (n x C x H x W, dtype elements) -> `layout`
+ * (zero_pad, tensor.py:225-235; halo and padding samples written as zeros).
+ * `dst` must hold usc_act_layout_elems(layout, n) elements. */
 int usc_pad_input(const usc_act_layout *layout, int32_t dtype, int32_t n, const void *src,
                   void *dst, void *stream);
+/* Inverse: `layout` -> plain NCHW (extract_interior, tensor.py:238-244). */
+int usc_unpad_output(const usc_act_layout *layout, int32_t dtype, int32_t n, const void *src,
+                     void *dst, void *stream);
 /* Direct sparse convolution -- replaces engine.py:64-111 sparse_conv_forward with
  * kernels.py:57-100 as its hot loop.  x_dev is in plan->in layout, blob_dev is
  * the device copy of usc_pack's output, y_dev receives n x D x Yh x Yw (plain)

@@ -27,10 +27,16 @@ class Geometry(ctypes.Structure):
 
 class ActLayout(ctypes.Structure):
     _fields_ = [("channels", c_i32), ("height", c_i32), ("width", c_i32), ("pad_h", c_i32),
-                ("pad_w", c_i32), ("hp", c_i32), ("ws", c_i32), ("sample_stride", c_i64)]
+                ("pad_w", c_i32), ("hp", c_i32), ("ws", c_i32), ("interleave", c_i32),
+                ("sample_stride", c_i64)]
 
     def key(self):
-        return (self.channels, self.height, self.width, self.pad_h, self.pad_w, self.hp, self.ws)
+        return (self.channels, self.height, self.width, self.pad_h, self.pad_w, self.hp, self.ws,
+                self.interleave)
+
+    def elems(self, n: int) -> int:
+        """Elements a buffer of n samples needs (usc_act_layout_elems)."""
+        return int(lib().usc_act_layout_elems(ctypes.byref(self), n))
 
 
 class ExecCfg(ctypes.Structure):
@@ -43,13 +49,15 @@ class Plan(ctypes.Structure):
                 ("in_", ActLayout), ("kernel", c_i32), ("P", c_i32), ("DT", c_i32), ("NS", c_i32),
                 ("CC", c_i32), ("threads", c_i32), ("TH", c_i32), ("HS", c_i32),
                 ("strips_per_row", c_i32), ("row_tiles", c_i32), ("sample_tiles", c_i32),
-                ("groups", c_i32), ("n_chunks", c_i32), ("transposed", c_i32),
+                ("groups", c_i32), ("n_chunks", c_i32), ("WS", c_i32), ("WC", c_i32), ("DW", c_i32),
+                ("SPRt", c_i32), ("col_tiles", c_i32), ("TWs", c_i32), ("transposed", c_i32),
                 ("smem_stage_bytes", c_i64), ("smem_bytes", c_i64), ("grid_x", c_i64),
                 ("grid_y", c_i64)]
 
     def describe(self) -> dict:
-        return dict(kernel="tiled" if self.kernel == 1 else "generic", P=self.P, DT=self.DT,
-                    NS=self.NS, CC=self.CC, TH=self.TH, threads=self.threads,
+        return dict(kernel={1: "tiled", 2: "generic", 3: "bi32"}[self.kernel], P=self.P, DT=self.DT,
+                    NS=self.NS, CC=self.CC, TH=self.TH, threads=self.threads, WS=self.WS,
+                    WC=self.WC, DW=self.DW,
                     grid=(self.grid_x, self.grid_y), smem_bytes=self.smem_bytes,
                     n_chunks=self.n_chunks, transposed=bool(self.transposed))
 
@@ -72,7 +80,8 @@ _SIGS = {
     "usc_device_sm_count": (c_i32, [c_i32]),
     "usc_geometry_check": (c_i32, [c_ptr]),
     "usc_geometry_out": (c_i32, [c_ptr, c_ptr, c_ptr]),
-    "usc_act_layout_make": (c_i32, [c_i32, c_i32, c_i32, c_i32, c_i32, c_i32, c_ptr]),
+    "usc_act_layout_make": (c_i32, [c_i32, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32, c_ptr]),
+    "usc_act_layout_elems": (c_i64, [c_ptr, c_i32]),
     "usc_csr_count": (c_i32, [c_ptr, c_ptr, c_ptr]),
     "usc_build_csr": (c_i32, [c_ptr, c_ptr, c_i64, c_ptr, c_ptr, c_ptr]),
     "usc_csr_validate": (c_i32, [c_ptr, c_ptr, c_i64, c_ptr, c_i64, c_i64, c_i64, c_ptr]),
@@ -81,6 +90,7 @@ _SIGS = {
     "usc_pack_size": (c_i32, [c_ptr, c_i64, c_ptr]),
     "usc_pack": (c_i32, [c_ptr, c_ptr, c_ptr, c_ptr, c_i64, c_ptr, c_ptr, c_i64, c_ptr]),
     "usc_pad_input": (c_i32, [c_ptr, c_i32, c_i32, c_ptr, c_ptr, c_ptr]),
+    "usc_unpad_output": (c_i32, [c_ptr, c_i32, c_i32, c_ptr, c_ptr, c_ptr]),
     "usc_conv_forward": (c_i32, [c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr]),
     "usc_sparse_conv_blocks": (c_i32, [c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_i64, c_i32, c_i64,
                                        c_i32, c_i32, c_i32, c_i32, c_i32, c_i32, c_ptr]),
@@ -151,7 +161,7 @@ def make_geometry(g) -> Geometry:
                     g.stride[0], g.stride[1], g.padding[0], g.padding[1])
 
 
-def act_layout(channels, h, w, ph, pw, elem_bytes) -> ActLayout:
+def act_layout(channels, h, w, ph, pw, elem_bytes, interleave: int = 0) -> ActLayout:
     lay = ActLayout()
-    check(lib().usc_act_layout_make(channels, h, w, ph, pw, elem_bytes, ref(lay)), "layout")
+    check(lib().usc_act_layout_make(channels, h, w, ph, pw, elem_bytes, interleave, ref(lay)), "layout")
     return lay

@@ -28,140 +28,13 @@
 #include <algorithm>
 #include <cstdint>
 
+#include "common.cuh"
 #include "usc_internal.h"
 
 using usc::fail;
 
 namespace {
-
-// --------------------------------------------------------------------------
-// PTX helpers: mbarrier + bulk async copy (TMA engine, non-tensor form)
-
-__device__ __forceinline__ uint32_t smem_u32(const void *p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void fence_mbar_init() {
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-__device__ __forceinline__ void fence_proxy_async() {
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-                 "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-            smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar))
-        : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        "@!p bra WAIT_%=;\n"
-        "}\n" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
-}
-
-// --------------------------------------------------------------------------
-// operand kinds
-
-template <int KIND> struct Kind;
-template <> struct Kind<USC_F32> { using TX = float;  using ACC = float; using TY = float;  };
-template <> struct Kind<USC_F16> { using TX = __half; using ACC = float; using TY = __half; };
-template <> struct Kind<USC_I8>  { using TX = int8_t; using ACC = int;   using TY = float;  };
-template <> struct Kind<USC_CB4> { using TX = __half; using ACC = float; using TY = __half; };
-
-// round_to_binary16 (tensor.py:48-63): RNE, finite overflow saturates to +-65504
-__device__ __forceinline__ __half sat_half(float v) {
-    __half h = __float2half_rn(v);
-    if (__hisinf(h) && isfinite(v)) h = __float2half_rn(copysignf(65504.0f, v));
-    return h;
-}
-__device__ __forceinline__ float round16f(float v) { return __half2float(sat_half(v)); }
-
-struct Epi {
-    int relu, saturate, saturate2, out_padded;
-    float cap, cap2, scale;
-    int oHp, oWs, oph, opw;
-    long long o_sample_stride;  // elements per sample of the padded output
-};
-
-// Apply the stored entries [e0, e1) of one output channel to P pixels.
-// xs points at the thread's first pixel's top-left tap in the staged tile.
-template <int KIND, int P, int SW>
-__device__ __forceinline__ void apply_entries(typename Kind<KIND>::ACC (&acc)[P], const void *ents,
-                                              int e0, int e1, const typename Kind<KIND>::TX *xs,
-                                              const float *tbl) {
-    if constexpr (KIND == USC_F32 || KIND == USC_F16) {
-        const int2 *E = static_cast<const int2 *>(ents);
-#pragma unroll 2
-        for (int e = e0; e < e1; ++e) {
-            const int2 en = __ldg(E + e);
-            const float th = __int_as_float(en.y);
-            const typename Kind<KIND>::TX *xp = xs + en.x;
-#pragma unroll
-            for (int p = 0; p < P; ++p) {
-                if constexpr (KIND == USC_F32)
-                    acc[p] = __fadd_rn(acc[p], __fmul_rn(th, xp[p * SW]));
-                else  // binary16 x binary16 is exact in fp32: FFMA == FMUL+FADD
-                    acc[p] = __fmaf_rn(th, __half2float(xp[p * SW]), acc[p]);
-            }
-        }
-    } else {
-        const int *E = static_cast<const int *>(ents);
-#pragma unroll 2
-        for (int e = e0; e < e1; ++e) {
-            const int en = __ldg(E + e);
-            if constexpr (KIND == USC_I8) {
-                const int th = en >> 24;  // signed code
-                const int8_t *xp = xs + (en & 0xFFFFFF);
-#pragma unroll
-                for (int p = 0; p < P; ++p) acc[p] += th * static_cast<int>(xp[p * SW]);
-            } else {
-                const float th = tbl[static_cast<unsigned>(en) >> 28];
-                const __half *xp = xs + (en & 0x0FFFFFFF);
-#pragma unroll
-                for (int p = 0; p < P; ++p)
-                    acc[p] = __fadd_rn(acc[p], __fmul_rn(th, __half2float(xp[p * SW])));
-            }
-        }
-    }
-}
-
-template <int KIND>
-__device__ __forceinline__ void store_one(typename Kind<KIND>::TY *y, long long idx,
-                                          typename Kind<KIND>::ACC acc, const Epi &ep) {
-    if constexpr (KIND == USC_F32) {
-        float v = acc;
-        if (ep.relu) v = v > 0.0f ? v : 0.0f;
-        y[idx] = v;
-    } else if constexpr (KIND == USC_I8) {
-        float v = __fmul_rn(static_cast<float>(acc), ep.scale);
-        if (ep.relu) v = v > 0.0f ? v : 0.0f;
-        y[idx] = v;
-    } else {
-        float v = acc;
-        if (ep.saturate) v = v > ep.cap ? ep.cap : v;  // np.minimum keeps NaN
-        v = round16f(v);
-        if (ep.relu) v = v > 0.0f ? v : 0.0f;
-        if (ep.saturate2) {
-            v = v > ep.cap2 ? ep.cap2 : v;
-            v = round16f(v);
-        }
-        y[idx] = __float2half_rn(v);  // exact: v is on the binary16 grid
-    }
-}
+using namespace usc_dev;
 
 struct TiledArgs {
     const void *x;
@@ -360,20 +233,45 @@ __global__ void __launch_bounds__(256)
 // --------------------------------------------------------------------------
 // elementwise utility kernels
 
+// plain NCHW -> any layout; writes every destination element (halo and padding
+// samples become zeros).  Destination-ordered so stores are coalesced.
 template <typename T>
-__global__ void k_pad(const T *__restrict__ src, T *__restrict__ dst, int n, int C, int H, int W,
-                      int ph, int pw, int Hp, int Ws) {
-    const long long total = (long long)n * C * Hp * Ws;
+__global__ void k_pad_any(const T *__restrict__ src, T *__restrict__ dst, int n, int H, int W,
+                          const LayoutD L, long long total) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
          i += (long long)gridDim.x * blockDim.x) {
-        const int x = static_cast<int>(i % Ws);
-        long long t = i / Ws;
-        const int y = static_cast<int>(t % Hp);
-        const long long pc = t / Hp;  // b*C + c
-        const int iy = y - ph, ix = x - pw;
+        long long t = i;
+        int lane = 0;
+        if (L.il == 32) {
+            lane = static_cast<int>(t & 31);
+            t >>= 5;
+        }
+        const int x = static_cast<int>(t % L.Ws);
+        t /= L.Ws;
+        const int y = static_cast<int>(t % L.Hp);
+        t /= L.Hp;
+        const int c = static_cast<int>(t % L.C);
+        const long long b = L.il == 32 ? (t / L.C) * 32 + lane : t / L.C;
+        const int iy = y - L.ph, ix = x - L.pw;
         T v{};
-        if (iy >= 0 && iy < H && ix >= 0 && ix < W) v = src[(pc * H + iy) * W + ix];
+        if (b < n && iy >= 0 && iy < H && ix >= 0 && ix < W) v = src[((b * L.C + c) * H + iy) * W + ix];
         dst[i] = v;
+    }
+}
+
+// any layout -> plain NCHW (n x C x H x W)
+template <typename T>
+__global__ void k_unpad_any(const T *__restrict__ src, T *__restrict__ dst, int H, int W, const LayoutD L,
+                            long long total) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int x = static_cast<int>(i % W);
+        long long t = i / W;
+        const int y = static_cast<int>(t % H);
+        t /= H;
+        const int c = static_cast<int>(t % L.C);
+        const long long b = t / L.C;
+        dst[i] = src[lay_index(L, b, c, y, x)];
     }
 }
 
@@ -396,36 +294,45 @@ __global__ void k_h2f(const __half *__restrict__ src, float *__restrict__ dst, l
 
 // nn.MaxPool2.forward (nn.py:124-135): value at np.argmax of the 2x2 window in
 // order (0,0),(0,1),(1,0),(1,1) -- first NaN if any, else first maximum.
+// Works between any two layouts; output-ordered (lane fastest for BI32).
 template <typename T>
-__global__ void k_maxpool2(const T *__restrict__ src, T *__restrict__ dst, int n, int C, int OH,
-                           int OW, int iHp, int iWs, int iph, int ipw, long long iss, int oHp, int oWs,
-                           int oph, int opw, long long oss) {
-    const long long total = (long long)n * C * OH * OW;
+__global__ void k_maxpool2(const T *__restrict__ src, T *__restrict__ dst, int n_total, int C, int OH,
+                           int OW, const LayoutD Li, const LayoutD Lo) {
+    const long long total = (long long)n_total * C * OH * OW;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
          i += (long long)gridDim.x * blockDim.x) {
-        const int x = static_cast<int>(i % OW);
-        long long t = i / OW;
+        long long t = i;
+        int lane = 0;
+        if (Lo.il == 32) {
+            lane = static_cast<int>(t & 31);
+            t >>= 5;
+        }
+        const int x = static_cast<int>(t % OW);
+        t /= OW;
         const int y = static_cast<int>(t % OH);
         t /= OH;
         const int c = static_cast<int>(t % C);
-        const long long b = t / C;
-        const T *p = src + b * iss + ((long long)c * iHp + 2 * y + iph) * iWs + 2 * x + ipw;
-        float v[4];
-        v[0] = static_cast<float>(p[0]);
-        v[1] = static_cast<float>(p[1]);
-        v[2] = static_cast<float>(p[iWs]);
-        v[3] = static_cast<float>(p[iWs + 1]);
+        const long long b = Lo.il == 32 ? (t / C) * 32 + lane : t / C;
+        const long long p00 = lay_index(Li, b, c, 2 * y, 2 * x);
+        const long long p01 = lay_index(Li, b, c, 2 * y, 2 * x + 1);
+        const long long p10 = lay_index(Li, b, c, 2 * y + 1, 2 * x);
+        const long long p11 = lay_index(Li, b, c, 2 * y + 1, 2 * x + 1);
+        const T w[4] = {src[p00], src[p01], src[p10], src[p11]};
         int m = 0;
-        if (!isnan(v[0]))
+        float vm = static_cast<float>(w[0]);
+        if (!isnan(vm))
             for (int k = 1; k < 4; ++k) {
-                if (isnan(v[k])) {
+                const float v = static_cast<float>(w[k]);
+                if (isnan(v)) {
                     m = k;
                     break;
                 }
-                if (v[k] > v[m]) m = k;
+                if (v > vm) {
+                    vm = v;
+                    m = k;
+                }
             }
-        const T *q = (m < 2) ? p + m : p + iWs + (m - 2);
-        dst[b * oss + ((long long)c * oHp + y + oph) * oWs + x + opw] = *q;
+        dst[lay_index(Lo, b, c, y, x)] = w[m];
     }
 }
 
@@ -508,6 +415,7 @@ Epi make_epi(const usc_epilogue *e) {
         ep.oph = e->out.pad_h;
         ep.opw = e->out.pad_w;
         ep.o_sample_stride = e->out.sample_stride;
+        ep.oil = e->out.interleave;
     }
     return ep;
 }
@@ -536,6 +444,9 @@ int usc_conv_forward(const usc_plan *pl, const void *blob, const void *x, void *
     if (ep.out_padded && (epi->out.channels != g.out_channels || epi->out.height != pl->out_h ||
                           epi->out.width != pl->out_w))
         return fail(USC_ERR_VALUE, "output layout does not match the plan");
+    if (pl->kernel == 3) return usc::launch_bi(pl, blob, x, y, ep, st);
+    if (ep.out_padded && ep.oil != 0)
+        return fail(USC_ERR_UNSUPPORTED, "kernels 1/2 write interleave-0 layouts only");
     // blob = [16 x f32 centroid table][int32 cpg, 16-B aligned][entries]
     const char *cb = static_cast<const char *>(blob);
     const long long cp_bytes = ((4LL * ((long long)pl->groups * pl->n_chunks * pl->DT + 1)) + 15) / 16 * 16;
@@ -615,25 +526,51 @@ int usc_sparse_conv_blocks(const float *xflat, const int64_t *row_ptr, const int
 int usc_pad_input(const usc_act_layout *l, int32_t dtype, int32_t n, const void *src, void *dst,
                   void *stream) {
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    const long long total = (long long)n * l->sample_stride;
+    const long long total = usc_act_layout_elems(l, n);
     const int grid = grid_for(total);
+    const LayoutD L = to_dev(*l);
     switch (usc::elem_bytes(dtype)) {
         case 4:
-            k_pad<float><<<grid, 256, 0, st>>>(static_cast<const float *>(src), static_cast<float *>(dst), n,
-                                               l->channels, l->height, l->width, l->pad_h, l->pad_w, l->hp, l->ws);
+            k_pad_any<float><<<grid, 256, 0, st>>>(static_cast<const float *>(src), static_cast<float *>(dst),
+                                                   n, l->height, l->width, L, total);
             break;
         case 2:
-            k_pad<uint16_t><<<grid, 256, 0, st>>>(static_cast<const uint16_t *>(src), static_cast<uint16_t *>(dst),
-                                                  n, l->channels, l->height, l->width, l->pad_h, l->pad_w,
-                                                  l->hp, l->ws);
+            k_pad_any<uint16_t><<<grid, 256, 0, st>>>(static_cast<const uint16_t *>(src),
+                                                      static_cast<uint16_t *>(dst), n, l->height, l->width, L,
+                                                      total);
             break;
         case 1:
-            k_pad<int8_t><<<grid, 256, 0, st>>>(static_cast<const int8_t *>(src), static_cast<int8_t *>(dst), n,
-                                                l->channels, l->height, l->width, l->pad_h, l->pad_w, l->hp, l->ws);
+            k_pad_any<int8_t><<<grid, 256, 0, st>>>(static_cast<const int8_t *>(src), static_cast<int8_t *>(dst),
+                                                    n, l->height, l->width, L, total);
             break;
         default: return fail(USC_ERR_VALUE, "unknown dtype %d", dtype);
     }
     return cuda_check("k_pad launch");
+}
+
+int usc_unpad_output(const usc_act_layout *l, int32_t dtype, int32_t n, const void *src, void *dst,
+                     void *stream) {
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const long long total = (long long)n * l->channels * l->height * l->width;
+    const int grid = grid_for(total);
+    const LayoutD L = to_dev(*l);
+    switch (usc::elem_bytes(dtype)) {
+        case 4:
+            k_unpad_any<float><<<grid, 256, 0, st>>>(static_cast<const float *>(src), static_cast<float *>(dst),
+                                                     l->height, l->width, L, total);
+            break;
+        case 2:
+            k_unpad_any<uint16_t><<<grid, 256, 0, st>>>(static_cast<const uint16_t *>(src),
+                                                        static_cast<uint16_t *>(dst), l->height, l->width, L,
+                                                        total);
+            break;
+        case 1:
+            k_unpad_any<int8_t><<<grid, 256, 0, st>>>(static_cast<const int8_t *>(src),
+                                                      static_cast<int8_t *>(dst), l->height, l->width, L, total);
+            break;
+        default: return fail(USC_ERR_VALUE, "unknown dtype %d", dtype);
+    }
+    return cuda_check("k_unpad launch");
 }
 
 int usc_round_binary16(const float *src, void *dst, int64_t count, int32_t to_half, void *stream) {
@@ -663,18 +600,20 @@ int usc_maxpool2(const usc_act_layout *in_l, const usc_act_layout *out_l, int32_
     const int OH = in_l->height / 2, OW = in_l->width / 2;
     if (out_l->height != OH || out_l->width != OW || out_l->channels != in_l->channels)
         return fail(USC_ERR_VALUE, "maxpool output layout mismatch");
+    if (in_l->interleave != out_l->interleave)
+        return fail(USC_ERR_VALUE, "maxpool layouts must share the interleave");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    const long long total = (long long)n * in_l->channels * OH * OW;
+    const int n_total = out_l->interleave == 32 ? (n + 31) / 32 * 32 : n;
+    const long long total = (long long)n_total * in_l->channels * OH * OW;
+    const LayoutD Li = to_dev(*in_l), Lo = to_dev(*out_l);
     if (dtype == USC_F32) {
-        k_maxpool2<float><<<grid_for(total), 256, 0, st>>>(
-            static_cast<const float *>(src), static_cast<float *>(dst), n, in_l->channels, OH, OW, in_l->hp,
-            in_l->ws, in_l->pad_h, in_l->pad_w, in_l->sample_stride, out_l->hp, out_l->ws, out_l->pad_h,
-            out_l->pad_w, out_l->sample_stride);
+        k_maxpool2<float><<<grid_for(total), 256, 0, st>>>(static_cast<const float *>(src),
+                                                           static_cast<float *>(dst), n_total,
+                                                           in_l->channels, OH, OW, Li, Lo);
     } else if (dtype == USC_F16 || dtype == USC_CB4) {
-        k_maxpool2<__half><<<grid_for(total), 256, 0, st>>>(
-            static_cast<const __half *>(src), static_cast<__half *>(dst), n, in_l->channels, OH, OW, in_l->hp,
-            in_l->ws, in_l->pad_h, in_l->pad_w, in_l->sample_stride, out_l->hp, out_l->ws, out_l->pad_h,
-            out_l->pad_w, out_l->sample_stride);
+        k_maxpool2<__half><<<grid_for(total), 256, 0, st>>>(static_cast<const __half *>(src),
+                                                            static_cast<__half *>(dst), n_total,
+                                                            in_l->channels, OH, OW, Li, Lo);
     } else {
         return fail(USC_ERR_VALUE, "maxpool dtype %d unsupported", dtype);
     }

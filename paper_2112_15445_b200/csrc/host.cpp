@@ -77,8 +77,9 @@ int usc_geometry_out(const usc_geometry *g, int32_t *out_h, int32_t *out_w) {
 }
 
 int usc_act_layout_make(int32_t channels, int32_t h, int32_t w, int32_t ph, int32_t pw,
-                        int32_t eb, usc_act_layout *out) {
-    if (channels < 1 || h < 1 || w < 1 || ph < 0 || pw < 0 || (eb != 1 && eb != 2 && eb != 4))
+                        int32_t eb, int32_t il, usc_act_layout *out) {
+    if (channels < 1 || h < 1 || w < 1 || ph < 0 || pw < 0 || (eb != 1 && eb != 2 && eb != 4) ||
+        (il != 0 && il != 32))
         return fail(USC_ERR_VALUE, "bad activation layout");
     out->channels = channels;
     out->height = h;
@@ -86,10 +87,21 @@ int usc_act_layout_make(int32_t channels, int32_t h, int32_t w, int32_t ph, int3
     out->pad_h = ph;
     out->pad_w = pw;
     out->hp = h + 2 * ph;
-    int per16 = 16 / eb;
-    out->ws = (w + 2 * pw + per16 - 1) / per16 * per16;
-    out->sample_stride = (int64_t)channels * out->hp * out->ws;
+    out->interleave = il;
+    if (il == 0) {
+        int per16 = 16 / eb;
+        out->ws = (w + 2 * pw + per16 - 1) / per16 * per16;
+        out->sample_stride = (int64_t)channels * out->hp * out->ws;
+    } else {
+        out->ws = w + 2 * pw;  // a pixel is 32*eb >= 32 bytes: always 16-B aligned
+        out->sample_stride = (int64_t)channels * out->hp * out->ws * 32;
+    }
     return USC_OK;
+}
+
+int64_t usc_act_layout_elems(const usc_act_layout *l, int32_t n) {
+    if (l->interleave == 32) return (int64_t)((n + 31) / 32) * l->sample_stride;
+    return (int64_t)n * l->sample_stride;
 }
 
 // ---------------------------------------------------------------------------
@@ -238,12 +250,79 @@ int usc_plan_make(const usc_geometry *g0, int32_t n, int32_t dtype, const usc_ex
     pl->g = g;
     usc_geometry_out(&g, &pl->out_h, &pl->out_w);
     const int eb = elem_bytes(dtype);
-    rc = usc_act_layout_make(g.in_channels, g.input_h, g.input_w, g.pad_h, g.pad_w, eb, &pl->in);
+    int kernel = c.kernel ? c.kernel : (dtype == USC_F32 ? 3 : 1);
+    if (g.stride_w > 2) kernel = 2;
+    rc = usc_act_layout_make(g.in_channels, g.input_h, g.input_w, g.pad_h, g.pad_w, eb,
+                             kernel == 3 ? 32 : 0, &pl->in);
     if (rc) return rc;
     const int Yh = pl->out_h, Yw = pl->out_w, Ws = pl->in.ws;
     const int threads = (c.threads == 128 || c.threads == 256) ? c.threads : 256;
-    int kernel = c.kernel ? c.kernel : 1;
-    if (g.stride_w > 2) kernel = 2;
+    if (kernel == 3 && dtype != USC_F32) return fail(USC_ERR_UNSUPPORTED, "BI kernel is fp32-only");
+    if (kernel == 3) {
+        // batch-interleaved: a CTA = 32 samples x (WS strips of P pixels) x (WC*DW channels);
+        // warp w owns strip w % WS for channel subgroup w / WS; lane = sample.
+        int P = c.pix_per_thread ? c.pix_per_thread : 0;
+        if (!P) {
+            P = 1;
+            for (int q : {4, 2}) if (Yw % q == 0) { P = q; break; }
+        }
+        if (P != 1 && P != 2 && P != 4) return fail(USC_ERR_VALUE, "BI pix_per_thread must be 1,2,4");
+        const int SPR = (Yw + P - 1) / P;
+        int WS, TH, SPRt;
+        if ((int64_t)Yh * SPR <= 8) {
+            WS = Yh * SPR;
+            TH = Yh;
+            SPRt = SPR;
+        } else if (SPR <= 8) {
+            TH = 8 / SPR;
+            WS = TH * SPR;
+            SPRt = SPR;
+        } else {
+            TH = 1;
+            SPRt = 8;
+            WS = 8;
+        }
+        int WC = 8 / WS;
+        if (WC < 1) WC = 1;
+        int DW = c.ch_per_cta ? std::max(1, c.ch_per_cta / WC) : std::max(4, 16 / WC);
+        if (DW > 16) DW = 16;
+        if (DW != 4 && DW != 8 && DW != 16) DW = DW < 4 ? 4 : (DW < 8 ? 8 : 16);
+        const int col_tiles = (SPR + SPRt - 1) / SPRt;
+        const bool full_rows = (col_tiles == 1 && SPR * P == Yw);
+        int TWs = full_rows ? pl->in.ws : (SPRt * P - 1) * g.stride_w + g.filter_w;
+        const int HS = (TH - 1) * g.stride_h + g.filter_h;
+        const int64_t per_ch = (int64_t)HS * TWs * 32 * eb;
+        int CC = c.chunk_channels ? c.chunk_channels : 64;
+        CC = std::min(CC, g.in_channels);
+        const int64_t budget = 100 * 1024;
+        while (CC > 1 && 2 * CC * per_ch > budget) --CC;
+        const int64_t stage = (CC * per_ch + 127) / 128 * 128;
+        if (2 * stage + 128 > 220 * 1024) return fail(USC_ERR_UNSUPPORTED, "BI tile does not fit smem");
+        pl->kernel = 3;
+        pl->P = P;
+        pl->WS = WS;
+        pl->WC = WC;
+        pl->DW = DW;
+        pl->DT = WC * DW;
+        pl->NS = 32;
+        pl->CC = CC;
+        pl->TH = TH;
+        pl->HS = HS;
+        pl->SPRt = SPRt;
+        pl->col_tiles = col_tiles;
+        pl->TWs = TWs;
+        pl->threads = 256;
+        pl->strips_per_row = SPR;
+        pl->row_tiles = (Yh + TH - 1) / TH;
+        pl->sample_tiles = (n + 31) / 32;
+        pl->groups = (g.out_channels + pl->DT - 1) / pl->DT;
+        pl->n_chunks = (g.in_channels + CC - 1) / CC;
+        pl->smem_stage_bytes = stage;
+        pl->smem_bytes = 2 * stage + 128;
+        pl->grid_x = (int64_t)pl->groups * pl->sample_tiles * pl->row_tiles * pl->col_tiles;
+        pl->grid_y = 1;
+        return USC_OK;
+    }
     if (kernel == 1) {
         int P = c.pix_per_thread ? c.pix_per_thread : std::min(4, pow2_floor(Yw));
         if (P != 1 && P != 2 && P != 4 && P != 8) return fail(USC_ERR_VALUE, "pix_per_thread must be 1,2,4,8");
@@ -396,9 +475,13 @@ int usc_pack(const usc_plan *pl, const int64_t *row_ptr, const int64_t *col, con
                         zero_seen.push_back(lam);
                     }
                     if (pl->transposed) std::swap(kh, kw);  // (c, kh, 0) -> (c, 0, kh)
-                    int64_t off = pl->kernel == 1
-                                      ? (c - (int64_t)k * CC) * cs_tiled + kh * Ws + kw
-                                      : (c * Hp + kh) * Ws + kw;
+                    int64_t off;
+                    if (pl->kernel == 1)
+                        off = (c - (int64_t)k * CC) * cs_tiled + kh * Ws + kw;
+                    else if (pl->kernel == 3)  // word offset in the [CC][HS][TWs][32] stage
+                        off = (((c - (int64_t)k * CC) * pl->HS + kh) * pl->TWs + kw) * 32;
+                    else
+                        off = (c * Hp + kh) * Ws + kw;
                     if (off >= max_off || off > INT32_MAX)
                         return fail(USC_ERR_UNSUPPORTED, "packed offset %lld too large", (long long)off);
                     char *e = ent + pos * eb;

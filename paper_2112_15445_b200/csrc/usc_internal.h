@@ -10,3 +10,13 @@ int fail(int code, const char *fmt, ...);
 int elem_bytes(int dtype);
 int entry_bytes(int dtype);
 }  // namespace usc
+
+#ifdef __CUDACC__
+namespace usc_dev {
+struct Epi;
+}
+namespace usc {
+int launch_bi(const usc_plan *pl, const void *blob, const void *x, void *y, const usc_dev::Epi &ep,
+              cudaStream_t st);
+}
+#endif

@@ -93,7 +93,7 @@ def make_plan(geometry: ConvGeometry, n: int, dtype: int, config: ExecConfig | N
 
 
 def _pack_key(plan: _lib.Plan, device) -> tuple:
-    return (plan.dtype, plan.kernel, plan.DT, plan.CC, plan.HS, plan.in_.ws, plan.in_.hp,
+    return (plan.dtype, plan.kernel, plan.DT, plan.CC, plan.HS, plan.TWs, plan.in_.ws, plan.in_.hp,
             plan.transposed, plan.groups, plan.n_chunks, str(device))
 
 
@@ -124,7 +124,7 @@ def padded_input(x_dev, plan: _lib.Plan, stream=None):
     """Plain NCHW storage tensor -> the plan's padded layout (zero_pad, tensor.py:225-235)."""
     import torch
     lay = plan.in_
-    out = torch.empty(plan.n * lay.sample_stride, dtype=x_dev.dtype, device=x_dev.device)
+    out = torch.empty(lay.elems(plan.n), dtype=x_dev.dtype, device=x_dev.device)
     _lib.check(_lib.lib().usc_pad_input(_lib.ref(lay), plan.dtype, plan.n, _lib.t_ptr(x_dev),
                                         _lib.t_ptr(out), _lib.stream_ptr(stream)), "pad")
     return out
@@ -241,18 +241,30 @@ def time_median_cuda(fn, repeats: int = 9, warmup: int = 2) -> float:
     return float(np.median(times))
 
 
-def tile_candidates(geometry: ConvGeometry, n: int, sb_values) -> list[ExecConfig]:
-    """The autotuner's search space: per usable sb (samples per CTA), pixels
-    per thread and output channels per CTA (the paper's hand-chosen block count,
-    PAPER.md:739-749, becomes a searched tile)."""
+def tile_candidates(geometry: ConvGeometry, n: int, sb_values, precision=PrecisionMode.BINARY32,
+                    kernels=None) -> list[ExecConfig]:
+    """The autotuner's search space (the paper's hand-chosen block count,
+    PAPER.md:739-749, becomes a searched tile).  Kernel 3 (batch-interleaved,
+    fp32): pixels per thread x output channels per CTA.  Kernel 1 (padded NCHW):
+    samples per CTA (the sb_S analogue) x pixels per thread x channels per CTA."""
     out = []
     yw = geometry.out_w if geometry.input_w != 1 else geometry.out_h
-    ps = [p for p in (2, 4, 8) if p <= max(2, yw)]
-    for sb in sb_values:
-        for p in ps:
-            for dt in (8, 16):
-                out.append(ExecConfig(sub_batch=sb, samples_per_cta=sb if sb > 1 else 0,
-                                      pix_per_thread=p, ch_per_cta=dt))
+    if kernels is None:
+        kernels = (3, 1) if precision is PrecisionMode.BINARY32 else (1,)
+    if 3 in kernels and precision is PrecisionMode.BINARY32:
+        for p in (1, 2, 4):
+            if p > yw:
+                continue
+            for dt in (8, 16, 32, 64):
+                out.append(ExecConfig(sub_batch=min(sb_values), pix_per_thread=p, ch_per_cta=dt,
+                                      kernel=3))
+    if 1 in kernels:
+        ps = [p for p in (2, 4, 8) if p <= max(2, yw)]
+        for sb in sb_values:
+            for p in ps:
+                for dt in (8, 16):
+                    out.append(ExecConfig(sub_batch=sb, samples_per_cta=sb if sb > 1 else 0,
+                                          pix_per_thread=p, ch_per_cta=dt, kernel=1))
     return out
 
 
@@ -271,7 +283,7 @@ def autotune_sb(input: DenseTensor4, filt: CsrFilter, candidates=SB_CANDIDATES, 
     x = input.device()
     results = []
     pads = {}
-    for cfg in tile_candidates(g, n, usable):
+    for cfg in tile_candidates(g, n, usable, input.precision):
         try:
             plan = make_plan(g, n, dtype, cfg)
         except ValueError:

@@ -73,14 +73,23 @@ class SparseVGG16:
     # -- buffers and plans ---------------------------------------------------
     def _buf(self, lay):
         import torch
-        return torch.zeros(self.batch * lay.sample_stride, dtype=self.tdtype, device=self.device)
+        return torch.zeros(lay.elems(self.batch), dtype=self.tdtype, device=self.device)
 
     def _build(self):
         n = self.batch
         self.plans, self.blobs, self.steps = [], [], []
         # input buffer of the first conv
+        plans = [make_plan(g, n, self.dtype, c) for g, c in zip(self.geoms, self.configs)]
+        # every layer reads the layout its plan wants: one interleave for the network
+        il = 32 if all(p.kernel == 3 for p in plans) else 0
+        if il == 0 and any(p.kernel == 3 for p in plans):
+            plans = [make_plan(g, n, self.dtype, ExecConfig(c.sub_batch, c.worker_count, c.pix_per_thread,
+                                                            c.ch_per_cta, c.samples_per_cta,
+                                                            c.chunk_channels, 1 if c.kernel in (0, 3) else c.kernel))
+                     for g, c in zip(self.geoms, self.configs)]
+        self.interleave = il
         g0 = self.geoms[0]
-        self.in_layout = _lib.act_layout(g0.in_channels, g0.input_h, g0.input_w, 1, 1, self.eb)
+        self.in_layout = _lib.act_layout(g0.in_channels, g0.input_h, g0.input_w, 1, 1, self.eb, il)
         self.x_buf = self._buf(self.in_layout)
         cur_buf, cur_lay = self.x_buf, self.in_layout
         self.nonzero_macs = 0
@@ -89,16 +98,16 @@ class SparseVGG16:
             if v == "M":
                 continue
             g = self.geoms[li]
-            plan = make_plan(g, n, self.dtype, self.configs[li])
+            plan = plans[li]
             blob, n_ent = device_pack(self.filters[li], plan, self.filters[li].weights, device=self.device)
             nxt = VGG16_CIFAR[i + 1] if i + 1 < len(VGG16_CIFAR) else None
             epi = _lib.Epilogue()
             epi.relu = 1
             epi.scale = 1.0
             if nxt == "M":
-                out_lay = _lib.act_layout(g.out_channels, g.out_h, g.out_w, 0, 0, self.eb)
+                out_lay = _lib.act_layout(g.out_channels, g.out_h, g.out_w, 0, 0, self.eb, il)
             else:
-                out_lay = _lib.act_layout(g.out_channels, g.out_h, g.out_w, 1, 1, self.eb)
+                out_lay = _lib.act_layout(g.out_channels, g.out_h, g.out_w, 1, 1, self.eb, il)
             epi.out_padded = 1
             epi.out = out_lay
             out_buf = self._buf(out_lay)
@@ -108,7 +117,7 @@ class SparseVGG16:
             if nxt == "M":
                 last = i + 2 >= len(VGG16_CIFAR)
                 ph = 0 if last else 1
-                pool_lay = _lib.act_layout(g.out_channels, g.out_h // 2, g.out_w // 2, ph, ph, self.eb)
+                pool_lay = _lib.act_layout(g.out_channels, g.out_h // 2, g.out_w // 2, ph, ph, self.eb, il)
                 pool_buf = self._buf(pool_lay)
                 self.steps.append(("pool", li, cur_lay, pool_lay, cur_buf, pool_buf))
                 cur_buf, cur_lay = pool_buf, pool_lay
@@ -136,8 +145,17 @@ class SparseVGG16:
                 _lib.check(L.usc_maxpool2(_lib.ref(lin), _lib.ref(lout), self.dtype, self.batch,
                                           _lib.t_ptr(xin), _lib.t_ptr(yout), sp), "pool")
 
-    def output(self):
-        return self.out_buf.view(self.batch, self.out_layout.channels, 1, 1)
+    def output(self, stream=None):
+        """(n, 512, 1, 1) plain NCHW features (unpacked from the last pool's layout)."""
+        import torch
+        lay = self.out_layout
+        if not hasattr(self, "_out_plain"):
+            self._out_plain = torch.empty((self.batch, lay.channels, lay.height, lay.width),
+                                          dtype=self.tdtype, device=self.device)
+        _lib.check(_lib.lib().usc_unpad_output(_lib.ref(lay), self.dtype, self.batch,
+                                               _lib.t_ptr(self.out_buf), _lib.t_ptr(self._out_plain),
+                                               _lib.stream_ptr(stream)), "unpad")
+        return self._out_plain
 
     def forward(self, x):
         self.load_input(x)
@@ -180,7 +198,8 @@ class SparseVGG16:
             g = self.geoms[li]
             usable = [sb for sb in (1, 2, 4, 8, 16, 32) if self.batch % sb == 0]
             results = []
-            for cfg in [ExecConfig()] + tile_candidates(g, self.batch, usable):
+            kern = (3,) if self.interleave == 32 else (1,)
+            for cfg in [self.configs[li]] + tile_candidates(g, self.batch, usable, self.precision, kern):
                 try:
                     plan = make_plan(g, self.batch, self.dtype, cfg)
                 except ValueError:

@@ -158,11 +158,19 @@ def test_int8_filter_matches_reference_composition(name):
 
 
 def test_planner_tiles():
-    # cfg1: 8x8 maps -> full-map tiles, several samples per CTA
-    p = make_plan(U.ConvGeometry(256, 256, 3, 3, 8, 8, padding=(1, 1)), 32, _lib.USC_F32, None)
+    # cfg1 fp32: batch-interleaved kernel, 32 samples per CTA, lane = sample
+    g1 = U.ConvGeometry(256, 256, 3, 3, 8, 8, padding=(1, 1))
+    p = make_plan(g1, 32, _lib.USC_F32, None)
+    assert p.kernel == 3 and p.in_.interleave == 32 and p.NS == 32 and p.in_.ws == 10
+    assert p.WS * p.WC <= 8 and p.DT == p.WC * p.DW and p.smem_bytes <= 220 * 1024
+    assert p.in_.elems(33) == 2 * 256 * 10 * 10 * 32
+    # padded-NCHW kernel: full-map tiles, several samples per CTA
+    p = make_plan(g1, 32, _lib.USC_F32, U.ExecConfig(kernel=1))
     assert p.kernel == 1 and p.TH == 8 and p.NS * 8 * p.strips_per_row <= 256
     assert p.in_.ws % 4 == 0 and p.in_.hp == 10 and p.groups == 16
     assert p.smem_bytes <= 220 * 1024
+    p = make_plan(g1, 32, _lib.USC_F16, None)
+    assert p.kernel == 1 and p.in_.ws % 8 == 0
     # 1-D layer runs transposed
     p = make_plan(U.ConvGeometry(64, 64, 2, 1, 300, 1), 8, _lib.USC_F32, None)
     assert p.transposed == 1 and p.out_w == 299 and p.out_h == 1
@@ -170,8 +178,11 @@ def test_planner_tiles():
     p = make_plan(U.ConvGeometry(4, 4, 3, 3, 10, 10, stride=(3, 3), padding=(1, 1)), 2, _lib.USC_F32, None)
     assert p.kernel == 2
     # 32x32 maps tile by rows
-    p = make_plan(U.ConvGeometry(64, 64, 3, 3, 32, 32, padding=(1, 1)), 256, _lib.USC_F32, None)
+    p = make_plan(U.ConvGeometry(64, 64, 3, 3, 32, 32, padding=(1, 1)), 256, _lib.USC_F32,
+                  U.ExecConfig(kernel=1))
     assert p.kernel == 1 and p.NS == 1 and p.row_tiles * p.TH >= 32
+    p = make_plan(U.ConvGeometry(64, 64, 3, 3, 32, 32, padding=(1, 1)), 256, _lib.USC_F32, None)
+    assert p.kernel == 3 and p.row_tiles * p.TH >= 32 and p.grid_x == p.groups * 8 * p.row_tiles
     with pytest.raises(ValueError):
         make_plan(U.ConvGeometry(4, 4, 3, 3, 8, 8, padding=(1, 1)), 6, _lib.USC_F32, U.ExecConfig(4))
 
