@@ -82,6 +82,7 @@ typedef struct usc_exec_cfg {
     int32_t chunk_channels;   /* CC: input channels per shared-memory stage */
     int32_t threads;          /* threads per CTA (128 or 256) */
     int32_t kernel;           /* 0 auto, 1 tiled (padded NCHW), 2 generic, 3 batch-interleaved */
+    int32_t pixel_warps;      /* kernel 3: warps over output strips (rest split the channels) */
 } usc_exec_cfg;
 
 /* Resolved plan for one (geometry, batch, dtype, cfg): tile shape, packing
@@ -99,6 +100,7 @@ typedef struct usc_plan {
     int32_t strips_per_row, row_tiles, sample_tiles, groups, n_chunks;
     int32_t WS, WC, DW;          /* BI kernel: warps over strips, warps over channels, channels/warp */
     int32_t SPRt, col_tiles, TWs;/* BI kernel: strips per tile row, column tiles, staged row width */
+    int32_t ent_stage_bytes;     /* BI kernel: shared-memory reserve for one chunk's entries */
     int32_t transposed;          /* 1D layer (W==1) run as its H/W transpose */
     int64_t smem_stage_bytes, smem_bytes;
     int64_t grid_x, grid_y;

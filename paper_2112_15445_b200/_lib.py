@@ -41,7 +41,8 @@ class ActLayout(ctypes.Structure):
 
 class ExecCfg(ctypes.Structure):
     _fields_ = [(n, c_i32) for n in ("sub_batch", "worker_count", "pix_per_thread", "ch_per_cta",
-                                     "samples_per_cta", "chunk_channels", "threads", "kernel")]
+                                     "samples_per_cta", "chunk_channels", "threads", "kernel",
+                                     "pixel_warps")]
 
 
 class Plan(ctypes.Structure):
@@ -50,7 +51,8 @@ class Plan(ctypes.Structure):
                 ("CC", c_i32), ("threads", c_i32), ("TH", c_i32), ("HS", c_i32),
                 ("strips_per_row", c_i32), ("row_tiles", c_i32), ("sample_tiles", c_i32),
                 ("groups", c_i32), ("n_chunks", c_i32), ("WS", c_i32), ("WC", c_i32), ("DW", c_i32),
-                ("SPRt", c_i32), ("col_tiles", c_i32), ("TWs", c_i32), ("transposed", c_i32),
+                ("SPRt", c_i32), ("col_tiles", c_i32), ("TWs", c_i32), ("ent_stage_bytes", c_i32),
+                ("transposed", c_i32),
                 ("smem_stage_bytes", c_i64), ("smem_bytes", c_i64), ("grid_x", c_i64),
                 ("grid_y", c_i64)]
 

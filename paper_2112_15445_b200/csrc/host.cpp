@@ -261,32 +261,41 @@ int usc_plan_make(const usc_geometry *g0, int32_t n, int32_t dtype, const usc_ex
     if (kernel == 3) {
         // batch-interleaved: a CTA = 32 samples x (WS strips of P pixels) x (WC*DW channels);
         // warp w owns strip w % WS for channel subgroup w / WS; lane = sample.
+        // defaults follow what the autotuner picks on B200 for 3x3 layers: 512 threads
+        // (1 CTA/SM, long channel chunks), 4 warps over pixels x 4 over channels
+        const int NT = (c.threads == 256) ? 256 : 512;
+        const int NW = NT / 32;
         int P = c.pix_per_thread ? c.pix_per_thread : 0;
         if (!P) {
             P = 1;
-            for (int q : {4, 2}) if (Yw % q == 0) { P = q; break; }
+            for (int q : {8, 4, 2}) if (Yw % q == 0) { P = q; break; }
         }
-        if (P != 1 && P != 2 && P != 4) return fail(USC_ERR_VALUE, "BI pix_per_thread must be 1,2,4");
+        if (P != 1 && P != 2 && P != 4 && P != 8)
+            return fail(USC_ERR_VALUE, "BI pix_per_thread must be 1,2,4,8");
         const int SPR = (Yw + P - 1) / P;
+        int WSmax = c.pixel_warps ? std::min(c.pixel_warps, NW) : std::min(4, NW);
         int WS, TH, SPRt;
-        if ((int64_t)Yh * SPR <= 8) {
+        if ((int64_t)Yh * SPR <= WSmax) {
             WS = Yh * SPR;
             TH = Yh;
             SPRt = SPR;
-        } else if (SPR <= 8) {
-            TH = 8 / SPR;
+        } else if (SPR <= WSmax) {
+            TH = WSmax / SPR;
             WS = TH * SPR;
             SPRt = SPR;
         } else {
             TH = 1;
-            SPRt = 8;
-            WS = 8;
+            SPRt = WSmax;
+            WS = WSmax;
         }
-        int WC = 8 / WS;
+        int WC = NW / WS;
         if (WC < 1) WC = 1;
-        int DW = c.ch_per_cta ? std::max(1, c.ch_per_cta / WC) : std::max(4, 16 / WC);
+        int DW = c.ch_per_cta ? std::max(1, c.ch_per_cta / WC) : (NT == 512 && WC <= 4 ? 8 : 4);
         if (DW > 16) DW = 16;
         if (DW != 4 && DW != 8 && DW != 16) DW = DW < 4 ? 4 : (DW < 8 ? 8 : 16);
+        const int acc_cap = NT == 512 ? 64 : 32;  // accumulators that fit the register cap
+        while (DW > 4 && DW * P > acc_cap) DW /= 2;
+        if (DW * P > acc_cap) return fail(USC_ERR_VALUE, "BI tile needs too many accumulators");
         const int col_tiles = (SPR + SPRt - 1) / SPRt;
         const bool full_rows = (col_tiles == 1 && SPR * P == Yw);
         int TWs = full_rows ? pl->in.ws : (SPRt * P - 1) * g.stride_w + g.filter_w;
@@ -294,10 +303,22 @@ int usc_plan_make(const usc_geometry *g0, int32_t n, int32_t dtype, const usc_ex
         const int64_t per_ch = (int64_t)HS * TWs * 32 * eb;
         int CC = c.chunk_channels ? c.chunk_channels : 64;
         CC = std::min(CC, g.in_channels);
-        const int64_t budget = 100 * 1024;
-        while (CC > 1 && 2 * CC * per_ch > budget) --CC;
+        // 2 stages; 256 threads -> 4 CTAs per SM, 512 threads -> 1 CTA per SM
+        const int64_t budget = c.chunk_channels ? INT64_MAX : (NT == 512 ? 190 * 1024 : 52 * 1024);
+        // per-stage entry buffer: DT*CC*Kh*Kw entries of 8 bytes (+1 alignment pad) is the
+        // exact worst case; reserve at most R bytes -- usc_pack rejects a filter whose
+        // densest (group, chunk) block exceeds the reserve (the caller then re-plans
+        // with fewer chunk channels)
+        const int64_t R = NT == 512 ? 24 * 1024 : 6 * 1024;
+        auto ent_bytes = [&](int cc) {
+            const int64_t worst = ((int64_t)(WC * DW) * cc * g.filter_h * g.filter_w * 8 + 16 + 127) / 128 * 128;
+            return c.chunk_channels ? worst : std::min(worst, R);
+        };
+        while (CC > 1 && 2 * (CC * per_ch + ent_bytes(CC)) > budget) --CC;
         const int64_t stage = (CC * per_ch + 127) / 128 * 128;
-        if (2 * stage + 128 > 220 * 1024) return fail(USC_ERR_UNSUPPORTED, "BI tile does not fit smem");
+        const int64_t ent_stage = ent_bytes(CC);
+        if (2 * (stage + ent_stage) + 128 > 220 * 1024)
+            return fail(USC_ERR_VALUE, "BI tile does not fit shared memory");
         pl->kernel = 3;
         pl->P = P;
         pl->WS = WS;
@@ -311,14 +332,15 @@ int usc_plan_make(const usc_geometry *g0, int32_t n, int32_t dtype, const usc_ex
         pl->SPRt = SPRt;
         pl->col_tiles = col_tiles;
         pl->TWs = TWs;
-        pl->threads = 256;
+        pl->threads = NT;
         pl->strips_per_row = SPR;
         pl->row_tiles = (Yh + TH - 1) / TH;
         pl->sample_tiles = (n + 31) / 32;
         pl->groups = (g.out_channels + pl->DT - 1) / pl->DT;
         pl->n_chunks = (g.in_channels + CC - 1) / CC;
         pl->smem_stage_bytes = stage;
-        pl->smem_bytes = 2 * stage + 128;
+        pl->ent_stage_bytes = static_cast<int32_t>(ent_stage);
+        pl->smem_bytes = 2 * (stage + ent_stage) + 128;
         pl->grid_x = (int64_t)pl->groups * pl->sample_tiles * pl->row_tiles * pl->col_tiles;
         pl->grid_y = 1;
         return USC_OK;
@@ -409,7 +431,11 @@ static int64_t align16(int64_t v) { return (v + 15) / 16 * 16; }
 
 int usc_pack_size(const usc_plan *pl, int64_t n_nz, int64_t *bytes) {
     int64_t cp = align16(4 * ((int64_t)pl->groups * pl->n_chunks * pl->DT + 1));
-    int64_t ent = align16((int64_t)pl->g.out_channels * n_nz * entry_bytes(pl->dtype));
+    // kernel 3 starts every (group, chunk) block on a 16-byte boundary (one pad
+    // entry at most per block) and reads up to 16 bytes past a block
+    int64_t n_ent = (int64_t)pl->g.out_channels * n_nz +
+                    (pl->kernel == 3 ? (int64_t)pl->groups * pl->n_chunks : 0);
+    int64_t ent = align16(n_ent * entry_bytes(pl->dtype)) + 64;
     *bytes = 64 + cp + ent;  // [16-float centroid table][cpg][entries]
     return USC_OK;
 }
@@ -449,6 +475,10 @@ int usc_pack(const usc_plan *pl, const int64_t *row_ptr, const int64_t *col, con
     for (int gi = 0; gi < G; ++gi)
         for (int k = 0; k < NC; ++k)
             for (int dl = 0; dl < DT; ++dl) {
+                if (pl->kernel == 3 && dl == 0 && (pos & 1)) {
+                    std::memset(ent + pos * eb, 0, eb);  // alignment pad, never referenced
+                    ++pos;
+                }
                 cpg[((int64_t)gi * NC + k) * DT + dl] = (int32_t)pos;
                 int d = gi * DT + dl;
                 if (d >= D) continue;
@@ -478,8 +508,8 @@ int usc_pack(const usc_plan *pl, const int64_t *row_ptr, const int64_t *col, con
                     int64_t off;
                     if (pl->kernel == 1)
                         off = (c - (int64_t)k * CC) * cs_tiled + kh * Ws + kw;
-                    else if (pl->kernel == 3)  // word offset in the [CC][HS][TWs][32] stage
-                        off = (((c - (int64_t)k * CC) * pl->HS + kh) * pl->TWs + kw) * 32;
+                    else if (pl->kernel == 3)  // byte offset in the [CC][HS][TWs][32] f32 stage
+                        off = (((c - (int64_t)k * CC) * pl->HS + kh) * pl->TWs + kw) * 128;
                     else
                         off = (c * Hp + kh) * Ws + kw;
                     if (off >= max_off || off > INT32_MAX)
@@ -512,6 +542,14 @@ int usc_pack(const usc_plan *pl, const int64_t *row_ptr, const int64_t *col, con
             }
     cpg[(int64_t)G * NC * DT] = (int32_t)pos;
     *n_entries = pos;
+    if (pl->kernel == 3) {
+        int64_t worst = 0;
+        for (int64_t b = 0; b < (int64_t)G * NC; ++b)
+            worst = std::max<int64_t>(worst, ((int64_t)cpg[(b + 1) * DT] - cpg[b * DT]) * 8 + 16);
+        if (worst > pl->ent_stage_bytes)
+            return fail(USC_ERR_VALUE, "entry block of %lld bytes exceeds the %d-byte stage reserve",
+                        (long long)worst, pl->ent_stage_bytes);
+    }
     return USC_OK;
 }
 

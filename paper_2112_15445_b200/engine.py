@@ -42,6 +42,8 @@ class ExecConfig:
     samples_per_cta: int = 0
     chunk_channels: int = 0
     kernel: int = 0
+    threads: int = 0
+    pixel_warps: int = 0
 
     def __post_init__(self):
         if self.sub_batch < 1:
@@ -56,7 +58,8 @@ class ExecConfig:
 
     def to_c(self) -> _lib.ExecCfg:
         return _lib.ExecCfg(self.sub_batch, self.worker_count, self.pix_per_thread, self.ch_per_cta,
-                            self.samples_per_cta, self.chunk_channels, 256, self.kernel)
+                            self.samples_per_cta, self.chunk_channels, self.threads, self.kernel,
+                            self.pixel_warps)
 
 
 @dataclass(frozen=True)
@@ -90,6 +93,27 @@ def make_plan(geometry: ConvGeometry, n: int, dtype: int, config: ExecConfig | N
     g = _lib.make_geometry(geometry)
     _lib.check(_lib.lib().usc_plan_make(_lib.ref(g), n, dtype, _lib.ref(cfg), _lib.ref(plan)), "plan")
     return plan
+
+
+def plan_for(filt: CsrFilter, n: int, dtype: int, config: ExecConfig | None, payload, table=None,
+             device=None):
+    """make_plan + device_pack; when the filter's densest entry block overflows the
+    kernel-3 stage reserve, re-plan with fewer chunk channels (exact worst-case
+    reserve at the end)."""
+    config = config or ExecConfig()
+    plan = make_plan(filt.geometry, n, dtype, config)
+    while True:
+        try:
+            blob, n_ent = device_pack(filt, plan, payload, table, device)
+            return plan, blob
+        except ValueError as exc:
+            if plan.kernel != 3 or "stage reserve" not in str(exc):
+                raise
+            cc = plan.CC // 2 if plan.CC > 1 else 1
+            fields = {f: getattr(config, f) for f in config.__dataclass_fields__}
+            fields["chunk_channels"] = cc
+            config = ExecConfig(**fields)
+            plan = make_plan(filt.geometry, n, dtype, config)
 
 
 def _pack_key(plan: _lib.Plan, device) -> tuple:
@@ -168,8 +192,7 @@ def sparse_conv_forward(input: DenseTensor4, filt: CsrFilter,
     _check_call(input, filt, config)
     g = filt.geometry
     dtype = dtype_of(input.precision)
-    plan = make_plan(g, input.n, dtype, config)
-    blob, _ = device_pack(filt, plan, filt.weights)
+    plan, blob = plan_for(filt, input.n, dtype, config, filt.weights)
     x = input.device()
     x_pad = padded_input(x, plan)
     y = torch.empty((input.n, g.out_channels, g.out_h, g.out_w), dtype=_storage_dtype(dtype),
@@ -252,12 +275,14 @@ def tile_candidates(geometry: ConvGeometry, n: int, sb_values, precision=Precisi
     if kernels is None:
         kernels = (3, 1) if precision is PrecisionMode.BINARY32 else (1,)
     if 3 in kernels and precision is PrecisionMode.BINARY32:
-        for p in (1, 2, 4):
-            if p > yw:
+        for p in (1, 2, 4, 8):
+            if p > max(1, yw):
                 continue
-            for dt in (8, 16, 32, 64):
-                out.append(ExecConfig(sub_batch=min(sb_values), pix_per_thread=p, ch_per_cta=dt,
-                                      kernel=3))
+            for nt, dts in ((256, (8, 16, 32)), (512, (16, 32, 64))):
+                for dt in dts:
+                    for pw in (0, 4):
+                        out.append(ExecConfig(sub_batch=min(sb_values), pix_per_thread=p,
+                                              ch_per_cta=dt, kernel=3, threads=nt, pixel_warps=pw))
     if 1 in kernels:
         ps = [p for p in (2, 4, 8) if p <= max(2, yw)]
         for sb in sb_values:
@@ -265,7 +290,17 @@ def tile_candidates(geometry: ConvGeometry, n: int, sb_values, precision=Precisi
                 for dt in (8, 16):
                     out.append(ExecConfig(sub_batch=sb, samples_per_cta=sb if sb > 1 else 0,
                                           pix_per_thread=p, ch_per_cta=dt, kernel=1))
-    return out
+    feasible, seen = [], set()
+    for cfg in out:  # drop tiles that do not fit and duplicates of the same resolved plan
+        try:
+            plan = make_plan(geometry, n, dtype_of(precision), cfg)
+        except ValueError:
+            continue
+        key = (plan.kernel, plan.P, plan.DT, plan.DW, plan.WS, plan.NS, plan.CC, plan.threads)
+        if key not in seen:
+            seen.add(key)
+            feasible.append(cfg)
+    return feasible
 
 
 def autotune_sb(input: DenseTensor4, filt: CsrFilter, candidates=SB_CANDIDATES, worker_count: int = 1,
@@ -285,10 +320,9 @@ def autotune_sb(input: DenseTensor4, filt: CsrFilter, candidates=SB_CANDIDATES, 
     pads = {}
     for cfg in tile_candidates(g, n, usable, input.precision):
         try:
-            plan = make_plan(g, n, dtype, cfg)
+            plan, blob = plan_for(filt, n, dtype, cfg, filt.weights)
         except ValueError:
             continue
-        blob, _ = device_pack(filt, plan, filt.weights)
         lk = plan.in_.key()
         if lk not in pads:
             pads[lk] = padded_input(x, plan)
@@ -301,5 +335,6 @@ def autotune_sb(input: DenseTensor4, filt: CsrFilter, candidates=SB_CANDIDATES, 
         for ms, cfg in results:
             if cfg.sub_batch == sb and ms <= best * (1.0 + noise_floor):
                 return ExecConfig(cfg.sub_batch, worker_count, cfg.pix_per_thread, cfg.ch_per_cta,
-                                  cfg.samples_per_cta, cfg.chunk_channels, cfg.kernel)
+                                  cfg.samples_per_cta, cfg.chunk_channels, cfg.kernel, cfg.threads,
+                                  cfg.pixel_warps)
     return ExecConfig(usable[0], worker_count)

@@ -20,7 +20,8 @@ import numpy as np
 
 from . import _lib
 from .csr import build_csr
-from .engine import ExecConfig, device_pack, launch, make_plan, time_median_cuda, tile_candidates
+from .engine import (ExecConfig, device_pack, launch, make_plan, plan_for, time_median_cuda,
+                     tile_candidates)
 from .pruning import synthesize_masked_weights
 from .tensor import ConvGeometry, PrecisionMode
 
@@ -46,6 +47,13 @@ def vgg16_rng(sparsity: float, seed: int = 0):
 def vgg16_weights(rng, sparsity: float, precision=PrecisionMode.BINARY32, unified: bool = False):
     """Random-init pruned weights, one DenseTensor4 per conv (bench.py:84-95 generator)."""
     return [synthesize_masked_weights(g, sparsity, rng, precision, unified) for g in vgg16_geometries()]
+
+
+def _cfg_of(plan, cfg: ExecConfig) -> ExecConfig:
+    """The config a network layer is planned with (its kernel family pinned)."""
+    fields = {f: getattr(cfg, f) for f in cfg.__dataclass_fields__}
+    fields["kernel"] = plan.kernel
+    return ExecConfig(**fields)
 
 
 class SparseVGG16:
@@ -85,9 +93,11 @@ class SparseVGG16:
         if il == 0 and any(p.kernel == 3 for p in plans):
             plans = [make_plan(g, n, self.dtype, ExecConfig(c.sub_batch, c.worker_count, c.pix_per_thread,
                                                             c.ch_per_cta, c.samples_per_cta,
-                                                            c.chunk_channels, 1 if c.kernel in (0, 3) else c.kernel))
+                                                            c.chunk_channels,
+                                                            1 if c.kernel in (0, 3) else c.kernel))
                      for g, c in zip(self.geoms, self.configs)]
         self.interleave = il
+        plan_cfgs = [_cfg_of(p, c) for p, c in zip(plans, self.configs)]
         g0 = self.geoms[0]
         self.in_layout = _lib.act_layout(g0.in_channels, g0.input_h, g0.input_w, 1, 1, self.eb, il)
         self.x_buf = self._buf(self.in_layout)
@@ -98,8 +108,8 @@ class SparseVGG16:
             if v == "M":
                 continue
             g = self.geoms[li]
-            plan = plans[li]
-            blob, n_ent = device_pack(self.filters[li], plan, self.filters[li].weights, device=self.device)
+            plan, blob = plan_for(self.filters[li], n, self.dtype, plan_cfgs[li], self.filters[li].weights,
+                                  device=self.device)
             nxt = VGG16_CIFAR[i + 1] if i + 1 < len(VGG16_CIFAR) else None
             epi = _lib.Epilogue()
             epi.relu = 1
@@ -201,11 +211,10 @@ class SparseVGG16:
             kern = (3,) if self.interleave == 32 else (1,)
             for cfg in [self.configs[li]] + tile_candidates(g, self.batch, usable, self.precision, kern):
                 try:
-                    plan = make_plan(g, self.batch, self.dtype, cfg)
+                    plan, blob = plan_for(self.filters[li], self.batch, self.dtype, cfg,
+                                          self.filters[li].weights, device=self.device)
                 except ValueError:
                     continue
-                blob, _ = device_pack(self.filters[li], plan, self.filters[li].weights,
-                                      device=self.device)
                 ms = time_median_cuda(lambda: launch(plan, blob, xin, yout, epi), repeats, warmup)
                 results.append((ms, cfg))
             best = min(ms for ms, _ in results)

@@ -30,7 +30,7 @@ import numpy as np
 
 from . import _lib
 from .csr import CsrFilter, build_csr
-from .engine import ExecConfig, device_pack, launch, make_plan, padded_input
+from .engine import ExecConfig, launch, padded_input, plan_for
 from .tensor import ConvGeometry, DenseTensor4, PrecisionMode, round_to_binary16
 
 MODES = ("passthrough", "16b/16b", "4b/16b")
@@ -254,8 +254,7 @@ def sparse_conv_forward_int8(xq: Int8Tensor, fq: Int8CsrFilter, config: ExecConf
     if int8_exact_bound(fq, xq) >= 2 ** 24:
         warnings.warn("int8 partial sums exceed 2**24: the fp32 reference composition rounds, "
                       "this kernel is exact", RuntimeWarning)
-    plan = make_plan(g, n, _lib.USC_I8, config)
-    blob, _ = device_pack(fq.filt, plan, fq.codes)
+    plan, blob = plan_for(fq.filt, n, _lib.USC_I8, config, fq.codes)
     x_pad = padded_input(xq.codes, plan)
     y = torch.empty((n, g.out_channels, g.out_h, g.out_w), dtype=torch.float32, device=x_pad.device)
     epi = _lib.Epilogue()
@@ -318,8 +317,7 @@ def sparse_conv_forward_codebook(x: DenseTensor4, fc: CodebookCsrFilter,
     xh = x.device()
     if xh.dtype != torch.float16:
         xh = round_to_binary16(xh).to(torch.float16)
-    plan = make_plan(g, x.n, _lib.USC_CB4, config)
-    blob, _ = device_pack(fc.filt, plan, fc.indices, fc.table)
+    plan, blob = plan_for(fc.filt, x.n, _lib.USC_CB4, config, fc.indices, fc.table)
     x_pad = padded_input(xh, plan)
     y = torch.empty((x.n, g.out_channels, g.out_h, g.out_w), dtype=torch.float16, device=xh.device)
     epi = _lib.Epilogue()

@@ -162,7 +162,7 @@ def test_planner_tiles():
     g1 = U.ConvGeometry(256, 256, 3, 3, 8, 8, padding=(1, 1))
     p = make_plan(g1, 32, _lib.USC_F32, None)
     assert p.kernel == 3 and p.in_.interleave == 32 and p.NS == 32 and p.in_.ws == 10
-    assert p.WS * p.WC <= 8 and p.DT == p.WC * p.DW and p.smem_bytes <= 220 * 1024
+    assert p.WS * p.WC <= p.threads // 32 and p.DT == p.WC * p.DW and p.smem_bytes <= 220 * 1024
     assert p.in_.elems(33) == 2 * 256 * 10 * 10 * 32
     # padded-NCHW kernel: full-map tiles, several samples per CTA
     p = make_plan(g1, 32, _lib.USC_F32, U.ExecConfig(kernel=1))

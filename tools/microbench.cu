@@ -71,6 +71,16 @@ __global__ void k_lds(float *out, int iters) {
     if (s == 1.2345f) out[0] = s;
 }
 
+__global__ void k_l2read(const float4 *__restrict__ src, long long n4, int reps, float *out) {
+    float4 acc = make_float4(0, 0, 0, 0);
+    for (int r = 0; r < reps; ++r)
+        for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4; i += (long long)gridDim.x * blockDim.x) {
+            float4 v = __ldcg(src + i);
+            acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+        }
+    if (acc.x + acc.y + acc.z + acc.w == 1.2345f) out[0] = acc.x;
+}
+
 int main() {
     float *out;
     cudaMalloc(&out, 4);
@@ -101,6 +111,23 @@ int main() {
     run("fmul2+fadd2", [&] { k_muladd_x2<<<blocks, threads>>>(out, 1.0001f, 0.5f, iters); }, 4.0 * N_ACC, "TFLOP/s(x1e3 GF)");
     run("ffma2", [&] { k_ffma_x2<<<blocks, threads>>>(out, 1.0001f, 0.5f, iters); }, 4.0 * N_ACC, "TFLOP/s(x1e3 GF)");
     run("lds32", [&] { k_lds<<<blocks, threads>>>(out, iters); }, 4.0 * N_ACC, "GB/s");
+    {
+        long long n4 = (64ll << 20) / 16;  // 64 MB: L2-resident
+        float4 *buf;
+        cudaMalloc(&buf, n4 * 16);
+        cudaMemset(buf, 0, n4 * 16);
+        int reps = 20;
+        k_l2read<<<sms * 4, 512>>>(buf, n4, 1, out);
+        cudaDeviceSynchronize();
+        cudaEventRecord(e0);
+        k_l2read<<<sms * 4, 512>>>(buf, n4, reps, out);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms;
+        cudaEventElapsedTime(&ms, e0, e1);
+        printf("{\"test\": \"l2_read_64MB\", \"rate\": %.1f, \"unit\": \"GB/s\"}\n", n4 * 16.0 * reps / ms / 1e6);
+        cudaFree(buf);
+    }
     cudaError_t e = cudaGetLastError();
     printf("{\"sms\": %d, \"err\": \"%s\"}\n", sms, cudaGetErrorString(e));
     return 0;
