@@ -210,6 +210,12 @@ int usc_maxpool2(const usc_act_layout *in_l, const usc_act_layout *out_l, int32_
 int usc_quantize_i8(const float *src, int8_t *dst, int64_t count, double sigma, int32_t bits,
                     void *stream);
 
+/* ---- diagnostics ----------------------------------------------------------
+ * Live CUDA-core peak of the exact fp32 path's instruction mix (IEEE multiply
+ * then add, never contracted) on `device`, in TFLOP/s (2 flops per pair); the
+ * roofline denominator bench.py reports the sparse conv kernel against. */
+int usc_peak_fp32_muladd(int32_t device, double *tflops);
+
 /* ---- quantisation primitives (host) -- quantization.py ------------------ */
 /* fit_fixed_point (quantization.py:41-58): from max|x| */
 int usc_fit_fixed_point(double amax, int32_t total_bits, int32_t *int_bits, int32_t *frac_bits,

@@ -100,6 +100,7 @@ _SIGS = {
     "usc_convert": (c_i32, [c_ptr, c_i32, c_ptr, c_i32, c_i64, c_ptr]),
     "usc_maxpool2": (c_i32, [c_ptr, c_ptr, c_i32, c_i32, c_ptr, c_ptr, c_ptr]),
     "usc_quantize_i8": (c_i32, [c_ptr, c_ptr, c_i64, ctypes.c_double, c_i32, c_ptr]),
+    "usc_peak_fp32_muladd": (c_i32, [c_i32, c_ptr]),
     "usc_fit_fixed_point": (c_i32, [ctypes.c_double, c_i32, c_ptr, c_ptr, c_ptr]),
     "usc_linear_codes": (c_i32, [c_ptr, c_i64, ctypes.c_double, c_i32, c_ptr]),
     "usc_kmeans_codebook": (c_i32, [c_ptr, c_i64, c_i32, c_i32, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr]),

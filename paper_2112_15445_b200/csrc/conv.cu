@@ -347,6 +347,23 @@ __global__ void k_quant_i8(const float *__restrict__ src, int8_t *__restrict__ d
     }
 }
 
+// FMUL+FADD throughput probe (8 independent chains per thread).
+__global__ void k_peak_muladd(float *out, float a, float b, int iters) {
+    float acc[8], x[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        acc[i] = threadIdx.x * 0.001f + i;
+        x[i] = b + i;
+    }
+    for (int it = 0; it < iters; ++it)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[i] = __fadd_rn(x[i], __fmul_rn(a, acc[i]));
+    float s = 0.0f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s += acc[i];
+    if (s == 1.2345f) out[0] = s;
+}
+
 int grid_for(long long total, int threads = 256) {
     long long g = (total + threads - 1) / threads;
     return static_cast<int>(std::max<long long>(1, std::min<long long>(g, 148LL * 32)));
@@ -431,6 +448,34 @@ int usc_device_sm_count(int device) {
         return -1;
     }
     return v;
+}
+
+int usc_peak_fp32_muladd(int32_t device, double *tflops) {
+    int sms = usc_device_sm_count(device);
+    if (sms <= 0) return fail(USC_ERR_CUDA, "no CUDA device %d", device);
+    cudaSetDevice(device);
+    float *out = nullptr;
+    cudaEvent_t e0, e1;
+    if (cudaMalloc(&out, 4) != cudaSuccess) return cuda_check("peak malloc");
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    const int blocks = sms * 8, threads = 256, iters = 8192;
+    k_peak_muladd<<<blocks, threads>>>(out, 1.0001f, 0.5f, iters);
+    float best = 1e30f;
+    for (int r = 0; r < 5; ++r) {
+        cudaEventRecord(e0);
+        k_peak_muladd<<<blocks, threads>>>(out, 1.0001f, 0.5f, iters);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms;
+        cudaEventElapsedTime(&ms, e0, e1);
+        best = ms < best ? ms : best;
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(out);
+    *tflops = (double)blocks * threads * iters * 8 * 2 / (best * 1e-3) / 1e12;
+    return cuda_check("peak probe");
 }
 
 int usc_conv_forward(const usc_plan *pl, const void *blob, const void *x, void *y,

@@ -1,0 +1,80 @@
+"""Summarise ncu captures into profiles/: per-launch list (gpu__time_duration) and
+the --set full report of the dominant kernel (DRAM traffic, throughputs, stall mix).
+
+    python tools/ncu_summary.py launches gpurun_out/launches.csv profiles/r01_launches.md
+    python tools/ncu_summary.py full gpurun_out/prof.ncu-rep profiles/r01_top_kernel.md [plan.json]
+"""
+import collections
+import csv
+import io
+import json
+import os
+import subprocess
+import sys
+
+
+def launches(src, dst):
+    rows = list(csv.reader(open(src)))
+    hi = next(i for i, r in enumerate(rows) if r and r[0] == "ID")
+    h = rows[hi]
+    ix = {n: i for i, n in enumerate(h)}
+    per = collections.OrderedDict()
+    for r in rows[hi + 1:]:
+        if len(r) < len(h) or r[ix["Metric Name"]] != "gpu__time_duration.sum":
+            continue
+        name = r[ix["Kernel Name"]]
+        v = float(r[ix["Metric Value"]].replace(",", ""))
+        unit = r[ix["Metric Unit"]]
+        us = {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3}[unit] * v
+        per.setdefault(name, []).append(us)
+    total = sum(sum(v) for v in per.values())
+    out = ["| kernel | launches | total us | mean us | share |", "|---|---|---|---|---|"]
+    for k, v in sorted(per.items(), key=lambda kv: -sum(kv[1])):
+        out.append(f"| `{k[:90]}` | {len(v)} | {sum(v):.1f} | {sum(v)/len(v):.2f} | {sum(v)/total:.3f} |")
+    open(dst, "w").write("\n".join(out) + "\n")
+    print("\n".join(out[:12]))
+
+
+def full(rep, dst, plan_path=None):
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    r = list(csv.reader(io.StringIO(raw)))
+    h, units, vals = r[0], r[1], r[2]
+    d = dict(zip(h, vals))
+    u = dict(zip(h, units))
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1e-3, "us": 1.0, "ms": 1e3}
+
+    def f(name):
+        try:
+            return float(d[name].replace(",", "")) * scale.get(u.get(name, ""), 1.0)
+        except (KeyError, ValueError):
+            return None
+    dram = (f("dram__bytes_read.sum") or 0) + (f("dram__bytes_write.sum") or 0)
+    keys = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+            "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+            "l1tex__throughput.avg.pct_of_peak_sustained_active", "lts__throughput.avg.pct_of_peak_sustained_elapsed",
+            "smsp__inst_executed.sum", "sm__warps_active.avg.pct_of_peak_sustained_active",
+            "launch__registers_per_thread", "launch__grid_size", "launch__block_size",
+            "smsp__inst_executed_pipe_fma.sum", "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
+            "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum"]
+    stalls = {k.replace("smsp__pcsamp_warps_issue_stalled_", ""): f(k) for k in h
+              if k.startswith("smsp__pcsamp_warps_issue_stalled_") and not k.endswith("not_issued")}
+    tot = sum(v for v in stalls.values() if v) or 1
+    lines = [f"# ncu --set full: {d.get('Kernel Name', '?')}", "", "| metric | value |", "|---|---|"]
+    for k in keys:
+        lines.append(f"| {k} | {d.get(k, 'n/a')} {u.get(k, '')} |")
+    lines += ["", f"DRAM traffic per launch: {dram:.0f} bytes", "", "| stall reason | share |", "|---|---|"]
+    for k, v in sorted(stalls.items(), key=lambda kv: -(kv[1] or 0))[:10]:
+        lines.append(f"| {k} | {100 * (v or 0) / tot:.1f}% |")
+    open(dst, "w").write("\n".join(lines) + "\n")
+    if plan_path:
+        plan = json.load(open(plan_path))
+        json.dump({"plan": plan, "dram_bytes": dram, "source": os.path.basename(rep)},
+                  open(os.path.join(os.path.dirname(dst), "traffic.json"), "w"), indent=1)
+    print("\n".join(lines))
+
+
+if __name__ == "__main__":
+    if sys.argv[1] == "launches":
+        launches(sys.argv[2], sys.argv[3])
+    else:
+        full(sys.argv[2], sys.argv[3], sys.argv[4] if len(sys.argv) > 4 else None)
