@@ -203,3 +203,23 @@ def test_packer_dedupes_zero_entries():
                                    _lib.np_ptr(f.weights), f.n_nz, None, _lib.np_ptr(blob), blob.size,
                                    _lib.ref(n)))
     assert n.value == 1 + 1 + 9  # one deduped padding entry + the genuine entries
+
+
+def test_layer_bench_csv_and_backend_choice():
+    from paper_2112_15445_b200 import layer_bench as LB
+    ref_csv = ",".join(LB.CSV_HEADER[:19]) + "\n" + \
+        "a@90%/binary32,vgg16-512x14,512,512,3,3,14,14,1,1,1,1,8,90,binary32,2,1.5,1.5,1.0\n" + \
+        "b@90%/binary32,vgg16-512x14,512,512,3,3,14,14,1,1,1,1,8,90,binary32,2,1.0,2.0,2.0\n"
+    rows = LB.rows_from_csv(ref_csv)  # the reference's 19-column CSV reads back
+    cfg = LB.backend_config(rows)
+    assert cfg["a@90%/binary32"]["backend"] == "dense"  # exact tie -> dense (bench.py:221)
+    assert cfg["b@90%/binary32"]["backend"] == "sparse"
+    again = LB.rows_from_csv(LB.rows_to_csv(rows))
+    assert [r.sparse_ms for r in again] == [1.5, 1.0]
+    assert "| a@90%/binary32 |" in LB.rows_to_markdown(rows)
+    assert LB.spearman_rho([1, 2, 3, 4], [4, 3, 2, 1]) == -1.0
+    assert LB.spearman_rho([1, 1, 2], [1, 1, 2]) == pytest.approx(1.0)
+    with pytest.raises(ValueError):
+        LB.backend_config(rows, expected_layers=["missing"])
+    for name in LB.PRESETS:
+        LB.preset_geometry(name)
