@@ -83,6 +83,9 @@ typedef struct usc_exec_cfg {
     int32_t threads;          /* threads per CTA (128 or 256) */
     int32_t kernel;           /* 0 auto, 1 tiled (padded NCHW), 2 generic, 3 batch-interleaved */
     int32_t pixel_warps;      /* kernel 3: warps over output strips (rest split the channels) */
+    int32_t stages;           /* kernel 3: shared-memory ring depth (2..4) */
+    int32_t rows_per_thread;  /* kernel 3: output rows per thread (1 or 2); pixels = rows x pix_per_thread */
+    int32_t ent_reserve;      /* kernel 3: shared-memory bytes reserved per stage for CSR entries (0 auto) */
 } usc_exec_cfg;
 
 /* Resolved plan for one (geometry, batch, dtype, cfg): tile shape, packing
@@ -101,6 +104,8 @@ typedef struct usc_plan {
     int32_t WS, WC, DW;          /* BI kernel: warps over strips, warps over channels, channels/warp */
     int32_t SPRt, col_tiles, TWs;/* BI kernel: strips per tile row, column tiles, staged row width */
     int32_t ent_stage_bytes;     /* BI kernel: shared-memory reserve for one chunk's entries */
+    int32_t stages;              /* BI kernel: shared-memory ring depth */
+    int32_t PR, PC;              /* BI kernel: a thread's pixel block = PR rows x PC columns (P = PR*PC) */
     int32_t transposed;          /* 1D layer (W==1) run as its H/W transpose */
     int64_t smem_stage_bytes, smem_bytes;
     int64_t grid_x, grid_y;
@@ -117,6 +122,8 @@ typedef struct usc_epilogue {
     float scale;                 /* USC_I8: sigma_w * sigma_x (exact power of two) */
     int32_t out_padded;          /* 0: plain NCHW output; 1: padded layout `out` */
     usc_act_layout out;          /* used when out_padded */
+    int32_t pool;                /* 1: fused 2x2/2 max-pool after ReLU (nn.py:124-135); `out` is the
+                                  * pooled layout; needs a BI plan with PR == 2 and even PC */
 } usc_epilogue;
 
 /* ---- library ---------------------------------------------------------- */
@@ -159,6 +166,8 @@ int usc_csr_to_dense(const usc_geometry *g, const int64_t *row_ptr, const int64_
  * the device.  Zero-weight entries are deduplicated per (channel, offset):
  * for finite inputs they are no-ops, and one copy per distinct offset keeps the
  * reference's NaN propagation exact.
+ * host_blob == NULL is a dry run: *n_entries receives the largest (group, chunk)
+ * entry block in bytes (kernel 3 plans; pass it back as usc_exec_cfg.ent_reserve).
  * payload: USC_F32/USC_F16 -> the CSR theta (fp32, binary16 values for F16);
  *          USC_I8 -> int8 codes (one per CSR entry, theta = code*sigma_w);
  *          USC_CB4 -> uint8 centroid indices (one per CSR entry) + 16-entry

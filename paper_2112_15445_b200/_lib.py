@@ -42,7 +42,7 @@ class ActLayout(ctypes.Structure):
 class ExecCfg(ctypes.Structure):
     _fields_ = [(n, c_i32) for n in ("sub_batch", "worker_count", "pix_per_thread", "ch_per_cta",
                                      "samples_per_cta", "chunk_channels", "threads", "kernel",
-                                     "pixel_warps")]
+                                     "pixel_warps", "stages", "rows_per_thread", "ent_reserve")]
 
 
 class Plan(ctypes.Structure):
@@ -51,7 +51,7 @@ class Plan(ctypes.Structure):
                 ("CC", c_i32), ("threads", c_i32), ("TH", c_i32), ("HS", c_i32),
                 ("strips_per_row", c_i32), ("row_tiles", c_i32), ("sample_tiles", c_i32),
                 ("groups", c_i32), ("n_chunks", c_i32), ("WS", c_i32), ("WC", c_i32), ("DW", c_i32),
-                ("SPRt", c_i32), ("col_tiles", c_i32), ("TWs", c_i32), ("ent_stage_bytes", c_i32),
+                ("SPRt", c_i32), ("col_tiles", c_i32), ("TWs", c_i32), ("ent_stage_bytes", c_i32), ("stages", c_i32), ("PR", c_i32), ("PC", c_i32),
                 ("transposed", c_i32),
                 ("smem_stage_bytes", c_i64), ("smem_bytes", c_i64), ("grid_x", c_i64),
                 ("grid_y", c_i64)]
@@ -59,7 +59,7 @@ class Plan(ctypes.Structure):
     def describe(self) -> dict:
         return dict(kernel={1: "tiled", 2: "generic", 3: "bi32"}[self.kernel], P=self.P, DT=self.DT,
                     NS=self.NS, CC=self.CC, TH=self.TH, threads=self.threads, WS=self.WS,
-                    WC=self.WC, DW=self.DW,
+                    WC=self.WC, DW=self.DW, PR=self.PR, PC=self.PC, stages=self.stages,
                     grid=(self.grid_x, self.grid_y), smem_bytes=self.smem_bytes,
                     n_chunks=self.n_chunks, transposed=bool(self.transposed))
 
@@ -67,7 +67,7 @@ class Plan(ctypes.Structure):
 class Epilogue(ctypes.Structure):
     _fields_ = [("relu", c_i32), ("saturate", c_i32), ("cap", ctypes.c_float), ("saturate2", c_i32),
                 ("cap2", ctypes.c_float), ("scale", ctypes.c_float), ("out_padded", c_i32),
-                ("out", ActLayout)]
+                ("out", ActLayout), ("pool", c_i32)]
 
 
 class CsrCorruptionError(ValueError):

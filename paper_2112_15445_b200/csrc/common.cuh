@@ -70,7 +70,7 @@ __device__ __forceinline__ float round16f(float v) { return __half2float(sat_hal
 struct Epi {
     int relu, saturate, saturate2, out_padded;
     float cap, cap2, scale;
-    int oHp, oWs, oph, opw, oil;
+    int oHp, oWs, oph, opw, oil, pool;
     long long o_sample_stride;  // elements per sample (il 0) / 32-sample block (il 32)
 };
 

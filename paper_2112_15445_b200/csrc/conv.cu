@@ -420,6 +420,7 @@ Epi make_epi(const usc_epilogue *e) {
         return ep;
     }
     ep.relu = e->relu;
+    ep.pool = e->pool;
     ep.saturate = e->saturate;
     ep.saturate2 = e->saturate2;
     ep.cap = e->cap;
@@ -486,9 +487,15 @@ int usc_conv_forward(const usc_plan *pl, const void *blob, const void *x, void *
     Epi ep = make_epi(epi);
     if (ep.out_padded && pl->transposed)
         return fail(USC_ERR_UNSUPPORTED, "padded output of a transposed 1-D plan");
-    if (ep.out_padded && (epi->out.channels != g.out_channels || epi->out.height != pl->out_h ||
-                          epi->out.width != pl->out_w))
+    if (ep.out_padded && !epi->pool &&
+        (epi->out.channels != g.out_channels || epi->out.height != pl->out_h || epi->out.width != pl->out_w))
         return fail(USC_ERR_VALUE, "output layout does not match the plan");
+    if (epi && epi->pool) {
+        if (pl->kernel != 3 || pl->PR != 2 || pl->PC % 2 || pl->out_h % 2 || pl->out_w % 2)
+            return fail(USC_ERR_VALUE, "fused max-pool needs a BI plan with 2-row, even-width pixel blocks");
+        if (!ep.out_padded || epi->out.height != pl->out_h / 2 || epi->out.width != pl->out_w / 2)
+            return fail(USC_ERR_VALUE, "fused max-pool needs the pooled output layout");
+    }
     if (pl->kernel == 3) return usc::launch_bi(pl, blob, x, y, ep, st);
     if (ep.out_padded && ep.oil != 0)
         return fail(USC_ERR_UNSUPPORTED, "kernels 1/2 write interleave-0 layouts only");

@@ -224,6 +224,20 @@ static int pow2_floor(int v) {
     return p;
 }
 
+// The k_bi instances compiled into the library (conv_bi*.cu; keep in sync).
+static bool bi_instance(int PC, int PR, int DW, int NT, int SW) {
+    if (NT == 512 && PR == 2) {
+        if (SW != 1) return false;
+        if (PC == 1) return DW == 4 || DW == 8 || DW == 16;
+        if (PC == 2) return DW == 2 || DW == 4 || DW == 8 || DW == 16;
+        if (PC == 4) return DW == 4 || DW == 8;
+        return PC == 8 && DW == 4;
+    }
+    if (PR != 1) return false;
+    if (PC == 1 || PC == 2 || PC == 4) return DW == 4 || DW == 8 || DW == 16;
+    return PC == 8 && (DW == 4 || DW == 8);
+}
+
 int usc_plan_make(const usc_geometry *g0, int32_t n, int32_t dtype, const usc_exec_cfg *cfg,
                   usc_plan *pl) {
     int rc = usc_geometry_check(g0);
@@ -265,62 +279,84 @@ int usc_plan_make(const usc_geometry *g0, int32_t n, int32_t dtype, const usc_ex
         // (1 CTA/SM, long channel chunks), 4 warps over pixels x 4 over channels
         const int NT = (c.threads == 256) ? 256 : 512;
         const int NW = NT / 32;
-        int P = c.pix_per_thread ? c.pix_per_thread : 0;
-        if (!P) {
-            P = 1;
-            for (int q : {8, 4, 2}) if (Yw % q == 0) { P = q; break; }
+        // default pixel block: 2 rows x 4 (or 2) columns when the map allows (P = 8,
+        // the autotuner's usual pick on B200), else one row of 8/4/2/1
+        int PR = c.rows_per_thread ? c.rows_per_thread
+                                   : ((Yh % 2 == 0 && g.stride_w == 1 && NT == 512 && Yw % 2 == 0) ? 2 : 1);
+        int PC = c.pix_per_thread ? c.pix_per_thread : 0;
+        if (!PC) {
+            PC = 1;
+            for (int q : {8, 4, 2})
+                if (Yw % q == 0 && q * PR <= 8) {
+                    PC = q;
+                    break;
+                }
         }
-        if (P != 1 && P != 2 && P != 4 && P != 8)
+        if (PC != 1 && PC != 2 && PC != 4 && PC != 8)
             return fail(USC_ERR_VALUE, "BI pix_per_thread must be 1,2,4,8");
-        const int SPR = (Yw + P - 1) / P;
+        if (PR != 1 && PR != 2) return fail(USC_ERR_VALUE, "BI rows_per_thread must be 1 or 2");
+        if (PR > Yh) PR = 1;
+        const int P = PR * PC;
+        if (P > 16) return fail(USC_ERR_VALUE, "BI pixel block larger than 16");
+        const int SPR = (Yw + PC - 1) / PC;   // strips per strip-row
+        const int SR = (Yh + PR - 1) / PR;    // strip-rows
         int WSmax = c.pixel_warps ? std::min(c.pixel_warps, NW) : std::min(4, NW);
-        int WS, TH, SPRt;
-        if ((int64_t)Yh * SPR <= WSmax) {
-            WS = Yh * SPR;
-            TH = Yh;
+        int WS, TSR, SPRt;
+        if ((int64_t)SR * SPR <= WSmax) {
+            WS = SR * SPR;
+            TSR = SR;
             SPRt = SPR;
         } else if (SPR <= WSmax) {
-            TH = WSmax / SPR;
-            WS = TH * SPR;
+            TSR = WSmax / SPR;
+            WS = TSR * SPR;
             SPRt = SPR;
         } else {
-            TH = 1;
+            TSR = 1;
             SPRt = WSmax;
             WS = WSmax;
         }
+        const int TH = TSR * PR;  // output rows per tile
         int WC = NW / WS;
         if (WC < 1) WC = 1;
-        int DW = c.ch_per_cta ? std::max(1, c.ch_per_cta / WC) : (NT == 512 && WC <= 4 ? 8 : 4);
+        int DW = c.ch_per_cta ? std::max(1, c.ch_per_cta / WC) : (NT == 512 && WC <= 4 ? 8 : (WC >= 16 ? 2 : 4));
         if (DW > 16) DW = 16;
-        if (DW != 4 && DW != 8 && DW != 16) DW = DW < 4 ? 4 : (DW < 8 ? 8 : 16);
+        if (DW != 2 && DW != 4 && DW != 8 && DW != 16) DW = DW < 2 ? 2 : (DW < 4 ? 2 : (DW < 8 ? 4 : 8));
         const int acc_cap = NT == 512 ? 64 : 32;  // accumulators that fit the register cap
-        while (DW > 4 && DW * P > acc_cap) DW /= 2;
+        while (DW > 2 && DW * P > acc_cap) DW /= 2;
         if (DW * P > acc_cap) return fail(USC_ERR_VALUE, "BI tile needs too many accumulators");
+        if (!bi_instance(PC, PR, DW, NT, g.stride_w) && DW == 2) DW = 4;
+        if (!bi_instance(PC, PR, DW, NT, g.stride_w) || DW * P > acc_cap)
+            return fail(USC_ERR_VALUE, "no BI kernel instance for PC=%d PR=%d DW=%d threads=%d", PC, PR, DW, NT);
+        if (PR == 2 && (NT != 512 || g.stride_w != 1))
+            return fail(USC_ERR_VALUE, "BI rows_per_thread=2 needs 512 threads and stride_w 1");
         const int col_tiles = (SPR + SPRt - 1) / SPRt;
-        const bool full_rows = (col_tiles == 1 && SPR * P == Yw);
-        int TWs = full_rows ? pl->in.ws : (SPRt * P - 1) * g.stride_w + g.filter_w;
+        const bool full_rows = (col_tiles == 1 && SPR * PC == Yw);
+        int TWs = full_rows ? pl->in.ws : (SPRt * PC - 1) * g.stride_w + g.filter_w;
         const int HS = (TH - 1) * g.stride_h + g.filter_h;
         const int64_t per_ch = (int64_t)HS * TWs * 32 * eb;
         int CC = c.chunk_channels ? c.chunk_channels : 64;
         CC = std::min(CC, g.in_channels);
-        // 2 stages; 256 threads -> 4 CTAs per SM, 512 threads -> 1 CTA per SM
-        const int64_t budget = c.chunk_channels ? INT64_MAX : (NT == 512 ? 190 * 1024 : 52 * 1024);
+        // S-stage ring; 512 compute threads -> 1 CTA/SM (~200 KB), 256 -> 2 CTAs/SM
+        const int S = c.stages ? std::max(2, std::min(4, c.stages)) : 2;
+        const int64_t budget = (NT == 512 ? 200 * 1024 : 100 * 1024) - 256;
         // per-stage entry buffer: DT*CC*Kh*Kw entries of 8 bytes (+1 alignment pad) is the
         // exact worst case; reserve at most R bytes -- usc_pack rejects a filter whose
         // densest (group, chunk) block exceeds the reserve (the caller then re-plans
         // with fewer chunk channels)
-        const int64_t R = NT == 512 ? 24 * 1024 : 6 * 1024;
+        const int64_t R = c.ent_reserve ? c.ent_reserve : (NT == 512 ? 16 * 1024 : 8 * 1024);
         auto ent_bytes = [&](int cc) {
             const int64_t worst = ((int64_t)(WC * DW) * cc * g.filter_h * g.filter_w * 8 + 16 + 127) / 128 * 128;
-            return c.chunk_channels ? worst : std::min(worst, R);
+            return std::min(worst, (R + 127) / 128 * 128);
         };
-        while (CC > 1 && 2 * (CC * per_ch + ent_bytes(CC)) > budget) --CC;
+        while (CC > 1 && S * (CC * per_ch + ent_bytes(CC)) > budget) --CC;
         const int64_t stage = (CC * per_ch + 127) / 128 * 128;
         const int64_t ent_stage = ent_bytes(CC);
-        if (2 * (stage + ent_stage) + 128 > 220 * 1024)
+        if (S * (stage + ent_stage) + 128 > 224 * 1024)
             return fail(USC_ERR_VALUE, "BI tile does not fit shared memory");
         pl->kernel = 3;
         pl->P = P;
+        pl->PR = PR;
+        pl->PC = PC;
         pl->WS = WS;
         pl->WC = WC;
         pl->DW = DW;
@@ -340,8 +376,13 @@ int usc_plan_make(const usc_geometry *g0, int32_t n, int32_t dtype, const usc_ex
         pl->n_chunks = (g.in_channels + CC - 1) / CC;
         pl->smem_stage_bytes = stage;
         pl->ent_stage_bytes = static_cast<int32_t>(ent_stage);
-        pl->smem_bytes = 2 * (stage + ent_stage) + 128;
-        pl->grid_x = (int64_t)pl->groups * pl->sample_tiles * pl->row_tiles * pl->col_tiles;
+        pl->stages = S;
+        pl->smem_bytes = S * (stage + ent_stage) + 128;
+        // persistent grid: at most one wave of resident CTAs, each walks its tiles
+        const int64_t tiles = (int64_t)pl->groups * pl->sample_tiles * pl->row_tiles * pl->col_tiles;
+        int sms = usc_device_sm_count(0);
+        if (sms <= 0) sms = 148;
+        pl->grid_x = std::min<int64_t>(tiles, (int64_t)sms * (NT == 512 ? 1 : 2));
         pl->grid_y = 1;
         return USC_OK;
     }
@@ -444,6 +485,13 @@ int usc_pack(const usc_plan *pl, const int64_t *row_ptr, const int64_t *col, con
              int64_t n_nz, const float *table, void *blob, int64_t blob_bytes, int64_t *n_entries) {
     int64_t need;
     usc_pack_size(pl, n_nz, &need);
+    const bool dry = blob == nullptr;  // dry run: *n_entries <- largest (group, chunk) block in bytes
+    std::vector<char> scratch;
+    if (dry) {
+        scratch.resize(need);
+        blob = scratch.data();
+        blob_bytes = need;
+    }
     if (blob_bytes < need) return fail(USC_ERR_VALUE, "pack buffer too small");
     const usc_geometry &g = pl->g;
     const int D = g.out_channels, DT = pl->DT, G = pl->groups, NC = pl->n_chunks, CC = pl->CC;
@@ -546,6 +594,10 @@ int usc_pack(const usc_plan *pl, const int64_t *row_ptr, const int64_t *col, con
         int64_t worst = 0;
         for (int64_t b = 0; b < (int64_t)G * NC; ++b)
             worst = std::max<int64_t>(worst, ((int64_t)cpg[(b + 1) * DT] - cpg[b * DT]) * 8 + 16);
+        if (dry) {
+            *n_entries = worst;
+            return USC_OK;
+        }
         if (worst > pl->ent_stage_bytes)
             return fail(USC_ERR_VALUE, "entry block of %lld bytes exceeds the %d-byte stage reserve",
                         (long long)worst, pl->ent_stage_bytes);

@@ -44,6 +44,9 @@ class ExecConfig:
     kernel: int = 0
     threads: int = 0
     pixel_warps: int = 0
+    stages: int = 0
+    rows_per_thread: int = 0
+    ent_reserve: int = 0
 
     def __post_init__(self):
         if self.sub_batch < 1:
@@ -59,7 +62,7 @@ class ExecConfig:
     def to_c(self) -> _lib.ExecCfg:
         return _lib.ExecCfg(self.sub_batch, self.worker_count, self.pix_per_thread, self.ch_per_cta,
                             self.samples_per_cta, self.chunk_channels, self.threads, self.kernel,
-                            self.pixel_warps)
+                            self.pixel_warps, self.stages, self.rows_per_thread, self.ent_reserve)
 
 
 @dataclass(frozen=True)
@@ -97,23 +100,42 @@ def make_plan(geometry: ConvGeometry, n: int, dtype: int, config: ExecConfig | N
 
 def plan_for(filt: CsrFilter, n: int, dtype: int, config: ExecConfig | None, payload, table=None,
              device=None):
-    """make_plan + device_pack; when the filter's densest entry block overflows the
-    kernel-3 stage reserve, re-plan with fewer chunk channels (exact worst-case
-    reserve at the end)."""
+    """make_plan + device_pack.  For kernel-3 plans the shared-memory entry reserve is
+    sized from the filter itself (a dry-run pack measures its densest (group, chunk)
+    block), then the plan is remade with that reserve."""
     config = config or ExecConfig()
     plan = make_plan(filt.geometry, n, dtype, config)
-    while True:
-        try:
-            blob, n_ent = device_pack(filt, plan, payload, table, device)
-            return plan, blob
-        except ValueError as exc:
-            if plan.kernel != 3 or "stage reserve" not in str(exc):
-                raise
-            cc = plan.CC // 2 if plan.CC > 1 else 1
-            fields = {f: getattr(config, f) for f in config.__dataclass_fields__}
-            fields["chunk_channels"] = cc
-            config = ExecConfig(**fields)
-            plan = make_plan(filt.geometry, n, dtype, config)
+    if plan.kernel == 3 and not config.ent_reserve:
+        fields = {f: getattr(config, f) for f in config.__dataclass_fields__}
+        best = None
+        reserve = plan.ent_stage_bytes
+        for _ in range(4):  # reserve <- densest block; more room for input channels
+            need = _max_block(filt, plan, payload, table)
+            if need <= plan.ent_stage_bytes:
+                best = plan
+                if plan.ent_stage_bytes - need < 1024:
+                    break
+            reserve = max(need, 256)
+            fields["ent_reserve"] = int(reserve)
+            plan = make_plan(filt.geometry, n, dtype, ExecConfig(**fields))
+        if best is None or (_max_block(filt, plan, payload, table) <= plan.ent_stage_bytes
+                            and plan.CC >= best.CC):
+            best = plan if _max_block(filt, plan, payload, table) <= plan.ent_stage_bytes else best
+        if best is None:
+            raise ValueError("no shared-memory entry reserve fits this filter")
+        plan = best
+    blob, _ = device_pack(filt, plan, payload, table, device)
+    return plan, blob
+
+
+def _max_block(filt, plan, payload, table=None) -> int:
+    worst = ctypes.c_int64(0)
+    tbl = None if table is None else np.ascontiguousarray(table, np.float32)
+    _lib.check(_lib.lib().usc_pack(_lib.ref(plan), _lib.np_ptr(filt.row_ptr), _lib.np_ptr(filt.col_offsets),
+                                   _lib.np_ptr(np.ascontiguousarray(payload)), filt.n_nz,
+                                   None if tbl is None else _lib.np_ptr(tbl), None, 0,
+                                   _lib.ref(worst)), "pack")
+    return int(worst.value)
 
 
 def _pack_key(plan: _lib.Plan, device) -> tuple:
@@ -275,14 +297,21 @@ def tile_candidates(geometry: ConvGeometry, n: int, sb_values, precision=Precisi
     if kernels is None:
         kernels = (3, 1) if precision is PrecisionMode.BINARY32 else (1,)
     if 3 in kernels and precision is PrecisionMode.BINARY32:
-        for p in (1, 2, 4, 8):
-            if p > max(1, yw):
+        yh = geometry.out_h if geometry.input_w != 1 else 1
+        for pr in (1, 2):
+            if pr > yh:
                 continue
-            for nt, dts in ((256, (8, 16, 32)), (512, (16, 32, 64))):
-                for dt in dts:
-                    for pw in (0, 4):
-                        out.append(ExecConfig(sub_batch=min(sb_values), pix_per_thread=p,
-                                              ch_per_cta=dt, kernel=3, threads=nt, pixel_warps=pw))
+            for p in (1, 2, 4, 8):
+                if p > max(1, yw) or pr * p > 16:
+                    continue
+                for nt, dts in ((256, (8, 16, 32)), (512, (16, 32, 64))):
+                    if pr == 2 and nt == 256:
+                        continue
+                    for dt in dts:
+                        for pw in (0, 4, 8):
+                            out.append(ExecConfig(sub_batch=min(sb_values), pix_per_thread=p,
+                                                  ch_per_cta=dt, kernel=3, threads=nt, pixel_warps=pw,
+                                                  stages=2, rows_per_thread=pr))
     if 1 in kernels:
         ps = [p for p in (2, 4, 8) if p <= max(2, yw)]
         for sb in sb_values:
@@ -296,7 +325,8 @@ def tile_candidates(geometry: ConvGeometry, n: int, sb_values, precision=Precisi
             plan = make_plan(geometry, n, dtype_of(precision), cfg)
         except ValueError:
             continue
-        key = (plan.kernel, plan.P, plan.DT, plan.DW, plan.WS, plan.NS, plan.CC, plan.threads)
+        key = (plan.kernel, plan.P, plan.PR, plan.DT, plan.DW, plan.WS, plan.NS, plan.CC, plan.threads,
+               plan.stages)
         if key not in seen:
             seen.add(key)
             feasible.append(cfg)
@@ -336,5 +366,5 @@ def autotune_sb(input: DenseTensor4, filt: CsrFilter, candidates=SB_CANDIDATES, 
             if cfg.sub_batch == sb and ms <= best * (1.0 + noise_floor):
                 return ExecConfig(cfg.sub_batch, worker_count, cfg.pix_per_thread, cfg.ch_per_cta,
                                   cfg.samples_per_cta, cfg.chunk_channels, cfg.kernel, cfg.threads,
-                                  cfg.pixel_warps)
+                                  cfg.pixel_warps, cfg.stages, cfg.rows_per_thread, cfg.ent_reserve)
     return ExecConfig(usable[0], worker_count)

@@ -74,9 +74,26 @@ class SparseVGG16:
         self.device = torch.device(device or "cuda")
         self.geoms = vgg16_geometries()
         self.filters = [build_csr(w, g) for w, g in zip(weights, self.geoms)]
-        self.configs = list(configs) if configs else [ExecConfig() for _ in self.geoms]
+        self.pre_pool = self._pre_pool_layers()
+        if configs:
+            self.configs = list(configs)
+        else:  # convs feeding a max-pool get 2-row pixel blocks so the pool fuses
+            self.configs = [ExecConfig(rows_per_thread=2, pix_per_thread=min(4, g.out_w))
+                            if li in self.pre_pool and self.dtype == _lib.USC_F32 else ExecConfig()
+                            for li, g in enumerate(self.geoms)]
         self.graph = None
         self._build()
+
+    @staticmethod
+    def _pre_pool_layers():
+        out, li = set(), 0
+        for i, v in enumerate(VGG16_CIFAR):
+            if v == "M":
+                continue
+            if i + 1 < len(VGG16_CIFAR) and VGG16_CIFAR[i + 1] == "M":
+                out.add(li)
+            li += 1
+        return out
 
     # -- buffers and plans ---------------------------------------------------
     def _buf(self, lay):
@@ -114,7 +131,13 @@ class SparseVGG16:
             epi = _lib.Epilogue()
             epi.relu = 1
             epi.scale = 1.0
-            if nxt == "M":
+            fuse = nxt == "M" and plan.kernel == 3 and plan.PR == 2 and plan.PC % 2 == 0
+            last = i + 2 >= len(VGG16_CIFAR)
+            if fuse:  # conv + ReLU + 2x2 max-pool in one kernel, pooled output padded for the next conv
+                ph = 0 if last else 1
+                out_lay = _lib.act_layout(g.out_channels, g.out_h // 2, g.out_w // 2, ph, ph, self.eb, il)
+                epi.pool = 1
+            elif nxt == "M":
                 out_lay = _lib.act_layout(g.out_channels, g.out_h, g.out_w, 0, 0, self.eb, il)
             else:
                 out_lay = _lib.act_layout(g.out_channels, g.out_h, g.out_w, 1, 1, self.eb, il)
@@ -124,7 +147,7 @@ class SparseVGG16:
             self.steps.append(("conv", li, plan, blob, cur_buf, out_buf, epi))
             self.nonzero_macs += int(np.count_nonzero(self.filters[li].weights)) * g.out_h * g.out_w * n
             cur_buf, cur_lay = out_buf, out_lay
-            if nxt == "M":
+            if nxt == "M" and not fuse:
                 last = i + 2 >= len(VGG16_CIFAR)
                 ph = 0 if last else 1
                 pool_lay = _lib.act_layout(g.out_channels, g.out_h // 2, g.out_w // 2, ph, ph, self.eb, il)
@@ -209,7 +232,10 @@ class SparseVGG16:
             usable = [sb for sb in (1, 2, 4, 8, 16, 32) if self.batch % sb == 0]
             results = []
             kern = (3,) if self.interleave == 32 else (1,)
-            for cfg in [self.configs[li]] + tile_candidates(g, self.batch, usable, self.precision, kern):
+            cands = [self.configs[li]] + tile_candidates(g, self.batch, usable, self.precision, kern)
+            if epi.pool:  # keep the pool fused: 2-row, even-width pixel blocks only
+                cands = [c for c in cands if c.rows_per_thread == 2 and c.pix_per_thread % 2 == 0]
+            for cfg in cands:
                 try:
                     plan, blob = plan_for(self.filters[li], self.batch, self.dtype, cfg,
                                           self.filters[li].weights, device=self.device)

@@ -182,7 +182,9 @@ def test_planner_tiles():
                   U.ExecConfig(kernel=1))
     assert p.kernel == 1 and p.NS == 1 and p.row_tiles * p.TH >= 32
     p = make_plan(U.ConvGeometry(64, 64, 3, 3, 32, 32, padding=(1, 1)), 256, _lib.USC_F32, None)
-    assert p.kernel == 3 and p.row_tiles * p.TH >= 32 and p.grid_x == p.groups * 8 * p.row_tiles
+    tiles = p.groups * 8 * p.row_tiles * p.col_tiles
+    assert p.kernel == 3 and p.row_tiles * p.TH >= 32 and p.grid_x == min(tiles, 148)
+    assert p.stages >= 2 and p.smem_bytes <= 224 * 1024
     with pytest.raises(ValueError):
         make_plan(U.ConvGeometry(4, 4, 3, 3, 8, 8, padding=(1, 1)), 6, _lib.USC_F32, U.ExecConfig(4))
 
