@@ -80,9 +80,11 @@ typedef struct usc_exec_cfg {
     int32_t ch_per_cta;       /* DT: output channels per CTA (4,8,16,32) */
     int32_t samples_per_cta;  /* NS: samples per CTA (full-map tiles) */
     int32_t chunk_channels;   /* CC: input channels per shared-memory stage */
-    int32_t threads;          /* threads per CTA (128 or 256) */
+    int32_t threads;          /* kernel 1: threads per CTA (128/256); kernel 3: compute threads
+                               * (256/384/512 = 8/12/16 compute warps, + 1 producer warp) */
     int32_t kernel;           /* 0 auto, 1 tiled (padded NCHW), 2 generic, 3 batch-interleaved */
-    int32_t pixel_warps;      /* kernel 3: warps over output strips (rest split the channels) */
+    int32_t pixel_warps;      /* kernel 3: warps over output strips (must divide the warps; the
+                               * rest split the CTA's ch_per_cta output channels) */
     int32_t stages;           /* kernel 3: shared-memory ring depth (2..4) */
     int32_t rows_per_thread;  /* kernel 3: output rows per thread (1 or 2); pixels = rows x pix_per_thread */
     int32_t ent_reserve;      /* kernel 3: shared-memory bytes reserved per stage for CSR entries (0 auto) */
@@ -174,6 +176,10 @@ int usc_csr_to_dense(const usc_geometry *g, const int64_t *row_ptr, const int64_
  *                     fp32 centroid table `table`. */
 int usc_plan_make(const usc_geometry *g, int32_t n, int32_t dtype, const usc_exec_cfg *cfg,
                   usc_plan *out);
+/* The batch-interleaved kernel's compiled tile instances: writes up to max_count
+ * records of 5 int32 (compute warps, PC, PR, DW, stride_w) and returns the total
+ * count.  The autotuner's kernel-3 search space (threads = warps*32). */
+int usc_bi_instances(int32_t *out, int32_t max_count);
 int usc_pack_size(const usc_plan *plan, int64_t n_nz, int64_t *bytes);
 int usc_pack(const usc_plan *plan, const int64_t *row_ptr, const int64_t *col_offsets,
              const void *payload, int64_t n_nz, const float *table, void *host_blob,

@@ -89,6 +89,7 @@ _SIGS = {
     "usc_csr_validate": (c_i32, [c_ptr, c_ptr, c_i64, c_ptr, c_i64, c_i64, c_i64, c_ptr]),
     "usc_csr_to_dense": (c_i32, [c_ptr, c_ptr, c_ptr, c_ptr, c_i64, c_ptr]),
     "usc_plan_make": (c_i32, [c_ptr, c_i32, c_i32, c_ptr, c_ptr]),
+    "usc_bi_instances": (c_i32, [c_ptr, c_i32]),
     "usc_pack_size": (c_i32, [c_ptr, c_i64, c_ptr]),
     "usc_pack": (c_i32, [c_ptr, c_ptr, c_ptr, c_ptr, c_i64, c_ptr, c_ptr, c_i64, c_ptr]),
     "usc_pad_input": (c_i32, [c_ptr, c_i32, c_i32, c_ptr, c_ptr, c_ptr]),
@@ -126,6 +127,15 @@ def lib():
             raise ImportError("libunsparse_b200.so ABI version mismatch")
         _lib = L
     return _lib
+
+
+def bi_instances() -> list[tuple[int, int, int, int, int]]:
+    """The batch-interleaved kernel's compiled tiles: (compute warps, PC, PR, DW, stride_w)."""
+    L = lib()
+    n = L.usc_bi_instances(None, 0)
+    buf = (c_i32 * (5 * n))()
+    L.usc_bi_instances(buf, n)
+    return [tuple(buf[5 * i:5 * i + 5]) for i in range(n)]
 
 
 def check(rc: int, what: str = ""):

@@ -5,13 +5,15 @@ namespace usc {
 
 int launch_bi(const usc_plan *pl, const void *blob, const void *x, void *y, const usc_dev::Epi &ep,
               cudaStream_t st) {
+    // blob = [64 B][int32 blk[G*n_chunks + 1], 16-B aligned][blocks] (usc_pack, kernel 3)
     const char *cb = static_cast<const char *>(blob);
-    const long long cp_bytes = ((4LL * ((long long)pl->groups * pl->n_chunks * pl->DT + 1)) + 15) / 16 * 16;
+    const long long nb = (long long)pl->groups * pl->n_chunks;
+    const long long cp_bytes = (4 * (nb + 1) + 15) / 16 * 16;
     usc_bi::BiArgs a{};
     a.x = static_cast<const float *>(x);
     a.y = static_cast<float *>(y);
-    a.cpg = reinterpret_cast<const int *>(cb + 64);
-    a.ents = reinterpret_cast<const int2 *>(cb + 64 + cp_bytes);
+    a.blk = reinterpret_cast<const int *>(cb + 64);
+    a.blocks = cb + 64 + cp_bytes;
     a.N = pl->n;
     a.C = pl->g.in_channels;
     a.D = pl->g.out_channels;
@@ -39,7 +41,11 @@ int launch_bi(const usc_plan *pl, const void *blob, const void *x, void *y, cons
     a.x_stage_bytes = static_cast<int>(pl->smem_stage_bytes);
     a.stage_bytes = static_cast<int>(pl->smem_stage_bytes + pl->ent_stage_bytes);
     a.ep = ep;
-    return pl->threads == 512 ? usc_bi::launch_16(pl, a, st) : usc_bi::launch_8(pl, a, st);
+    switch (pl->threads) {
+        case 256: return usc_bi::launch_w8(pl, a, st);
+        case 384: return usc_bi::launch_w12(pl, a, st);
+        default: return usc_bi::launch_w16(pl, a, st);
+    }
 }
 
 }  // namespace usc

@@ -8,24 +8,30 @@
 // is one conflict-free 128-byte wavefront and every output store is one
 // coalesced 128-byte line.
 //
-// Persistent, warp-specialised CTA:
-//   * warp NWC (the last) is the producer: one elected lane streams, for every
-//     tile this CTA owns and every chunk of CC input channels, the input tile
-//     ([CC][HS][TWs][32] floats) plus that (group, chunk)'s CSR entry block into
-//     an S-stage shared-memory ring with cp.async.bulk (UBLKCP, the TMA engine),
-//     completing on full[s] and waiting on empty[s] before reuse;
-//   * warps 0..NWC-1 compute: warp w owns strip w % WS (P consecutive output
-//     pixels of a row) for the DW output channels of subgroup w / WS, lane =
-//     sample, DW*P fp32 accumulators for the whole input-channel loop; after a
-//     stage each warp arrives on empty[s] -- no CTA-wide barrier in the loop.
-//   * tiles = (channel group fastest, column tile, row tile, 32-sample block); a
-//     CTA takes tiles blockIdx.x, +gridDim.x, ... so the producer runs ahead into
-//     the next tile while the compute warps store the previous one.
+// Persistent, warp-specialised CTA of NWC compute warps + 1 producer warp:
+//   * the producer's elected lane streams, for every tile this CTA owns and
+//     every chunk of CC input channels, the input tile ([CC][HS][TWs][32]
+//     floats) plus that (group, chunk)'s entry block into an S-stage shared
+//     memory ring with cp.async.bulk (UBLKCP, the TMA engine), completing on
+//     full[s] and waiting on empty[s] before reuse;
+//   * compute warp w owns strip w % WS (a PR x PC output-pixel block) for the DW
+//     output channels of subgroup w / WS; lane = sample; DW*P fp32 accumulators
+//     live for the whole input-channel loop; after a stage each warp arrives on
+//     empty[s] -- no CTA-wide barrier inside the loop.
+//   * entry block of one (group, chunk): int2 hdr[DT] = {first, end} entry index
+//     of every output channel's run, then the runs, each starting 16-byte aligned
+//     so two entries are one LDS.128 broadcast.  Everything the compute warps
+//     read in the loop is in shared memory.
+//   * the register budget is what sets NWC: warps are spread over 4 SM
+//     sub-partitions, so (NWC+1) warps leave 65536 / (4 * ceil((NWC+1)/4) * 32)
+//     registers per thread: 168 for NWC = 8, 128 for NWC = 12, 96 for NWC = 16.
 //
 // Per output element the arithmetic is the reference's: stored-order entries
 // (ascending (c, kh, kw)), IEEE fp32 multiply then add (__fmul_rn/__fadd_rn),
 // so results are bit-identical to the reference for every tile configuration.
 #pragma once
+#include <utility>
+
 #include "common.cuh"
 
 namespace usc_bi {
@@ -34,8 +40,8 @@ using namespace usc_dev;
 struct BiArgs {
     const float *x;
     float *y;
-    const int *cpg;
-    const int2 *ents;
+    const int *blk;          // byte offset of every (group, chunk) block, G*n_chunks+1
+    const char *blocks;      // block base (16-byte aligned)
     int N, C, D, n_chunks, CC, DT;
     int HS, TWs, Hp, Wp, Yh, Yw, s_h;
     int WS, WC, SPRt, TH, row_tiles, col_tiles, G, tiles, S;
@@ -49,10 +55,127 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
-template <int PC, int PR, int DW, int SW, int NWC, int MINB>
-__global__ void __launch_bounds__((NWC + 1) * 32, MINB) k_bi(const BiArgs a) {
-    constexpr int P = PC * PR;                          // a thread's pixel block: PR rows x PC cols
-    constexpr int U = P >= 8 ? 2 : (P >= 4 ? 4 : 8);  // U*P = 16-32 loads in flight
+// shared-memory loads on 32-bit addresses with immediate offsets (LDS [R+imm]);
+// not volatile: the address depends on an entry read after the stage's mbarrier
+// wait, which keeps them behind it
+template <int OFF>
+__device__ __forceinline__ float lds_f32(uint32_t a) {
+    float v;
+    asm("ld.shared.f32 %0, [%1+%2];" : "=f"(v) : "r"(a), "n"(OFF));
+    return v;
+}
+__device__ __forceinline__ int4 lds_v4(uint32_t a) {
+    int4 v;
+    asm("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ int2 lds_v2(uint32_t a) {
+    int2 v;
+    asm("ld.shared.v2.b32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
+    return v;
+}
+
+// the P pixels of a thread for one tap: row 0 at a0, row 1 at a1 (bytes), columns
+// SW*128 bytes apart
+template <int PC, int PR, int SW, int... I>
+__device__ __forceinline__ void load_px_(float *v, uint32_t a0, uint32_t a1, std::integer_sequence<int, I...>) {
+    ((v[I] = (I / PC == 0) ? lds_f32<(I % PC) * SW * 128>(a0) : lds_f32<(I % PC) * SW * 128>(a1)), ...);
+}
+template <int PC, int PR, int SW>
+__device__ __forceinline__ void load_px(float (&v)[PC * PR], uint32_t a0, uint32_t a1) {
+    load_px_<PC, PR, SW>(v, a0, a1, std::make_integer_sequence<int, PC * PR>{});
+}
+
+// acc[p] += t0*v0[p], then += t1*v1[p]: IEEE multiply then add, stored order
+template <int P>
+__device__ __forceinline__ void mac_pair(float (&acc)[P], float (&v0)[P], float (&v1)[P], const int4 &n) {
+    const float t0 = __int_as_float(n.y), t1 = __int_as_float(n.w);
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+        v0[p] = __fmul_rn(t0, v0[p]);
+        v1[p] = __fmul_rn(t1, v1[p]);
+    }
+#pragma unroll
+    for (int p = 0; p < P; ++p) acc[p] = __fadd_rn(acc[p], v0[p]);
+#pragma unroll
+    for (int p = 0; p < P; ++p) acc[p] = __fadd_rn(acc[p], v1[p]);
+}
+
+template <int PC, int PR, int SW>
+__device__ __forceinline__ void load_pair(float (&v0)[PC * PR], float (&v1)[PC * PR], uint32_t xs, uint32_t rs,
+                                          const int4 &n) {
+    const uint32_t p0 = xs + n.x, p1 = xs + n.z;
+    load_px<PC, PR, SW>(v0, p0, p0 + rs);
+    load_px<PC, PR, SW>(v1, p1, p1 + rs);
+}
+
+// One output channel's run of entries [ep, ee) (byte addresses, ep 16-B aligned),
+// two entries (one LDS.128) per step.  PIPE: software pipelined -- the next pair's
+// 2P pixel loads are issued before this pair's math (ping-pong registers), so the
+// shared-memory latency hides inside one warp.  Reads of the entry after a run stay
+// inside the stage's 16-byte slack.
+template <int PC, int PR, int SW, bool PIPE>
+__device__ __forceinline__ void run_pairs(float (&acc)[PC * PR], uint32_t xs, uint32_t rs, uint32_t ep,
+                                          uint32_t ee) {
+    constexpr int P = PC * PR;
+    int4 nn = lds_v4(ep);
+    if constexpr (PIPE) {
+        if (ep + 16 <= ee) {
+            float a0[P], a1[P], b0[P], b1[P];
+            int4 n = nn;
+            load_pair<PC, PR, SW>(a0, a1, xs, rs, n);
+            ep += 16;
+            nn = lds_v4(ep);
+#pragma unroll 1
+            while (true) {  // a* hold pair n; nn is the pair at ep
+                if (ep + 16 > ee) {
+                    mac_pair<P>(acc, a0, a1, n);
+                    break;
+                }
+                load_pair<PC, PR, SW>(b0, b1, xs, rs, nn);
+                int4 m = nn;
+                ep += 16;
+                nn = lds_v4(ep);
+                mac_pair<P>(acc, a0, a1, n);
+                n = m;
+                if (ep + 16 > ee) {
+                    mac_pair<P>(acc, b0, b1, n);
+                    break;
+                }
+                load_pair<PC, PR, SW>(a0, a1, xs, rs, nn);
+                m = nn;
+                ep += 16;
+                nn = lds_v4(ep);
+                mac_pair<P>(acc, b0, b1, n);
+                n = m;
+            }
+        }
+    } else {
+#pragma unroll 1
+        for (; ep + 16 <= ee; ep += 16) {
+            float v0[P], v1[P];
+            load_pair<PC, PR, SW>(v0, v1, xs, rs, nn);
+            const int4 n = nn;
+            nn = lds_v4(ep + 16);
+            mac_pair<P>(acc, v0, v1, n);
+        }
+    }
+    if (ep < ee) {  // odd run: the last entry is nn.x, nn.y
+        float v0[P];
+        const uint32_t p0 = xs + nn.x;
+        load_px<PC, PR, SW>(v0, p0, p0 + rs);
+        const float t0 = __int_as_float(nn.y);
+#pragma unroll
+        for (int p = 0; p < P; ++p) acc[p] = __fadd_rn(acc[p], __fmul_rn(t0, v0[p]));
+    }
+}
+
+template <int PC, int PR, int DW, int SW, int NWC>
+__global__ void __launch_bounds__((NWC + 1) * 32, 1) k_bi(const BiArgs a) {
+    constexpr int P = PC * PR;  // a thread's pixel block: PR rows x PC cols
+    // software-pipeline the pair loop when the second value set fits the register cap
+    constexpr int REGCAP = NWC <= 8 ? 168 : (NWC <= 12 ? 128 : 96);
+    constexpr bool PIPE = DW * P + 4 * P + 40 <= REGCAP;
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t *full = reinterpret_cast<uint64_t *>(smem);
     uint64_t *empty = full + 8;
@@ -71,7 +194,8 @@ __global__ void __launch_bounds__((NWC + 1) * 32, MINB) k_bi(const BiArgs a) {
     if (warp == NWC) {
         // ---------------- producer warp ----------------
         if (lane == 0) {
-            int it = 0;
+            int s = 0;
+            uint32_t ph = 1;
             for (int t = blockIdx.x; t < a.tiles; t += gridDim.x) {
                 int q = t;
                 const int g = q % a.G;
@@ -84,19 +208,16 @@ __global__ void __launch_bounds__((NWC + 1) * 32, MINB) k_bi(const BiArgs a) {
                 const int x0 = ct * a.SPRt * PC * SW;
                 const int rows = min(a.HS, a.Hp - y0);
                 const float *xblk = a.x + (long long)sb * a.x_blk_stride;
-                const int *cpg_g = a.cpg + (long long)g * a.n_chunks * a.DT;
+                const int *blk_g = a.blk + g * a.n_chunks;
                 const int plane_words = a.HS * a.TWs * 32;
-                for (int k = 0; k < a.n_chunks; ++k, ++it) {
-                    const int s = it % a.S;
-                    mbar_wait(&empty[s], ((it / a.S) & 1) ^ 1);
-                    float *dst = reinterpret_cast<float *>(ring + (long long)s * a.stage_bytes);
-                    char *edst = reinterpret_cast<char *>(ring + (long long)s * a.stage_bytes + a.x_stage_bytes);
+                for (int k = 0; k < a.n_chunks; ++k) {
+                    mbar_wait(&empty[s], ph);
+                    unsigned char *st = ring + s * a.stage_bytes;
+                    float *dst = reinterpret_cast<float *>(st);
                     const int c0 = k * a.CC;
                     const int cc = min(a.CC, a.C - c0);
-                    // the (group, chunk) entry block: 16-byte aligned start (packer),
-                    // 16-byte rounded size (the pack has tail slack)
-                    const int blk_lo = __ldg(cpg_g + k * a.DT), blk_hi = __ldg(cpg_g + k * a.DT + a.DT);
-                    const uint32_t eb = static_cast<uint32_t>((blk_hi - blk_lo) * 8 + 15) & ~15u;
+                    const int lo = __ldg(blk_g + k), hi = __ldg(blk_g + k + 1);
+                    const uint32_t eb = static_cast<uint32_t>(hi - lo);
                     fence_proxy_async();
                     if (a.full_rows) {
                         if (y0 == 0 && rows == a.Hp && a.HS == a.Hp) {
@@ -124,7 +245,11 @@ __global__ void __launch_bounds__((NWC + 1) * 32, MINB) k_bi(const BiArgs a) {
                                          xblk + ((((long long)(c0 + c) * a.Hp + y0 + rr) * a.Wp) + x0) * 32,
                                          bytes, &full[s]);
                     }
-                    if (eb) bulk_g2s(edst, a.ents + blk_lo, eb, &full[s]);
+                    bulk_g2s(st + a.x_stage_bytes, a.blocks + lo, eb, &full[s]);
+                    if (++s == a.S) {
+                        s = 0;
+                        ph ^= 1;
+                    }
                 }
             }
         }
@@ -136,9 +261,10 @@ __global__ void __launch_bounds__((NWC + 1) * 32, MINB) k_bi(const BiArgs a) {
     const bool active = wc < a.WC;
     const int tr = wsi / a.SPRt, tcs = wsi - tr * a.SPRt;  // strip-row, strip within the tile
     const int base = ((tr * PR * a.s_h) * a.TWs + tcs * PC * SW) * 32 + lane;
-    const int rstep = a.s_h * a.TWs * 32;  // floats between a thread's two pixel rows
-    const int bl = lane <= DW ? lane : -wc * DW;  // lane DW+1 reads the block start
-    int it = 0;
+    const uint32_t rs = a.s_h * a.TWs * 128;  // bytes between a thread's two pixel rows
+    const int hdr_bytes = a.DT * 8;
+    int s = 0;
+    uint32_t ph = 0;
     for (int t = blockIdx.x; t < a.tiles; t += gridDim.x) {
         int q = t;
         const int g = q % a.G;
@@ -156,64 +282,27 @@ __global__ void __launch_bounds__((NWC + 1) * 32, MINB) k_bi(const BiArgs a) {
 #pragma unroll
             for (int p = 0; p < P; ++p) acc[i][p] = 0.0f;
 
-        // chunk boundaries of this warp's DW channels (lanes 0..DW) and the block
-        // start (lane DW+1), one chunk ahead
-        const int *cp = a.cpg + (long long)g * a.n_chunks * a.DT + wc * DW;
-        int bnd = (active && lane <= DW + 1) ? __ldg(cp + bl) : 0;
-        for (int k = 0; k < a.n_chunks; ++k, ++it) {
-            const int s = it % a.S;
-            const int bnd_cur = bnd;
-            if (active && lane <= DW + 1 && k + 1 < a.n_chunks) bnd = __ldg(cp + (k + 1) * a.DT + bl);
-            mbar_wait(&full[s], (it / a.S) & 1);
+        for (int k = 0; k < a.n_chunks; ++k) {
+            const unsigned char *st = ring + s * a.stage_bytes;
+            mbar_wait(&full[s], ph);
             if (active) {
-                const unsigned char *st = ring + (long long)s * a.stage_bytes;
-                const char *xs = reinterpret_cast<const char *>(reinterpret_cast<const float *>(st) + base);
-                const int blk0 = __shfl_sync(0xffffffffu, bnd_cur, DW + 1);
-                const int2 *eb = reinterpret_cast<const int2 *>(st + a.x_stage_bytes) - blk0;
+                const uint32_t xs = smem_u32(st) + base * 4;  // this thread's first pixel, tap (0,0,0)
+                const uint32_t bp = smem_u32(st) + a.x_stage_bytes;
+                const uint32_t hdr = bp + wc * DW * 8, E = bp + hdr_bytes;
 #pragma unroll
                 for (int dw = 0; dw < DW; ++dw) {
-                    const int e0 = __shfl_sync(0xffffffffu, bnd_cur, dw);
-                    const int e1 = __shfl_sync(0xffffffffu, bnd_cur, dw + 1);
-                    int e = e0;
-                    // U entries per step: all U*P loads are in flight before the math;
-                    // products first, then the adds in stored order (no FMUL->FADD stall)
-#pragma unroll 1
-                    for (; e + U <= e1; e += U) {
-                        int2 n[U];
-#pragma unroll
-                        for (int u = 0; u < U; ++u) n[u] = eb[e + u];
-                        float v[U][P];
-#pragma unroll
-                        for (int u = 0; u < U; ++u) {
-                            const float *xp = reinterpret_cast<const float *>(xs + n[u].x);
-#pragma unroll
-                            for (int p = 0; p < P; ++p) v[u][p] = xp[(p / PC) * rstep + (p % PC) * SW * 32];
-                        }
-#pragma unroll
-                        for (int u = 0; u < U; ++u) {
-                            const float th = __int_as_float(n[u].y);
-#pragma unroll
-                            for (int p = 0; p < P; ++p) v[u][p] = __fmul_rn(th, v[u][p]);
-                        }
-#pragma unroll
-                        for (int u = 0; u < U; ++u)
-#pragma unroll
-                            for (int p = 0; p < P; ++p) acc[dw][p] = __fadd_rn(acc[dw][p], v[u][p]);
-                    }
-#pragma unroll 1
-                    for (; e < e1; ++e) {
-                        const int2 n0 = eb[e];
-                        const float *x0p = reinterpret_cast<const float *>(xs + n0.x);
-                        const float t0 = __int_as_float(n0.y);
-#pragma unroll
-                        for (int p = 0; p < P; ++p)
-                            acc[dw][p] = __fadd_rn(acc[dw][p],
-                                                   __fmul_rn(t0, x0p[(p / PC) * rstep + (p % PC) * SW * 32]));
-                    }
+                    const int2 h = lds_v2(hdr + dw * 8);  // run [h.x, h.y), h.x even
+                    uint32_t ep = E + h.x * 8;
+                    const uint32_t ee = E + h.y * 8;
+                    run_pairs<PC, PR, SW, PIPE>(acc[dw], xs, rs, ep, ee);
                 }
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[s]);
+            if (++s == a.S) {
+                s = 0;
+                ph ^= 1;
+            }
         }
 
         // epilogue: obase + dw*dstride + row*rstride + col*cstride for all three output
@@ -266,12 +355,12 @@ __global__ void __launch_bounds__((NWC + 1) * 32, MINB) k_bi(const BiArgs a) {
                         float m = w4[0];
                         if (!isnan(m)) {
 #pragma unroll
-                            for (int q = 1; q < 4; ++q) {
-                                if (isnan(w4[q])) {
-                                    m = w4[q];
+                            for (int q2 = 1; q2 < 4; ++q2) {
+                                if (isnan(w4[q2])) {
+                                    m = w4[q2];
                                     break;
                                 }
-                                if (w4[q] > m) m = w4[q];
+                                if (w4[q2] > m) m = w4[q2];
                             }
                         }
                         a.y[obase + dw * dstride + j * cstride] = m;
@@ -287,9 +376,9 @@ __global__ void __launch_bounds__((NWC + 1) * 32, MINB) k_bi(const BiArgs a) {
     }
 }
 
-template <int PC, int PR, int DW, int SW, int NWC, int MINB>
+template <int PC, int PR, int DW, int SW, int NWC>
 int launch_inst(const usc_plan *pl, const BiArgs &a, cudaStream_t st) {
-    auto fn = k_bi<PC, PR, DW, SW, NWC, MINB>;
+    auto fn = k_bi<PC, PR, DW, SW, NWC>;
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 224 * 1024);
@@ -301,33 +390,8 @@ int launch_inst(const usc_plan *pl, const BiArgs &a, cudaStream_t st) {
     return USC_OK;
 }
 
-// instantiated tiles: DW * PR * PC <= 64 accumulators
-#define USC_BI(PCC, PRR, DD) \
-    if (PC == PCC && PR == PRR && DW == DD) return launch_inst<PCC, PRR, DD, SW, NWC, MINB>(pl, a, st);
-
-template <int SW, int NWC, int MINB>
-int launch_rows1(const usc_plan *pl, const BiArgs &a, cudaStream_t st) {
-    const int PC = pl->PC, PR = pl->PR, DW = pl->DW;
-    USC_BI(1, 1, 4) USC_BI(1, 1, 8) USC_BI(1, 1, 16)
-    USC_BI(2, 1, 4) USC_BI(2, 1, 8) USC_BI(2, 1, 16)
-    USC_BI(4, 1, 4) USC_BI(4, 1, 8) USC_BI(4, 1, 16)
-    USC_BI(8, 1, 4) USC_BI(8, 1, 8)
-    return usc::fail(USC_ERR_UNSUPPORTED, "no BI kernel instance for PC=%d PR=%d DW=%d", PC, PR, DW);
-}
-
-template <int SW, int NWC, int MINB>
-int launch_rows2(const usc_plan *pl, const BiArgs &a, cudaStream_t st) {
-    const int PC = pl->PC, PR = pl->PR, DW = pl->DW;
-    USC_BI(1, 2, 4) USC_BI(1, 2, 8) USC_BI(1, 2, 16)
-    USC_BI(2, 2, 2) USC_BI(2, 2, 4) USC_BI(2, 2, 8) USC_BI(2, 2, 16)
-    USC_BI(4, 2, 4) USC_BI(4, 2, 8)
-    USC_BI(8, 2, 4)
-    return usc::fail(USC_ERR_UNSUPPORTED, "no BI kernel instance for PC=%d PR=%d DW=%d", PC, PR, DW);
-}
-#undef USC_BI
-
-int launch_16(const usc_plan *pl, const BiArgs &a, cudaStream_t st);  // 16 compute warps, 1 CTA/SM
-int launch_16r2(const usc_plan *pl, const BiArgs &a, cudaStream_t st);  // ... with 2-row pixel blocks
-int launch_8(const usc_plan *pl, const BiArgs &a, cudaStream_t st);   // 8 compute warps, 2 CTAs/SM
+int launch_w8(const usc_plan *pl, const BiArgs &a, cudaStream_t st);   // 8 compute warps (168 regs)
+int launch_w12(const usc_plan *pl, const BiArgs &a, cudaStream_t st);  // 12 compute warps (128 regs)
+int launch_w16(const usc_plan *pl, const BiArgs &a, cudaStream_t st);  // 16 compute warps (96 regs)
 
 }  // namespace usc_bi

@@ -5,6 +5,7 @@
 //
 // References are to /root/reference/pkg/src/unsparse/<file>:<line>.
 #include "usc_internal.h"
+#include "bi_instances.h"
 
 #include <algorithm>
 #include <cmath>
@@ -224,18 +225,47 @@ static int pow2_floor(int v) {
     return p;
 }
 
-// The k_bi instances compiled into the library (conv_bi*.cu; keep in sync).
-static bool bi_instance(int PC, int PR, int DW, int NT, int SW) {
-    if (NT == 512 && PR == 2) {
-        if (SW != 1) return false;
-        if (PC == 1) return DW == 4 || DW == 8 || DW == 16;
-        if (PC == 2) return DW == 2 || DW == 4 || DW == 8 || DW == 16;
-        if (PC == 4) return DW == 4 || DW == 8;
-        return PC == 8 && DW == 4;
+// The k_bi instances compiled into the library (bi_instances.h).
+static bool bi_instance(int PC, int PR, int DW, int NW, int SW) {
+#define X(PC_, PR_, DW_, SW_) \
+    if (PC == PC_ && PR == PR_ && DW == DW_ && SW == SW_) return true;
+    if (NW == 8) {
+        USC_BI_W8(X)
+    } else if (NW == 12) {
+        USC_BI_W12(X)
+    } else if (NW == 16) {
+        USC_BI_W16(X)
     }
-    if (PR != 1) return false;
-    if (PC == 1 || PC == 2 || PC == 4) return DW == 4 || DW == 8 || DW == 16;
-    return PC == 8 && (DW == 4 || DW == 8);
+#undef X
+    return false;
+}
+
+int usc_bi_instances(int32_t *out, int32_t max_count) {
+    int n = 0;
+#define X(PC_, PR_, DW_, SW_)                                  \
+    if (n < max_count && out) {                                \
+        int32_t *o = out + 5 * n;                              \
+        o[0] = NW_;                                            \
+        o[1] = PC_;                                            \
+        o[2] = PR_;                                            \
+        o[3] = DW_;                                            \
+        o[4] = SW_;                                            \
+    }                                                          \
+    ++n;
+    {
+        const int NW_ = 8;
+        USC_BI_W8(X)
+    }
+    {
+        const int NW_ = 12;
+        USC_BI_W12(X)
+    }
+    {
+        const int NW_ = 16;
+        USC_BI_W16(X)
+    }
+#undef X
+    return n;
 }
 
 int usc_plan_make(const usc_geometry *g0, int32_t n, int32_t dtype, const usc_exec_cfg *cfg,
@@ -273,19 +303,16 @@ int usc_plan_make(const usc_geometry *g0, int32_t n, int32_t dtype, const usc_ex
     const int threads = (c.threads == 128 || c.threads == 256) ? c.threads : 256;
     if (kernel == 3 && dtype != USC_F32) return fail(USC_ERR_UNSUPPORTED, "BI kernel is fp32-only");
     if (kernel == 3) {
-        // batch-interleaved: a CTA = 32 samples x (WS strips of P pixels) x (WC*DW channels);
-        // warp w owns strip w % WS for channel subgroup w / WS; lane = sample.
-        // defaults follow what the autotuner picks on B200 for 3x3 layers: 512 threads
-        // (1 CTA/SM, long channel chunks), 4 warps over pixels x 4 over channels
-        const int NT = (c.threads == 256) ? 256 : 512;
-        const int NW = NT / 32;
-        // default pixel block: 2 rows x 4 (or 2) columns when the map allows (P = 8,
-        // the autotuner's usual pick on B200), else one row of 8/4/2/1
-        int PR = c.rows_per_thread ? c.rows_per_thread
-                                   : ((Yh % 2 == 0 && g.stride_w == 1 && NT == 512 && Yw % 2 == 0) ? 2 : 1);
-        int PC = c.pix_per_thread ? c.pix_per_thread : 0;
-        if (!PC) {
-            PC = 1;
+        // batch-interleaved: a CTA = 32 samples x (WS strips of PR x PC pixels) x (WC*DW
+        // channels), NW compute warps (threads = NW*32) + 1 producer warp; warp w owns
+        // strip w % WS for channel subgroup w / WS; lane = sample.
+        const bool even = Yh % 2 == 0 && Yw % 2 == 0 && g.stride_w == 1;
+        int PR = c.rows_per_thread ? c.rows_per_thread : (even && Yh >= 2 ? 2 : 1);
+        if (PR != 1 && PR != 2) return fail(USC_ERR_VALUE, "BI rows_per_thread must be 1 or 2");
+        if (PR > Yh) PR = 1;
+        int PC = c.pix_per_thread;
+        if (!PC) {  // widest block that divides the row, else 4 with a partial last strip
+            PC = Yw >= 4 ? 4 : (Yw >= 2 ? 2 : 1);
             for (int q : {8, 4, 2})
                 if (Yw % q == 0 && q * PR <= 8) {
                     PC = q;
@@ -294,61 +321,86 @@ int usc_plan_make(const usc_geometry *g0, int32_t n, int32_t dtype, const usc_ex
         }
         if (PC != 1 && PC != 2 && PC != 4 && PC != 8)
             return fail(USC_ERR_VALUE, "BI pix_per_thread must be 1,2,4,8");
-        if (PR != 1 && PR != 2) return fail(USC_ERR_VALUE, "BI rows_per_thread must be 1 or 2");
-        if (PR > Yh) PR = 1;
         const int P = PR * PC;
-        if (P > 16) return fail(USC_ERR_VALUE, "BI pixel block larger than 16");
-        const int SPR = (Yw + PC - 1) / PC;   // strips per strip-row
-        const int SR = (Yh + PR - 1) / PR;    // strip-rows
-        int WSmax = c.pixel_warps ? std::min(c.pixel_warps, NW) : std::min(4, NW);
-        int WS, TSR, SPRt;
-        if ((int64_t)SR * SPR <= WSmax) {
-            WS = SR * SPR;
-            TSR = SR;
-            SPRt = SPR;
-        } else if (SPR <= WSmax) {
-            TSR = WSmax / SPR;
-            WS = TSR * SPR;
-            SPRt = SPR;
-        } else {
-            TSR = 1;
-            SPRt = WSmax;
-            WS = WSmax;
+        const int SPR = (Yw + PC - 1) / PC;  // strips per strip-row
+        const int SR = (Yh + PR - 1) / PR;   // strip-rows
+        // warps: the requested count, else the first of 8/12/16 with a compiled
+        // instance for this pixel block (channels per warp 8, 16 or 4 unless given)
+        int NW = 0, WS = 0, WC = 0, DW = 0;
+        for (int nw : {8, 12, 16}) {
+            if (c.threads && c.threads != nw * 32) continue;
+            // pixel warps: as given, else the largest divisor of the warps (<= warps/4)
+            // whose strips tile the map's strip grid
+            auto tileable = [&](int w) {
+                for (int t = 1; t <= w; ++t)
+                    if (w % t == 0 && t <= SR && w / t <= SPR) return true;
+                return false;
+            };
+            int ws = c.pixel_warps;
+            if (ws && (ws > nw || nw % ws))
+                return fail(USC_ERR_VALUE, "pixel_warps %d must divide %d warps", ws, nw);
+            if (!ws)
+                for (ws = std::max(1, nw / 4); ws > 1; --ws)
+                    if (nw % ws == 0 && tileable(ws)) break;
+            const int wc = nw / ws;
+            if (c.ch_per_cta && c.ch_per_cta % wc)
+                return fail(USC_ERR_VALUE, "ch_per_cta %d not a multiple of %d channel warps", c.ch_per_cta, wc);
+            for (int dw : {8, 16, 4}) {
+                if (c.ch_per_cta) dw = c.ch_per_cta / wc;
+                if (bi_instance(PC, PR, dw, nw, g.stride_w)) {
+                    NW = nw, WS = ws, WC = wc, DW = dw;
+                    break;
+                }
+                if (c.ch_per_cta) break;
+            }
+            if (NW) break;
         }
+        if (!NW)
+            return fail(USC_ERR_VALUE, "no BI kernel instance for PC=%d PR=%d threads=%d ch_per_cta=%d stride=%d",
+                        PC, PR, c.threads, c.ch_per_cta, g.stride_w);
+        // tile = TSR strip-rows x SPRt strips (TSR*SPRt == WS): fewest tiles (strip work),
+        // then the smallest staged footprint
+        int TSR = 1, SPRt = WS;
+        int64_t best_tiles = INT64_MAX, best_foot = INT64_MAX;
+        for (int tsr = 1; tsr <= WS; ++tsr) {
+            if (WS % tsr) continue;
+            const int sprt = WS / tsr;
+            // strips of a tile stay inside the map (a full-row stage is exactly Yw wide)
+            if (sprt > SPR || (tsr > SR && tsr > 1)) continue;
+            const int64_t tiles = (int64_t)((SR + tsr - 1) / tsr) * ((SPR + sprt - 1) / sprt);
+            const int ct = (SPR + sprt - 1) / sprt;
+            const int tws = (ct == 1 && SPR * PC == Yw) ? pl->in.ws : (sprt * PC - 1) * g.stride_w + g.filter_w;
+            const int64_t foot = tiles * ((int64_t)(tsr * PR - 1) * g.stride_h + g.filter_h) * tws;
+            if (tiles < best_tiles || (tiles == best_tiles && foot < best_foot)) {
+                best_tiles = tiles;
+                best_foot = foot;
+                TSR = tsr;
+                SPRt = sprt;
+            }
+        }
+        if (best_tiles == INT64_MAX)
+            return fail(USC_ERR_VALUE, "%d pixel warps do not tile a %dx%d strip grid", WS, SR, SPR);
         const int TH = TSR * PR;  // output rows per tile
-        int WC = NW / WS;
-        if (WC < 1) WC = 1;
-        int DW = c.ch_per_cta ? std::max(1, c.ch_per_cta / WC) : (NT == 512 && WC <= 4 ? 8 : (WC >= 16 ? 2 : 4));
-        if (DW > 16) DW = 16;
-        if (DW != 2 && DW != 4 && DW != 8 && DW != 16) DW = DW < 2 ? 2 : (DW < 4 ? 2 : (DW < 8 ? 4 : 8));
-        const int acc_cap = NT == 512 ? 64 : 32;  // accumulators that fit the register cap
-        while (DW > 2 && DW * P > acc_cap) DW /= 2;
-        if (DW * P > acc_cap) return fail(USC_ERR_VALUE, "BI tile needs too many accumulators");
-        if (!bi_instance(PC, PR, DW, NT, g.stride_w) && DW == 2) DW = 4;
-        if (!bi_instance(PC, PR, DW, NT, g.stride_w) || DW * P > acc_cap)
-            return fail(USC_ERR_VALUE, "no BI kernel instance for PC=%d PR=%d DW=%d threads=%d", PC, PR, DW, NT);
-        if (PR == 2 && (NT != 512 || g.stride_w != 1))
-            return fail(USC_ERR_VALUE, "BI rows_per_thread=2 needs 512 threads and stride_w 1");
         const int col_tiles = (SPR + SPRt - 1) / SPRt;
         const bool full_rows = (col_tiles == 1 && SPR * PC == Yw);
-        int TWs = full_rows ? pl->in.ws : (SPRt * PC - 1) * g.stride_w + g.filter_w;
+        const int TWs = full_rows ? pl->in.ws : (SPRt * PC - 1) * g.stride_w + g.filter_w;
         const int HS = (TH - 1) * g.stride_h + g.filter_h;
         const int64_t per_ch = (int64_t)HS * TWs * 32 * eb;
+        const int DT = WC * DW;
         int CC = c.chunk_channels ? c.chunk_channels : 64;
         CC = std::min(CC, g.in_channels);
-        // S-stage ring; 512 compute threads -> 1 CTA/SM (~200 KB), 256 -> 2 CTAs/SM
         const int S = c.stages ? std::max(2, std::min(4, c.stages)) : 2;
-        const int64_t budget = (NT == 512 ? 200 * 1024 : 100 * 1024) - 256;
-        // per-stage entry buffer: DT*CC*Kh*Kw entries of 8 bytes (+1 alignment pad) is the
-        // exact worst case; reserve at most R bytes -- usc_pack rejects a filter whose
-        // densest (group, chunk) block exceeds the reserve (the caller then re-plans
-        // with fewer chunk channels)
-        const int64_t R = c.ent_reserve ? c.ent_reserve : (NT == 512 ? 16 * 1024 : 8 * 1024);
+        const int64_t budget = 200 * 1024;
+        // per-stage entry block: hdr DT*8 + runs padded to even (16-B aligned starts) +
+        // 16 B read slack.  The exact worst case is DT*CC*Kh*Kw entries; reserve at most
+        // R bytes -- usc_pack rejects a filter whose densest (group, chunk) block
+        // exceeds it (the caller re-plans with the measured size).
+        const int64_t R = c.ent_reserve ? c.ent_reserve : 24 * 1024;
         auto ent_bytes = [&](int cc) {
-            const int64_t worst = ((int64_t)(WC * DW) * cc * g.filter_h * g.filter_w * 8 + 16 + 127) / 128 * 128;
-            return std::min(worst, (R + 127) / 128 * 128);
+            const int64_t worst = (int64_t)DT * 8 + ((int64_t)DT * cc * g.filter_h * g.filter_w + DT) * 8 + 16;
+            return (std::min(worst, R) + 127) / 128 * 128;
         };
-        while (CC > 1 && S * (CC * per_ch + ent_bytes(CC)) > budget) --CC;
+        while (CC > 1 && S * ((CC * per_ch + 127) / 128 * 128 + ent_bytes(CC)) > budget) --CC;
         const int64_t stage = (CC * per_ch + 127) / 128 * 128;
         const int64_t ent_stage = ent_bytes(CC);
         if (S * (stage + ent_stage) + 128 > 224 * 1024)
@@ -360,7 +412,7 @@ int usc_plan_make(const usc_geometry *g0, int32_t n, int32_t dtype, const usc_ex
         pl->WS = WS;
         pl->WC = WC;
         pl->DW = DW;
-        pl->DT = WC * DW;
+        pl->DT = DT;
         pl->NS = 32;
         pl->CC = CC;
         pl->TH = TH;
@@ -368,21 +420,21 @@ int usc_plan_make(const usc_geometry *g0, int32_t n, int32_t dtype, const usc_ex
         pl->SPRt = SPRt;
         pl->col_tiles = col_tiles;
         pl->TWs = TWs;
-        pl->threads = NT;
+        pl->threads = NW * 32;
         pl->strips_per_row = SPR;
         pl->row_tiles = (Yh + TH - 1) / TH;
         pl->sample_tiles = (n + 31) / 32;
-        pl->groups = (g.out_channels + pl->DT - 1) / pl->DT;
+        pl->groups = (g.out_channels + DT - 1) / DT;
         pl->n_chunks = (g.in_channels + CC - 1) / CC;
         pl->smem_stage_bytes = stage;
         pl->ent_stage_bytes = static_cast<int32_t>(ent_stage);
         pl->stages = S;
         pl->smem_bytes = S * (stage + ent_stage) + 128;
-        // persistent grid: at most one wave of resident CTAs, each walks its tiles
+        // persistent grid: one CTA per SM, each walks its tiles
         const int64_t tiles = (int64_t)pl->groups * pl->sample_tiles * pl->row_tiles * pl->col_tiles;
         int sms = usc_device_sm_count(0);
         if (sms <= 0) sms = 148;
-        pl->grid_x = std::min<int64_t>(tiles, (int64_t)sms * (NT == 512 ? 1 : 2));
+        pl->grid_x = std::min<int64_t>(tiles, sms);
         pl->grid_y = 1;
         return USC_OK;
     }
@@ -471,12 +523,15 @@ int usc_plan_make(const usc_geometry *g0, int32_t n, int32_t dtype, const usc_ex
 static int64_t align16(int64_t v) { return (v + 15) / 16 * 16; }
 
 int usc_pack_size(const usc_plan *pl, int64_t n_nz, int64_t *bytes) {
-    int64_t cp = align16(4 * ((int64_t)pl->groups * pl->n_chunks * pl->DT + 1));
-    // kernel 3 starts every (group, chunk) block on a 16-byte boundary (one pad
-    // entry at most per block) and reads up to 16 bytes past a block
-    int64_t n_ent = (int64_t)pl->g.out_channels * n_nz +
-                    (pl->kernel == 3 ? (int64_t)pl->groups * pl->n_chunks : 0);
-    int64_t ent = align16(n_ent * entry_bytes(pl->dtype)) + 64;
+    const int64_t nb = (int64_t)pl->groups * pl->n_chunks;
+    if (pl->kernel == 3) {
+        // [64 B][int32 blk[nb+1]][blocks: hdr int2[DT], runs padded to even, 16-B rounded]
+        *bytes = 64 + align16(4 * (nb + 1)) + nb * ((int64_t)pl->DT * 8 + 16) +
+                 ((int64_t)pl->g.out_channels * n_nz + nb * pl->DT) * 8 + 64;
+        return USC_OK;
+    }
+    int64_t cp = align16(4 * (nb * pl->DT + 1));
+    int64_t ent = align16((int64_t)pl->g.out_channels * n_nz * entry_bytes(pl->dtype)) + 64;
     *bytes = 64 + cp + ent;  // [16-float centroid table][cpg][entries]
     return USC_OK;
 }
@@ -513,55 +568,133 @@ int usc_pack(const usc_plan *pl, const int64_t *row_ptr, const int64_t *col, con
     const int64_t cs_tiled = (int64_t)pl->HS * Ws;  // channel stride inside a stage
     std::memset(blob, 0, 64);
     if (pl->dtype == USC_CB4) std::memcpy(blob, table, 16 * sizeof(float));
+    // one stored entry j of channel d -> (input channel, offset in the kernel's staged
+    // tile), or off = -1 to drop it (a repeated zero-weight offset)
+    const int64_t max_off = pl->dtype == USC_I8 ? (1 << 24) : (1 << 28);
+    std::vector<int64_t> zero_seen;
+    auto decode = [&](int64_t j, int64_t *cpos, int64_t *off) -> int {
+        const int64_t lam = col[j];
+        int64_t c = lam / plane0, rem = lam % plane0, kh = rem / Wp0, kw = rem % Wp0;
+        if (lam < 0 || c >= g.in_channels || kh >= Kh0 || kw >= Kw0)
+            return fail(USC_ERR_CORRUPT, "offset %lld does not decode to a tap", (long long)lam);
+        *cpos = c;
+        bool zero;
+        switch (pl->dtype) {
+            case USC_F32:
+            case USC_F16: zero = ((const float *)payload)[j] == 0.0f; break;
+            case USC_I8: zero = ((const int8_t *)payload)[j] == 0; break;
+            default: zero = table[((const uint8_t *)payload)[j] & 15] == 0.0f; break;
+        }
+        if (zero) {
+            // a zero-weight entry only matters when x is non-finite, where one copy
+            // per distinct offset already yields the NaN
+            if (std::find(zero_seen.begin(), zero_seen.end(), lam) != zero_seen.end()) {
+                *off = -1;
+                return USC_OK;
+            }
+            zero_seen.push_back(lam);
+        }
+        if (pl->transposed) std::swap(kh, kw);  // (c, kh, 0) -> (c, 0, kh)
+        const int64_t cl = c - (c / CC) * CC;
+        if (pl->kernel == 1)
+            *off = cl * cs_tiled + kh * Ws + kw;
+        else if (pl->kernel == 3)  // byte offset in the [CC][HS][TWs][32] f32 stage
+            *off = ((cl * pl->HS + kh) * pl->TWs + kw) * 128;
+        else
+            *off = (c * Hp + kh) * Ws + kw;
+        if (*off >= max_off || *off > INT32_MAX)
+            return fail(USC_ERR_UNSUPPORTED, "packed offset %lld too large", (long long)*off);
+        return USC_OK;
+    };
+    if (pl->kernel == 3) {
+        // blocks (group, chunk): int2 hdr[DT] = {first, end} entry index of each output
+        // channel's run (relative to the entries after hdr), runs start at even indices
+        const int64_t nb = (int64_t)G * NC;
+        int32_t *blk = (int32_t *)((char *)blob + 64);
+        char *base = (char *)blob + 64 + align16(4 * (nb + 1));
+        const int64_t cap = blob_bytes - (base - (char *)blob);
+        int64_t pos = 0, worst = 0, total = 0;
+        std::vector<int64_t> cpos_of(n_nz), off_of(n_nz);
+        for (int gi = 0; gi < G; ++gi) {
+            // decode every channel of the group once, then emit per chunk
+            std::vector<std::vector<std::pair<int64_t, int64_t>>> per(DT);  // (chunk, off) per dl
+            std::vector<std::vector<int64_t>> src(DT);
+            for (int dl = 0; dl < DT; ++dl) {
+                const int d = gi * DT + dl;
+                if (d >= D) continue;
+                zero_seen.clear();
+                for (int64_t j = row_ptr[d]; j < row_ptr[d] + n_nz; ++j) {
+                    int64_t cpos, off;
+                    int rc = decode(j, &cpos, &off);
+                    if (rc) return rc;
+                    if (off < 0) continue;
+                    per[dl].push_back({cpos / CC, off});
+                    src[dl].push_back(j);
+                }
+            }
+            for (int k = 0; k < NC; ++k) {
+                blk[(int64_t)gi * NC + k] = (int32_t)pos;
+                char *b = base + pos;
+                int32_t *hdr = (int32_t *)b;
+                int64_t e = 0;  // entry index after the header
+                std::vector<int32_t> runs(2 * DT);
+                std::vector<std::pair<int64_t, int64_t>> out;  // (off, j)
+                for (int dl = 0; dl < DT; ++dl) {
+                    if (e & 1) {
+                        out.push_back({-1, -1});  // alignment pad, never referenced
+                        ++e;
+                    }
+                    runs[2 * dl] = (int32_t)e;
+                    for (size_t i = 0; i < per[dl].size(); ++i)  // stored order within the chunk
+                        if (per[dl][i].first == k) {
+                            out.push_back({per[dl][i].second, src[dl][i]});
+                            ++e;
+                        }
+                    runs[2 * dl + 1] = (int32_t)e;
+                }
+                const int64_t bytes = align16((int64_t)DT * 8 + e * 8);
+                if (!dry && pos + bytes + 16 > cap) return fail(USC_ERR_VALUE, "pack buffer too small");
+                if (!dry) {
+                    std::memcpy(hdr, runs.data(), (size_t)DT * 8);
+                    char *ents = b + (int64_t)DT * 8;
+                    std::memset(ents, 0, (size_t)(bytes - (int64_t)DT * 8));
+                    for (int64_t i = 0; i < (int64_t)out.size(); ++i) {
+                        if (out[i].first < 0) continue;
+                        int32_t v[2];
+                        v[0] = (int32_t)out[i].first;
+                        std::memcpy(&v[1], &((const float *)payload)[out[i].second], 4);
+                        std::memcpy(ents + i * 8, v, 8);
+                    }
+                }
+                total += (int64_t)out.size();
+                worst = std::max(worst, bytes + 16);
+                pos += bytes;
+            }
+        }
+        if (!dry) blk[nb] = (int32_t)pos;
+        *n_entries = dry ? worst : total;
+        if (!dry && worst > pl->ent_stage_bytes)
+            return fail(USC_ERR_VALUE, "entry block of %lld bytes exceeds the %d-byte stage reserve",
+                        (long long)worst, pl->ent_stage_bytes);
+        return USC_OK;
+    }
     int32_t *cpg = (int32_t *)((char *)blob + 64);
     const int64_t cp_bytes = align16(4 * ((int64_t)G * NC * DT + 1));
     char *ent = (char *)blob + 64 + cp_bytes;
     const int eb = entry_bytes(pl->dtype);
-    const int64_t max_off = pl->dtype == USC_I8 ? (1 << 24) : (1 << 28);
     int64_t pos = 0;
-    std::vector<int64_t> zero_seen;
     for (int gi = 0; gi < G; ++gi)
         for (int k = 0; k < NC; ++k)
             for (int dl = 0; dl < DT; ++dl) {
-                if (pl->kernel == 3 && dl == 0 && (pos & 1)) {
-                    std::memset(ent + pos * eb, 0, eb);  // alignment pad, never referenced
-                    ++pos;
-                }
                 cpg[((int64_t)gi * NC + k) * DT + dl] = (int32_t)pos;
                 int d = gi * DT + dl;
                 if (d >= D) continue;
                 zero_seen.clear();
                 for (int64_t j = row_ptr[d]; j < row_ptr[d] + n_nz; ++j) {
-                    int64_t lam = col[j];
-                    int64_t c = lam / plane0, rem = lam % plane0, kh = rem / Wp0, kw = rem % Wp0;
-                    if (lam < 0 || c >= g.in_channels || kh >= Kh0 || kw >= Kw0)
-                        return fail(USC_ERR_CORRUPT, "offset %lld does not decode to a tap",
-                                    (long long)lam);
-                    if (c / CC != k) continue;
-                    bool zero;
-                    switch (pl->dtype) {
-                        case USC_F32:
-                        case USC_F16: zero = ((const float *)payload)[j] == 0.0f; break;
-                        case USC_I8: zero = ((const int8_t *)payload)[j] == 0; break;
-                        default: zero = table[((const uint8_t *)payload)[j] & 15] == 0.0f; break;
-                    }
-                    if (zero) {
-                        // a zero-weight entry only matters when x is non-finite, where
-                        // one copy per distinct offset already yields the NaN
-                        if (std::find(zero_seen.begin(), zero_seen.end(), lam) != zero_seen.end())
-                            continue;
-                        zero_seen.push_back(lam);
-                    }
-                    if (pl->transposed) std::swap(kh, kw);  // (c, kh, 0) -> (c, 0, kh)
-                    int64_t off;
-                    if (pl->kernel == 1)
-                        off = (c - (int64_t)k * CC) * cs_tiled + kh * Ws + kw;
-                    else if (pl->kernel == 3)  // byte offset in the [CC][HS][TWs][32] f32 stage
-                        off = (((c - (int64_t)k * CC) * pl->HS + kh) * pl->TWs + kw) * 128;
-                    else
-                        off = (c * Hp + kh) * Ws + kw;
-                    if (off >= max_off || off > INT32_MAX)
-                        return fail(USC_ERR_UNSUPPORTED, "packed offset %lld too large", (long long)off);
+                    int64_t c, off;
+                    int rc = decode(j, &c, &off);
+                    if (rc) return rc;
+                    if (off < 0 || c / CC != k) continue;
                     char *e = ent + pos * eb;
                     switch (pl->dtype) {
                         case USC_F32:
@@ -590,18 +723,6 @@ int usc_pack(const usc_plan *pl, const int64_t *row_ptr, const int64_t *col, con
             }
     cpg[(int64_t)G * NC * DT] = (int32_t)pos;
     *n_entries = pos;
-    if (pl->kernel == 3) {
-        int64_t worst = 0;
-        for (int64_t b = 0; b < (int64_t)G * NC; ++b)
-            worst = std::max<int64_t>(worst, ((int64_t)cpg[(b + 1) * DT] - cpg[b * DT]) * 8 + 16);
-        if (dry) {
-            *n_entries = worst;
-            return USC_OK;
-        }
-        if (worst > pl->ent_stage_bytes)
-            return fail(USC_ERR_VALUE, "entry block of %lld bytes exceeds the %d-byte stage reserve",
-                        (long long)worst, pl->ent_stage_bytes);
-    }
     return USC_OK;
 }
 

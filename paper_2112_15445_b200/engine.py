@@ -140,7 +140,7 @@ def _max_block(filt, plan, payload, table=None) -> int:
 
 def _pack_key(plan: _lib.Plan, device) -> tuple:
     return (plan.dtype, plan.kernel, plan.DT, plan.CC, plan.HS, plan.TWs, plan.in_.ws, plan.in_.hp,
-            plan.transposed, plan.groups, plan.n_chunks, str(device))
+            plan.transposed, plan.groups, plan.n_chunks, plan.ent_stage_bytes, str(device))
 
 
 def device_pack(filt: CsrFilter, plan: _lib.Plan, payload: np.ndarray, table=None, device=None):
@@ -297,21 +297,21 @@ def tile_candidates(geometry: ConvGeometry, n: int, sb_values, precision=Precisi
     if kernels is None:
         kernels = (3, 1) if precision is PrecisionMode.BINARY32 else (1,)
     if 3 in kernels and precision is PrecisionMode.BINARY32:
-        yh = geometry.out_h if geometry.input_w != 1 else 1
-        for pr in (1, 2):
-            if pr > yh:
+        # every compiled k_bi instance x every split of its warps into pixel warps (WS)
+        # and channel warps; skip pixel blocks wider/taller than the map and splits
+        # that leave pixel warps idle
+        yh = geometry.out_h if geometry.input_w != 1 else geometry.out_w
+        sw = geometry.stride[1] if geometry.input_w != 1 else geometry.stride[0]
+        for nw, pc, pr, dw, isw in _lib.bi_instances():
+            if isw != sw or pc > max(1, yw) and pc > 1 or pr > yh:
                 continue
-            for p in (1, 2, 4, 8):
-                if p > max(1, yw) or pr * p > 16:
-                    continue
-                for nt, dts in ((256, (8, 16, 32)), (512, (16, 32, 64))):
-                    if pr == 2 and nt == 256:
-                        continue
-                    for dt in dts:
-                        for pw in (0, 4, 8):
-                            out.append(ExecConfig(sub_batch=min(sb_values), pix_per_thread=p,
-                                                  ch_per_cta=dt, kernel=3, threads=nt, pixel_warps=pw,
-                                                  stages=2, rows_per_thread=pr))
+            strips = -(-yh // pr) * -(-yw // pc)
+            for ws in (w for w in range(1, nw + 1) if nw % w == 0):
+                if ws > strips:
+                    break
+                out.append(ExecConfig(sub_batch=min(sb_values), pix_per_thread=pc, rows_per_thread=pr,
+                                      ch_per_cta=dw * (nw // ws), kernel=3, threads=nw * 32,
+                                      pixel_warps=ws, stages=2))
     if 1 in kernels:
         ps = [p for p in (2, 4, 8) if p <= max(2, yw)]
         for sb in sb_values:
@@ -325,8 +325,8 @@ def tile_candidates(geometry: ConvGeometry, n: int, sb_values, precision=Precisi
             plan = make_plan(geometry, n, dtype_of(precision), cfg)
         except ValueError:
             continue
-        key = (plan.kernel, plan.P, plan.PR, plan.DT, plan.DW, plan.WS, plan.NS, plan.CC, plan.threads,
-               plan.stages)
+        key = (plan.kernel, plan.P, plan.PR, plan.PC, plan.DT, plan.DW, plan.WS, plan.NS, plan.CC,
+               plan.threads, plan.stages)
         if key not in seen:
             seen.add(key)
             feasible.append(cfg)
