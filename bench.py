@@ -176,7 +176,7 @@ def time_per_launch(model, steps=20):
             b.record()
             evs.append((a, b))
         torch.cuda.synchronize()
-        times[(st[0], st[1])] = float(np.mean([a.elapsed_time(b) for a, b in evs]))
+        times[(st[0], st[1])] = float(np.median([a.elapsed_time(b) for a, b in evs]))
     return times
 
 

@@ -5,15 +5,18 @@ namespace usc {
 
 int launch_bi(const usc_plan *pl, const void *blob, const void *x, void *y, const usc_dev::Epi &ep,
               cudaStream_t st) {
-    // blob = [64 B][int32 blk[G*n_chunks + 1], 16-B aligned][blocks] (usc_pack, kernel 3)
+    // blob = [64 B][int32 blk[G*n_chunks + 1]][int32 perm[G*DT]][blocks], each part 16-B
+    // aligned (usc_pack, kernel 3)
     const char *cb = static_cast<const char *>(blob);
     const long long nb = (long long)pl->groups * pl->n_chunks;
     const long long cp_bytes = (4 * (nb + 1) + 15) / 16 * 16;
     usc_bi::BiArgs a{};
     a.x = static_cast<const float *>(x);
     a.y = static_cast<float *>(y);
+    const long long perm_bytes = (4LL * pl->groups * pl->DT + 15) / 16 * 16;
     a.blk = reinterpret_cast<const int *>(cb + 64);
-    a.blocks = cb + 64 + cp_bytes;
+    a.perm = reinterpret_cast<const int *>(cb + 64 + cp_bytes);
+    a.blocks = cb + 64 + cp_bytes + perm_bytes;
     a.N = pl->n;
     a.C = pl->g.in_channels;
     a.D = pl->g.out_channels;

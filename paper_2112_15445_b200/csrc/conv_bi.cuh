@@ -41,6 +41,7 @@ struct BiArgs {
     const float *x;
     float *y;
     const int *blk;          // byte offset of every (group, chunk) block, G*n_chunks+1
+    const int *perm;         // output channel of every (group, warp, slot); -1 = empty
     const char *blocks;      // block base (16-byte aligned)
     int N, C, D, n_chunks, CC, DT;
     int HS, TWs, Hp, Wp, Yh, Yw, s_h;
@@ -305,41 +306,42 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1) k_bi(const BiArgs a) {
             }
         }
 
-        // epilogue: obase + dw*dstride + row*rstride + col*cstride for all three output
+        // epilogue: obase + d*dstride + row*rstride + col*cstride for all three output
         // layouts; ReLU (nn.py:96-98) then, if fused, the 2x2/2 max-pool (nn.py:124-135)
         const int b = sb * 32 + lane;
         if (!active || b >= a.N || r >= a.Yh) continue;
-        const int d0 = g * a.DT + wc * DW;
+        const int *pm = a.perm + g * a.DT + wc * DW;  // this warp's output channels (balanced)
         const bool pool = PR == 2 && a.ep.pool;
         const int orow = pool ? r / 2 : r, ocol = pool ? col0 / 2 : col0;
-        long long obase, dstride;
+        long long obase, dstride;  // element of (b, d, orow, ocol) = obase + d*dstride
         int rstride, cstride;
         if (!a.ep.out_padded) {
             const int oh = pool ? a.Yh / 2 : a.Yh, ow = pool ? a.Yw / 2 : a.Yw;
-            obase = (((long long)b * a.D + d0) * oh + orow) * ow + ocol;
+            obase = ((long long)b * a.D * oh + orow) * ow + ocol;
             dstride = (long long)oh * ow;
             rstride = ow;
             cstride = 1;
         } else if (a.ep.oil == 32) {
             obase = (long long)sb * a.ep.o_sample_stride +
-                    ((((long long)d0 * a.ep.oHp + orow + a.ep.oph) * a.ep.oWs + ocol + a.ep.opw) << 5) + lane;
+                    ((((long long)orow + a.ep.oph) * a.ep.oWs + ocol + a.ep.opw) << 5) + lane;
             dstride = (long long)a.ep.oHp * a.ep.oWs * 32;
             rstride = a.ep.oWs * 32;
             cstride = 32;
         } else {
             obase = (long long)b * a.ep.o_sample_stride +
-                    ((long long)d0 * a.ep.oHp + orow + a.ep.oph) * a.ep.oWs + ocol + a.ep.opw;
+                    ((long long)orow + a.ep.oph) * a.ep.oWs + ocol + a.ep.opw;
             dstride = (long long)a.ep.oHp * a.ep.oWs;
             rstride = a.ep.oWs;
             cstride = 1;
         }
-        const int ndw = min(DW, a.D - d0);
         const int ncol = min(PC, a.Yw - col0);
         const int nrow = min(PR, a.Yh - r);
         const bool relu = a.ep.relu != 0;
 #pragma unroll
         for (int dw = 0; dw < DW; ++dw) {
-            if (dw >= ndw) break;
+            const int d = __ldg(pm + dw);
+            if (d < 0) continue;
+            const long long od = obase + d * dstride;
             float v[P];
 #pragma unroll
             for (int p = 0; p < P; ++p) {
@@ -363,7 +365,7 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1) k_bi(const BiArgs a) {
                                 if (w4[q2] > m) m = w4[q2];
                             }
                         }
-                        a.y[obase + dw * dstride + j * cstride] = m;
+                        a.y[od + j * cstride] = m;
                     }
                     continue;
                 }
@@ -371,7 +373,7 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1) k_bi(const BiArgs a) {
 #pragma unroll
             for (int p = 0; p < P; ++p)
                 if ((p / PC) < nrow && (p % PC) < ncol)
-                    a.y[obase + dw * dstride + (p / PC) * rstride + (p % PC) * cstride] = v[p];
+                    a.y[od + (p / PC) * rstride + (p % PC) * cstride] = v[p];
         }
     }
 }

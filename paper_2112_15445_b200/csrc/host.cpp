@@ -525,8 +525,10 @@ static int64_t align16(int64_t v) { return (v + 15) / 16 * 16; }
 int usc_pack_size(const usc_plan *pl, int64_t n_nz, int64_t *bytes) {
     const int64_t nb = (int64_t)pl->groups * pl->n_chunks;
     if (pl->kernel == 3) {
-        // [64 B][int32 blk[nb+1]][blocks: hdr int2[DT], runs padded to even, 16-B rounded]
-        *bytes = 64 + align16(4 * (nb + 1)) + nb * ((int64_t)pl->DT * 8 + 16) +
+        // [64 B][int32 blk[nb+1]][int32 perm[G*DT]][blocks: hdr int2[DT], runs padded to
+        // even, 16-B rounded]
+        *bytes = 64 + align16(4 * (nb + 1)) + align16(4 * (int64_t)pl->groups * pl->DT) +
+                 nb * ((int64_t)pl->DT * 8 + 16) +
                  ((int64_t)pl->g.out_channels * n_nz + nb * pl->DT) * 8 + 64;
         return USC_OK;
     }
@@ -607,35 +609,65 @@ int usc_pack(const usc_plan *pl, const int64_t *row_ptr, const int64_t *col, con
         return USC_OK;
     };
     if (pl->kernel == 3) {
-        // blocks (group, chunk): int2 hdr[DT] = {first, end} entry index of each output
-        // channel's run (relative to the entries after hdr), runs start at even indices
+        // blob = [64 B][int32 blk[nb+1]][int32 perm[G*DT]][blocks].  Block (group, chunk):
+        // int2 hdr[DT] = {first, end} entry index of each slot's run (relative to the
+        // entries after hdr), runs start at even indices (16-B aligned pairs).
+        // perm: output channel of every (group, warp, slot), -1 for an empty slot.  The
+        // assignment balances the warps: channels in decreasing entry count go to the
+        // warp whose worst per-chunk load grows least (the ring lets a warp run at most
+        // stages-1 chunks ahead of the slowest, so per-chunk balance is what counts).
         const int64_t nb = (int64_t)G * NC;
+        const int WC = pl->WC, DW = pl->DW;
         int32_t *blk = (int32_t *)((char *)blob + 64);
-        char *base = (char *)blob + 64 + align16(4 * (nb + 1));
+        int32_t *perm = (int32_t *)((char *)blob + 64 + align16(4 * (nb + 1)));
+        char *base = (char *)perm + align16(4 * (int64_t)G * DT);
         const int64_t cap = blob_bytes - (base - (char *)blob);
-        int64_t pos = 0, worst = 0, total = 0;
-        std::vector<int64_t> cpos_of(n_nz), off_of(n_nz);
-        for (int gi = 0; gi < G; ++gi) {
-            // decode every channel of the group once, then emit per chunk
-            std::vector<std::vector<std::pair<int64_t, int64_t>>> per(DT);  // (chunk, off) per dl
-            std::vector<std::vector<int64_t>> src(DT);
-            for (int dl = 0; dl < DT; ++dl) {
-                const int d = gi * DT + dl;
-                if (d >= D) continue;
-                zero_seen.clear();
-                for (int64_t j = row_ptr[d]; j < row_ptr[d] + n_nz; ++j) {
-                    int64_t cpos, off;
-                    int rc = decode(j, &cpos, &off);
-                    if (rc) return rc;
-                    if (off < 0) continue;
-                    per[dl].push_back({cpos / CC, off});
-                    src[dl].push_back(j);
+        std::vector<std::vector<std::pair<int64_t, int64_t>>> per(D);  // (chunk, off) per d
+        std::vector<std::vector<int64_t>> src(D);
+        std::vector<int64_t> cnt((size_t)D * NC, 0);
+        for (int d = 0; d < D; ++d) {
+            zero_seen.clear();
+            for (int64_t j = row_ptr[d]; j < row_ptr[d] + n_nz; ++j) {
+                int64_t cpos, off;
+                int rc = decode(j, &cpos, &off);
+                if (rc) return rc;
+                if (off < 0) continue;
+                per[d].push_back({cpos / CC, off});
+                src[d].push_back(j);
+                ++cnt[(size_t)d * NC + cpos / CC];
+            }
+        }
+        std::vector<int> order(D);
+        for (int d = 0; d < D; ++d) order[d] = d;
+        std::stable_sort(order.begin(), order.end(),
+                         [&](int x, int y) { return per[x].size() > per[y].size(); });
+        const int bins = G * WC;
+        std::vector<int64_t> load((size_t)bins * NC, 0), tot(bins, 0);
+        std::vector<int> used(bins, 0);
+        std::vector<int32_t> slot((size_t)G * DT, -1);
+        for (int d : order) {
+            int best = -1;
+            int64_t bmax = INT64_MAX, btot = INT64_MAX;
+            for (int bi = 0; bi < bins; ++bi) {
+                if (used[bi] == DW) continue;
+                int64_t m = 0;
+                for (int k = 0; k < NC; ++k)
+                    m = std::max(m, load[(size_t)bi * NC + k] + cnt[(size_t)d * NC + k]);
+                if (m < bmax || (m == bmax && tot[bi] < btot)) {
+                    best = bi;
+                    bmax = m;
+                    btot = tot[bi];
                 }
             }
+            for (int k = 0; k < NC; ++k) load[(size_t)best * NC + k] += cnt[(size_t)d * NC + k];
+            tot[best] += (int64_t)per[d].size();
+            slot[(size_t)(best / WC) * DT + (best % WC) * DW + used[best]++] = d;
+        }
+        int64_t pos = 0, worst = 0, total = 0;
+        for (int gi = 0; gi < G; ++gi)
             for (int k = 0; k < NC; ++k) {
                 blk[(int64_t)gi * NC + k] = (int32_t)pos;
                 char *b = base + pos;
-                int32_t *hdr = (int32_t *)b;
                 int64_t e = 0;  // entry index after the header
                 std::vector<int32_t> runs(2 * DT);
                 std::vector<std::pair<int64_t, int64_t>> out;  // (off, j)
@@ -645,17 +677,19 @@ int usc_pack(const usc_plan *pl, const int64_t *row_ptr, const int64_t *col, con
                         ++e;
                     }
                     runs[2 * dl] = (int32_t)e;
-                    for (size_t i = 0; i < per[dl].size(); ++i)  // stored order within the chunk
-                        if (per[dl][i].first == k) {
-                            out.push_back({per[dl][i].second, src[dl][i]});
-                            ++e;
-                        }
+                    const int d = slot[(size_t)gi * DT + dl];
+                    if (d >= 0)
+                        for (size_t i = 0; i < per[d].size(); ++i)  // stored order within the chunk
+                            if (per[d][i].first == k) {
+                                out.push_back({per[d][i].second, src[d][i]});
+                                ++e;
+                            }
                     runs[2 * dl + 1] = (int32_t)e;
                 }
                 const int64_t bytes = align16((int64_t)DT * 8 + e * 8);
                 if (!dry && pos + bytes + 16 > cap) return fail(USC_ERR_VALUE, "pack buffer too small");
                 if (!dry) {
-                    std::memcpy(hdr, runs.data(), (size_t)DT * 8);
+                    std::memcpy(b, runs.data(), (size_t)DT * 8);
                     char *ents = b + (int64_t)DT * 8;
                     std::memset(ents, 0, (size_t)(bytes - (int64_t)DT * 8));
                     for (int64_t i = 0; i < (int64_t)out.size(); ++i) {
@@ -670,8 +704,10 @@ int usc_pack(const usc_plan *pl, const int64_t *row_ptr, const int64_t *col, con
                 worst = std::max(worst, bytes + 16);
                 pos += bytes;
             }
+        if (!dry) {
+            blk[nb] = (int32_t)pos;
+            std::memcpy(perm, slot.data(), slot.size() * 4);
         }
-        if (!dry) blk[nb] = (int32_t)pos;
         *n_entries = dry ? worst : total;
         if (!dry && worst > pl->ent_stage_bytes)
             return fail(USC_ERR_VALUE, "entry block of %lld bytes exceeds the %d-byte stage reserve",

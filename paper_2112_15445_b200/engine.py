@@ -309,9 +309,10 @@ def tile_candidates(geometry: ConvGeometry, n: int, sb_values, precision=Precisi
             for ws in (w for w in range(1, nw + 1) if nw % w == 0):
                 if ws > strips:
                     break
-                out.append(ExecConfig(sub_batch=min(sb_values), pix_per_thread=pc, rows_per_thread=pr,
-                                      ch_per_cta=dw * (nw // ws), kernel=3, threads=nw * 32,
-                                      pixel_warps=ws, stages=2))
+                for st in (2, 3):
+                    out.append(ExecConfig(sub_batch=min(sb_values), pix_per_thread=pc, rows_per_thread=pr,
+                                          ch_per_cta=dw * (nw // ws), kernel=3, threads=nw * 32,
+                                          pixel_warps=ws, stages=st))
     if 1 in kernels:
         ps = [p for p in (2, 4, 8) if p <= max(2, yw)]
         for sb in sb_values:
