@@ -57,16 +57,17 @@ typedef struct usc_geometry {
  *  interleave == 0  "padded NCHW": [n][C][Hp][Ws], zero halo (pad_h, pad_w), row
  *                   stride Ws rounded up to a multiple of 16 bytes;
  *                   element (b,c,y,x) at ((b*C + c)*Hp + y+pad_h)*Ws + x+pad_w.
- *  interleave == 32 "batch-interleaved" (BI32): [ceil(n/32)][C][Hp][Wp][32], zero
- *                   halo, 32 samples innermost so one warp reads one 128-byte
- *                   line per pixel; element (b,c,y,x) at
- *                   (((b/32*C + c)*Hp + y+pad_h)*Wp + x+pad_w)*32 + b%32.
- * sample_stride is the stride of one sample (il 0) or one 32-sample block (il 32). */
+ *  interleave == IL "batch-interleaved" (BI32 / BI64, IL = 32 or 64):
+ *                   [ceil(n/IL)][C][Hp][Wp][IL], zero halo, IL samples innermost so
+ *                   a warp reads one (BI32) or two (BI64, two samples per lane)
+ *                   128-byte lines per pixel; element (b,c,y,x) at
+ *                   (((b/IL*C + c)*Hp + y+pad_h)*Wp + x+pad_w)*IL + b%IL.
+ * sample_stride is the stride of one sample (il 0) or one IL-sample block. */
 typedef struct usc_act_layout {
     int32_t channels, height, width;   /* logical (unpadded) plane */
     int32_t pad_h, pad_w;              /* halo */
     int32_t hp, ws;                    /* padded height, padded (+aligned for il 0) row stride */
-    int32_t interleave;                /* 0 or 32 */
+    int32_t interleave;                /* 0, 32 or 64 */
     int64_t sample_stride;             /* elements per sample (il 0) / per 32-sample block (il 32) */
 } usc_act_layout;
 
@@ -78,7 +79,8 @@ typedef struct usc_exec_cfg {
     int32_t worker_count;     /* accepted for API parity; the GPU ignores it */
     int32_t pix_per_thread;   /* P: consecutive output pixels per thread (1,2,4,8) */
     int32_t ch_per_cta;       /* DT: output channels per CTA (4,8,16,32) */
-    int32_t samples_per_cta;  /* NS: samples per CTA (full-map tiles) */
+    int32_t samples_per_cta;  /* NS: samples per CTA (kernel 1: full-map tiles; kernel 3: the
+                               * interleave, 32 = BI32 or 64 = BI64) */
     int32_t chunk_channels;   /* CC: input channels per shared-memory stage */
     int32_t threads;          /* kernel 1: threads per CTA (128/256); kernel 3: compute threads
                                * (256/384/512 = 8/12/16 compute warps, + 1 producer warp) */
@@ -177,8 +179,9 @@ int usc_csr_to_dense(const usc_geometry *g, const int64_t *row_ptr, const int64_
 int usc_plan_make(const usc_geometry *g, int32_t n, int32_t dtype, const usc_exec_cfg *cfg,
                   usc_plan *out);
 /* The batch-interleaved kernel's compiled tile instances: writes up to max_count
- * records of 5 int32 (compute warps, PC, PR, DW, stride_w) and returns the total
- * count.  The autotuner's kernel-3 search space (threads = warps*32). */
+ * records of 6 int32 (compute warps, PC, PR, DW, stride_w, samples per lane) and
+ * returns the total count.  The autotuner's kernel-3 search space (threads =
+ * warps*32, samples_per_cta = 32*samples per lane). */
 int usc_bi_instances(int32_t *out, int32_t max_count);
 int usc_pack_size(const usc_plan *plan, int64_t n_nz, int64_t *bytes);
 int usc_pack(const usc_plan *plan, const int64_t *row_ptr, const int64_t *col_offsets,

@@ -129,13 +129,14 @@ def lib():
     return _lib
 
 
-def bi_instances() -> list[tuple[int, int, int, int, int]]:
-    """The batch-interleaved kernel's compiled tiles: (compute warps, PC, PR, DW, stride_w)."""
+def bi_instances() -> list[tuple[int, int, int, int, int, int]]:
+    """The batch-interleaved kernel's compiled tiles: (compute warps, PC, PR, DW,
+    stride_w, samples per lane)."""
     L = lib()
     n = L.usc_bi_instances(None, 0)
-    buf = (c_i32 * (5 * n))()
+    buf = (c_i32 * (6 * n))()
     L.usc_bi_instances(buf, n)
-    return [tuple(buf[5 * i:5 * i + 5]) for i in range(n)]
+    return [tuple(buf[6 * i:6 * i + 6]) for i in range(n)]
 
 
 def check(rc: int, what: str = ""):

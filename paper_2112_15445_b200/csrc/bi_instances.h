@@ -1,20 +1,25 @@
 // bi_instances.h -- the k_bi tile instances compiled into the library, one list
-// per compute-warp count.  X(PC, PR, DW, SW): a thread's pixel block is PR rows x
-// PC columns (column stride SW), DW output channels per warp.  The planner
-// (host.cpp) and the launchers (conv_bi_w*.cu) both expand these lists, so they
-// cannot disagree.  DW*PC*PR accumulators must fit the register cap of the warp
-// count: 168 (8 compute warps), 128 (12), 96 (16).
+// per compute-warp count.  X(PC, PR, DW, SW, SPL): a thread's pixel block is PR rows
+// x PC columns (column stride SW), DW output channels per warp, SPL samples per lane
+// (1: BI32 layout, 2: BI64).  The planner (host.cpp) and the launchers
+// (conv_bi_w*.cu) both expand these lists, so they cannot disagree.  SPL*DW*PC*PR
+// accumulator registers must fit the register cap of the warp count: 168 (8 compute
+// warps), 128 (12), 96 (16).
 #pragma once
 
-#define USC_BI_W8(X)                                                                       \
-    X(4, 2, 8, 1) X(8, 2, 4, 1) X(8, 1, 8, 1) X(4, 2, 16, 1) X(8, 2, 8, 1) X(4, 1, 16, 1) \
-    X(2, 2, 16, 1) X(8, 1, 16, 1) X(2, 2, 8, 1) X(1, 1, 16, 1) X(2, 2, 4, 1) X(2, 2, 2, 1)  \
-    X(2, 1, 4, 1) X(1, 1, 4, 1) X(4, 1, 8, 2) X(8, 1, 8, 2)
+#define USC_BI_W8(X)                                                                                      \
+    X(4, 2, 8, 1, 1) X(8, 2, 4, 1, 1) X(8, 1, 8, 1, 1) X(4, 2, 16, 1, 1) X(8, 2, 8, 1, 1) X(4, 1, 16, 1, 1) \
+    X(2, 2, 16, 1, 1) X(8, 1, 16, 1, 1) X(2, 2, 8, 1, 1) X(1, 1, 16, 1, 1) X(2, 2, 4, 1, 1)                \
+    X(2, 2, 2, 1, 1) X(2, 1, 4, 1, 1) X(1, 1, 4, 1, 1) X(4, 1, 8, 2, 1) X(8, 1, 8, 2, 1)                  \
+    X(4, 2, 4, 1, 2) X(8, 1, 4, 1, 2) X(2, 2, 8, 1, 2) X(4, 2, 8, 1, 2) X(8, 2, 4, 1, 2) X(2, 2, 4, 1, 2)   \
+    X(4, 1, 8, 1, 2) X(2, 1, 8, 1, 2) X(1, 1, 8, 1, 2) X(2, 2, 2, 1, 2) X(4, 1, 4, 2, 2)
 
-#define USC_BI_W12(X)                                                                     \
-    X(4, 2, 8, 1) X(8, 2, 4, 1) X(8, 1, 8, 1) X(2, 2, 16, 1) X(4, 1, 16, 1) X(2, 2, 8, 1) \
-    X(4, 2, 4, 1) X(8, 1, 4, 1) X(2, 1, 16, 1) X(4, 1, 8, 2)
+#define USC_BI_W12(X)                                                                                     \
+    X(4, 2, 8, 1, 1) X(8, 2, 4, 1, 1) X(8, 1, 8, 1, 1) X(2, 2, 16, 1, 1) X(4, 1, 16, 1, 1) X(2, 2, 8, 1, 1) \
+    X(4, 2, 4, 1, 1) X(8, 1, 4, 1, 1) X(2, 1, 16, 1, 1) X(4, 1, 8, 2, 1)                                   \
+    X(4, 2, 4, 1, 2) X(2, 2, 8, 1, 2) X(8, 1, 4, 1, 2) X(2, 2, 4, 1, 2) X(4, 1, 4, 1, 2)
 
-#define USC_BI_W16(X)                                                                     \
-    X(2, 2, 8, 1) X(4, 2, 4, 1) X(2, 2, 4, 1) X(4, 1, 8, 1) X(8, 1, 4, 1) X(1, 1, 16, 1) \
-    X(2, 1, 16, 1) X(1, 2, 16, 1) X(2, 2, 2, 1) X(4, 1, 4, 2) X(2, 1, 8, 2) X(1, 1, 8, 2)
+#define USC_BI_W16(X)                                                                                     \
+    X(2, 2, 8, 1, 1) X(4, 2, 4, 1, 1) X(2, 2, 4, 1, 1) X(4, 1, 8, 1, 1) X(8, 1, 4, 1, 1) X(1, 1, 16, 1, 1) \
+    X(2, 1, 16, 1, 1) X(1, 2, 16, 1, 1) X(2, 2, 2, 1, 1) X(4, 1, 4, 2, 1) X(2, 1, 8, 2, 1) X(1, 1, 8, 2, 1) \
+    X(2, 2, 4, 1, 2) X(4, 1, 4, 1, 2) X(2, 2, 2, 1, 2) X(4, 2, 2, 1, 2) X(1, 1, 8, 1, 2)

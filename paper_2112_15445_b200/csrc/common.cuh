@@ -71,7 +71,7 @@ struct Epi {
     int relu, saturate, saturate2, out_padded;
     float cap, cap2, scale;
     int oHp, oWs, oph, opw, oil, pool;
-    long long o_sample_stride;  // elements per sample (il 0) / 32-sample block (il 32)
+    long long o_sample_stride;  // elements per sample (il 0) / interleave block (il 32, 64)
 };
 
 // Apply the stored entries [e0, e1) of one output channel to P pixels.
@@ -144,11 +144,11 @@ __device__ __forceinline__ void store_one(typename Kind<KIND>::TY *y, long long 
 // element offset of logical (b, c, y, x) in an activation layout
 struct LayoutD {
     int C, Hp, Ws, ph, pw, il;
-    long long ss;  // sample (il 0) / block (il 32) stride
+    long long ss;  // sample (il 0) / block (il 32, 64) stride
 };
 __device__ __forceinline__ long long lay_index(const LayoutD &L, long long b, int c, int y, int x) {
-    if (L.il == 32)
-        return (b >> 5) * L.ss + ((((long long)c * L.Hp + y + L.ph) * L.Ws + x + L.pw) << 5) + (b & 31);
+    if (L.il)
+        return (b / L.il) * L.ss + (((long long)c * L.Hp + y + L.ph) * L.Ws + x + L.pw) * L.il + b % L.il;
     return b * L.ss + ((long long)c * L.Hp + y + L.ph) * L.Ws + x + L.pw;
 }
 inline LayoutD to_dev(const usc_act_layout &l) {

@@ -242,16 +242,16 @@ __global__ void k_pad_any(const T *__restrict__ src, T *__restrict__ dst, int n,
          i += (long long)gridDim.x * blockDim.x) {
         long long t = i;
         int lane = 0;
-        if (L.il == 32) {
-            lane = static_cast<int>(t & 31);
-            t >>= 5;
+        if (L.il) {
+            lane = static_cast<int>(t % L.il);
+            t /= L.il;
         }
         const int x = static_cast<int>(t % L.Ws);
         t /= L.Ws;
         const int y = static_cast<int>(t % L.Hp);
         t /= L.Hp;
         const int c = static_cast<int>(t % L.C);
-        const long long b = L.il == 32 ? (t / L.C) * 32 + lane : t / L.C;
+        const long long b = L.il ? (t / L.C) * L.il + lane : t / L.C;
         const int iy = y - L.ph, ix = x - L.pw;
         T v{};
         if (b < n && iy >= 0 && iy < H && ix >= 0 && ix < W) v = src[((b * L.C + c) * H + iy) * W + ix];
@@ -294,7 +294,7 @@ __global__ void k_h2f(const __half *__restrict__ src, float *__restrict__ dst, l
 
 // nn.MaxPool2.forward (nn.py:124-135): value at np.argmax of the 2x2 window in
 // order (0,0),(0,1),(1,0),(1,1) -- first NaN if any, else first maximum.
-// Works between any two layouts; output-ordered (lane fastest for BI32).
+// Works between any two layouts; output-ordered (sample fastest for BI layouts).
 template <typename T>
 __global__ void k_maxpool2(const T *__restrict__ src, T *__restrict__ dst, int n_total, int C, int OH,
                            int OW, const LayoutD Li, const LayoutD Lo) {
@@ -303,16 +303,16 @@ __global__ void k_maxpool2(const T *__restrict__ src, T *__restrict__ dst, int n
          i += (long long)gridDim.x * blockDim.x) {
         long long t = i;
         int lane = 0;
-        if (Lo.il == 32) {
-            lane = static_cast<int>(t & 31);
-            t >>= 5;
+        if (Lo.il) {
+            lane = static_cast<int>(t % Lo.il);
+            t /= Lo.il;
         }
         const int x = static_cast<int>(t % OW);
         t /= OW;
         const int y = static_cast<int>(t % OH);
         t /= OH;
         const int c = static_cast<int>(t % C);
-        const long long b = Lo.il == 32 ? (t / C) * 32 + lane : t / C;
+        const long long b = Lo.il ? (t / C) * Lo.il + lane : t / C;
         const long long p00 = lay_index(Li, b, c, 2 * y, 2 * x);
         const long long p01 = lay_index(Li, b, c, 2 * y, 2 * x + 1);
         const long long p10 = lay_index(Li, b, c, 2 * y + 1, 2 * x);
@@ -655,7 +655,8 @@ int usc_maxpool2(const usc_act_layout *in_l, const usc_act_layout *out_l, int32_
     if (in_l->interleave != out_l->interleave)
         return fail(USC_ERR_VALUE, "maxpool layouts must share the interleave");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    const int n_total = out_l->interleave == 32 ? (n + 31) / 32 * 32 : n;
+    const int il = out_l->interleave;
+    const int n_total = il ? (n + il - 1) / il * il : n;
     const long long total = (long long)n_total * in_l->channels * OH * OW;
     const LayoutD Li = to_dev(*in_l), Lo = to_dev(*out_l);
     if (dtype == USC_F32) {

@@ -1,7 +1,23 @@
-// conv_bi.cu -- host-side launcher of the batch-interleaved kernel (conv_bi.cuh).
+// conv_bi.cu -- host-side launcher of the batch-interleaved kernel (conv_bi.cuh):
+// builds the TMA tensor map of the input and the kernel arguments.
+#include <cudaTypedefs.h>
+
 #include "conv_bi.cuh"
 
 namespace usc {
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link)
+static PFN_cuTensorMapEncodeTiled_v12000 encode_tiled() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
 
 int launch_bi(const usc_plan *pl, const void *blob, const void *x, void *y, const usc_dev::Epi &ep,
               cudaStream_t st) {
@@ -10,23 +26,35 @@ int launch_bi(const usc_plan *pl, const void *blob, const void *x, void *y, cons
     const char *cb = static_cast<const char *>(blob);
     const long long nb = (long long)pl->groups * pl->n_chunks;
     const long long cp_bytes = (4 * (nb + 1) + 15) / 16 * 16;
-    usc_bi::BiArgs a{};
-    a.x = static_cast<const float *>(x);
-    a.y = static_cast<float *>(y);
     const long long perm_bytes = (4LL * pl->groups * pl->DT + 15) / 16 * 16;
+    const int IL = pl->in.interleave;
+    if (IL != 32 && IL != 64) return fail(USC_ERR_VALUE, "BI plan needs a 32/64-interleaved input");
+    usc_bi::BiArgs a{};
+    // x: [Nb][C][Hp][Wp][IL] fp32; TMA dims innermost first, box = one chunk's tile
+    auto enc = encode_tiled();
+    if (!enc) return fail(USC_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    const cuuint64_t dims[5] = {(cuuint64_t)IL, (cuuint64_t)pl->in.ws, (cuuint64_t)pl->in.hp,
+                                (cuuint64_t)pl->g.in_channels, (cuuint64_t)((pl->n + IL - 1) / IL)};
+    const cuuint64_t px = (cuuint64_t)IL * 4;
+    const cuuint64_t strides[4] = {px, px * pl->in.ws, px * pl->in.ws * pl->in.hp,
+                                   px * pl->in.ws * pl->in.hp * pl->g.in_channels};
+    const cuuint32_t box[5] = {(cuuint32_t)IL, (cuuint32_t)pl->TWs, (cuuint32_t)pl->HS, (cuuint32_t)pl->CC, 1};
+    const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+    CUresult r = enc(&a.xmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, const_cast<void *>(x), dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(USC_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    a.y = static_cast<float *>(y);
     a.blk = reinterpret_cast<const int *>(cb + 64);
     a.perm = reinterpret_cast<const int *>(cb + 64 + cp_bytes);
     a.blocks = cb + 64 + cp_bytes + perm_bytes;
     a.N = pl->n;
-    a.C = pl->g.in_channels;
     a.D = pl->g.out_channels;
     a.n_chunks = pl->n_chunks;
     a.CC = pl->CC;
     a.DT = pl->DT;
     a.HS = pl->HS;
     a.TWs = pl->TWs;
-    a.Hp = pl->in.hp;
-    a.Wp = pl->in.ws;
     a.Yh = pl->out_h;
     a.Yw = pl->out_w;
     a.s_h = pl->g.stride_h;
@@ -39,8 +67,6 @@ int launch_bi(const usc_plan *pl, const void *blob, const void *x, void *y, cons
     a.G = pl->groups;
     a.tiles = pl->groups * pl->sample_tiles * pl->row_tiles * pl->col_tiles;
     a.S = pl->stages;
-    a.full_rows = (pl->col_tiles == 1 && pl->TWs == pl->in.ws) ? 1 : 0;
-    a.x_blk_stride = pl->in.sample_stride;
     a.x_stage_bytes = static_cast<int>(pl->smem_stage_bytes);
     a.stage_bytes = static_cast<int>(pl->smem_stage_bytes + pl->ent_stage_bytes);
     a.ep = ep;

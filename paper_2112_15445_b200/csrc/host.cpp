@@ -80,7 +80,7 @@ int usc_geometry_out(const usc_geometry *g, int32_t *out_h, int32_t *out_w) {
 int usc_act_layout_make(int32_t channels, int32_t h, int32_t w, int32_t ph, int32_t pw,
                         int32_t eb, int32_t il, usc_act_layout *out) {
     if (channels < 1 || h < 1 || w < 1 || ph < 0 || pw < 0 || (eb != 1 && eb != 2 && eb != 4) ||
-        (il != 0 && il != 32))
+        (il != 0 && il != 32 && il != 64))
         return fail(USC_ERR_VALUE, "bad activation layout");
     out->channels = channels;
     out->height = h;
@@ -94,14 +94,14 @@ int usc_act_layout_make(int32_t channels, int32_t h, int32_t w, int32_t ph, int3
         out->ws = (w + 2 * pw + per16 - 1) / per16 * per16;
         out->sample_stride = (int64_t)channels * out->hp * out->ws;
     } else {
-        out->ws = w + 2 * pw;  // a pixel is 32*eb >= 32 bytes: always 16-B aligned
-        out->sample_stride = (int64_t)channels * out->hp * out->ws * 32;
+        out->ws = w + 2 * pw;  // a pixel is il*eb >= 32 bytes: always 16-B aligned
+        out->sample_stride = (int64_t)channels * out->hp * out->ws * il;
     }
     return USC_OK;
 }
 
 int64_t usc_act_layout_elems(const usc_act_layout *l, int32_t n) {
-    if (l->interleave == 32) return (int64_t)((n + 31) / 32) * l->sample_stride;
+    if (l->interleave) return (int64_t)((n + l->interleave - 1) / l->interleave) * l->sample_stride;
     return (int64_t)n * l->sample_stride;
 }
 
@@ -226,9 +226,9 @@ static int pow2_floor(int v) {
 }
 
 // The k_bi instances compiled into the library (bi_instances.h).
-static bool bi_instance(int PC, int PR, int DW, int NW, int SW) {
-#define X(PC_, PR_, DW_, SW_) \
-    if (PC == PC_ && PR == PR_ && DW == DW_ && SW == SW_) return true;
+static bool bi_instance(int PC, int PR, int DW, int NW, int SW, int SPL) {
+#define X(PC_, PR_, DW_, SW_, SPL_) \
+    if (PC == PC_ && PR == PR_ && DW == DW_ && SW == SW_ && SPL == SPL_) return true;
     if (NW == 8) {
         USC_BI_W8(X)
     } else if (NW == 12) {
@@ -242,14 +242,15 @@ static bool bi_instance(int PC, int PR, int DW, int NW, int SW) {
 
 int usc_bi_instances(int32_t *out, int32_t max_count) {
     int n = 0;
-#define X(PC_, PR_, DW_, SW_)                                  \
+#define X(PC_, PR_, DW_, SW_, SPL_)                             \
     if (n < max_count && out) {                                \
-        int32_t *o = out + 5 * n;                              \
+        int32_t *o = out + 6 * n;                              \
         o[0] = NW_;                                            \
         o[1] = PC_;                                            \
         o[2] = PR_;                                            \
         o[3] = DW_;                                            \
         o[4] = SW_;                                            \
+        o[5] = SPL_;                                           \
     }                                                          \
     ++n;
     {
@@ -296,8 +297,13 @@ int usc_plan_make(const usc_geometry *g0, int32_t n, int32_t dtype, const usc_ex
     const int eb = elem_bytes(dtype);
     int kernel = c.kernel ? c.kernel : (dtype == USC_F32 ? 3 : 1);
     if (g.stride_w > 2) kernel = 2;
-    rc = usc_act_layout_make(g.in_channels, g.input_h, g.input_w, g.pad_h, g.pad_w, eb,
-                             kernel == 3 ? 32 : 0, &pl->in);
+    // kernel 3 sample interleave: samples_per_cta 32 (BI32) or 64 (BI64, two samples per
+    // lane); default BI64 once the batch fills two 32-sample blocks
+    int IL = 0;
+    if (kernel == 3) {
+        IL = (c.samples_per_cta == 32 || c.samples_per_cta == 64) ? c.samples_per_cta : (n > 32 ? 64 : 32);
+    }
+    rc = usc_act_layout_make(g.in_channels, g.input_h, g.input_w, g.pad_h, g.pad_w, eb, IL, &pl->in);
     if (rc) return rc;
     const int Yh = pl->out_h, Yw = pl->out_w, Ws = pl->in.ws;
     const int threads = (c.threads == 128 || c.threads == 256) ? c.threads : 256;
@@ -347,7 +353,7 @@ int usc_plan_make(const usc_geometry *g0, int32_t n, int32_t dtype, const usc_ex
                 return fail(USC_ERR_VALUE, "ch_per_cta %d not a multiple of %d channel warps", c.ch_per_cta, wc);
             for (int dw : {8, 16, 4}) {
                 if (c.ch_per_cta) dw = c.ch_per_cta / wc;
-                if (bi_instance(PC, PR, dw, nw, g.stride_w)) {
+                if (bi_instance(PC, PR, dw, nw, g.stride_w, IL / 32)) {
                     NW = nw, WS = ws, WC = wc, DW = dw;
                     break;
                 }
@@ -369,7 +375,9 @@ int usc_plan_make(const usc_geometry *g0, int32_t n, int32_t dtype, const usc_ex
             if (sprt > SPR || (tsr > SR && tsr > 1)) continue;
             const int64_t tiles = (int64_t)((SR + tsr - 1) / tsr) * ((SPR + sprt - 1) / sprt);
             const int ct = (SPR + sprt - 1) / sprt;
-            const int tws = (ct == 1 && SPR * PC == Yw) ? pl->in.ws : (sprt * PC - 1) * g.stride_w + g.filter_w;
+            const int tws = (ct == 1 && SPR * PC == Yw && pl->in.ws <= 256) ? pl->in.ws
+                                                                             : (sprt * PC - 1) * g.stride_w + g.filter_w;
+            if (tws > 256 || (int64_t)(tsr * PR - 1) * g.stride_h + g.filter_h > 256) continue;  // TMA box
             const int64_t foot = tiles * ((int64_t)(tsr * PR - 1) * g.stride_h + g.filter_h) * tws;
             if (tiles < best_tiles || (tiles == best_tiles && foot < best_foot)) {
                 best_tiles = tiles;
@@ -382,13 +390,13 @@ int usc_plan_make(const usc_geometry *g0, int32_t n, int32_t dtype, const usc_ex
             return fail(USC_ERR_VALUE, "%d pixel warps do not tile a %dx%d strip grid", WS, SR, SPR);
         const int TH = TSR * PR;  // output rows per tile
         const int col_tiles = (SPR + SPRt - 1) / SPRt;
-        const bool full_rows = (col_tiles == 1 && SPR * PC == Yw);
+        const bool full_rows = (col_tiles == 1 && SPR * PC == Yw && pl->in.ws <= 256);
         const int TWs = full_rows ? pl->in.ws : (SPRt * PC - 1) * g.stride_w + g.filter_w;
         const int HS = (TH - 1) * g.stride_h + g.filter_h;
-        const int64_t per_ch = (int64_t)HS * TWs * 32 * eb;
+        const int64_t per_ch = (int64_t)HS * TWs * IL * eb;  // one channel of the TMA box
         const int DT = WC * DW;
         int CC = c.chunk_channels ? c.chunk_channels : 64;
-        CC = std::min(CC, g.in_channels);
+        CC = std::min(std::min(CC, g.in_channels), 256);
         const int S = c.stages ? std::max(2, std::min(4, c.stages)) : 2;
         const int64_t budget = 200 * 1024;
         // per-stage entry block: hdr DT*8 + runs padded to even (16-B aligned starts) +
@@ -413,7 +421,7 @@ int usc_plan_make(const usc_geometry *g0, int32_t n, int32_t dtype, const usc_ex
         pl->WC = WC;
         pl->DW = DW;
         pl->DT = DT;
-        pl->NS = 32;
+        pl->NS = IL;
         pl->CC = CC;
         pl->TH = TH;
         pl->HS = HS;
@@ -423,7 +431,7 @@ int usc_plan_make(const usc_geometry *g0, int32_t n, int32_t dtype, const usc_ex
         pl->threads = NW * 32;
         pl->strips_per_row = SPR;
         pl->row_tiles = (Yh + TH - 1) / TH;
-        pl->sample_tiles = (n + 31) / 32;
+        pl->sample_tiles = (n + IL - 1) / IL;
         pl->groups = (g.out_channels + DT - 1) / DT;
         pl->n_chunks = (g.in_channels + CC - 1) / CC;
         pl->smem_stage_bytes = stage;
@@ -600,8 +608,8 @@ int usc_pack(const usc_plan *pl, const int64_t *row_ptr, const int64_t *col, con
         const int64_t cl = c - (c / CC) * CC;
         if (pl->kernel == 1)
             *off = cl * cs_tiled + kh * Ws + kw;
-        else if (pl->kernel == 3)  // byte offset in the [CC][HS][TWs][32] f32 stage
-            *off = ((cl * pl->HS + kh) * pl->TWs + kw) * 128;
+        else if (pl->kernel == 3)  // byte offset in the [CC][HS][TWs][IL] f32 stage
+            *off = ((cl * pl->HS + kh) * pl->TWs + kw) * 4 * pl->in.interleave;
         else
             *off = (c * Hp + kh) * Ws + kw;
         if (*off >= max_off || *off > INT32_MAX)

@@ -302,8 +302,8 @@ def tile_candidates(geometry: ConvGeometry, n: int, sb_values, precision=Precisi
         # that leave pixel warps idle
         yh = geometry.out_h if geometry.input_w != 1 else geometry.out_w
         sw = geometry.stride[1] if geometry.input_w != 1 else geometry.stride[0]
-        for nw, pc, pr, dw, isw in _lib.bi_instances():
-            if isw != sw or pc > max(1, yw) and pc > 1 or pr > yh:
+        for nw, pc, pr, dw, isw, spl in _lib.bi_instances():
+            if isw != sw or pc > max(1, yw) and pc > 1 or pr > yh or (spl == 2 and n <= 32):
                 continue
             strips = -(-yh // pr) * -(-yw // pc)
             for ws in (w for w in range(1, nw + 1) if nw % w == 0):
@@ -312,7 +312,7 @@ def tile_candidates(geometry: ConvGeometry, n: int, sb_values, precision=Precisi
                 for st in (2, 3):
                     out.append(ExecConfig(sub_batch=min(sb_values), pix_per_thread=pc, rows_per_thread=pr,
                                           ch_per_cta=dw * (nw // ws), kernel=3, threads=nw * 32,
-                                          pixel_warps=ws, stages=st))
+                                          pixel_warps=ws, stages=st, samples_per_cta=32 * spl))
     if 1 in kernels:
         ps = [p for p in (2, 4, 8) if p <= max(2, yw)]
         for sb in sb_values:

@@ -49,10 +49,13 @@ def vgg16_weights(rng, sparsity: float, precision=PrecisionMode.BINARY32, unifie
     return [synthesize_masked_weights(g, sparsity, rng, precision, unified) for g in vgg16_geometries()]
 
 
-def _cfg_of(plan, cfg: ExecConfig) -> ExecConfig:
-    """The config a network layer is planned with (its kernel family pinned)."""
+def _cfg_of(plan, cfg: ExecConfig, il: int = 0) -> ExecConfig:
+    """The config a network layer is planned with (its kernel family and, for the
+    batch-interleaved kernel, the network's sample interleave pinned)."""
     fields = {f: getattr(cfg, f) for f in cfg.__dataclass_fields__}
     fields["kernel"] = plan.kernel
+    if plan.kernel == 3 and il:
+        fields["samples_per_cta"] = il
     return ExecConfig(**fields)
 
 
@@ -106,7 +109,8 @@ class SparseVGG16:
         # input buffer of the first conv
         plans = [make_plan(g, n, self.dtype, c) for g, c in zip(self.geoms, self.configs)]
         # every layer reads the layout its plan wants: one interleave for the network
-        il = 32 if all(p.kernel == 3 for p in plans) else 0
+        # (BI32 or BI64, that of the first layer's plan)
+        il = plans[0].in_.interleave if all(p.kernel == 3 for p in plans) else 0
         if il == 0 and any(p.kernel == 3 for p in plans):
             plans = [make_plan(g, n, self.dtype, ExecConfig(c.sub_batch, c.worker_count, c.pix_per_thread,
                                                             c.ch_per_cta, c.samples_per_cta,
@@ -114,7 +118,7 @@ class SparseVGG16:
                                                             1 if c.kernel in (0, 3) else c.kernel))
                      for g, c in zip(self.geoms, self.configs)]
         self.interleave = il
-        plan_cfgs = [_cfg_of(p, c) for p, c in zip(plans, self.configs)]
+        plan_cfgs = [_cfg_of(p, c, il) for p, c in zip(plans, self.configs)]
         g0 = self.geoms[0]
         self.in_layout = _lib.act_layout(g0.in_channels, g0.input_h, g0.input_w, 1, 1, self.eb, il)
         self.x_buf = self._buf(self.in_layout)
@@ -231,8 +235,10 @@ class SparseVGG16:
             g = self.geoms[li]
             usable = [sb for sb in (1, 2, 4, 8, 16, 32) if self.batch % sb == 0]
             results = []
-            kern = (3,) if self.interleave == 32 else (1,)
-            cands = [self.configs[li]] + tile_candidates(g, self.batch, usable, self.precision, kern)
+            kern = (3,) if self.interleave else (1,)
+            cands = [_cfg_of(plan0, self.configs[li], self.interleave)] + [
+                c for c in tile_candidates(g, self.batch, usable, self.precision, kern)
+                if not self.interleave or c.samples_per_cta == self.interleave]
             if epi.pool:  # keep the pool fused: 2-row, even-width pixel blocks only
                 cands = [c for c in cands if c.rows_per_thread == 2 and c.pix_per_thread % 2 == 0]
             for cfg in cands:
