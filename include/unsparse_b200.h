@@ -90,6 +90,8 @@ typedef struct usc_exec_cfg {
     int32_t stages;           /* kernel 3: shared-memory ring depth (2..4) */
     int32_t rows_per_thread;  /* kernel 3: output rows per thread (1 or 2); pixels = rows x pix_per_thread */
     int32_t ent_reserve;      /* kernel 3: shared-memory bytes reserved per stage for CSR entries (0 auto) */
+    int32_t pixel_classes;    /* kernel 3, 1x1 pixel blocks: 1 = per-pixel-class entry runs that drop
+                               * the taps landing on the zero halo (exact for finite weights) */
 } usc_exec_cfg;
 
 /* Resolved plan for one (geometry, batch, dtype, cfg): tile shape, packing
@@ -111,6 +113,10 @@ typedef struct usc_plan {
     int32_t stages;              /* BI kernel: shared-memory ring depth */
     int32_t PR, PC;              /* BI kernel: a thread's pixel block = PR rows x PC columns (P = PR*PC) */
     int32_t transposed;          /* 1D layer (W==1) run as its H/W transpose */
+    int32_t ncls_r, ncls_c;      /* BI kernel: pixel classes (rows x columns with the same valid taps);
+                                  * 1 x 1 = no classes */
+    int32_t tail_full, tail_split;  /* BI kernel: tiles [0, tail_full) run whole, each later tile as
+                                     * tail_split slot-subset items (balances the last wave) */
     int64_t smem_stage_bytes, smem_bytes;
     int64_t grid_x, grid_y;
 } usc_plan;

@@ -42,7 +42,8 @@ class ActLayout(ctypes.Structure):
 class ExecCfg(ctypes.Structure):
     _fields_ = [(n, c_i32) for n in ("sub_batch", "worker_count", "pix_per_thread", "ch_per_cta",
                                      "samples_per_cta", "chunk_channels", "threads", "kernel",
-                                     "pixel_warps", "stages", "rows_per_thread", "ent_reserve")]
+                                     "pixel_warps", "stages", "rows_per_thread", "ent_reserve",
+                                     "pixel_classes")]
 
 
 class Plan(ctypes.Structure):
@@ -52,16 +53,18 @@ class Plan(ctypes.Structure):
                 ("strips_per_row", c_i32), ("row_tiles", c_i32), ("sample_tiles", c_i32),
                 ("groups", c_i32), ("n_chunks", c_i32), ("WS", c_i32), ("WC", c_i32), ("DW", c_i32),
                 ("SPRt", c_i32), ("col_tiles", c_i32), ("TWs", c_i32), ("ent_stage_bytes", c_i32), ("stages", c_i32), ("PR", c_i32), ("PC", c_i32),
-                ("transposed", c_i32),
+                ("transposed", c_i32), ("ncls_r", c_i32), ("ncls_c", c_i32), ("tail_full", c_i32),
+                ("tail_split", c_i32),
                 ("smem_stage_bytes", c_i64), ("smem_bytes", c_i64), ("grid_x", c_i64),
                 ("grid_y", c_i64)]
 
     def describe(self) -> dict:
-        return dict(kernel={1: "tiled", 2: "generic", 3: "bi32"}[self.kernel], P=self.P, DT=self.DT,
+        return dict(kernel={1: "tiled", 2: "generic", 3: f"bi{self.NS}"}[self.kernel], P=self.P, DT=self.DT,
                     NS=self.NS, CC=self.CC, TH=self.TH, threads=self.threads, WS=self.WS,
                     WC=self.WC, DW=self.DW, PR=self.PR, PC=self.PC, stages=self.stages,
                     grid=(self.grid_x, self.grid_y), smem_bytes=self.smem_bytes,
-                    n_chunks=self.n_chunks, transposed=bool(self.transposed))
+                    n_chunks=self.n_chunks, transposed=bool(self.transposed),
+                    pixel_classes=self.ncls_r * self.ncls_c, tail_split=self.tail_split)
 
 
 class Epilogue(ctypes.Structure):

@@ -21,8 +21,8 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_tiled() {
 
 int launch_bi(const usc_plan *pl, const void *blob, const void *x, void *y, const usc_dev::Epi &ep,
               cudaStream_t st) {
-    // blob = [64 B][int32 blk[G*n_chunks + 1]][int32 perm[G*DT]][blocks], each part 16-B
-    // aligned (usc_pack, kernel 3)
+    // blob = [64 B][int32 blk[G*n_chunks + 1]][int32 perm[G*DT]][int32 rowcls[Yh], colcls[Yw]]
+    // [blocks], each part 16-B aligned (usc_pack, kernel 3)
     const char *cb = static_cast<const char *>(blob);
     const long long nb = (long long)pl->groups * pl->n_chunks;
     const long long cp_bytes = (4 * (nb + 1) + 15) / 16 * 16;
@@ -47,7 +47,12 @@ int launch_bi(const usc_plan *pl, const void *blob, const void *x, void *y, cons
     a.y = static_cast<float *>(y);
     a.blk = reinterpret_cast<const int *>(cb + 64);
     a.perm = reinterpret_cast<const int *>(cb + 64 + cp_bytes);
-    a.blocks = cb + 64 + cp_bytes + perm_bytes;
+    const long long ctab_bytes = (4LL * (pl->out_h + pl->out_w) + 15) / 16 * 16;
+    a.rowcls = reinterpret_cast<const int *>(cb + 64 + cp_bytes + perm_bytes);
+    a.colcls = a.rowcls + pl->out_h;
+    a.ncls_c = pl->ncls_c > 0 ? pl->ncls_c : 1;
+    a.ncls = (pl->ncls_r > 0 ? pl->ncls_r : 1) * a.ncls_c;
+    a.blocks = cb + 64 + cp_bytes + perm_bytes + ctab_bytes;
     a.N = pl->n;
     a.D = pl->g.out_channels;
     a.n_chunks = pl->n_chunks;
@@ -67,6 +72,11 @@ int launch_bi(const usc_plan *pl, const void *blob, const void *x, void *y, cons
     a.G = pl->groups;
     a.tiles = pl->groups * pl->sample_tiles * pl->row_tiles * pl->col_tiles;
     a.S = pl->stages;
+    // tail split chosen by the planner (usc_plan_make): tiles [0, tail_full) whole,
+    // the rest as tail_split slot-subset items each
+    a.split = pl->tail_split > 1 ? pl->tail_split : 1;
+    a.tfull = a.split > 1 ? pl->tail_full : a.tiles;
+    a.items = a.tfull + a.split * (a.tiles - a.tfull);
     a.x_stage_bytes = static_cast<int>(pl->smem_stage_bytes);
     a.stage_bytes = static_cast<int>(pl->smem_stage_bytes + pl->ent_stage_bytes);
     a.ep = ep;

@@ -23,10 +23,12 @@
 //     output-channel slots of subgroup w / WS; DW*P accumulators per lane (SPL
 //     samples each) live for the whole input-channel loop; after a stage each warp
 //     arrives on empty[s] -- no CTA-wide barrier inside the loop;
-//   * entry block of one (group, chunk): int2 hdr[DT] = {first, end} entry index of
-//     every slot's run, then the runs, each starting 16-byte aligned so two entries
-//     are one LDS.128 broadcast.  Slots map to output channels through perm[]
-//     (the packer balances the warps' per-chunk work);
+//   * entry block of one (group, chunk): int2 hdr[NCLS][DT] = {first, end} entry
+//     index of every (pixel class, slot) run, then the runs, each starting 16-byte
+//     aligned so two entries are one LDS.128 broadcast.  Slots map to output
+//     channels through perm[] (the packer balances the warps' per-chunk work).  With
+//     pixel classes (1x1 pixel blocks on small maps) a pixel's run omits the taps that
+//     land on its zero halo: theta*0 adds +-0, a no-op for the never -0 accumulator;
 //   * the register budget sets NWC: warps are spread over 4 SM sub-partitions, so
 //     (NWC+1) warps leave 65536 / (4 * ceil((NWC+1)/4) * 32) registers per thread:
 //     168 for NWC = 8, 128 for NWC = 12, 96 for NWC = 16.
@@ -50,9 +52,12 @@ struct BiArgs {
     const int *blk;          // byte offset of every (group, chunk) block, G*n_chunks+1
     const int *perm;         // output channel of every (group, warp, slot); -1 = empty
     const char *blocks;      // block base (16-byte aligned)
+    const int *rowcls, *colcls;  // pixel class of every output row / column
+    int ncls, ncls_c;        // classes (runs per slot), column classes
     int N, D, n_chunks, CC, DT;
     int HS, TWs, Yh, Yw, s_h;
     int WS, WC, SPRt, TH, row_tiles, col_tiles, G, tiles, S;
+    int items, tfull, split;  // work items: tiles [0, tfull) whole, the rest split in `split` slot subsets
     int x_stage_bytes, stage_bytes;
     Epi ep;
 };
@@ -239,6 +244,19 @@ __device__ __forceinline__ float pool4(float w0, float w1, float w2, float w3) {
     return m;
 }
 
+// Work item -> (tile, slot part).  The last tiles of the schedule are split into
+// `split` interleaved slot subsets (part p runs slots dw % split == p) so the final
+// round of the persistent grid is not a partial wave of whole tiles.
+__device__ __forceinline__ int item_tile(const BiArgs &a, int it, int &part) {
+    if (it < a.tfull) {
+        part = -1;
+        return it;
+    }
+    const int j = it - a.tfull;
+    part = j % a.split;
+    return a.tfull + j / a.split;
+}
+
 template <int PC, int PR, int DW, int SW, int NWC, int SPL>
 __global__ void __launch_bounds__((NWC + 1) * 32, 1) k_bi(const __grid_constant__ BiArgs a) {
     constexpr int P = PC * PR;      // a thread's pixel block: PR rows x PC cols
@@ -269,8 +287,9 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1) k_bi(const __grid_constant_
             int s = 0;
             uint32_t ph = 1;
             const uint32_t xbytes = static_cast<uint32_t>(a.CC) * a.HS * a.TWs * PXB;  // full box
-            for (int t = blockIdx.x; t < a.tiles; t += gridDim.x) {
-                int q = t;
+            for (int it = blockIdx.x; it < a.items; it += gridDim.x) {
+                int part;
+                int q = item_tile(a, it, part);
                 const int g = q % a.G;
                 q /= a.G;
                 const int ct = q % a.col_tiles;
@@ -304,11 +323,12 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1) k_bi(const __grid_constant_
     const int tr = wsi / a.SPRt, tcs = wsi - tr * a.SPRt;  // strip-row, strip within the tile
     const uint32_t base = ((tr * PR * a.s_h) * a.TWs + tcs * PC * SW) * PXB + lane * 4 * SPL;
     const uint32_t rs = a.s_h * a.TWs * PXB;  // bytes between a thread's two pixel rows
-    const int hdr_bytes = a.DT * 8;
+    const int hdr_bytes = a.ncls * a.DT * 8;
     int s = 0;
     uint32_t ph = 0;
-    for (int t = blockIdx.x; t < a.tiles; t += gridDim.x) {
-        int q = t;
+    for (int it = blockIdx.x; it < a.items; it += gridDim.x) {
+        int part;
+        int q = item_tile(a, it, part);
         const int g = q % a.G;
         q /= a.G;
         const int ct = q % a.col_tiles;
@@ -317,6 +337,9 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1) k_bi(const __grid_constant_
         const int sb = q / a.row_tiles;
         const int r = rt * a.TH + tr * PR;
         const int col0 = (ct * a.SPRt + tcs) * PC;
+        // pixel class (1x1 blocks): selects the runs without this pixel's halo taps
+        const int cls = (a.ncls > 1 && r < a.Yh && col0 < a.Yw)
+                            ? __ldg(a.rowcls + r) * a.ncls_c + __ldg(a.colcls + col0) : 0;
 
         A acc[DW][P];
 #pragma unroll
@@ -330,10 +353,11 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1) k_bi(const __grid_constant_
             if (active) {
                 const uint32_t xs = st + base;  // this thread's first pixel, tap (0,0,0)
                 const uint32_t bp = st + a.x_stage_bytes;
-                const uint32_t hdr = bp + wc * DW * 8, E = bp + hdr_bytes;
+                const uint32_t hdr = bp + (cls * a.DT + wc * DW) * 8, E = bp + hdr_bytes;
 #pragma unroll
                 for (int dw = 0; dw < DW; ++dw) {
                     const int2 h = lds_v2(hdr + dw * 8);  // run [h.x, h.y), h.x even
+                    if (part >= 0 && dw % a.split != part) continue;
                     run_pairs<PC, PR, SW, SPL, PIPE>(acc[dw], xs, rs, E + h.x * 8, E + h.y * 8);
                 }
             }
@@ -384,6 +408,7 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1) k_bi(const __grid_constant_
         const bool relu = a.ep.relu != 0;
 #pragma unroll
         for (int dw = 0; dw < DW; ++dw) {
+            if (part >= 0 && dw % a.split != part) continue;
             const int d = __ldg(pm + dw);
             if (d < 0) continue;
             const long long od = obase + d * dstride;

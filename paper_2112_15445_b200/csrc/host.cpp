@@ -225,6 +225,25 @@ static int pow2_floor(int v) {
     return p;
 }
 
+// Pixel classes of one output axis: output index y reads padded input indices
+// y*stride + k (k < K); bit k of its mask is set when that index is inside the
+// image (not the zero halo).  Indices with equal masks form one class.
+static void tap_classes(int Y, int stride, int pad, int K, int X, std::vector<int> &cls,
+                        std::vector<uint32_t> &masks) {
+    cls.assign(Y, 0);
+    masks.clear();
+    for (int y = 0; y < Y; ++y) {
+        uint32_t m = 0;
+        for (int k = 0; k < K && k < 32; ++k) {
+            const int i = y * stride + k - pad;
+            if (i >= 0 && i < X) m |= 1u << k;
+        }
+        size_t id = std::find(masks.begin(), masks.end(), m) - masks.begin();
+        if (id == masks.size()) masks.push_back(m);
+        cls[y] = (int)id;
+    }
+}
+
 // The k_bi instances compiled into the library (bi_instances.h).
 static bool bi_instance(int PC, int PR, int DW, int NW, int SW, int SPL) {
 #define X(PC_, PR_, DW_, SW_, SPL_) \
@@ -395,6 +414,18 @@ int usc_plan_make(const usc_geometry *g0, int32_t n, int32_t dtype, const usc_ex
         const int HS = (TH - 1) * g.stride_h + g.filter_h;
         const int64_t per_ch = (int64_t)HS * TWs * IL * eb;  // one channel of the TMA box
         const int DT = WC * DW;
+        // per-pixel-class runs (1x1 pixel blocks): one entry run per (class, slot) without
+        // the taps that land on the zero halo
+        int ncr = 1, ncc = 1;
+        if (c.pixel_classes && PC == 1 && PR == 1 && g.filter_h <= 32 && g.filter_w <= 32) {
+            std::vector<int> cl;
+            std::vector<uint32_t> mk;
+            tap_classes(Yh, g.stride_h, g.pad_h, g.filter_h, g.input_h, cl, mk);
+            ncr = (int)mk.size();
+            tap_classes(Yw, g.stride_w, g.pad_w, g.filter_w, g.input_w, cl, mk);
+            ncc = (int)mk.size();
+        }
+        const int NCLS = ncr * ncc;
         int CC = c.chunk_channels ? c.chunk_channels : 64;
         CC = std::min(std::min(CC, g.in_channels), 256);
         const int S = c.stages ? std::max(2, std::min(4, c.stages)) : 2;
@@ -405,7 +436,8 @@ int usc_plan_make(const usc_geometry *g0, int32_t n, int32_t dtype, const usc_ex
         // exceeds it (the caller re-plans with the measured size).
         const int64_t R = c.ent_reserve ? c.ent_reserve : 24 * 1024;
         auto ent_bytes = [&](int cc) {
-            const int64_t worst = (int64_t)DT * 8 + ((int64_t)DT * cc * g.filter_h * g.filter_w + DT) * 8 + 16;
+            const int64_t worst =
+                (int64_t)NCLS * DT * 8 + NCLS * ((int64_t)DT * cc * g.filter_h * g.filter_w + DT) * 8 + 16;
             return (std::min(worst, R) + 127) / 128 * 128;
         };
         while (CC > 1 && S * ((CC * per_ch + 127) / 128 * 128 + ent_bytes(CC)) > budget) --CC;
@@ -414,6 +446,8 @@ int usc_plan_make(const usc_geometry *g0, int32_t n, int32_t dtype, const usc_ex
         if (S * (stage + ent_stage) + 128 > 224 * 1024)
             return fail(USC_ERR_VALUE, "BI tile does not fit shared memory");
         pl->kernel = 3;
+        pl->ncls_r = ncr;
+        pl->ncls_c = ncc;
         pl->P = P;
         pl->PR = PR;
         pl->PC = PC;
@@ -444,6 +478,38 @@ int usc_plan_make(const usc_geometry *g0, int32_t n, int32_t dtype, const usc_ex
         if (sms <= 0) sms = 148;
         pl->grid_x = std::min<int64_t>(tiles, sms);
         pl->grid_y = 1;
+        // last-wave balance: split the last R tiles into F interleaved slot subsets
+        // (F | DW) when that shortens the round-robin makespan (whole tile = 1 unit)
+        pl->tail_full = (int32_t)tiles;
+        pl->tail_split = 1;
+        {
+            const int64_t C = sms;
+            auto makespan = [&](int64_t R, int F) {
+                const int64_t full = tiles - R, nsplit = F * R;
+                double worst = 0;
+                for (int64_t c = 0; c < C; ++c) {
+                    const int64_t nf = full / C + (c < full % C);
+                    const int64_t cs = ((c - full) % C + C) % C;
+                    const int64_t ns = nsplit / C + (cs < nsplit % C);
+                    worst = std::max(worst, nf + ns / (double)F);
+                }
+                return worst;
+            };
+            double best = makespan(0, 1);
+            for (int F : {2, 4}) {
+                if (DW % F) continue;
+                for (int64_t R = 1; R <= std::min<int64_t>(tiles, C); ++R) {
+                    const double m = makespan(R, F);
+                    if (m < best - 1e-9) {
+                        best = m;
+                        pl->tail_full = (int32_t)(tiles - R);
+                        pl->tail_split = F;
+                    }
+                }
+            }
+            const int64_t items = pl->tail_full + (int64_t)pl->tail_split * (tiles - pl->tail_full);
+            pl->grid_x = std::min<int64_t>(items, sms);
+        }
         return USC_OK;
     }
     if (kernel == 1) {
@@ -535,9 +601,10 @@ int usc_pack_size(const usc_plan *pl, int64_t n_nz, int64_t *bytes) {
     if (pl->kernel == 3) {
         // [64 B][int32 blk[nb+1]][int32 perm[G*DT]][blocks: hdr int2[DT], runs padded to
         // even, 16-B rounded]
+        const int64_t ncls = std::max(1, pl->ncls_r * pl->ncls_c);
         *bytes = 64 + align16(4 * (nb + 1)) + align16(4 * (int64_t)pl->groups * pl->DT) +
-                 nb * ((int64_t)pl->DT * 8 + 16) +
-                 ((int64_t)pl->g.out_channels * n_nz + nb * pl->DT) * 8 + 64;
+                 align16(4 * ((int64_t)pl->out_h + pl->out_w)) + nb * (ncls * pl->DT * 8 + 16) +
+                 ncls * ((int64_t)pl->g.out_channels * n_nz + nb * pl->DT) * 8 + 64;
         return USC_OK;
     }
     int64_t cp = align16(4 * (nb * pl->DT + 1));
@@ -582,6 +649,7 @@ int usc_pack(const usc_plan *pl, const int64_t *row_ptr, const int64_t *col, con
     // tile), or off = -1 to drop it (a repeated zero-weight offset)
     const int64_t max_off = pl->dtype == USC_I8 ? (1 << 24) : (1 << 28);
     std::vector<int64_t> zero_seen;
+    int64_t dec_kh = 0, dec_kw = 0;  // tap of the last decoded entry (plan orientation)
     auto decode = [&](int64_t j, int64_t *cpos, int64_t *off) -> int {
         const int64_t lam = col[j];
         int64_t c = lam / plane0, rem = lam % plane0, kh = rem / Wp0, kw = rem % Wp0;
@@ -605,6 +673,8 @@ int usc_pack(const usc_plan *pl, const int64_t *row_ptr, const int64_t *col, con
             zero_seen.push_back(lam);
         }
         if (pl->transposed) std::swap(kh, kw);  // (c, kh, 0) -> (c, 0, kh)
+        dec_kh = kh;
+        dec_kw = kw;
         const int64_t cl = c - (c / CC) * CC;
         if (pl->kernel == 1)
             *off = cl * cs_tiled + kh * Ws + kw;
@@ -626,12 +696,26 @@ int usc_pack(const usc_plan *pl, const int64_t *row_ptr, const int64_t *col, con
         // stages-1 chunks ahead of the slowest, so per-chunk balance is what counts).
         const int64_t nb = (int64_t)G * NC;
         const int WC = pl->WC, DW = pl->DW;
+        const int NCLS = std::max(1, pl->ncls_r * pl->ncls_c);
         int32_t *blk = (int32_t *)((char *)blob + 64);
         int32_t *perm = (int32_t *)((char *)blob + 64 + align16(4 * (nb + 1)));
-        char *base = (char *)perm + align16(4 * (int64_t)G * DT);
+        int32_t *ctab = (int32_t *)((char *)perm + align16(4 * (int64_t)G * DT));  // rowcls[Yh], colcls[Yw]
+        char *base = (char *)ctab + align16(4 * ((int64_t)pl->out_h + pl->out_w));
         const int64_t cap = blob_bytes - (base - (char *)blob);
+        std::vector<int> rowcls(pl->out_h, 0), colcls(pl->out_w, 0);
+        std::vector<uint32_t> rmask(NCLS, ~0u), cmask(NCLS, ~0u);
+        // halo taps are dropped only when every weight is finite (theta*0 must be +-0)
+        bool finite = true;
+        if (pl->dtype == USC_F32 || pl->dtype == USC_F16)
+            for (int64_t j = 0; j < (int64_t)D * n_nz && finite; ++j)
+                finite = std::isfinite(((const float *)payload)[j]);
+        if (NCLS > 1 && finite) {
+            tap_classes(pl->out_h, g.stride_h, g.pad_h, g.filter_h, g.input_h, rowcls, rmask);
+            tap_classes(pl->out_w, g.stride_w, g.pad_w, g.filter_w, g.input_w, colcls, cmask);
+        }
         std::vector<std::vector<std::pair<int64_t, int64_t>>> per(D);  // (chunk, off) per d
         std::vector<std::vector<int64_t>> src(D);
+        std::vector<std::vector<uint16_t>> tap(D);  // kh << 8 | kw per entry
         std::vector<int64_t> cnt((size_t)D * NC, 0);
         for (int d = 0; d < D; ++d) {
             zero_seen.clear();
@@ -642,6 +726,7 @@ int usc_pack(const usc_plan *pl, const int64_t *row_ptr, const int64_t *col, con
                 if (off < 0) continue;
                 per[d].push_back({cpos / CC, off});
                 src[d].push_back(j);
+                tap[d].push_back((uint16_t)(dec_kh << 8 | dec_kw));
                 ++cnt[(size_t)d * NC + cpos / CC];
             }
         }
@@ -677,29 +762,39 @@ int usc_pack(const usc_plan *pl, const int64_t *row_ptr, const int64_t *col, con
                 blk[(int64_t)gi * NC + k] = (int32_t)pos;
                 char *b = base + pos;
                 int64_t e = 0;  // entry index after the header
-                std::vector<int32_t> runs(2 * DT);
+                std::vector<int32_t> runs(2 * (size_t)NCLS * DT);
                 std::vector<std::pair<int64_t, int64_t>> out;  // (off, j)
-                for (int dl = 0; dl < DT; ++dl) {
-                    if (e & 1) {
-                        out.push_back({-1, -1});  // alignment pad, never referenced
-                        ++e;
-                    }
-                    runs[2 * dl] = (int32_t)e;
-                    const int d = slot[(size_t)gi * DT + dl];
-                    if (d >= 0)
-                        for (size_t i = 0; i < per[d].size(); ++i)  // stored order within the chunk
-                            if (per[d][i].first == k) {
+                for (int cls = 0; cls < NCLS; ++cls) {
+                    const int ncc = std::max(1, pl->ncls_c);  // class = row class * ncc + column class
+                    const uint32_t rm = rmask[cls / ncc], cm = cmask[cls % ncc];
+                    for (int dl = 0; dl < DT; ++dl) {
+                        if (e & 1) {
+                            out.push_back({-1, -1});  // alignment pad, never referenced
+                            ++e;
+                        }
+                        const size_t h = (size_t)cls * DT + dl;
+                        runs[2 * h] = (int32_t)e;
+                        const int d = slot[(size_t)gi * DT + dl];
+                        if (d >= 0)
+                            for (size_t i = 0; i < per[d].size(); ++i) {  // stored order within the chunk
+                                if (per[d][i].first != k) continue;
+                                // a tap on this class's zero halo adds theta*0 = +-0: skipped
+                                // (exact: acc is never -0 and theta is finite)
+                                if (NCLS > 1 && !((rm >> (tap[d][i] >> 8)) & 1 && (cm >> (tap[d][i] & 255)) & 1))
+                                    continue;
                                 out.push_back({per[d][i].second, src[d][i]});
                                 ++e;
                             }
-                    runs[2 * dl + 1] = (int32_t)e;
+                        runs[2 * h + 1] = (int32_t)e;
+                    }
                 }
-                const int64_t bytes = align16((int64_t)DT * 8 + e * 8);
+                const int64_t hdr = (int64_t)NCLS * DT * 8;
+                const int64_t bytes = align16(hdr + e * 8);
                 if (!dry && pos + bytes + 16 > cap) return fail(USC_ERR_VALUE, "pack buffer too small");
                 if (!dry) {
-                    std::memcpy(b, runs.data(), (size_t)DT * 8);
-                    char *ents = b + (int64_t)DT * 8;
-                    std::memset(ents, 0, (size_t)(bytes - (int64_t)DT * 8));
+                    std::memcpy(b, runs.data(), (size_t)hdr);
+                    char *ents = b + hdr;
+                    std::memset(ents, 0, (size_t)(bytes - hdr));
                     for (int64_t i = 0; i < (int64_t)out.size(); ++i) {
                         if (out[i].first < 0) continue;
                         int32_t v[2];
@@ -715,6 +810,8 @@ int usc_pack(const usc_plan *pl, const int64_t *row_ptr, const int64_t *col, con
         if (!dry) {
             blk[nb] = (int32_t)pos;
             std::memcpy(perm, slot.data(), slot.size() * 4);
+            std::memcpy(ctab, rowcls.data(), rowcls.size() * 4);
+            std::memcpy(ctab + pl->out_h, colcls.data(), colcls.size() * 4);
         }
         *n_entries = dry ? worst : total;
         if (!dry && worst > pl->ent_stage_bytes)

@@ -47,6 +47,7 @@ class ExecConfig:
     stages: int = 0
     rows_per_thread: int = 0
     ent_reserve: int = 0
+    pixel_classes: int = 0
 
     def __post_init__(self):
         if self.sub_batch < 1:
@@ -62,7 +63,8 @@ class ExecConfig:
     def to_c(self) -> _lib.ExecCfg:
         return _lib.ExecCfg(self.sub_batch, self.worker_count, self.pix_per_thread, self.ch_per_cta,
                             self.samples_per_cta, self.chunk_channels, self.threads, self.kernel,
-                            self.pixel_warps, self.stages, self.rows_per_thread, self.ent_reserve)
+                            self.pixel_warps, self.stages, self.rows_per_thread, self.ent_reserve,
+                            self.pixel_classes)
 
 
 @dataclass(frozen=True)
@@ -101,31 +103,36 @@ def make_plan(geometry: ConvGeometry, n: int, dtype: int, config: ExecConfig | N
 def plan_for(filt: CsrFilter, n: int, dtype: int, config: ExecConfig | None, payload, table=None,
              device=None):
     """make_plan + device_pack.  For kernel-3 plans the shared-memory entry reserve is
-    sized from the filter itself (a dry-run pack measures its densest (group, chunk)
-    block), then the plan is remade with that reserve."""
+    sized from the filter itself: a plan at chunk length CC is packed dry to measure
+    its densest (group, chunk) block, then re-planned with exactly that reserve; when
+    input tile + entries no longer fit, CC shrinks until they do."""
+    plan = fit_plan(filt, n, dtype, config, payload, table)
+    blob, _ = device_pack(filt, plan, payload, table, device)
+    return plan, blob
+
+
+def fit_plan(filt: CsrFilter, n: int, dtype: int, config: ExecConfig | None, payload, table=None) -> _lib.Plan:
+    """The planning half of plan_for (host only)."""
     config = config or ExecConfig()
     plan = make_plan(filt.geometry, n, dtype, config)
     if plan.kernel == 3 and not config.ent_reserve:
         fields = {f: getattr(config, f) for f in config.__dataclass_fields__}
-        best = None
-        reserve = plan.ent_stage_bytes
-        for _ in range(4):  # reserve <- densest block; more room for input channels
-            need = _max_block(filt, plan, payload, table)
-            if need <= plan.ent_stage_bytes:
-                best = plan
-                if plan.ent_stage_bytes - need < 1024:
-                    break
-            reserve = max(need, 256)
-            fields["ent_reserve"] = int(reserve)
-            plan = make_plan(filt.geometry, n, dtype, ExecConfig(**fields))
-        if best is None or (_max_block(filt, plan, payload, table) <= plan.ent_stage_bytes
-                            and plan.CC >= best.CC):
-            best = plan if _max_block(filt, plan, payload, table) <= plan.ent_stage_bytes else best
+        cc, best = plan.CC, None
+        while cc >= 1 and best is None:
+            fields.update(chunk_channels=cc, ent_reserve=256)
+            try:
+                probe = make_plan(filt.geometry, n, dtype, ExecConfig(**fields))
+                fields.update(chunk_channels=probe.CC,
+                              ent_reserve=max(256, _max_block(filt, probe, payload, table)))
+                best = make_plan(filt.geometry, n, dtype, ExecConfig(**fields))
+            except ValueError:
+                if config.chunk_channels:
+                    raise
+                cc = cc * 3 // 4 if cc > 1 else 0
         if best is None:
-            raise ValueError("no shared-memory entry reserve fits this filter")
+            raise ValueError("no chunk length fits this filter's entry blocks in shared memory")
         plan = best
-    blob, _ = device_pack(filt, plan, payload, table, device)
-    return plan, blob
+    return plan
 
 
 def _max_block(filt, plan, payload, table=None) -> int:
@@ -140,7 +147,8 @@ def _max_block(filt, plan, payload, table=None) -> int:
 
 def _pack_key(plan: _lib.Plan, device) -> tuple:
     return (plan.dtype, plan.kernel, plan.DT, plan.CC, plan.HS, plan.TWs, plan.in_.ws, plan.in_.hp,
-            plan.transposed, plan.groups, plan.n_chunks, plan.ent_stage_bytes, str(device))
+            plan.transposed, plan.groups, plan.n_chunks, plan.ent_stage_bytes, plan.WC, plan.DW,
+            plan.ncls_r, plan.ncls_c, plan.in_.interleave, str(device))
 
 
 def device_pack(filt: CsrFilter, plan: _lib.Plan, payload: np.ndarray, table=None, device=None):
@@ -309,10 +317,14 @@ def tile_candidates(geometry: ConvGeometry, n: int, sb_values, precision=Precisi
             for ws in (w for w in range(1, nw + 1) if nw % w == 0):
                 if ws > strips:
                     break
+                # per-pixel-class runs (halo taps dropped) for 1x1 blocks on small maps
+                classes = (0, 1) if pc == 1 and pr == 1 and yh * yw <= 64 else (0,)
                 for st in (2, 3):
-                    out.append(ExecConfig(sub_batch=min(sb_values), pix_per_thread=pc, rows_per_thread=pr,
-                                          ch_per_cta=dw * (nw // ws), kernel=3, threads=nw * 32,
-                                          pixel_warps=ws, stages=st, samples_per_cta=32 * spl))
+                    for pcl in classes:
+                        out.append(ExecConfig(sub_batch=min(sb_values), pix_per_thread=pc, rows_per_thread=pr,
+                                              ch_per_cta=dw * (nw // ws), kernel=3, threads=nw * 32,
+                                              pixel_warps=ws, stages=st, samples_per_cta=32 * spl,
+                                              pixel_classes=pcl))
     if 1 in kernels:
         ps = [p for p in (2, 4, 8) if p <= max(2, yw)]
         for sb in sb_values:
@@ -327,7 +339,7 @@ def tile_candidates(geometry: ConvGeometry, n: int, sb_values, precision=Precisi
         except ValueError:
             continue
         key = (plan.kernel, plan.P, plan.PR, plan.PC, plan.DT, plan.DW, plan.WS, plan.NS, plan.CC,
-               plan.threads, plan.stages)
+               plan.threads, plan.stages, plan.ncls_r, plan.ncls_c)
         if key not in seen:
             seen.add(key)
             feasible.append(cfg)
@@ -367,5 +379,6 @@ def autotune_sb(input: DenseTensor4, filt: CsrFilter, candidates=SB_CANDIDATES, 
             if cfg.sub_batch == sb and ms <= best * (1.0 + noise_floor):
                 return ExecConfig(cfg.sub_batch, worker_count, cfg.pix_per_thread, cfg.ch_per_cta,
                                   cfg.samples_per_cta, cfg.chunk_channels, cfg.kernel, cfg.threads,
-                                  cfg.pixel_warps, cfg.stages, cfg.rows_per_thread, cfg.ent_reserve)
+                                  cfg.pixel_warps, cfg.stages, cfg.rows_per_thread, cfg.ent_reserve,
+                                  cfg.pixel_classes)
     return ExecConfig(usable[0], worker_count)

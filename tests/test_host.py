@@ -225,3 +225,21 @@ def test_layer_bench_csv_and_backend_choice():
         LB.backend_config(rows, expected_layers=["missing"])
     for name in LB.PRESETS:
         LB.preset_geometry(name)
+
+
+@pytest.mark.parametrize("name", ["cfg1-vgg16-256x8", "sweep-3x3-256x8-98", "vgg16-512x14"])
+def test_every_tile_candidate_fits_its_filter(name):
+    """plan_for's entry-reserve search: every autotuner candidate yields a plan whose
+    densest (group, chunk) entry block fits the shared-memory reserve."""
+    from golden_util import golden, layer_inputs, geom
+    rec = golden()["layers"][name]
+    g = geom(rec["geometry"])
+    _, w = layer_inputs(name, g, rec["sparsity"], rec["batch"], False)
+    c, d, kh, kw, h, ww, st, pd = rec["geometry"]
+    gg = U.ConvGeometry(c, d, kh, kw, h, ww, tuple(st), tuple(pd))
+    f = U.build_csr(U.DenseTensor4.from_array(w), gg)
+    for cfg in U.engine.tile_candidates(gg, rec["batch"], [1, 2]):
+        p = U.engine.fit_plan(f, rec["batch"], _lib.USC_F32, cfg, f.weights)
+        if p.kernel == 3:
+            assert U.engine._max_block(f, p, f.weights) <= p.ent_stage_bytes
+            assert p.smem_bytes <= 224 * 1024
