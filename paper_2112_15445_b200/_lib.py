@@ -132,14 +132,14 @@ def lib():
     return _lib
 
 
-def bi_instances() -> list[tuple[int, int, int, int, int, int]]:
+def bi_instances(binary16: bool = False) -> list[tuple[int, int, int, int, int, int]]:
     """The batch-interleaved kernel's compiled tiles: (compute warps, PC, PR, DW,
-    stride_w, samples per lane)."""
+    stride_w, samples per lane), fp32 or binary16-input (F16/CB4) families."""
     L = lib()
     n = L.usc_bi_instances(None, 0)
-    buf = (c_i32 * (6 * n))()
+    buf = (c_i32 * (7 * n))()
     L.usc_bi_instances(buf, n)
-    return [tuple(buf[6 * i:6 * i + 6]) for i in range(n)]
+    return [tuple(buf[7 * i:7 * i + 6]) for i in range(n) if buf[7 * i + 6] == int(binary16)]
 
 
 def check(rc: int, what: str = ""):

@@ -30,21 +30,22 @@ int launch_bi(const usc_plan *pl, const void *blob, const void *x, void *y, cons
     const int IL = pl->in.interleave;
     if (IL != 32 && IL != 64) return fail(USC_ERR_VALUE, "BI plan needs a 32/64-interleaved input");
     usc_bi::BiArgs a{};
-    // x: [Nb][C][Hp][Wp][IL] fp32; TMA dims innermost first, box = one chunk's tile
+    // x: [Nb][C][Hp][Wp][IL] fp32 or binary16; TMA dims innermost first, box = one chunk's tile
     auto enc = encode_tiled();
     if (!enc) return fail(USC_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
     const cuuint64_t dims[5] = {(cuuint64_t)IL, (cuuint64_t)pl->in.ws, (cuuint64_t)pl->in.hp,
                                 (cuuint64_t)pl->g.in_channels, (cuuint64_t)((pl->n + IL - 1) / IL)};
-    const cuuint64_t px = (cuuint64_t)IL * 4;
+    const bool h16 = pl->dtype == USC_F16 || pl->dtype == USC_CB4;  // binary16 activations
+    const cuuint64_t px = (cuuint64_t)IL * (h16 ? 2 : 4);
     const cuuint64_t strides[4] = {px, px * pl->in.ws, px * pl->in.ws * pl->in.hp,
                                    px * pl->in.ws * pl->in.hp * pl->g.in_channels};
     const cuuint32_t box[5] = {(cuuint32_t)IL, (cuuint32_t)pl->TWs, (cuuint32_t)pl->HS, (cuuint32_t)pl->CC, 1};
     const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
-    CUresult r = enc(&a.xmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, const_cast<void *>(x), dims, strides, box, estr,
+    CUresult r = enc(&a.xmap, h16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, const_cast<void *>(x), dims, strides, box, estr,
                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail(USC_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
-    a.y = static_cast<float *>(y);
+    a.y = y;
     a.blk = reinterpret_cast<const int *>(cb + 64);
     a.perm = reinterpret_cast<const int *>(cb + 64 + cp_bytes);
     const long long ctab_bytes = (4LL * (pl->out_h + pl->out_w) + 15) / 16 * 16;
@@ -80,6 +81,7 @@ int launch_bi(const usc_plan *pl, const void *blob, const void *x, void *y, cons
     a.x_stage_bytes = static_cast<int>(pl->smem_stage_bytes);
     a.stage_bytes = static_cast<int>(pl->smem_stage_bytes + pl->ent_stage_bytes);
     a.ep = ep;
+    if (h16) return usc_bi::launch_h(pl, a, st);
     switch (pl->threads) {
         case 256: return usc_bi::launch_w8(pl, a, st);
         case 384: return usc_bi::launch_w12(pl, a, st);

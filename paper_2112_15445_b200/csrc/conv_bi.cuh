@@ -47,8 +47,8 @@ namespace usc_bi {
 using namespace usc_dev;
 
 struct BiArgs {
-    CUtensorMap xmap;        // x as 5-D [Nb][C][Hp][Wp][IL] fp32 (innermost first in the map)
-    float *y;
+    CUtensorMap xmap;        // x as 5-D [Nb][C][Hp][Wp][IL] (innermost first in the map)
+    void *y;                 // fp32 (F32) or binary16 (F16, CB4) output
     const int *blk;          // byte offset of every (group, chunk) block, G*n_chunks+1
     const int *perm;         // output channel of every (group, warp, slot); -1 = empty
     const char *blocks;      // block base (16-byte aligned)
@@ -76,17 +76,12 @@ __device__ __forceinline__ void tma_load_5d(void *dst, const CUtensorMap *map, i
 }
 
 // ---------------------------------------------------------------------------
-// lane value types: SPL samples per lane
-
-template <int SPL> struct LaneT;
-template <> struct LaneT<1> {
-    using V = float;  // one tap value
-    using A = float;  // one accumulator
-};
-template <> struct LaneT<2> {
-    using V = float2;
-    using A = unsigned long long;  // packed (sample 2l, sample 2l+1) for FADD2
-};
+// lane value types and arithmetic per operand kind, SPL samples per lane
+//   F32 (binary32 x, fp32 theta): FMUL then FADD (SPL 2: two FMUL + one FADD2).
+//   F16 (binary16 x, binary16 theta): one FHFMA (fma.rn.f32.f16) per MAC -- the
+//       binary16 x binary16 product is exact in fp32, so fma == FMUL+FADD bitwise.
+//   CB4 (binary16 x, fp32 codebook centroid): products have up to 26 significant
+//       bits, so FMUL then FADD (x widened with two conversions).
 
 // shared-memory loads on 32-bit addresses with immediate offsets (LDS [R+imm]);
 // not volatile: the address depends on an entry read after the stage's mbarrier
@@ -99,6 +94,10 @@ template <int OFF>
 __device__ __forceinline__ void lds_val(float2 &v, uint32_t a) {
     asm("ld.shared.v2.f32 {%0, %1}, [%2+%3];" : "=f"(v.x), "=f"(v.y) : "r"(a), "n"(OFF));
 }
+template <int OFF>
+__device__ __forceinline__ void lds_val(uint32_t &v, uint32_t a) {
+    asm("ld.shared.b32 %0, [%1+%2];" : "=r"(v) : "r"(a), "n"(OFF));
+}
 __device__ __forceinline__ int4 lds_v4(uint32_t a) {
     int4 v;
     asm("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
@@ -109,23 +108,71 @@ __device__ __forceinline__ int2 lds_v2(uint32_t a) {
     asm("ld.shared.v2.b32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
     return v;
 }
-
-// product t*v, rounded (IEEE multiply)
-__device__ __forceinline__ float mul_v(float t, float v) { return __fmul_rn(t, v); }
-__device__ __forceinline__ float2 mul_v(float t, float2 v) { return make_float2(__fmul_rn(t, v.x), __fmul_rn(t, v.y)); }
-// acc + product, rounded (IEEE add)
-__device__ __forceinline__ void add_v(float &acc, float p) { acc = __fadd_rn(acc, p); }
-__device__ __forceinline__ void add_v(unsigned long long &acc, float2 p) {
+__device__ __forceinline__ void fadd2(unsigned long long &acc, float lo, float hi) {
     unsigned long long q;
-    asm("mov.b64 %0, {%1, %2};" : "=l"(q) : "f"(p.x), "f"(p.y));
+    asm("mov.b64 %0, {%1, %2};" : "=l"(q) : "f"(lo), "f"(hi));
     asm("add.rn.f32x2 %0, %0, %1;" : "+l"(acc) : "l"(q));
 }
-__device__ __forceinline__ void zero_a(float &a) { a = 0.0f; }
-__device__ __forceinline__ void zero_a(unsigned long long &a) { a = 0ull; }  // (+0.0f, +0.0f)
-__device__ __forceinline__ void unpack_a(float a, float (&o)[1]) { o[0] = a; }
-__device__ __forceinline__ void unpack_a(unsigned long long a, float (&o)[2]) {
-    asm("mov.b64 {%0, %1}, %2;" : "=f"(o[0]), "=f"(o[1]) : "l"(a));
+__device__ __forceinline__ void unpack2(unsigned long long a, float &lo, float &hi) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(a));
 }
+__device__ __forceinline__ float2 h2f2(uint32_t v) {
+    float2 f;
+    asm("{.reg .f16 l, h;\n mov.b32 {l, h}, %2;\n cvt.f32.f16 %0, l;\n cvt.f32.f16 %1, h;}"
+        : "=f"(f.x), "=f"(f.y) : "r"(v));
+    return f;
+}
+
+template <int KIND, int SPL> struct Ops;
+template <> struct Ops<USC_F32, 1> {
+    using V = float;
+    using A = float;
+    static constexpr int EB = 4;  // bytes per staged sample value
+    __device__ static void zero(A &a) { a = 0.0f; }
+    __device__ static V prod(uint32_t t, V v) { return __fmul_rn(__uint_as_float(t), v); }
+    __device__ static void acc(A &a, V p) { a = __fadd_rn(a, p); }
+    __device__ static void unpack(A a, float (&o)[1]) { o[0] = a; }
+};
+template <> struct Ops<USC_F32, 2> {
+    using V = float2;
+    using A = unsigned long long;  // packed (sample 2l, sample 2l+1) for FADD2
+    static constexpr int EB = 4;
+    __device__ static void zero(A &a) { a = 0ull; }  // (+0.0f, +0.0f)
+    __device__ static V prod(uint32_t t, V v) {
+        return make_float2(__fmul_rn(__uint_as_float(t), v.x), __fmul_rn(__uint_as_float(t), v.y));
+    }
+    __device__ static void acc(A &a, V p) { fadd2(a, p.x, p.y); }
+    __device__ static void unpack(A a, float (&o)[2]) { unpack2(a, o[0], o[1]); }
+};
+template <> struct Ops<USC_CB4, 2> {
+    using V = uint32_t;            // binary16 pair (sample 2l, 2l+1)
+    using A = unsigned long long;
+    static constexpr int EB = 2;
+    __device__ static void zero(A &a) { a = 0ull; }
+    __device__ static float2 prod(uint32_t t, V v) {
+        const float2 x = h2f2(v);
+        return make_float2(__fmul_rn(__uint_as_float(t), x.x), __fmul_rn(__uint_as_float(t), x.y));
+    }
+    __device__ static void acc(A &a, float2 p) { fadd2(a, p.x, p.y); }
+    __device__ static void unpack(A a, float (&o)[2]) { unpack2(a, o[0], o[1]); }
+};
+template <> struct Ops<USC_F16, 2> {
+    using V = uint32_t;  // binary16 pair
+    using A = float2;
+    static constexpr int EB = 2;
+    __device__ static void zero(A &a) { a = make_float2(0.0f, 0.0f); }
+    // theta: binary16 bits in the low half of t; fp32 += f16*f16, one rounding
+    __device__ static void fma(A &a, uint32_t t, V v) {
+        const unsigned short th = static_cast<unsigned short>(t), lo = static_cast<unsigned short>(v),
+                             hi = static_cast<unsigned short>(v >> 16);
+        asm("fma.rn.f32.f16 %0, %1, %2, %0;" : "+f"(a.x) : "h"(th), "h"(lo));
+        asm("fma.rn.f32.f16 %0, %1, %2, %0;" : "+f"(a.y) : "h"(th), "h"(hi));
+    }
+    __device__ static void unpack(A a, float (&o)[2]) {
+        o[0] = a.x;
+        o[1] = a.y;
+    }
+};
 
 // the P pixels of a thread for one tap: row 0 at a0, row 1 at a1 (bytes), columns
 // SW pixels (SW*PXB bytes) apart
@@ -133,33 +180,57 @@ template <int PC, int PXB, int SW, typename V, int... I>
 __device__ __forceinline__ void load_px_(V *v, uint32_t a0, uint32_t a1, std::integer_sequence<int, I...>) {
     ((I / PC == 0 ? lds_val<(I % PC) * SW * PXB>(v[I], a0) : lds_val<(I % PC) * SW * PXB>(v[I], a1)), ...);
 }
-template <int PC, int PR, int SW, int SPL>
-__device__ __forceinline__ void load_px(typename LaneT<SPL>::V (&v)[PC * PR], uint32_t a0, uint32_t a1) {
-    load_px_<PC, 128 * SPL, SW>(v, a0, a1, std::make_integer_sequence<int, PC * PR>{});
+template <int KIND, int PC, int PR, int SW, int SPL>
+__device__ __forceinline__ void load_px(typename Ops<KIND, SPL>::V (&v)[PC * PR], uint32_t a0, uint32_t a1) {
+    load_px_<PC, 32 * SPL * Ops<KIND, SPL>::EB, SW>(v, a0, a1, std::make_integer_sequence<int, PC * PR>{});
 }
 
-// acc[p] += t0*v0[p], then += t1*v1[p]: products first, then the adds in stored order
-template <int P, int SPL>
-__device__ __forceinline__ void mac_pair(typename LaneT<SPL>::A (&acc)[P], typename LaneT<SPL>::V (&v0)[P],
-                                         typename LaneT<SPL>::V (&v1)[P], const int4 &n) {
-    const float t0 = __int_as_float(n.y), t1 = __int_as_float(n.w);
+// acc[p] += t*v[p] for one entry (stored order: call in entry order)
+template <int KIND, int SPL, int P>
+__device__ __forceinline__ void mac_one(typename Ops<KIND, SPL>::A (&acc)[P], typename Ops<KIND, SPL>::V (&v)[P],
+                                        uint32_t t) {
+    using O = Ops<KIND, SPL>;
+    if constexpr (KIND == USC_F16) {
 #pragma unroll
-    for (int p = 0; p < P; ++p) {
-        v0[p] = mul_v(t0, v0[p]);
-        v1[p] = mul_v(t1, v1[p]);
+        for (int p = 0; p < P; ++p) O::fma(acc[p], t, v[p]);
+    } else {
+        decltype(O::prod(t, v[0])) q[P];
+#pragma unroll
+        for (int p = 0; p < P; ++p) q[p] = O::prod(t, v[p]);
+#pragma unroll
+        for (int p = 0; p < P; ++p) O::acc(acc[p], q[p]);
     }
-#pragma unroll
-    for (int p = 0; p < P; ++p) add_v(acc[p], v0[p]);
-#pragma unroll
-    for (int p = 0; p < P; ++p) add_v(acc[p], v1[p]);
 }
 
-template <int PC, int PR, int SW, int SPL>
-__device__ __forceinline__ void load_pair(typename LaneT<SPL>::V (&v0)[PC * PR], typename LaneT<SPL>::V (&v1)[PC * PR],
-                                          uint32_t xs, uint32_t rs, const int4 &n) {
+// two entries n = {off0, t0, off1, t1}: products first, then the adds in stored order
+template <int KIND, int SPL, int P>
+__device__ __forceinline__ void mac_pair(typename Ops<KIND, SPL>::A (&acc)[P], typename Ops<KIND, SPL>::V (&v0)[P],
+                                         typename Ops<KIND, SPL>::V (&v1)[P], const int4 &n) {
+    using O = Ops<KIND, SPL>;
+    if constexpr (KIND == USC_F16) {
+        mac_one<KIND, SPL, P>(acc, v0, static_cast<uint32_t>(n.y));
+        mac_one<KIND, SPL, P>(acc, v1, static_cast<uint32_t>(n.w));
+    } else {
+        decltype(O::prod(0u, v0[0])) q0[P], q1[P];
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+            q0[p] = O::prod(static_cast<uint32_t>(n.y), v0[p]);
+            q1[p] = O::prod(static_cast<uint32_t>(n.w), v1[p]);
+        }
+#pragma unroll
+        for (int p = 0; p < P; ++p) O::acc(acc[p], q0[p]);
+#pragma unroll
+        for (int p = 0; p < P; ++p) O::acc(acc[p], q1[p]);
+    }
+}
+
+template <int KIND, int PC, int PR, int SW, int SPL>
+__device__ __forceinline__ void load_pair(typename Ops<KIND, SPL>::V (&v0)[PC * PR],
+                                          typename Ops<KIND, SPL>::V (&v1)[PC * PR], uint32_t xs, uint32_t rs,
+                                          const int4 &n) {
     const uint32_t p0 = xs + n.x, p1 = xs + n.z;
-    load_px<PC, PR, SW, SPL>(v0, p0, p0 + rs);
-    load_px<PC, PR, SW, SPL>(v1, p1, p1 + rs);
+    load_px<KIND, PC, PR, SW, SPL>(v0, p0, p0 + rs);
+    load_px<KIND, PC, PR, SW, SPL>(v1, p1, p1 + rs);
 }
 
 // One slot's run of entries [ep, ee) (byte addresses, ep 16-B aligned), two entries
@@ -167,40 +238,40 @@ __device__ __forceinline__ void load_pair(typename LaneT<SPL>::V (&v0)[PC * PR],
 // are issued before this pair's math (ping-pong registers), so the shared-memory
 // latency hides inside one warp.  Reads of the entry after a run stay inside the
 // stage's 16-byte slack.
-template <int PC, int PR, int SW, int SPL, bool PIPE>
-__device__ __forceinline__ void run_pairs(typename LaneT<SPL>::A (&acc)[PC * PR], uint32_t xs, uint32_t rs,
+template <int KIND, int PC, int PR, int SW, int SPL, bool PIPE>
+__device__ __forceinline__ void run_pairs(typename Ops<KIND, SPL>::A (&acc)[PC * PR], uint32_t xs, uint32_t rs,
                                           uint32_t ep, uint32_t ee) {
     constexpr int P = PC * PR;
-    using V = typename LaneT<SPL>::V;
+    using V = typename Ops<KIND, SPL>::V;
     int4 nn = lds_v4(ep);
     if constexpr (PIPE) {
         if (ep + 16 <= ee) {
             V a0[P], a1[P], b0[P], b1[P];
             int4 n = nn;
-            load_pair<PC, PR, SW, SPL>(a0, a1, xs, rs, n);
+            load_pair<KIND, PC, PR, SW, SPL>(a0, a1, xs, rs, n);
             ep += 16;
             nn = lds_v4(ep);
 #pragma unroll 1
             while (true) {  // a* hold pair n; nn is the pair at ep
                 if (ep + 16 > ee) {
-                    mac_pair<P, SPL>(acc, a0, a1, n);
+                    mac_pair<KIND, SPL, P>(acc, a0, a1, n);
                     break;
                 }
-                load_pair<PC, PR, SW, SPL>(b0, b1, xs, rs, nn);
+                load_pair<KIND, PC, PR, SW, SPL>(b0, b1, xs, rs, nn);
                 int4 m = nn;
                 ep += 16;
                 nn = lds_v4(ep);
-                mac_pair<P, SPL>(acc, a0, a1, n);
+                mac_pair<KIND, SPL, P>(acc, a0, a1, n);
                 n = m;
                 if (ep + 16 > ee) {
-                    mac_pair<P, SPL>(acc, b0, b1, n);
+                    mac_pair<KIND, SPL, P>(acc, b0, b1, n);
                     break;
                 }
-                load_pair<PC, PR, SW, SPL>(a0, a1, xs, rs, nn);
+                load_pair<KIND, PC, PR, SW, SPL>(a0, a1, xs, rs, nn);
                 m = nn;
                 ep += 16;
                 nn = lds_v4(ep);
-                mac_pair<P, SPL>(acc, b0, b1, n);
+                mac_pair<KIND, SPL, P>(acc, b0, b1, n);
                 n = m;
             }
         }
@@ -208,21 +279,37 @@ __device__ __forceinline__ void run_pairs(typename LaneT<SPL>::A (&acc)[PC * PR]
 #pragma unroll 1
         for (; ep + 16 <= ee; ep += 16) {
             V v0[P], v1[P];
-            load_pair<PC, PR, SW, SPL>(v0, v1, xs, rs, nn);
+            load_pair<KIND, PC, PR, SW, SPL>(v0, v1, xs, rs, nn);
             const int4 n = nn;
             nn = lds_v4(ep + 16);
-            mac_pair<P, SPL>(acc, v0, v1, n);
+            mac_pair<KIND, SPL, P>(acc, v0, v1, n);
         }
     }
     if (ep < ee) {  // odd run: the last entry is nn.x, nn.y
         V v0[P];
         const uint32_t p0 = xs + nn.x;
-        load_px<PC, PR, SW, SPL>(v0, p0, p0 + rs);
-        const float t0 = __int_as_float(nn.y);
-#pragma unroll
-        for (int p = 0; p < P; ++p) v0[p] = mul_v(t0, v0[p]);
-#pragma unroll
-        for (int p = 0; p < P; ++p) add_v(acc[p], v0[p]);
+        load_px<KIND, PC, PR, SW, SPL>(v0, p0, p0 + rs);
+        mac_one<KIND, SPL, P>(acc, v0, static_cast<uint32_t>(nn.y));
+    }
+}
+
+// output value of one accumulator (store_one semantics, common.cuh): F32 -> ReLU;
+// F16/CB4 -> the _half_hook order of quantization.py:238-244 (saturate, binary16
+// rounding, ReLU, saturate2 + rounding)
+template <int KIND>
+__device__ __forceinline__ float epi_value(float v, const Epi &ep) {
+    // ReLU is np.where(v > 0, v, 0) (nn.py:96-98): NaN -> 0
+    if constexpr (KIND == USC_F32) {
+        return ep.relu ? (v > 0.0f ? v : 0.0f) : v;
+    } else {
+        if (ep.saturate) v = v > ep.cap ? ep.cap : v;  // np.minimum keeps NaN
+        v = round16f(v);
+        if (ep.relu) v = v > 0.0f ? v : 0.0f;
+        if (ep.saturate2) {
+            v = v > ep.cap2 ? ep.cap2 : v;
+            v = round16f(v);
+        }
+        return v;
     }
 }
 
@@ -257,15 +344,17 @@ __device__ __forceinline__ int item_tile(const BiArgs &a, int it, int &part) {
     return a.tfull + j / a.split;
 }
 
-template <int PC, int PR, int DW, int SW, int NWC, int SPL>
+template <int KIND, int PC, int PR, int DW, int SW, int NWC, int SPL>
 __global__ void __launch_bounds__((NWC + 1) * 32, 1) k_bi(const __grid_constant__ BiArgs a) {
-    constexpr int P = PC * PR;      // a thread's pixel block: PR rows x PC cols
-    constexpr int IL = 32 * SPL;    // samples per interleave block
-    constexpr int PXB = 4 * IL;     // bytes per staged pixel
-    using A = typename LaneT<SPL>::A;
+    using O = Ops<KIND, SPL>;
+    using A = typename O::A;
+    constexpr int P = PC * PR;          // a thread's pixel block: PR rows x PC cols
+    constexpr int IL = 32 * SPL;        // samples per interleave block
+    constexpr int PXB = O::EB * IL;     // bytes per staged pixel
     // software-pipeline the pair loop when the second value set fits the register cap
     constexpr int REGCAP = NWC <= 8 ? 168 : (NWC <= 12 ? 128 : 96);
-    constexpr bool PIPE = SPL * (DW * P + 4 * P) + 40 <= REGCAP;
+    constexpr int VR = (KIND == USC_F32) ? SPL : 1;  // registers per staged value
+    constexpr bool PIPE = SPL * DW * P + 4 * P * VR + 40 <= REGCAP;
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t *full = reinterpret_cast<uint64_t *>(smem);
     uint64_t *empty = full + 8;
@@ -321,7 +410,7 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1) k_bi(const __grid_constant_
     const int wsi = warp % a.WS, wc = warp / a.WS;
     const bool active = wc < a.WC;
     const int tr = wsi / a.SPRt, tcs = wsi - tr * a.SPRt;  // strip-row, strip within the tile
-    const uint32_t base = ((tr * PR * a.s_h) * a.TWs + tcs * PC * SW) * PXB + lane * 4 * SPL;
+    const uint32_t base = ((tr * PR * a.s_h) * a.TWs + tcs * PC * SW) * PXB + lane * O::EB * SPL;
     const uint32_t rs = a.s_h * a.TWs * PXB;  // bytes between a thread's two pixel rows
     const int hdr_bytes = a.ncls * a.DT * 8;
     int s = 0;
@@ -345,7 +434,7 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1) k_bi(const __grid_constant_
 #pragma unroll
         for (int i = 0; i < DW; ++i)
 #pragma unroll
-            for (int p = 0; p < P; ++p) zero_a(acc[i][p]);
+            for (int p = 0; p < P; ++p) O::zero(acc[i][p]);
 
         for (int k = 0; k < a.n_chunks; ++k) {
             const uint32_t st = smem_u32(ring + s * a.stage_bytes);
@@ -358,7 +447,7 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1) k_bi(const __grid_constant_
                 for (int dw = 0; dw < DW; ++dw) {
                     const int2 h = lds_v2(hdr + dw * 8);  // run [h.x, h.y), h.x even
                     if (part >= 0 && dw % a.split != part) continue;
-                    run_pairs<PC, PR, SW, SPL, PIPE>(acc[dw], xs, rs, E + h.x * 8, E + h.y * 8);
+                    run_pairs<KIND, PC, PR, SW, SPL, PIPE>(acc[dw], xs, rs, E + h.x * 8, E + h.y * 8);
                 }
             }
             __syncwarp();
@@ -369,8 +458,9 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1) k_bi(const __grid_constant_
             }
         }
 
-        // epilogue: ReLU (nn.py:96-98) then, if fused, the 2x2/2 max-pool
-        // (nn.py:124-135); element (b, d, row, col) of the output layout is
+        // epilogue: epi_value (ReLU, nn.py:96-98; binary16 hook for F16/CB4) then, if
+        // fused, the 2x2/2 max-pool (nn.py:124-135); element (b, d, row, col) of the
+        // output layout is
         // obase + d*dstride + row*rstride + col*cstride (+ j*sstride for the lane's
         // j-th sample)
         if (!active || r >= a.Yh) continue;
@@ -402,10 +492,9 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1) k_bi(const __grid_constant_
             rstride = a.ep.oWs;
             cstride = 1;
         }
-        const bool vec = SPL == 2 && oil == IL;  // the lane's two samples adjacent: one 8-byte store
+        const bool vec = SPL == 2 && oil == IL;  // the lane's two samples adjacent: one vector store
         const int ncol = min(PC, a.Yw - col0);
         const int nrow = min(PR, a.Yh - r);
-        const bool relu = a.ep.relu != 0;
 #pragma unroll
         for (int dw = 0; dw < DW; ++dw) {
             if (part >= 0 && dw % a.split != part) continue;
@@ -415,10 +504,9 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1) k_bi(const __grid_constant_
             float v[P][SPL];
 #pragma unroll
             for (int p = 0; p < P; ++p) {
-                unpack_a(acc[dw][p], v[p]);
+                O::unpack(acc[dw][p], v[p]);
 #pragma unroll
-                for (int j = 0; j < SPL; ++j)
-                    if (relu) v[p][j] = v[p][j] > 0.0f ? v[p][j] : 0.0f;
+                for (int j = 0; j < SPL; ++j) v[p][j] = epi_value<KIND>(v[p][j], a.ep);
             }
             // the thread's outputs: PC/2 pooled values of one row, or its P pixels
             float o[P][SPL];
@@ -452,21 +540,34 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1) k_bi(const __grid_constant_
 #pragma unroll
             for (int i = 0; i < P; ++i) {
                 if (i >= no || !ok[i]) continue;
-                if (vec) {
-                    *reinterpret_cast<float2 *>(a.y + off[i]) = make_float2(o[i][0], o[i][SPL - 1]);
-                } else {
+                if constexpr (KIND == USC_F32) {
+                    float *y = static_cast<float *>(a.y);
+                    if (vec) {
+                        *reinterpret_cast<float2 *>(y + off[i]) = make_float2(o[i][0], o[i][SPL - 1]);
+                    } else {
 #pragma unroll
-                    for (int j = 0; j < SPL; ++j)
-                        if (b0 + j < a.N) a.y[off[i] + j * sstride] = o[i][j];
+                        for (int j = 0; j < SPL; ++j)
+                            if (b0 + j < a.N) y[off[i] + j * sstride] = o[i][j];
+                    }
+                } else {  // values are on the binary16 grid: the conversion is exact
+                    __half *y = static_cast<__half *>(a.y);
+                    if (vec) {
+                        *reinterpret_cast<__half2 *>(y + off[i]) =
+                            __halves2half2(__float2half_rn(o[i][0]), __float2half_rn(o[i][SPL - 1]));
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < SPL; ++j)
+                            if (b0 + j < a.N) y[off[i] + j * sstride] = __float2half_rn(o[i][j]);
+                    }
                 }
             }
         }
     }
 }
 
-template <int PC, int PR, int DW, int SW, int NWC, int SPL>
+template <int KIND, int PC, int PR, int DW, int SW, int NWC, int SPL>
 int launch_inst(const usc_plan *pl, const BiArgs &a, cudaStream_t st) {
-    auto fn = k_bi<PC, PR, DW, SW, NWC, SPL>;
+    auto fn = k_bi<KIND, PC, PR, DW, SW, NWC, SPL>;
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 224 * 1024);
@@ -478,8 +579,11 @@ int launch_inst(const usc_plan *pl, const BiArgs &a, cudaStream_t st) {
     return USC_OK;
 }
 
-int launch_w8(const usc_plan *pl, const BiArgs &a, cudaStream_t st);   // 8 compute warps (168 regs)
-int launch_w12(const usc_plan *pl, const BiArgs &a, cudaStream_t st);  // 12 compute warps (128 regs)
-int launch_w16(const usc_plan *pl, const BiArgs &a, cudaStream_t st);  // 16 compute warps (96 regs)
+// fp32 instances with 8 (168 regs), 12 (128) and 16 (96) compute warps; binary16-input
+// (F16, CB4) instances
+int launch_w8(const usc_plan *pl, const BiArgs &a, cudaStream_t st);
+int launch_w12(const usc_plan *pl, const BiArgs &a, cudaStream_t st);
+int launch_w16(const usc_plan *pl, const BiArgs &a, cudaStream_t st);
+int launch_h(const usc_plan *pl, const BiArgs &a, cudaStream_t st);
 
 }  // namespace usc_bi

@@ -245,7 +245,16 @@ static void tap_classes(int Y, int stride, int pad, int K, int X, std::vector<in
 }
 
 // The k_bi instances compiled into the library (bi_instances.h).
-static bool bi_instance(int PC, int PR, int DW, int NW, int SW, int SPL) {
+static bool bi_instance(int PC, int PR, int DW, int NW, int SW, int SPL, int dtype) {
+    if (dtype == USC_F16 || dtype == USC_CB4) {
+        if (SPL != 2) return false;
+#define XH(NW_, PC_, PR_, DW_, SW_) \
+    if (NW == NW_ && PC == PC_ && PR == PR_ && DW == DW_ && SW == SW_) return true;
+        USC_BI_H(XH)
+#undef XH
+        return false;
+    }
+    if (dtype != USC_F32) return false;
 #define X(PC_, PR_, DW_, SW_, SPL_) \
     if (PC == PC_ && PR == PR_ && DW == DW_ && SW == SW_ && SPL == SPL_) return true;
     if (NW == 8) {
@@ -261,17 +270,20 @@ static bool bi_instance(int PC, int PR, int DW, int NW, int SW, int SPL) {
 
 int usc_bi_instances(int32_t *out, int32_t max_count) {
     int n = 0;
-#define X(PC_, PR_, DW_, SW_, SPL_)                             \
+#define X7(NW_, PC_, PR_, DW_, SW_, SPL_, K_)                   \
     if (n < max_count && out) {                                \
-        int32_t *o = out + 6 * n;                              \
+        int32_t *o = out + 7 * n;                              \
         o[0] = NW_;                                            \
         o[1] = PC_;                                            \
         o[2] = PR_;                                            \
         o[3] = DW_;                                            \
         o[4] = SW_;                                            \
         o[5] = SPL_;                                           \
+        o[6] = K_;                                             \
     }                                                          \
     ++n;
+#define X(PC_, PR_, DW_, SW_, SPL_) X7(NW_, PC_, PR_, DW_, SW_, SPL_, 0)
+#define XH(NWH_, PC_, PR_, DW_, SW_) X7(NWH_, PC_, PR_, DW_, SW_, 2, 1)
     {
         const int NW_ = 8;
         USC_BI_W8(X)
@@ -284,7 +296,10 @@ int usc_bi_instances(int32_t *out, int32_t max_count) {
         const int NW_ = 16;
         USC_BI_W16(X)
     }
+    USC_BI_H(XH)
 #undef X
+#undef XH
+#undef X7
     return n;
 }
 
@@ -298,6 +313,14 @@ int usc_plan_make(const usc_geometry *g0, int32_t n, int32_t dtype, const usc_ex
     if (c.sub_batch < 1) c.sub_batch = 1;
     if (n % c.sub_batch)
         return fail(USC_ERR_VALUE, "sub_batch %d does not divide batch %d", c.sub_batch, n);
+    if (c.kernel == 0 && dtype != USC_I8) {
+        // auto: the batch-interleaved kernel when a compiled tile fits this layer, else
+        // the padded-NCHW kernel
+        usc_exec_cfg k3 = c;
+        k3.kernel = 3;
+        if (usc_plan_make(g0, n, dtype, &k3, pl) == USC_OK) return USC_OK;
+        c.kernel = 1;
+    }
     std::memset(pl, 0, sizeof *pl);
     pl->dtype = dtype;
     pl->n = n;
@@ -314,19 +337,20 @@ int usc_plan_make(const usc_geometry *g0, int32_t n, int32_t dtype, const usc_ex
     pl->g = g;
     usc_geometry_out(&g, &pl->out_h, &pl->out_w);
     const int eb = elem_bytes(dtype);
-    int kernel = c.kernel ? c.kernel : (dtype == USC_F32 ? 3 : 1);
+    int kernel = c.kernel ? c.kernel : (dtype == USC_I8 ? 1 : 3);
     if (g.stride_w > 2) kernel = 2;
     // kernel 3 sample interleave: samples_per_cta 32 (BI32) or 64 (BI64, two samples per
     // lane); default BI64 once the batch fills two 32-sample blocks
     int IL = 0;
     if (kernel == 3) {
         IL = (c.samples_per_cta == 32 || c.samples_per_cta == 64) ? c.samples_per_cta : (n > 32 ? 64 : 32);
+        if (dtype == USC_F16 || dtype == USC_CB4) IL = 64;  // binary16 pairs: BI64 only
     }
     rc = usc_act_layout_make(g.in_channels, g.input_h, g.input_w, g.pad_h, g.pad_w, eb, IL, &pl->in);
     if (rc) return rc;
     const int Yh = pl->out_h, Yw = pl->out_w, Ws = pl->in.ws;
     const int threads = (c.threads == 128 || c.threads == 256) ? c.threads : 256;
-    if (kernel == 3 && dtype != USC_F32) return fail(USC_ERR_UNSUPPORTED, "BI kernel is fp32-only");
+    if (kernel == 3 && dtype == USC_I8) return fail(USC_ERR_UNSUPPORTED, "BI kernel has no int8 variant");
     if (kernel == 3) {
         // batch-interleaved: a CTA = 32 samples x (WS strips of PR x PC pixels) x (WC*DW
         // channels), NW compute warps (threads = NW*32) + 1 producer warp; warp w owns
@@ -343,6 +367,29 @@ int usc_plan_make(const usc_geometry *g0, int32_t n, int32_t dtype, const usc_ex
                     PC = q;
                     break;
                 }
+        }
+        if (!c.pix_per_thread || !c.rows_per_thread) {
+            // no compiled instance for the preferred block: the first (PR, PC) that has one
+            auto any_inst = [&](int pr, int pc) {
+                for (int nw : {8, 12, 16})
+                    for (int dw : {2, 4, 8, 16})
+                        if (bi_instance(pc, pr, dw, nw, g.stride_w, IL / 32, dtype)) return true;
+                return false;
+            };
+            if (!any_inst(PR, PC)) {
+                bool found = false;
+                for (int pr : {PR, 1})
+                    for (int pc : {8, 4, 2, 1}) {
+                        if (found || (c.rows_per_thread && pr != c.rows_per_thread) ||
+                            (c.pix_per_thread && pc != c.pix_per_thread) || pr > Yh)
+                            continue;
+                        if (any_inst(pr, pc)) {
+                            PR = pr;
+                            PC = pc;
+                            found = true;
+                        }
+                    }
+            }
         }
         if (PC != 1 && PC != 2 && PC != 4 && PC != 8)
             return fail(USC_ERR_VALUE, "BI pix_per_thread must be 1,2,4,8");
@@ -370,9 +417,9 @@ int usc_plan_make(const usc_geometry *g0, int32_t n, int32_t dtype, const usc_ex
             const int wc = nw / ws;
             if (c.ch_per_cta && c.ch_per_cta % wc)
                 return fail(USC_ERR_VALUE, "ch_per_cta %d not a multiple of %d channel warps", c.ch_per_cta, wc);
-            for (int dw : {8, 16, 4}) {
+            for (int dw : {8, 16, 4, 2}) {
                 if (c.ch_per_cta) dw = c.ch_per_cta / wc;
-                if (bi_instance(PC, PR, dw, nw, g.stride_w, IL / 32)) {
+                if (bi_instance(PC, PR, dw, nw, g.stride_w, IL / 32, dtype)) {
                     NW = nw, WS = ws, WC = wc, DW = dw;
                     break;
                 }
@@ -596,6 +643,46 @@ int usc_plan_make(const usc_geometry *g0, int32_t n, int32_t dtype, const usc_ex
 
 static int64_t align16(int64_t v) { return (v + 15) / 16 * 16; }
 
+// binary16 bits of an fp32 value (round to nearest even; exact for the binary16-grid
+// weights of a BINARY16 filter)
+static uint16_t f32_to_f16_bits(float f) {
+    uint32_t x;
+    std::memcpy(&x, &f, 4);
+    const uint32_t sign = (x >> 16) & 0x8000u;
+    const uint32_t ax = x & 0x7fffffffu;
+    if (ax >= 0x7f800000u) return (uint16_t)(sign | 0x7c00u | (ax > 0x7f800000u ? 0x200u : 0u));  // inf/nan
+    if (ax >= 0x477ff000u) return (uint16_t)(sign | 0x7c00u);  // rounds past 65504 -> inf
+    if (ax < 0x33000001u) return (uint16_t)sign;               // < half the smallest subnormal
+    const int e = (int)(ax >> 23);
+    uint32_t m = (ax & 0x7fffffu) | 0x800000u;
+    int shift = 126 - e;  // normal half exponent field = e - 112; subnormal below
+    uint32_t hb;
+    if (e >= 113) {  // normal
+        hb = ((uint32_t)(e - 112) << 10) | ((m >> 13) & 0x3ffu);
+        const uint32_t rem = m & 0x1fffu;
+        if (rem > 0x1000u || (rem == 0x1000u && (hb & 1u))) ++hb;
+    } else {         // subnormal: value = m * 2^(e-150), unit 2^-24
+        shift = 126 - e;  // 14 + (113 - e)
+        const uint32_t q = m >> shift, rem = m & ((1u << shift) - 1u), half = 1u << (shift - 1);
+        hb = q;
+        if (rem > half || (rem == half && (hb & 1u))) ++hb;
+    }
+    return (uint16_t)(sign | hb);
+}
+
+// the 32-bit theta word of stored entry j in a kernel-3 entry: fp32 bits (F32), the
+// binary16 bits in the low half (F16, FHFMA operand), the decoded fp32 centroid (CB4)
+static int32_t theta_word(int dtype, const void *payload, const float *table, int64_t j) {
+    int32_t w = 0;
+    if (dtype == USC_F16) return (int32_t)f32_to_f16_bits(((const float *)payload)[j]);
+    if (dtype == USC_CB4) {
+        std::memcpy(&w, &table[((const uint8_t *)payload)[j] & 15], 4);
+        return w;
+    }
+    std::memcpy(&w, &((const float *)payload)[j], 4);
+    return w;
+}
+
 int usc_pack_size(const usc_plan *pl, int64_t n_nz, int64_t *bytes) {
     const int64_t nb = (int64_t)pl->groups * pl->n_chunks;
     if (pl->kernel == 3) {
@@ -679,7 +766,7 @@ int usc_pack(const usc_plan *pl, const int64_t *row_ptr, const int64_t *col, con
         if (pl->kernel == 1)
             *off = cl * cs_tiled + kh * Ws + kw;
         else if (pl->kernel == 3)  // byte offset in the [CC][HS][TWs][IL] f32 stage
-            *off = ((cl * pl->HS + kh) * pl->TWs + kw) * 4 * pl->in.interleave;
+            *off = ((cl * pl->HS + kh) * pl->TWs + kw) * elem_bytes(pl->dtype) * pl->in.interleave;
         else
             *off = (c * Hp + kh) * Ws + kw;
         if (*off >= max_off || *off > INT32_MAX)
@@ -706,9 +793,16 @@ int usc_pack(const usc_plan *pl, const int64_t *row_ptr, const int64_t *col, con
         std::vector<uint32_t> rmask(NCLS, ~0u), cmask(NCLS, ~0u);
         // halo taps are dropped only when every weight is finite (theta*0 must be +-0)
         bool finite = true;
-        if (pl->dtype == USC_F32 || pl->dtype == USC_F16)
-            for (int64_t j = 0; j < (int64_t)D * n_nz && finite; ++j)
-                finite = std::isfinite(((const float *)payload)[j]);
+        for (int64_t j = 0; j < (int64_t)D * n_nz && finite; ++j) {
+            float t;
+            const int32_t w = theta_word(pl->dtype, payload, table, j);
+            if (pl->dtype == USC_F16) {
+                finite = (w & 0x7c00) != 0x7c00;
+                continue;
+            }
+            std::memcpy(&t, &w, 4);
+            finite = std::isfinite(t);
+        }
         if (NCLS > 1 && finite) {
             tap_classes(pl->out_h, g.stride_h, g.pad_h, g.filter_h, g.input_h, rowcls, rmask);
             tap_classes(pl->out_w, g.stride_w, g.pad_w, g.filter_w, g.input_w, colcls, cmask);
@@ -799,7 +893,7 @@ int usc_pack(const usc_plan *pl, const int64_t *row_ptr, const int64_t *col, con
                         if (out[i].first < 0) continue;
                         int32_t v[2];
                         v[0] = (int32_t)out[i].first;
-                        std::memcpy(&v[1], &((const float *)payload)[out[i].second], 4);
+                        v[1] = theta_word(pl->dtype, payload, table, out[i].second);
                         std::memcpy(ents + i * 8, v, 8);
                     }
                 }

@@ -303,15 +303,16 @@ def tile_candidates(geometry: ConvGeometry, n: int, sb_values, precision=Precisi
     out = []
     yw = geometry.out_w if geometry.input_w != 1 else geometry.out_h
     if kernels is None:
-        kernels = (3, 1) if precision is PrecisionMode.BINARY32 else (1,)
-    if 3 in kernels and precision is PrecisionMode.BINARY32:
+        kernels = (3, 1)
+    if 3 in kernels:
         # every compiled k_bi instance x every split of its warps into pixel warps (WS)
         # and channel warps; skip pixel blocks wider/taller than the map and splits
         # that leave pixel warps idle
         yh = geometry.out_h if geometry.input_w != 1 else geometry.out_w
         sw = geometry.stride[1] if geometry.input_w != 1 else geometry.stride[0]
-        for nw, pc, pr, dw, isw, spl in _lib.bi_instances():
-            if isw != sw or pc > max(1, yw) and pc > 1 or pr > yh or (spl == 2 and n <= 32):
+        h16 = precision is PrecisionMode.BINARY16
+        for nw, pc, pr, dw, isw, spl in _lib.bi_instances(h16):
+            if isw != sw or pc > max(1, yw) and pc > 1 or pr > yh or (spl == 2 and n <= 32 and not h16):
                 continue
             strips = -(-yh // pr) * -(-yw // pc)
             for ws in (w for w in range(1, nw + 1) if nw % w == 0):

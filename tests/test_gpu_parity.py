@@ -32,8 +32,6 @@ def test_random_corpus_bitwise(kernel):
     for rec in golden()["random_cases"]:
         x, w, g, sb = oracle.random_case(rng, binary16=rec["binary16"])
         prec = F16 if rec["binary16"] else F32
-        if kernel == 3 and prec is F16:
-            continue
         filt = U.build_csr(U.DenseTensor4.from_array(w, prec), G(rec["geometry"]))
         out = U.sparse_conv_forward(U.DenseTensor4.from_array(x, prec), filt,
                                     U.ExecConfig(sb, kernel=kernel))
@@ -201,3 +199,28 @@ def test_round_to_binary16_device():
     x = (rng.standard_normal(100000) * np.exp(rng.uniform(-20, 12, 100000))).astype(np.float32)
     got = U.round_to_binary16(torch.from_numpy(x).cuda()).cpu().numpy()
     assert np.array_equal(got, oracle.round_to_binary16(x))
+
+
+def test_vgg16_binary16_network_vs_oracle():
+    """BINARY16 VGG-16 on the BI64 kernel (FHFMA, binary16 epilogue + fused pool)
+    against the reference composition: binary16 conv (fp32 accumulate, saturating
+    RNE output, engine.py:109-110), ReLU, max-pool."""
+    import torch
+    from paper_2112_15445_b200.models import VGG16_CIFAR, SparseVGG16, vgg16_rng, vgg16_weights
+    rng = vgg16_rng(0.93, seed=7)
+    ws = vgg16_weights(rng, 0.93, precision=F16)
+    x = oracle.round_to_binary16(rng.standard_normal((64, 3, 32, 32)).astype(np.float32))
+    m = SparseVGG16(ws, 64, precision=F16)
+    assert m.interleave == 64
+    got = m.forward(torch.from_numpy(x).cuda().half()).float().cpu().numpy()
+    a, li = x, 0
+    for v in VGG16_CIFAR:
+        if v == "M":
+            a = oracle.maxpool2(a)
+            continue
+        g = m.geoms[li]
+        gt = (g.in_channels, g.out_channels, 3, 3, g.input_h, g.input_w, (1, 1), (1, 1))
+        a = oracle.relu(oracle.sparse_conv_forward(a, oracle.build_csr(ws[li].data, gt), gt, binary16=True,
+                                                   threads=oracle.max_threads()))
+        li += 1
+    assert np.array_equal(got, a)

@@ -169,8 +169,12 @@ def test_planner_tiles():
     assert p.kernel == 1 and p.TH == 8 and p.NS * 8 * p.strips_per_row <= 256
     assert p.in_.ws % 4 == 0 and p.in_.hp == 10 and p.groups == 16
     assert p.smem_bytes <= 220 * 1024
-    p = make_plan(g1, 32, _lib.USC_F16, None)
+    p = make_plan(g1, 32, _lib.USC_F16, None)  # binary16: the BI64 kernel (two samples per lane)
+    assert p.kernel == 3 and p.in_.interleave == 64
+    p = make_plan(g1, 32, _lib.USC_F16, U.ExecConfig(kernel=1))
     assert p.kernel == 1 and p.in_.ws % 8 == 0
+    p = make_plan(g1, 32, _lib.USC_I8, None)  # int8 stays on the padded-NCHW kernel
+    assert p.kernel == 1
     # 1-D layer runs transposed
     p = make_plan(U.ConvGeometry(64, 64, 2, 1, 300, 1), 8, _lib.USC_F32, None)
     assert p.transposed == 1 and p.out_w == 299 and p.out_h == 1
