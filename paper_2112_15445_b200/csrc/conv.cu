@@ -28,6 +28,8 @@
 #include <algorithm>
 #include <cstdint>
 
+#include <type_traits>
+
 #include "common.cuh"
 #include "usc_internal.h"
 
@@ -235,8 +237,8 @@ __global__ void __launch_bounds__(256)
 
 // plain NCHW -> any layout; writes every destination element (halo and padding
 // samples become zeros).  Destination-ordered so stores are coalesced.
-template <typename T>
-__global__ void k_pad_any(const T *__restrict__ src, T *__restrict__ dst, int n, int H, int W,
+template <typename T, typename TD = T>
+__global__ void k_pad_any(const T *__restrict__ src, TD *__restrict__ dst, int n, int H, int W,
                           const LayoutD L, long long total) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
          i += (long long)gridDim.x * blockDim.x) {
@@ -255,7 +257,10 @@ __global__ void k_pad_any(const T *__restrict__ src, T *__restrict__ dst, int n,
         const int iy = y - L.ph, ix = x - L.pw;
         T v{};
         if (b < n && iy >= 0 && iy < H && ix >= 0 && ix < W) v = src[((b * L.C + c) * H + iy) * W + ix];
-        dst[i] = v;
+        if constexpr (std::is_same<T, TD>::value)
+            dst[i] = v;
+        else  // int8 code -> binary16 (exact)
+            dst[i] = __short2half_rn(static_cast<short>(v));
     }
 }
 
@@ -592,8 +597,14 @@ int usc_pad_input(const usc_act_layout *l, int32_t dtype, int32_t n, const void 
                                                       total);
             break;
         case 1:
-            k_pad_any<int8_t><<<grid, 256, 0, st>>>(static_cast<const int8_t *>(src), static_cast<int8_t *>(dst),
-                                                    n, l->height, l->width, L, total);
+            if (l->interleave)  // the BI kernel stages int8 codes as binary16
+                k_pad_any<int8_t, __half><<<grid, 256, 0, st>>>(static_cast<const int8_t *>(src),
+                                                                static_cast<__half *>(dst), n, l->height,
+                                                                l->width, L, total);
+            else
+                k_pad_any<int8_t><<<grid, 256, 0, st>>>(static_cast<const int8_t *>(src),
+                                                        static_cast<int8_t *>(dst), n, l->height, l->width, L,
+                                                        total);
             break;
         default: return fail(USC_ERR_VALUE, "unknown dtype %d", dtype);
     }

@@ -35,7 +35,7 @@ int launch_bi(const usc_plan *pl, const void *blob, const void *x, void *y, cons
     if (!enc) return fail(USC_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
     const cuuint64_t dims[5] = {(cuuint64_t)IL, (cuuint64_t)pl->in.ws, (cuuint64_t)pl->in.hp,
                                 (cuuint64_t)pl->g.in_channels, (cuuint64_t)((pl->n + IL - 1) / IL)};
-    const bool h16 = pl->dtype == USC_F16 || pl->dtype == USC_CB4;  // binary16 activations
+    const bool h16 = pl->dtype != USC_F32;  // binary16-staged activations (F16, CB4, I8 codes)
     const cuuint64_t px = (cuuint64_t)IL * (h16 ? 2 : 4);
     const cuuint64_t strides[4] = {px, px * pl->in.ws, px * pl->in.ws * pl->in.hp,
                                    px * pl->in.ws * pl->in.hp * pl->g.in_channels};
@@ -81,7 +81,9 @@ int launch_bi(const usc_plan *pl, const void *blob, const void *x, void *y, cons
     a.x_stage_bytes = static_cast<int>(pl->smem_stage_bytes);
     a.stage_bytes = static_cast<int>(pl->smem_stage_bytes + pl->ent_stage_bytes);
     a.ep = ep;
-    if (h16) return usc_bi::launch_h(pl, a, st);
+    if (pl->dtype == USC_F16) return usc_bi::launch_h16(pl, a, st);
+    if (pl->dtype == USC_CB4) return usc_bi::launch_hcb(pl, a, st);
+    if (pl->dtype == USC_I8) return usc_bi::launch_hi8(pl, a, st);
     switch (pl->threads) {
         case 256: return usc_bi::launch_w8(pl, a, st);
         case 384: return usc_bi::launch_w12(pl, a, st);

@@ -48,7 +48,7 @@ using namespace usc_dev;
 
 struct BiArgs {
     CUtensorMap xmap;        // x as 5-D [Nb][C][Hp][Wp][IL] (innermost first in the map)
-    void *y;                 // fp32 (F32) or binary16 (F16, CB4) output
+    void *y;                 // fp32 (F32, I8) or binary16 (F16, CB4) output
     const int *blk;          // byte offset of every (group, chunk) block, G*n_chunks+1
     const int *perm;         // output channel of every (group, warp, slot); -1 = empty
     const char *blocks;      // block base (16-byte aligned)
@@ -82,6 +82,7 @@ __device__ __forceinline__ void tma_load_5d(void *dst, const CUtensorMap *map, i
 //       binary16 x binary16 product is exact in fp32, so fma == FMUL+FADD bitwise.
 //   CB4 (binary16 x, fp32 codebook centroid): products have up to 26 significant
 //       bits, so FMUL then FADD (x widened with two conversions).
+//   I8  (int8 codes staged as binary16, code weights): the F16 arithmetic, exact.
 
 // shared-memory loads on 32-bit addresses with immediate offsets (LDS [R+imm]);
 // not volatile: the address depends on an entry read after the stage's mbarrier
@@ -174,6 +175,11 @@ template <> struct Ops<USC_F16, 2> {
     }
 };
 
+// int8 codes staged as binary16 (exact): the F16 arithmetic; every product and partial
+// sum is an integer below 2^24 (checked by the caller), so the fp32 accumulator equals
+// the int32 sum exactly and the epilogue scales it by sigma_w*sigma_x
+template <> struct Ops<USC_I8, 2> : Ops<USC_F16, 2> {};
+
 // the P pixels of a thread for one tap: row 0 at a0, row 1 at a1 (bytes), columns
 // SW pixels (SW*PXB bytes) apart
 template <int PC, int PXB, int SW, typename V, int... I>
@@ -190,7 +196,7 @@ template <int KIND, int SPL, int P>
 __device__ __forceinline__ void mac_one(typename Ops<KIND, SPL>::A (&acc)[P], typename Ops<KIND, SPL>::V (&v)[P],
                                         uint32_t t) {
     using O = Ops<KIND, SPL>;
-    if constexpr (KIND == USC_F16) {
+    if constexpr (KIND == USC_F16 || KIND == USC_I8) {
 #pragma unroll
         for (int p = 0; p < P; ++p) O::fma(acc[p], t, v[p]);
     } else {
@@ -207,7 +213,7 @@ template <int KIND, int SPL, int P>
 __device__ __forceinline__ void mac_pair(typename Ops<KIND, SPL>::A (&acc)[P], typename Ops<KIND, SPL>::V (&v0)[P],
                                          typename Ops<KIND, SPL>::V (&v1)[P], const int4 &n) {
     using O = Ops<KIND, SPL>;
-    if constexpr (KIND == USC_F16) {
+    if constexpr (KIND == USC_F16 || KIND == USC_I8) {
         mac_one<KIND, SPL, P>(acc, v0, static_cast<uint32_t>(n.y));
         mac_one<KIND, SPL, P>(acc, v1, static_cast<uint32_t>(n.w));
     } else {
@@ -300,6 +306,9 @@ template <int KIND>
 __device__ __forceinline__ float epi_value(float v, const Epi &ep) {
     // ReLU is np.where(v > 0, v, 0) (nn.py:96-98): NaN -> 0
     if constexpr (KIND == USC_F32) {
+        return ep.relu ? (v > 0.0f ? v : 0.0f) : v;
+    } else if constexpr (KIND == USC_I8) {  // fp32 out = acc * sigma_w * sigma_x (power of two)
+        v = __fmul_rn(v, ep.scale);
         return ep.relu ? (v > 0.0f ? v : 0.0f) : v;
     } else {
         if (ep.saturate) v = v > ep.cap ? ep.cap : v;  // np.minimum keeps NaN
@@ -540,7 +549,7 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1) k_bi(const __grid_constant_
 #pragma unroll
             for (int i = 0; i < P; ++i) {
                 if (i >= no || !ok[i]) continue;
-                if constexpr (KIND == USC_F32) {
+                if constexpr (KIND == USC_F32 || KIND == USC_I8) {
                     float *y = static_cast<float *>(a.y);
                     if (vec) {
                         *reinterpret_cast<float2 *>(y + off[i]) = make_float2(o[i][0], o[i][SPL - 1]);
@@ -584,6 +593,8 @@ int launch_inst(const usc_plan *pl, const BiArgs &a, cudaStream_t st) {
 int launch_w8(const usc_plan *pl, const BiArgs &a, cudaStream_t st);
 int launch_w12(const usc_plan *pl, const BiArgs &a, cudaStream_t st);
 int launch_w16(const usc_plan *pl, const BiArgs &a, cudaStream_t st);
-int launch_h(const usc_plan *pl, const BiArgs &a, cudaStream_t st);
+int launch_h16(const usc_plan *pl, const BiArgs &a, cudaStream_t st);
+int launch_hcb(const usc_plan *pl, const BiArgs &a, cudaStream_t st);
+int launch_hi8(const usc_plan *pl, const BiArgs &a, cudaStream_t st);
 
 }  // namespace usc_bi

@@ -246,7 +246,7 @@ static void tap_classes(int Y, int stride, int pad, int K, int X, std::vector<in
 
 // The k_bi instances compiled into the library (bi_instances.h).
 static bool bi_instance(int PC, int PR, int DW, int NW, int SW, int SPL, int dtype) {
-    if (dtype == USC_F16 || dtype == USC_CB4) {
+    if (dtype == USC_F16 || dtype == USC_CB4 || dtype == USC_I8) {
         if (SPL != 2) return false;
 #define XH(NW_, PC_, PR_, DW_, SW_) \
     if (NW == NW_ && PC == PC_ && PR == PR_ && DW == DW_ && SW == SW_) return true;
@@ -313,7 +313,7 @@ int usc_plan_make(const usc_geometry *g0, int32_t n, int32_t dtype, const usc_ex
     if (c.sub_batch < 1) c.sub_batch = 1;
     if (n % c.sub_batch)
         return fail(USC_ERR_VALUE, "sub_batch %d does not divide batch %d", c.sub_batch, n);
-    if (c.kernel == 0 && dtype != USC_I8) {
+    if (c.kernel == 0) {
         // auto: the batch-interleaved kernel when a compiled tile fits this layer, else
         // the padded-NCHW kernel
         usc_exec_cfg k3 = c;
@@ -336,21 +336,22 @@ int usc_plan_make(const usc_geometry *g0, int32_t n, int32_t dtype, const usc_ex
     }
     pl->g = g;
     usc_geometry_out(&g, &pl->out_h, &pl->out_w);
-    const int eb = elem_bytes(dtype);
-    int kernel = c.kernel ? c.kernel : (dtype == USC_I8 ? 1 : 3);
+    // staged element size: the BI kernel holds int8 codes as binary16 (exact, |code| <= 127)
+    int kernel = c.kernel ? c.kernel : 3;
     if (g.stride_w > 2) kernel = 2;
+    const int eb = (kernel == 3 && dtype == USC_I8) ? 2 : elem_bytes(dtype);
+
     // kernel 3 sample interleave: samples_per_cta 32 (BI32) or 64 (BI64, two samples per
     // lane); default BI64 once the batch fills two 32-sample blocks
     int IL = 0;
     if (kernel == 3) {
         IL = (c.samples_per_cta == 32 || c.samples_per_cta == 64) ? c.samples_per_cta : (n > 32 ? 64 : 32);
-        if (dtype == USC_F16 || dtype == USC_CB4) IL = 64;  // binary16 pairs: BI64 only
+        if (dtype != USC_F32) IL = 64;  // binary16-staged kinds: BI64 only
     }
     rc = usc_act_layout_make(g.in_channels, g.input_h, g.input_w, g.pad_h, g.pad_w, eb, IL, &pl->in);
     if (rc) return rc;
     const int Yh = pl->out_h, Yw = pl->out_w, Ws = pl->in.ws;
     const int threads = (c.threads == 128 || c.threads == 256) ? c.threads : 256;
-    if (kernel == 3 && dtype == USC_I8) return fail(USC_ERR_UNSUPPORTED, "BI kernel has no int8 variant");
     if (kernel == 3) {
         // batch-interleaved: a CTA = 32 samples x (WS strips of PR x PC pixels) x (WC*DW
         // channels), NW compute warps (threads = NW*32) + 1 producer warp; warp w owns
@@ -671,10 +672,11 @@ static uint16_t f32_to_f16_bits(float f) {
 }
 
 // the 32-bit theta word of stored entry j in a kernel-3 entry: fp32 bits (F32), the
-// binary16 bits in the low half (F16, FHFMA operand), the decoded fp32 centroid (CB4)
+// binary16 bits in the low half (F16; I8 codes, exact), the decoded fp32 centroid (CB4)
 static int32_t theta_word(int dtype, const void *payload, const float *table, int64_t j) {
     int32_t w = 0;
     if (dtype == USC_F16) return (int32_t)f32_to_f16_bits(((const float *)payload)[j]);
+    if (dtype == USC_I8) return (int32_t)f32_to_f16_bits((float)((const int8_t *)payload)[j]);
     if (dtype == USC_CB4) {
         std::memcpy(&w, &table[((const uint8_t *)payload)[j] & 15], 4);
         return w;
@@ -766,7 +768,7 @@ int usc_pack(const usc_plan *pl, const int64_t *row_ptr, const int64_t *col, con
         if (pl->kernel == 1)
             *off = cl * cs_tiled + kh * Ws + kw;
         else if (pl->kernel == 3)  // byte offset in the [CC][HS][TWs][IL] f32 stage
-            *off = ((cl * pl->HS + kh) * pl->TWs + kw) * elem_bytes(pl->dtype) * pl->in.interleave;
+            *off = ((cl * pl->HS + kh) * pl->TWs + kw) * (pl->dtype == USC_F32 ? 4 : 2) * pl->in.interleave;
         else
             *off = (c * Hp + kh) * Ws + kw;
         if (*off >= max_off || *off > INT32_MAX)
@@ -796,7 +798,7 @@ int usc_pack(const usc_plan *pl, const int64_t *row_ptr, const int64_t *col, con
         for (int64_t j = 0; j < (int64_t)D * n_nz && finite; ++j) {
             float t;
             const int32_t w = theta_word(pl->dtype, payload, table, j);
-            if (pl->dtype == USC_F16) {
+            if (pl->dtype == USC_F16 || pl->dtype == USC_I8) {
                 finite = (w & 0x7c00) != 0x7c00;
                 continue;
             }

@@ -178,7 +178,9 @@ def padded_input(x_dev, plan: _lib.Plan, stream=None):
     """Plain NCHW storage tensor -> the plan's padded layout (zero_pad, tensor.py:225-235)."""
     import torch
     lay = plan.in_
-    out = torch.empty(lay.elems(plan.n), dtype=x_dev.dtype, device=x_dev.device)
+    # the batch-interleaved kernel stages int8 codes as binary16 (exact)
+    dt = torch.float16 if (plan.kernel == 3 and plan.dtype == _lib.USC_I8) else x_dev.dtype
+    out = torch.empty(lay.elems(plan.n), dtype=dt, device=x_dev.device)
     _lib.check(_lib.lib().usc_pad_input(_lib.ref(lay), plan.dtype, plan.n, _lib.t_ptr(x_dev),
                                         _lib.t_ptr(out), _lib.stream_ptr(stream)), "pad")
     return out

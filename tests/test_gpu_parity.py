@@ -114,7 +114,7 @@ def test_int8_kernel_equals_reference_composition(name):
     fq = U.build_csr_int8(U.DenseTensor4.from_array(w), gg)
     xq = U.quantize_input_int8(_dev(x))
     assert xq.params.sigma == rec["sigma_x"]
-    for cfg in (U.ExecConfig(), U.ExecConfig(kernel=2)):
+    for cfg in (U.ExecConfig(), U.ExecConfig(kernel=1), U.ExecConfig(kernel=2)):
         out = U.sparse_conv_forward_int8(xq, fq, cfg)
         assert sha(out.data) == rec["out"], cfg
 
@@ -127,7 +127,7 @@ def test_codebook_kernel_equals_reference_composition(name):
     gg = G(rec["geometry"])
     fc = U.build_csr_codebook(U.DenseTensor4.from_array(w), gg)
     x16 = _dev(oracle.round_to_binary16(x), F16)
-    for cfg in (U.ExecConfig(), U.ExecConfig(kernel=2)):
+    for cfg in (U.ExecConfig(), U.ExecConfig(kernel=1), U.ExecConfig(kernel=2)):
         plain = U.sparse_conv_forward_codebook(x16, fc, config=cfg)
         assert sha(plain.data) == sha(oracle.round_to_binary16(_conv_ref(x16.data, fc, g)))
         out = U.sparse_conv_forward_codebook(x16, fc, 0.99, rec["calibrated_max"], config=cfg)

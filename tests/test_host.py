@@ -173,8 +173,9 @@ def test_planner_tiles():
     assert p.kernel == 3 and p.in_.interleave == 64
     p = make_plan(g1, 32, _lib.USC_F16, U.ExecConfig(kernel=1))
     assert p.kernel == 1 and p.in_.ws % 8 == 0
-    p = make_plan(g1, 32, _lib.USC_I8, None)  # int8 stays on the padded-NCHW kernel
-    assert p.kernel == 1
+    p = make_plan(g1, 32, _lib.USC_I8, None)  # int8 codes staged as binary16 in BI64
+    assert p.kernel == 3 and p.in_.interleave == 64
+    assert make_plan(g1, 32, _lib.USC_I8, U.ExecConfig(kernel=1)).kernel == 1
     # 1-D layer runs transposed
     p = make_plan(U.ConvGeometry(64, 64, 2, 1, 300, 1), 8, _lib.USC_F32, None)
     assert p.transposed == 1 and p.out_w == 299 and p.out_h == 1
