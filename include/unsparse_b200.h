@@ -134,6 +134,12 @@ typedef struct usc_epilogue {
     usc_act_layout out;          /* used when out_padded */
     int32_t pool;                /* 1: fused 2x2/2 max-pool after ReLU (nn.py:124-135); `out` is the
                                   * pooled layout; needs a BI plan with PR == 2 and even PC */
+    int32_t requant;             /* USC_I8, BI kernel: 1 = requantise the ReLU output to the next
+                                  * layer's fixed-point codes (linear_quantize, quantization.py:61-76):
+                                  * clip(copysign(floor(|v*rq_scale| + 0.5)), +-rq_limit), written as
+                                  * binary16 codes (the BI kernel's int8 staging) */
+    float rq_scale;              /* 1/sigma of the next layer's input (a power of two) */
+    int32_t rq_limit;            /* 2^(bits-1) - 1 */
 } usc_epilogue;
 
 /* ---- library ---------------------------------------------------------- */

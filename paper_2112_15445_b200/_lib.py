@@ -70,7 +70,8 @@ class Plan(ctypes.Structure):
 class Epilogue(ctypes.Structure):
     _fields_ = [("relu", c_i32), ("saturate", c_i32), ("cap", ctypes.c_float), ("saturate2", c_i32),
                 ("cap2", ctypes.c_float), ("scale", ctypes.c_float), ("out_padded", c_i32),
-                ("out", ActLayout), ("pool", c_i32)]
+                ("out", ActLayout), ("pool", c_i32), ("requant", c_i32), ("rq_scale", ctypes.c_float),
+                ("rq_limit", c_i32)]
 
 
 class CsrCorruptionError(ValueError):

@@ -71,6 +71,8 @@ struct Epi {
     int relu, saturate, saturate2, out_padded;
     float cap, cap2, scale;
     int oHp, oWs, oph, opw, oil, pool;
+    int requant, rq_limit;
+    float rq_scale;
     long long o_sample_stride;  // elements per sample (il 0) / interleave block (il 32, 64)
 };
 

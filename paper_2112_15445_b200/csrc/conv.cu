@@ -432,6 +432,9 @@ Epi make_epi(const usc_epilogue *e) {
     ep.cap2 = e->cap2;
     ep.scale = e->scale;
     ep.out_padded = e->out_padded;
+    ep.requant = e->requant;
+    ep.rq_scale = e->rq_scale;
+    ep.rq_limit = e->rq_limit;
     if (e->out_padded) {
         ep.oHp = e->out.hp;
         ep.oWs = e->out.ws;
@@ -501,6 +504,8 @@ int usc_conv_forward(const usc_plan *pl, const void *blob, const void *x, void *
         if (!ep.out_padded || epi->out.height != pl->out_h / 2 || epi->out.width != pl->out_w / 2)
             return fail(USC_ERR_VALUE, "fused max-pool needs the pooled output layout");
     }
+    if (ep.requant && (pl->kernel != 3 || pl->dtype != USC_I8))
+        return fail(USC_ERR_UNSUPPORTED, "requantising epilogue needs an int8 BI plan");
     if (pl->kernel == 3) return usc::launch_bi(pl, blob, x, y, ep, st);
     if (ep.out_padded && ep.oil != 0)
         return fail(USC_ERR_UNSUPPORTED, "kernels 1/2 write interleave-0 layouts only");

@@ -48,7 +48,7 @@ using namespace usc_dev;
 
 struct BiArgs {
     CUtensorMap xmap;        // x as 5-D [Nb][C][Hp][Wp][IL] (innermost first in the map)
-    void *y;                 // fp32 (F32, I8) or binary16 (F16, CB4) output
+    void *y;                 // fp32 (F32, I8) or binary16 (F16, CB4; I8 requantised codes) output
     const int *blk;          // byte offset of every (group, chunk) block, G*n_chunks+1
     const int *perm;         // output channel of every (group, warp, slot); -1 = empty
     const char *blocks;      // block base (16-byte aligned)
@@ -309,7 +309,14 @@ __device__ __forceinline__ float epi_value(float v, const Epi &ep) {
         return ep.relu ? (v > 0.0f ? v : 0.0f) : v;
     } else if constexpr (KIND == USC_I8) {  // fp32 out = acc * sigma_w * sigma_x (power of two)
         v = __fmul_rn(v, ep.scale);
-        return ep.relu ? (v > 0.0f ? v : 0.0f) : v;
+        if (ep.relu) v = v > 0.0f ? v : 0.0f;
+        if (ep.requant) {  // next layer's codes (linear_quantize in fp64, quantization.py:61-76)
+            const double q = static_cast<double>(v) * ep.rq_scale;
+            double c = copysign(floor(fabs(q) + 0.5), q);
+            c = c < -ep.rq_limit ? -ep.rq_limit : (c > ep.rq_limit ? ep.rq_limit : c);
+            v = static_cast<float>(c);
+        }
+        return v;
     } else {
         if (ep.saturate) v = v > ep.cap ? ep.cap : v;  // np.minimum keeps NaN
         v = round16f(v);
@@ -549,7 +556,7 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1) k_bi(const __grid_constant_
 #pragma unroll
             for (int i = 0; i < P; ++i) {
                 if (i >= no || !ok[i]) continue;
-                if constexpr (KIND == USC_F32 || KIND == USC_I8) {
+                if (KIND == USC_F32 || (KIND == USC_I8 && !a.ep.requant)) {
                     float *y = static_cast<float *>(a.y);
                     if (vec) {
                         *reinterpret_cast<float2 *>(y + off[i]) = make_float2(o[i][0], o[i][SPL - 1]);

@@ -59,33 +59,111 @@ def _cfg_of(plan, cfg: ExecConfig, il: int = 0) -> ExecConfig:
     return ExecConfig(**fields)
 
 
+MODES = ("fp32", "fp16", "int8", "cb4")
+
+
 class SparseVGG16:
     """Pruned VGG-16 CIFAR-10 conv trunk on one GPU, for a fixed batch.
 
-    forward(x) takes a plain NCHW (n,3,32,32) CUDA tensor (fp32, or fp16 for
-    BINARY16) and returns the (n,512,1,1) features.
+    Modes (the reference's precision modes, quantization.py:257-301, plus the int8
+    composition of SURVEY.md §8c):
+      fp32 -- BINARY32, bit-identical to sparse_conv_forward + ReLU + MaxPool2;
+      fp16 -- 16b/16b: binary16 weights and activations (every conv output rounds to
+              binary16), fp32 accumulation;
+      int8 -- 8-bit fixed point: each layer's input is linear_quantize(a, sigma_L) with
+              sigma_L calibrated (fit_fixed_point of the calibration batch's max|a|),
+              weights linear_quantize(w, fit_fixed_point(w, 8)); the conv epilogue
+              requantises the ReLU output straight to the next layer's codes;
+      cb4  -- 4b/16b: 16-centroid codebook weights (kmeans_codebook, psi 16), binary16
+              activations saturated at `saturation` x the calibrated maxima of the conv
+              and ReLU outputs (_half_hook), binary16 network input.
+    forward(x) takes a plain NCHW (n,3,32,32) CUDA tensor (fp32; fp16 for fp16/cb4)
+    and returns the (n,512,1,1) features (fp32 for fp32/int8, fp16 otherwise).
     """
 
     def __init__(self, weights, batch: int, precision=PrecisionMode.BINARY32, configs=None,
-                 device=None):
+                 device=None, mode: str | None = None, calibration=None, saturation: float = 0.99):
         import torch
-        self.precision = precision
-        self.dtype = _lib.USC_F16 if precision is PrecisionMode.BINARY16 else _lib.USC_F32
-        self.tdtype = torch.float16 if self.dtype == _lib.USC_F16 else torch.float32
-        self.eb = 2 if self.dtype == _lib.USC_F16 else 4
+        mode = mode or ("fp16" if precision is PrecisionMode.BINARY16 else "fp32")
+        if mode not in MODES:
+            raise ValueError(f"unknown mode {mode!r}; expected one of {MODES}")
+        self.mode = mode
+        self.precision = PrecisionMode.BINARY32 if mode == "fp32" else PrecisionMode.BINARY16
+        self.dtype = {"fp32": _lib.USC_F32, "fp16": _lib.USC_F16, "int8": _lib.USC_I8,
+                      "cb4": _lib.USC_CB4}[mode]
+        # staged activation storage: binary16 for every mode but fp32 (int8 codes exact)
+        self.tdtype = torch.float32 if mode == "fp32" else torch.float16
+        self.eb = 4 if mode == "fp32" else 2
         self.batch = batch
         self.device = torch.device(device or "cuda")
         self.geoms = vgg16_geometries()
-        self.filters = [build_csr(w, g) for w, g in zip(weights, self.geoms)]
+        self.tables = [None] * len(self.geoms)
+        if mode in ("fp32", "fp16"):
+            self.filters = [build_csr(w, g) for w, g in zip(weights, self.geoms)]
+            self.payloads = [f.weights for f in self.filters]
+        elif mode == "int8":
+            from .quantization import build_csr_int8
+            self.qfilters = [build_csr_int8(w, g) for w, g in zip(weights, self.geoms)]
+            self.filters = [q.filt for q in self.qfilters]
+            self.payloads = [q.codes for q in self.qfilters]
+        else:
+            from .quantization import build_csr_codebook
+            self.qfilters = [build_csr_codebook(w, g) for w, g in zip(weights, self.geoms)]
+            self.filters = [q.filt for q in self.qfilters]
+            self.payloads = [q.indices for q in self.qfilters]
+            self.tables = [q.table for q in self.qfilters]
         self.pre_pool = self._pre_pool_layers()
+        self.saturation = saturation
+        self.layer_params = [dict() for _ in self.geoms]
+        if mode in ("int8", "cb4"):
+            if calibration is None:
+                raise ValueError(f"{mode} needs calibration inputs")
+            self.calibrate(calibration)
         if configs:
             self.configs = list(configs)
         else:  # convs feeding a max-pool get 2-row pixel blocks so the pool fuses
             self.configs = [ExecConfig(rows_per_thread=2, pix_per_thread=min(4, g.out_w))
-                            if li in self.pre_pool and self.dtype == _lib.USC_F32 else ExecConfig()
+                            if li in self.pre_pool else ExecConfig()
                             for li, g in enumerate(self.geoms)]
         self.graph = None
         self._build()
+
+    # -- calibration (quantised modes) -----------------------------------------------
+    def calibrate(self, x):
+        """int8: per-layer input scales sigma_L = fit_fixed_point(max|a_L|, 8) along the
+        quantised network; cb4: maxima of every conv and ReLU output of the codebook
+        network in fp32 without hooks (calibrate_activation_maxima,
+        quantization.py:223-235).  Runs the layers eagerly through the public API."""
+        import torch
+        from .engine import sparse_conv_forward
+        from .quantization import quantize_input_int8, sparse_conv_forward_int8
+        from .tensor import DenseTensor4, round_to_binary16
+        a = x.to(self.device).float()
+        if self.mode == "cb4":
+            a = round_to_binary16(a)
+        self.sigmas = []
+        for li, g in enumerate(self.geoms):
+            if self.mode == "int8":
+                xq = quantize_input_int8(DenseTensor4(a))
+                self.sigmas.append(xq.params)
+                y = sparse_conv_forward_int8(xq, self.qfilters[li], relu=True).device()
+                a = y
+            else:
+                conv = sparse_conv_forward(DenseTensor4(a), self.filters[li]).device()
+                relu = torch.where(conv > 0, conv, torch.zeros_like(conv))
+                cmax, rmax = float(conv.max().item()), float(relu.max().item())
+                self.layer_params[li].update(
+                    cap=float(np.float32(self.saturation * cmax)), cap2=float(np.float32(self.saturation * rmax)))
+                a = relu
+            if li in self.pre_pool:
+                a = torch.nn.functional.max_pool2d(a, 2)
+        if self.mode == "int8":
+            for li in range(len(self.geoms)):
+                p = self.layer_params[li]
+                p["scale"] = float(np.float32(self.qfilters[li].params.sigma * self.sigmas[li].sigma))
+                if li + 1 < len(self.geoms):
+                    p["rq_scale"] = float(np.float32(1.0 / self.sigmas[li + 1].sigma))
+                    p["rq_limit"] = 2 ** (self.sigmas[li + 1].total_bits - 1) - 1
 
     @staticmethod
     def _pre_pool_layers():
@@ -99,11 +177,16 @@ class SparseVGG16:
         return out
 
     # -- buffers and plans ---------------------------------------------------
-    def _buf(self, lay):
+    def _buf(self, lay, dtype=None):
         import torch
-        return torch.zeros(lay.elems(self.batch), dtype=self.tdtype, device=self.device)
+        return torch.zeros(lay.elems(self.batch), dtype=dtype or self.tdtype, device=self.device)
+
+    def _plan_for(self, li, cfg):
+        return plan_for(self.filters[li], self.batch, self.dtype, cfg, self.payloads[li], self.tables[li],
+                        device=self.device)
 
     def _build(self):
+        import torch
         n = self.batch
         self.plans, self.blobs, self.steps = [], [], []
         # input buffer of the first conv
@@ -129,12 +212,21 @@ class SparseVGG16:
             if v == "M":
                 continue
             g = self.geoms[li]
-            plan, blob = plan_for(self.filters[li], n, self.dtype, plan_cfgs[li], self.filters[li].weights,
-                                  device=self.device)
+            plan, blob = self._plan_for(li, plan_cfgs[li])
             nxt = VGG16_CIFAR[i + 1] if i + 1 < len(VGG16_CIFAR) else None
             epi = _lib.Epilogue()
             epi.relu = 1
             epi.scale = 1.0
+            lp = self.layer_params[li]
+            out_dtype = None
+            if self.mode == "int8":
+                epi.scale = lp["scale"]
+                if "rq_scale" in lp:  # requantise to the next layer's codes
+                    epi.requant, epi.rq_scale, epi.rq_limit = 1, lp["rq_scale"], lp["rq_limit"]
+                else:  # the last layer: fp32 features
+                    out_dtype = torch.float32
+            elif self.mode == "cb4":  # _half_hook of the conv and of the ReLU
+                epi.saturate, epi.cap, epi.saturate2, epi.cap2 = 1, lp["cap"], 1, lp["cap2"]
             fuse = nxt == "M" and plan.kernel == 3 and plan.PR == 2 and plan.PC % 2 == 0
             last = i + 2 >= len(VGG16_CIFAR)
             if fuse:  # conv + ReLU + 2x2 max-pool in one kernel, pooled output padded for the next conv
@@ -147,7 +239,7 @@ class SparseVGG16:
                 out_lay = _lib.act_layout(g.out_channels, g.out_h, g.out_w, 1, 1, self.eb, il)
             epi.out_padded = 1
             epi.out = out_lay
-            out_buf = self._buf(out_lay)
+            out_buf = self._buf(out_lay, out_dtype)
             self.steps.append(("conv", li, plan, blob, cur_buf, out_buf, epi))
             self.nonzero_macs += int(np.count_nonzero(self.filters[li].weights)) * g.out_h * g.out_w * n
             cur_buf, cur_lay = out_buf, out_lay
@@ -155,7 +247,7 @@ class SparseVGG16:
                 last = i + 2 >= len(VGG16_CIFAR)
                 ph = 0 if last else 1
                 pool_lay = _lib.act_layout(g.out_channels, g.out_h // 2, g.out_w // 2, ph, ph, self.eb, il)
-                pool_buf = self._buf(pool_lay)
+                pool_buf = self._buf(pool_lay, cur_buf.dtype)
                 self.steps.append(("pool", li, cur_lay, pool_lay, cur_buf, pool_buf))
                 cur_buf, cur_lay = pool_buf, pool_lay
             li += 1
@@ -163,7 +255,16 @@ class SparseVGG16:
 
     # -- execution -------------------------------------------------------------
     def load_input(self, x, stream=None):
-        """Plain NCHW device tensor -> the first conv's padded input buffer."""
+        """Plain NCHW device tensor -> the first conv's padded input buffer (int8: the
+        calibrated first-layer codes, quantised on the device)."""
+        import torch
+        if self.mode == "int8":
+            if not hasattr(self, "_codes_in"):
+                self._codes_in = torch.empty(x.shape, dtype=torch.int8, device=self.device)
+            p0 = self.sigmas[0]
+            _lib.check(_lib.lib().usc_quantize_i8(_lib.t_ptr(x), _lib.t_ptr(self._codes_in), x.numel(),
+                                                  p0.sigma, p0.total_bits, _lib.stream_ptr(stream)), "quantize")
+            x = self._codes_in
         _lib.check(_lib.lib().usc_pad_input(_lib.ref(self.in_layout), self.dtype, self.batch,
                                             _lib.t_ptr(x), _lib.t_ptr(self.x_buf),
                                             _lib.stream_ptr(stream)), "pad")
@@ -179,7 +280,8 @@ class SparseVGG16:
                                               _lib.t_ptr(yout), _lib.ref(epi), sp), "conv")
             else:
                 _, _, lin, lout, xin, yout = st
-                _lib.check(L.usc_maxpool2(_lib.ref(lin), _lib.ref(lout), self.dtype, self.batch,
+                pdt = _lib.USC_F32 if xin.element_size() == 4 else _lib.USC_F16
+                _lib.check(L.usc_maxpool2(_lib.ref(lin), _lib.ref(lout), pdt, self.batch,
                                           _lib.t_ptr(xin), _lib.t_ptr(yout), sp), "pool")
 
     def output(self, stream=None):
@@ -188,8 +290,9 @@ class SparseVGG16:
         lay = self.out_layout
         if not hasattr(self, "_out_plain"):
             self._out_plain = torch.empty((self.batch, lay.channels, lay.height, lay.width),
-                                          dtype=self.tdtype, device=self.device)
-        _lib.check(_lib.lib().usc_unpad_output(_lib.ref(lay), self.dtype, self.batch,
+                                          dtype=self.out_buf.dtype, device=self.device)
+        odt = _lib.USC_F32 if self.out_buf.element_size() == 4 else _lib.USC_F16
+        _lib.check(_lib.lib().usc_unpad_output(_lib.ref(lay), odt, self.batch,
                                                _lib.t_ptr(self.out_buf), _lib.t_ptr(self._out_plain),
                                                _lib.stream_ptr(stream)), "unpad")
         return self._out_plain
@@ -243,8 +346,7 @@ class SparseVGG16:
                 cands = [c for c in cands if c.rows_per_thread == 2 and c.pix_per_thread % 2 == 0]
             for cfg in cands:
                 try:
-                    plan, blob = plan_for(self.filters[li], self.batch, self.dtype, cfg,
-                                          self.filters[li].weights, device=self.device)
+                    plan, blob = self._plan_for(li, cfg)
                 except ValueError:
                     continue
                 ms = time_median_cuda(lambda: launch(plan, blob, xin, yout, epi), repeats, warmup)

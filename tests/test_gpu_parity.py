@@ -224,3 +224,62 @@ def test_vgg16_binary16_network_vs_oracle():
                                                    threads=oracle.max_threads()))
         li += 1
     assert np.array_equal(got, a)
+
+
+def _vgg_oracle(m, x, conv_fn):
+    """Reference composition of the VGG-16 trunk with a per-layer conv function."""
+    from paper_2112_15445_b200.models import VGG16_CIFAR
+    a, li = x, 0
+    for v in VGG16_CIFAR:
+        if v == "M":
+            a = oracle.maxpool2(a)
+            continue
+        g = m.geoms[li]
+        gt = (g.in_channels, g.out_channels, 3, 3, g.input_h, g.input_w, (1, 1), (1, 1))
+        a = conv_fn(li, a, gt)
+        li += 1
+    return a
+
+
+def test_vgg16_int8_network_vs_oracle():
+    """8-bit fixed-point VGG-16 (calibrated per-layer input scales, requantising
+    epilogue) equals the reference composition layer by layer: linear_quantize the
+    input with the layer's sigma, sparse_conv_forward with build_csr(linear_quantize(w)),
+    ReLU, max-pool (quantization.py:41-76, csr.py:86-112, engine.py:64-111)."""
+    import torch
+    from paper_2112_15445_b200.models import SparseVGG16, vgg16_rng, vgg16_weights
+    rng = vgg16_rng(0.93, seed=11)
+    ws = vgg16_weights(rng, 0.93)
+    x = rng.standard_normal((64, 3, 32, 32)).astype(np.float32)
+    m = SparseVGG16(ws, 64, mode="int8", calibration=torch.from_numpy(x).cuda())
+    got = m.forward(torch.from_numpy(x).cuda()).cpu().numpy()
+
+    def conv(li, a, gt):
+        s = m.sigmas[li]
+        p = dict(total_bits=s.total_bits, sigma=s.sigma, mu=0.0)
+        xq = oracle.linear_quantize(a.astype(np.float32), p)
+        f = m.filters[li]
+        return oracle.relu(oracle.sparse_conv_forward(xq, (f.row_ptr, f.col_offsets, f.weights, f.n_nz), gt,
+                                                      threads=oracle.max_threads()))
+    assert np.array_equal(got, _vgg_oracle(m, x, conv))
+
+
+def test_vgg16_codebook_network_vs_oracle():
+    """4b/16b VGG-16: codebook weights, binary16 activations with the _half_hook
+    saturation at 0.99 x the calibrated conv / ReLU maxima (quantization.py:223-301)."""
+    import torch
+    from paper_2112_15445_b200.models import SparseVGG16, vgg16_rng, vgg16_weights
+    rng = vgg16_rng(0.93, seed=13)
+    ws = vgg16_weights(rng, 0.93)
+    x = oracle.round_to_binary16(rng.standard_normal((64, 3, 32, 32)).astype(np.float32))
+    m = SparseVGG16(ws, 64, mode="cb4", calibration=torch.from_numpy(x).cuda())
+    got = m.forward(torch.from_numpy(x).cuda().half()).float().cpu().numpy()
+
+    def conv(li, a, gt):
+        f, lp = m.filters[li], m.layer_params[li]
+        y = oracle.sparse_conv_forward(a, (f.row_ptr, f.col_offsets, f.weights, f.n_nz), gt,
+                                       threads=oracle.max_threads())
+        y = oracle.round_to_binary16(np.minimum(y, np.float32(lp["cap"])))
+        y = oracle.relu(y)
+        return oracle.round_to_binary16(np.minimum(y, np.float32(lp["cap2"])))
+    assert np.array_equal(got, _vgg_oracle(m, x, conv))
