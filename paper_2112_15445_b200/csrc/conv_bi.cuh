@@ -329,6 +329,11 @@ __device__ __forceinline__ float epi_value(float v, const Epi &ep) {
     }
 }
 
+__device__ __forceinline__ uint32_t pack_h2(float lo, float hi) {  // exact: values on the binary16 grid
+    const __half2 h = __halves2half2(__float2half_rn(lo), __float2half_rn(hi));
+    return *reinterpret_cast<const uint32_t *>(&h);
+}
+
 // max-pool of a 2x2 window in np.argmax order (nn.py:124-135): first NaN, else
 // first maximum
 __device__ __forceinline__ float pool4(float w0, float w1, float w2, float w3) {
@@ -553,10 +558,40 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1) k_bi(const __grid_constant_
                 }
                 no = P;
             }
+            const bool f32out = KIND == USC_F32 || (KIND == USC_I8 && !a.ep.requant);
+            // sample-major layouts (plain NCHW / padded NCHW): a lane's pixels of one row are
+            // contiguous, so full 4-pixel groups go out as one 16-byte (fp32) or 8-byte
+            // (binary16) store per sample instead of four scalar ones
+            if constexpr (PC % 4 == 0) {
+                if (!vec && cstride == 1 && (sstride & 3) == 0 && (reinterpret_cast<uintptr_t>(a.y) & 15) == 0) {
+                    const int rows = no / PC > 0 ? no / PC : 1, per = no < PC ? no : PC;  // pooled: 1 row
+#pragma unroll
+                    for (int rr = 0; rr < PR; ++rr) {
+                        if (rr >= rows) break;
+#pragma unroll
+                        for (int q = 0; q < PC / 4; ++q) {
+                            const int i = rr * per + 4 * q;
+                            if (4 * q + 3 >= per || !ok[i] || !ok[i + 3] || (off[i] & 3)) continue;
+#pragma unroll
+                            for (int j = 0; j < SPL; ++j) {
+                                if (b0 + j >= a.N) continue;
+                                if (f32out)
+                                    *reinterpret_cast<float4 *>(static_cast<float *>(a.y) + off[i] + j * sstride) =
+                                        make_float4(o[i][j], o[i + 1][j], o[i + 2][j], o[i + 3][j]);
+                                else
+                                    *reinterpret_cast<uint2 *>(static_cast<__half *>(a.y) + off[i] + j * sstride) =
+                                        make_uint2(pack_h2(o[i][j], o[i + 1][j]), pack_h2(o[i + 2][j], o[i + 3][j]));
+                            }
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) ok[i + u] = false;  // stored
+                        }
+                    }
+                }
+            }
 #pragma unroll
             for (int i = 0; i < P; ++i) {
                 if (i >= no || !ok[i]) continue;
-                if (KIND == USC_F32 || (KIND == USC_I8 && !a.ep.requant)) {
+                if (f32out) {
                     float *y = static_cast<float *>(a.y);
                     if (vec) {
                         *reinterpret_cast<float2 *>(y + off[i]) = make_float2(o[i][0], o[i][SPL - 1]);

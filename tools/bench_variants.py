@@ -78,6 +78,27 @@ def vgg16_fp16(steps):
             "speedup_vs_cudnn": round(cd / ms, 3)}
 
 
+def vgg16_quantised(mode, steps):
+    """int8 / cb4 VGG-16 at batch 256 (cfg4): calibrated on the timed batch itself."""
+    from paper_2112_15445_b200.models import SparseVGG16, vgg16_rng, vgg16_weights
+    from paper_2112_15445_b200.tensor import round_to_binary16
+    batch = 256
+    ws = vgg16_weights(vgg16_rng(0.93, 0), 0.93)
+    x = torch.randn(batch, 3, 32, 32, device="cuda")
+    if mode == "cb4":
+        x = round_to_binary16(x)
+    m = SparseVGG16(ws, batch, mode=mode, calibration=x)
+    m.autotune(repeats=3, warmup=1)
+    m.capture()
+    m.load_input(x if mode == "int8" else x.half())
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
+    ms = timed(lambda: m.graph.replay(), steps, flush)
+    return {"config": f"pruned VGG-16 CIFAR-10 93% {mode}, batch 256",
+            "dtype": {"int8": "int8 codes (staged binary16), exact fp32 accumulate",
+                      "cb4": "4-bit codebook weights, binary16 activations"}[mode],
+            "images_per_s": round(batch / (ms / 1e3), 1), "ms_per_step": round(ms, 4)}
+
+
 def sweep(steps):
     from paper_2112_15445_b200 import DenseTensor4, autotune_sb, build_csr, sparse_conv_forward
     from paper_2112_15445_b200.engine import launch, padded_input, plan_for, time_median_cuda
@@ -118,6 +139,9 @@ def main():
     args = ap.parse_args()
     if args.only in (None, "vgg16-fp16"):
         print(json.dumps({"variant": "vgg16-fp16", **vgg16_fp16(args.steps)}), flush=True)
+    for mode in ("int8", "cb4"):
+        if args.only in (None, f"vgg16-{mode}"):
+            print(json.dumps({"variant": f"vgg16-{mode}", **vgg16_quantised(mode, args.steps)}), flush=True)
     if args.only in (None, "sweep"):
         for row in sweep(args.steps):
             print(json.dumps({"variant": "sweep", **row}), flush=True)
