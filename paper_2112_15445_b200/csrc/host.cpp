@@ -465,13 +465,19 @@ int usc_plan_make(const usc_geometry *g0, int32_t n, int32_t dtype, const usc_ex
         // per-pixel-class runs (1x1 pixel blocks): one entry run per (class, slot) without
         // the taps that land on the zero halo
         int ncr = 1, ncc = 1;
-        if (c.pixel_classes && PC == 1 && PR == 1 && g.filter_h <= 32 && g.filter_w <= 32) {
+        // (row classes need 1-row blocks, column classes 1-column blocks: every pixel of a
+        // thread's block must share the valid-tap set along a classed axis)
+        if (c.pixel_classes && (PC == 1 || PR == 1) && g.filter_h <= 32 && g.filter_w <= 32) {
             std::vector<int> cl;
             std::vector<uint32_t> mk;
-            tap_classes(Yh, g.stride_h, g.pad_h, g.filter_h, g.input_h, cl, mk);
-            ncr = (int)mk.size();
-            tap_classes(Yw, g.stride_w, g.pad_w, g.filter_w, g.input_w, cl, mk);
-            ncc = (int)mk.size();
+            if (PR == 1) {
+                tap_classes(Yh, g.stride_h, g.pad_h, g.filter_h, g.input_h, cl, mk);
+                ncr = (int)mk.size();
+            }
+            if (PC == 1) {
+                tap_classes(Yw, g.stride_w, g.pad_w, g.filter_w, g.input_w, cl, mk);
+                ncc = (int)mk.size();
+            }
         }
         const int NCLS = ncr * ncc;
         int CC = c.chunk_channels ? c.chunk_channels : 64;
@@ -806,8 +812,8 @@ int usc_pack(const usc_plan *pl, const int64_t *row_ptr, const int64_t *col, con
             finite = std::isfinite(t);
         }
         if (NCLS > 1 && finite) {
-            tap_classes(pl->out_h, g.stride_h, g.pad_h, g.filter_h, g.input_h, rowcls, rmask);
-            tap_classes(pl->out_w, g.stride_w, g.pad_w, g.filter_w, g.input_w, colcls, cmask);
+            if (pl->ncls_r > 1) tap_classes(pl->out_h, g.stride_h, g.pad_h, g.filter_h, g.input_h, rowcls, rmask);
+            if (pl->ncls_c > 1) tap_classes(pl->out_w, g.stride_w, g.pad_w, g.filter_w, g.input_w, colcls, cmask);
         }
         std::vector<std::vector<std::pair<int64_t, int64_t>>> per(D);  // (chunk, off) per d
         std::vector<std::vector<int64_t>> src(D);

@@ -321,7 +321,7 @@ def tile_candidates(geometry: ConvGeometry, n: int, sb_values, precision=Precisi
                 if ws > strips:
                     break
                 # per-pixel-class runs (halo taps dropped) for 1x1 blocks on small maps
-                classes = (0, 1) if pc == 1 and pr == 1 and yh * yw <= 64 else (0,)
+                classes = (0, 1) if (pc == 1 or pr == 1) and yh * yw <= 64 else (0,)
                 for st in (2, 3):
                     for pcl in classes:
                         out.append(ExecConfig(sub_batch=min(sb_values), pix_per_thread=pc, rows_per_thread=pr,
