@@ -165,6 +165,16 @@ int64_t usc_act_layout_elems(const usc_act_layout *layout, int32_t n);
 int usc_csr_count(const float *w, const usc_geometry *g, int64_t *n_nz);
 int usc_build_csr(const float *w, const usc_geometry *g, int64_t n_nz, int64_t *row_ptr,
                   int64_t *col_offsets, float *theta);
+/* Device-side encoder (csr.py:86-112 on the GPU, bit-identical to usc_build_csr), for
+ * pruning loops that re-encode every iteration.  w: device f32 D x C x Kh x Kw.
+ * Pass 1 writes the per-channel genuine-nonzero counts (int32[D]) and their maximum
+ * (int32[1]); the caller reads n_nz = max(1, max) to size col/theta (D*n_nz), then
+ * pass 2 writes row_ptr (int64[D+1]), col_offsets (int64) and theta (f32) on the device. */
+int usc_csr_count_device(const float *w_dev, const usc_geometry *g, int32_t *counts_dev, int32_t *max_count_dev,
+                         void *stream);
+int usc_build_csr_device(const float *w_dev, const usc_geometry *g, const int32_t *counts_dev,
+                         const int32_t *max_count_dev, int64_t *row_ptr_dev, int64_t *col_offsets_dev,
+                         float *theta_dev, void *stream);
 /* CsrFilter.validate (csr.py:66-83).  On USC_ERR_CORRUPT, *bad_index receives
  * the first entry whose offset does not decode to a tap (or -1 for a
  * row_ptr / length violation). */

@@ -283,3 +283,23 @@ def test_vgg16_codebook_network_vs_oracle():
         y = oracle.relu(y)
         return oracle.round_to_binary16(np.minimum(y, np.float32(lp["cap2"])))
     assert np.array_equal(got, _vgg_oracle(m, x, conv))
+
+
+@pytest.mark.parametrize("name", ["cfg1-vgg16-256x8", "vgg16-512x14", "resnet50-1x1-64x256", "sweep-3x3-256x8-98",
+                                  "cnn1d-300x64-k3"])
+def test_device_encoder_bitwise(name):
+    """usc_build_csr_device == build_csr (csr.py:86-112): RP, Lambda, theta, n_nz."""
+    import torch
+    rec = golden()["layers"][name]
+    g = geom(rec["geometry"])
+    _, w = layer_inputs(name, g, rec["sparsity"], rec["batch"], rec["binary16"])
+    gg = G(rec["geometry"])
+    host = U.build_csr(U.DenseTensor4.from_array(w), gg)
+    dev = U.build_csr_device(torch.from_numpy(np.ascontiguousarray(w)).cuda(), gg)
+    assert dev.n_nz == host.n_nz == rec["csr"]["n_nz"]
+    assert np.array_equal(dev.row_ptr, host.row_ptr) and np.array_equal(dev.col_offsets, host.col_offsets)
+    assert np.array_equal(dev.weights.view(np.uint32), host.weights.view(np.uint32))
+    for k in ("row_ptr", "col_offsets", "weights"):  # and the reference's own digests
+        assert sha(getattr(dev, k)) == rec["csr"][k]
+    zero = np.zeros_like(w)
+    assert U.build_csr_device(torch.from_numpy(zero).cuda(), gg).n_nz == 1  # max(1, 0)
