@@ -4,6 +4,9 @@
   * vgg16-fp16  -- pruned VGG-16 CIFAR-10, 93% sparsity, BINARY16 (binary16 storage,
     fp32 accumulate, binary16 hook), batch 256, vs cuDNN fp16 (channels_last, tensor
     cores) on the same masked weights;
+  * vgg16-int8 / vgg16-cb4 -- the quantised networks of configs[3];
+  * resnet50-fp16 -- configs[2]: the 53 convs of ResNet-50 CIFAR at 90%, BINARY16, vs
+    cuDNN fp16 on tensor cores (layer sum);
   * sweep       -- one 3x3 layer shape at batch 1024 across sparsities 50-98%
     (configs[4]), fp32, vs cuDNN fp32 (TF32 off).
 
@@ -21,6 +24,15 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
+
+
+def measured_hbm_peak() -> float:
+    """HBM GB/s from the driver-written MEASURED_PEAKS.json, else the profiling
+    guide's B200 fallback."""
+    p = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        return float(json.load(open(p)).get("hbm_gbs", 6650.0))
+    return 6650.0
 
 
 def timed(fn, steps, flush=None):
@@ -99,17 +111,102 @@ def vgg16_quantised(mode, steps):
             "images_per_s": round(batch / (ms / 1e3), 1), "ms_per_step": round(ms, 4)}
 
 
-def sweep(steps):
+def _resident_launch(plan, blob, xp, d, g, batch, dtype):
+    """One layer launch writing the engine's resident layout (the plan's interleave,
+    zero halo of 1 as the next 3x3 layer reads) -- what a network layer does; the
+    plain-NCHW output of sparse_conv_forward is a host-facing convenience."""
+    from paper_2112_15445_b200 import _lib
+    from paper_2112_15445_b200.engine import launch
+    il = plan.in_.interleave
+    lay = _lib.act_layout(d, g.out_h, g.out_w, 1, 1, 4 if dtype == torch.float32 else 2, il)
+    y = torch.zeros(lay.elems(batch), dtype=dtype, device="cuda")
+    epi = _lib.Epilogue()
+    epi.scale, epi.out_padded, epi.out = 1.0, 1, lay
+    return lambda: launch(plan, blob, xp, y, epi)
+
+
+def resnet50_cifar_convs():
+    """(name, geometry kwargs, torch stride/padding, count) for the 53 convs of ResNet-50
+    on 32x32 inputs (3x3 stem, no max-pool, bottleneck stages at 32/16/8/4, stride on the
+    3x3 and the projection).  Stride-2 layers use the reference's exact geometries
+    (ConvGeometry rejects 32 -> 16 with pad 1, tensor.py:186-190): the 3x3 reads a
+    top/left pre-padded 33x33 input with pad 0, the 1x1 projection a 31x31 crop."""
+    out = [("stem-3x3-3x64-32", dict(c=3, d=64, k=3, hw=32, s=1, p=1), 1)]
+    c_in, hw = 64, 32
+    for width, blocks, stride in ((64, 3, 1), (128, 4, 2), (256, 6, 2), (512, 3, 2)):
+        for b in range(blocks):
+            s = stride if b == 0 else 1
+            out.append((f"1x1-{c_in}x{width}-{hw}", dict(c=c_in, d=width, k=1, hw=hw, s=1, p=0), 1))
+            out.append((f"3x3-{width}x{width}-{hw}-s{s}", dict(c=width, d=width, k=3, hw=hw, s=s, p=1), 1))
+            hw_out = hw // s
+            out.append((f"1x1-{width}x{4 * width}-{hw_out}", dict(c=width, d=4 * width, k=1, hw=hw_out, s=1, p=0), 1))
+            if b == 0:
+                out.append((f"proj-1x1-{c_in}x{4 * width}-{hw}-s{s}", dict(c=c_in, d=4 * width, k=1, hw=hw, s=s, p=0), 1))
+            c_in, hw = 4 * width, hw_out
+    merged = {}
+    for name, kw, n in out:
+        merged.setdefault(name, [kw, 0])[1] += n
+    return [(k, v[0], v[1]) for k, v in merged.items()]
+
+
+def resnet50_fp16(batch=256, sparsity=0.9):
+    """cfg3: per-layer binary16 sparse conv vs cuDNN fp16 (tensor cores), summed over the
+    53 convs of ResNet-50 CIFAR (layer-sum; residual adds and the classifier excluded)."""
+    from paper_2112_15445_b200 import DenseTensor4, PrecisionMode, autotune_sb, build_csr
+    from paper_2112_15445_b200.engine import launch, padded_input, plan_for, time_median_cuda
+    from paper_2112_15445_b200.pruning import synthesize_masked_weights
+    from paper_2112_15445_b200.tensor import ConvGeometry
+    F16 = PrecisionMode.BINARY16
+    rows, tot_s, tot_c, n_convs = [], 0.0, 0.0, 0
+    torch.backends.cudnn.benchmark = True
+    for name, kw, count in resnet50_cifar_convs():
+        c, d, k, hw, s, p = kw["c"], kw["d"], kw["k"], kw["hw"], kw["s"], kw["p"]
+        if s == 2 and k == 3:
+            g = ConvGeometry(c, d, 3, 3, hw + 1, hw + 1, stride=(2, 2))
+        elif s == 2:
+            g = ConvGeometry(c, d, 1, 1, hw - 1, hw - 1, stride=(2, 2))
+        else:
+            g = ConvGeometry(c, d, k, k, hw, hw, padding=(p, p))
+        rng = np.random.default_rng([0, len(name), c, d, hw])
+        w = synthesize_masked_weights(g, sparsity, rng, F16)
+        f = build_csr(w, g)
+        x = torch.randn(batch, c, g.input_h, g.input_w, device="cuda").half()
+        cfg = autotune_sb(DenseTensor4(x, F16), f, repeats=3, warmup=1)
+        plan, blob = plan_for(f, batch, 1, cfg, f.weights)
+        xp = padded_input(x, plan)
+        ms = time_median_cuda(_resident_launch(plan, blob, xp, d, g, batch, torch.float16), 9, 2)
+        xt = torch.randn(batch, c, hw, hw, device="cuda").half().contiguous(memory_format=torch.channels_last)
+        wt = torch.from_numpy(np.array(w.data)).cuda().half().contiguous(memory_format=torch.channels_last)
+        cd = time_median_cuda(lambda: torch.nn.functional.conv2d(xt, wt, stride=s, padding=p), 9, 2)
+        rows.append({"layer": name, "count": count, "us": round(ms * 1e3, 1), "cudnn_fp16_us": round(cd * 1e3, 1),
+                     "kernel": plan.describe()["kernel"]})
+        tot_s += ms * count
+        tot_c += cd * count
+        n_convs += count
+    return {"config": f"pruned ResNet-50 CIFAR {int(sparsity * 100)}% BINARY16, batch {batch}, 53-conv layer sum",
+            "convs": n_convs, "sparse_ms": round(tot_s, 4), "cudnn_fp16_ms": round(tot_c, 4),
+            "images_per_s_conv_only": round(batch / (tot_s / 1e3), 1),
+            "cudnn_images_per_s_conv_only": round(batch / (tot_c / 1e3), 1),
+            "speedup_vs_cudnn": round(tot_c / tot_s, 3), "layers": rows}
+
+
+SWEEP_SHAPES = {"r50-3x3-64x32": (64, 64, 3, 32), "r50-3x3-256x8": (256, 256, 3, 8),
+                "r50-1x1-64x256-32": (64, 256, 1, 32), "r50-1x1-256x64-32": (256, 64, 1, 32)}
+
+
+def sweep(steps, shapes=None, sparsities=(0.5, 0.7, 0.9, 0.95, 0.98)):
     from paper_2112_15445_b200 import DenseTensor4, autotune_sb, build_csr, sparse_conv_forward
     from paper_2112_15445_b200.engine import launch, padded_input, plan_for, time_median_cuda
     from paper_2112_15445_b200.pruning import synthesize_masked_weights
     from paper_2112_15445_b200.tensor import ConvGeometry
     out = []
     batch = 1024
-    for name, (c, d, hw) in {"r50-3x3-64x32": (64, 64, 32), "r50-3x3-256x8": (256, 256, 8)}.items():
-        g = ConvGeometry(c, d, 3, 3, hw, hw, padding=(1, 1))
+    for name, (c, d, k, hw) in SWEEP_SHAPES.items():
+        if shapes and name not in shapes:
+            continue
+        g = ConvGeometry(c, d, k, k, hw, hw, padding=(k // 2, k // 2))
         x = torch.randn(batch, c, hw, hw, device="cuda")
-        for s in (0.5, 0.7, 0.9, 0.95, 0.98):
+        for s in sparsities:
             rng = np.random.default_rng([0, int(s * 1000)])
             w = synthesize_masked_weights(g, s, rng)
             f = build_csr(w, g)
@@ -117,16 +214,22 @@ def sweep(steps):
             cfg = autotune_sb(xd, f, repeats=3, warmup=1)
             plan, blob = plan_for(f, batch, 0, cfg, f.weights)
             xp = padded_input(x, plan)
+            ms = time_median_cuda(_resident_launch(plan, blob, xp, d, g, batch, torch.float32), 9, 2)
             y = torch.empty(batch, d, hw, hw, device="cuda")
-            ms = time_median_cuda(lambda: launch(plan, blob, xp, y), 9, 2)
+            ms_plain = time_median_cuda(lambda: launch(plan, blob, xp, y), 9, 2)
             torch.backends.cudnn.benchmark = True
             torch.backends.cudnn.allow_tf32 = False
             wd = torch.from_numpy(np.array(w.data)).cuda()
-            cd = time_median_cuda(lambda: torch.nn.functional.conv2d(x, wd, padding=1), 9, 2)
+            cd = time_median_cuda(lambda: torch.nn.functional.conv2d(x, wd, padding=k // 2), 9, 2)
             genuine = int(np.count_nonzero(f.weights))
             flops = 2.0 * genuine * hw * hw * batch
+            # algorithmic bytes: input + output once + 8 B per entry
+            nbytes = 4.0 * batch * (c + d) * hw * hw + 8.0 * genuine
             out.append({"layer": name, "sparsity": s, "batch": batch, "us": round(ms * 1e3, 1),
+                        "us_plain_nchw_out": round(ms_plain * 1e3, 1),
                         "nonzero_tflops": round(flops / (ms / 1e3) / 1e12, 2),
+                        "hbm_gbs": round(nbytes / (ms / 1e3) / 1e9, 1),
+                        "hbm_frac": round(nbytes / (ms / 1e3) / 1e9 / measured_hbm_peak(), 3),
                         "cudnn_fp32_us": round(cd * 1e3, 1), "speedup_vs_cudnn": round(cd / ms, 3),
                         "plan": plan.describe()})
     return out
@@ -142,8 +245,11 @@ def main():
     for mode in ("int8", "cb4"):
         if args.only in (None, f"vgg16-{mode}"):
             print(json.dumps({"variant": f"vgg16-{mode}", **vgg16_quantised(mode, args.steps)}), flush=True)
-    if args.only in (None, "sweep"):
-        for row in sweep(args.steps):
+    if args.only in (None, "resnet50-fp16"):
+        print(json.dumps({"variant": "resnet50-fp16", **resnet50_fp16()}), flush=True)
+    if args.only in (None, "sweep") or (args.only or "").startswith("sweep:"):
+        shapes = args.only.split(":", 1)[1].split(",") if args.only and ":" in args.only else None
+        for row in sweep(args.steps, shapes):
             print(json.dumps({"variant": "sweep", **row}), flush=True)
 
 
