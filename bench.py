@@ -398,6 +398,16 @@ def main():
                 "hbm": {"achieved": round(achieved_gbs, 1), "peak": hbm_peak, "unit": "GB/s",
                         "frac": round(achieved_gbs / hbm_peak, 4), "peak_source": peak_kind},
                 "plan": plan.describe()}
+    # the roof this kernel actually meets: every MAC reads one staged fp32 x
+    # value through the 128 B/clk/SM shared-memory port -> 32 MAC/clk/SM
+    clk_mhz = clk.summary().get("sm_mhz") or 1965.0
+    n_sm = torch.cuda.get_device_properties(device).multi_processor_count
+    smem_peak_tf = 32 * 2 * n_sm * clk_mhz * 1e6 / 1e12
+    roofline["smem"] = {"achieved": round(achieved_tf, 3), "peak": round(smem_peak_tf, 2), "unit": "TFLOP/s",
+                        "frac": round(achieved_tf / smem_peak_tf, 4),
+                        "peak_source": f"128 B/clk/SM shared-memory loads = 32 fp32 MAC/clk/SM x {n_sm} SMs x "
+                                       f"{clk_mhz:.0f} MHz (median SM clock under load)",
+                        "achieved_smem_gbs": round(s["flops"] / 2 * 4 / (dom_ms / 1e3) / 1e9, 1)}
     layers = [{"layer": li, "us": round(conv_ms[li] * 1e3, 1),
                "nonzero_tflops": round(stats[li]["flops"] / (conv_ms[li] / 1e3) / 1e12, 2),
                "gbs": round(stats[li]["bytes"] / (conv_ms[li] / 1e3) / 1e9, 1)} for li in sorted(conv_ms)]
