@@ -59,7 +59,7 @@ class Plan(ctypes.Structure):
                 ("grid_y", c_i64)]
 
     def describe(self) -> dict:
-        return dict(kernel={1: "tiled", 2: "generic", 3: f"bi{self.NS}"}[self.kernel], P=self.P, DT=self.DT,
+        return dict(kernel={1: "tiled", 2: "generic", 3: f"bi{self.NS}", 4: "bt64"}[self.kernel], P=self.P, DT=self.DT,
                     NS=self.NS, CC=self.CC, TH=self.TH, threads=self.threads, WS=self.WS,
                     WC=self.WC, DW=self.DW, PR=self.PR, PC=self.PC, stages=self.stages,
                     grid=(self.grid_x, self.grid_y), smem_bytes=self.smem_bytes,
@@ -135,14 +135,16 @@ def lib():
     return _lib
 
 
-def bi_instances(binary16: bool = False) -> list[tuple[int, int, int, int, int, int]]:
-    """The batch-interleaved kernel's compiled tiles: (compute warps, PC, PR, DW,
-    stride_w, samples per lane), fp32 or binary16-input (F16/CB4) families."""
+def bi_instances(binary16: bool = False, tmem: bool = False) -> list[tuple[int, int, int, int, int, int]]:
+    """The batch-interleaved kernels' compiled tiles: (compute warps, PC, PR, DW,
+    stride_w, samples per lane) of the fp32 (kernel 3), binary16-input (F16/CB4/I8,
+    kernel 3) or tensor-memory fp32 (kernel 4) family."""
     L = lib()
     n = L.usc_bi_instances(None, 0)
     buf = (c_i32 * (7 * n))()
     L.usc_bi_instances(buf, n)
-    return [tuple(buf[7 * i:7 * i + 6]) for i in range(n) if buf[7 * i + 6] == int(binary16)]
+    kind = 2 if tmem else int(binary16)
+    return [tuple(buf[7 * i:7 * i + 6]) for i in range(n) if buf[7 * i + 6] == kind]
 
 
 def check(rc: int, what: str = ""):

@@ -31,3 +31,9 @@
     X(8, 1, 1, 8, 1) X(8, 4, 1, 8, 2) X(12, 4, 2, 4, 1) X(12, 2, 2, 8, 1) X(12, 8, 1, 4, 1)            \
     X(12, 2, 2, 4, 1) X(16, 2, 2, 4, 1) X(16, 4, 1, 4, 1) X(16, 2, 2, 2, 1) X(16, 4, 2, 2, 1)          \
     X(16, 1, 1, 8, 1) X(16, 4, 1, 4, 2)
+
+// tensor-memory-fed fp32 BI64 kernel (kernel 4, conv_bt.cuh).  X(NW, PC, PR, DW),
+// NW a multiple of 4 (the compute warps of each lane quarter fill its TMEM copy).
+#define USC_BT(X)                                                                               \
+    X(8, 2, 2, 8) X(8, 4, 2, 4) X(8, 4, 1, 8) X(8, 8, 1, 4) X(8, 2, 1, 16) X(12, 2, 2, 8) X(12, 4, 2, 4) \
+    X(12, 4, 1, 8) X(12, 8, 1, 4) X(16, 2, 2, 4) X(16, 4, 1, 4) X(16, 2, 1, 8)

@@ -499,14 +499,14 @@ int usc_conv_forward(const usc_plan *pl, const void *blob, const void *x, void *
         (epi->out.channels != g.out_channels || epi->out.height != pl->out_h || epi->out.width != pl->out_w))
         return fail(USC_ERR_VALUE, "output layout does not match the plan");
     if (epi && epi->pool) {
-        if (pl->kernel != 3 || pl->PR != 2 || pl->PC % 2 || pl->out_h % 2 || pl->out_w % 2)
+        if (pl->kernel < 3 || pl->PR != 2 || pl->PC % 2 || pl->out_h % 2 || pl->out_w % 2)
             return fail(USC_ERR_VALUE, "fused max-pool needs a BI plan with 2-row, even-width pixel blocks");
         if (!ep.out_padded || epi->out.height != pl->out_h / 2 || epi->out.width != pl->out_w / 2)
             return fail(USC_ERR_VALUE, "fused max-pool needs the pooled output layout");
     }
-    if (ep.requant && (pl->kernel != 3 || pl->dtype != USC_I8))
+    if (ep.requant && (pl->kernel < 3 || pl->dtype != USC_I8))
         return fail(USC_ERR_UNSUPPORTED, "requantising epilogue needs an int8 BI plan");
-    if (pl->kernel == 3) return usc::launch_bi(pl, blob, x, y, ep, st);
+    if (pl->kernel == 3 || pl->kernel == 4) return usc::launch_bi(pl, blob, x, y, ep, st);
     if (ep.out_padded && ep.oil != 0)
         return fail(USC_ERR_UNSUPPORTED, "kernels 1/2 write interleave-0 layouts only");
     // blob = [16 x f32 centroid table][int32 cpg, 16-B aligned][entries]

@@ -2,7 +2,7 @@
 // builds the TMA tensor map of the input and the kernel arguments.
 #include <cudaTypedefs.h>
 
-#include "conv_bi.cuh"
+#include "conv_bt.cuh"
 
 namespace usc {
 
@@ -81,6 +81,7 @@ int launch_bi(const usc_plan *pl, const void *blob, const void *x, void *y, cons
     a.x_stage_bytes = static_cast<int>(pl->smem_stage_bytes);
     a.stage_bytes = static_cast<int>(pl->smem_stage_bytes + pl->ent_stage_bytes);
     a.ep = ep;
+    if (pl->kernel == 4) return usc_bi::launch_bt(pl, a, st);
     if (pl->dtype == USC_F16) return usc_bi::launch_h16(pl, a, st);
     if (pl->dtype == USC_CB4) return usc_bi::launch_hcb(pl, a, st);
     if (pl->dtype == USC_I8) return usc_bi::launch_hi8(pl, a, st);

@@ -365,6 +365,147 @@ __device__ __forceinline__ int item_tile(const BiArgs &a, int it, int &part) {
     return a.tfull + j / a.split;
 }
 
+// Epilogue of one tile for one warp: epi_value (ReLU, nn.py:96-98; binary16 hook for
+// F16/CB4; int8 scale/requantise) then, if fused, the 2x2/2 max-pool (nn.py:124-135);
+// element (b, d, row, col) of the output layout is obase + d*dstride + row*rstride +
+// col*cstride (+ j*sstride for the lane's j-th sample)
+template <int KIND, int PC, int PR, int DW, int SPL>
+__device__ __forceinline__ void store_tile(const BiArgs &a, typename Ops<KIND, SPL>::A (&acc)[DW][PC * PR],
+                                           int g, int wc, int sb, int r, int col0, int part, int lane) {
+    using O = Ops<KIND, SPL>;
+    constexpr int P = PC * PR;
+    constexpr int IL = 32 * SPL;
+    const int *pm = a.perm + g * a.DT + wc * DW;  // this warp's output channels (balanced)
+    const bool pool = PR == 2 && a.ep.pool;
+    const int orow = pool ? r / 2 : r, ocol = pool ? col0 / 2 : col0;
+    const int b0 = sb * IL + lane * SPL;  // first sample of this lane
+    const int oil = a.ep.out_padded ? a.ep.oil : 0;
+    long long obase, dstride, sstride;
+    int rstride, cstride;
+    if (!a.ep.out_padded) {
+        const int oh = pool ? a.Yh / 2 : a.Yh, ow = pool ? a.Yw / 2 : a.Yw;
+        obase = ((long long)b0 * a.D * oh + orow) * ow + ocol;
+        dstride = (long long)oh * ow;
+        sstride = (long long)a.D * oh * ow;
+        rstride = ow;
+        cstride = 1;
+    } else if (oil) {
+        obase = (long long)(b0 / oil) * a.ep.o_sample_stride +
+                (((long long)orow + a.ep.oph) * a.ep.oWs + ocol + a.ep.opw) * oil + b0 % oil;
+        dstride = (long long)a.ep.oHp * a.ep.oWs * oil;
+        sstride = 1;
+        rstride = a.ep.oWs * oil;
+        cstride = oil;
+    } else {
+        obase = (long long)b0 * a.ep.o_sample_stride + ((long long)orow + a.ep.oph) * a.ep.oWs + ocol + a.ep.opw;
+        dstride = (long long)a.ep.oHp * a.ep.oWs;
+        sstride = a.ep.o_sample_stride;
+        rstride = a.ep.oWs;
+        cstride = 1;
+    }
+    const bool vec = SPL == 2 && oil == IL;  // the lane's two samples adjacent: one vector store
+    const int ncol = min(PC, a.Yw - col0);
+    const int nrow = min(PR, a.Yh - r);
+#pragma unroll
+    for (int dw = 0; dw < DW; ++dw) {
+        if (part >= 0 && dw % a.split != part) continue;
+        const int d = __ldg(pm + dw);
+        if (d < 0) continue;
+        const long long od = obase + d * dstride;
+        float v[P][SPL];
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+            O::unpack(acc[dw][p], v[p]);
+#pragma unroll
+            for (int j = 0; j < SPL; ++j) v[p][j] = epi_value<KIND>(v[p][j], a.ep);
+        }
+        // the thread's outputs: PC/2 pooled values of one row, or its P pixels
+        float o[P][SPL];
+        long long off[P];
+        bool ok[P];
+        int no = 0;
+        if constexpr (PR == 2 && PC % 2 == 0) {
+            if (pool) {
+#pragma unroll
+                for (int c2 = 0; c2 < PC / 2; ++c2) {
+#pragma unroll
+                    for (int j = 0; j < SPL; ++j)
+                        o[c2][j] = pool4(v[2 * c2][j], v[2 * c2 + 1][j], v[PC + 2 * c2][j],
+                                         v[PC + 2 * c2 + 1][j]);
+                    off[c2] = od + c2 * cstride;
+                    ok[c2] = 2 * c2 < ncol;
+                }
+                no = PC / 2;
+            }
+        }
+        if (no == 0) {
+#pragma unroll
+            for (int p = 0; p < P; ++p) {
+#pragma unroll
+                for (int j = 0; j < SPL; ++j) o[p][j] = v[p][j];
+                off[p] = od + (p / PC) * rstride + (p % PC) * cstride;
+                ok[p] = (p / PC) < nrow && (p % PC) < ncol;
+            }
+            no = P;
+        }
+        const bool f32out = KIND == USC_F32 || (KIND == USC_I8 && !a.ep.requant);
+        // sample-major layouts (plain NCHW / padded NCHW): a lane's pixels of one row are
+        // contiguous, so full 4-pixel groups go out as one 16-byte (fp32) or 8-byte
+        // (binary16) store per sample instead of four scalar ones
+        if constexpr (PC % 4 == 0) {
+            if (!vec && cstride == 1 && (sstride & 3) == 0 && (reinterpret_cast<uintptr_t>(a.y) & 15) == 0) {
+                const int rows = no / PC > 0 ? no / PC : 1, per = no < PC ? no : PC;  // pooled: 1 row
+#pragma unroll
+                for (int rr = 0; rr < PR; ++rr) {
+                    if (rr >= rows) break;
+#pragma unroll
+                    for (int q = 0; q < PC / 4; ++q) {
+                        const int i = rr * per + 4 * q;
+                        if (4 * q + 3 >= per || !ok[i] || !ok[i + 3] || (off[i] & 3)) continue;
+#pragma unroll
+                        for (int j = 0; j < SPL; ++j) {
+                            if (b0 + j >= a.N) continue;
+                            if (f32out)
+                                *reinterpret_cast<float4 *>(static_cast<float *>(a.y) + off[i] + j * sstride) =
+                                    make_float4(o[i][j], o[i + 1][j], o[i + 2][j], o[i + 3][j]);
+                            else
+                                *reinterpret_cast<uint2 *>(static_cast<__half *>(a.y) + off[i] + j * sstride) =
+                                    make_uint2(pack_h2(o[i][j], o[i + 1][j]), pack_h2(o[i + 2][j], o[i + 3][j]));
+                        }
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) ok[i + u] = false;  // stored
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < P; ++i) {
+            if (i >= no || !ok[i]) continue;
+            if (f32out) {
+                float *y = static_cast<float *>(a.y);
+                if (vec) {
+                    *reinterpret_cast<float2 *>(y + off[i]) = make_float2(o[i][0], o[i][SPL - 1]);
+                } else {
+#pragma unroll
+                    for (int j = 0; j < SPL; ++j)
+                        if (b0 + j < a.N) y[off[i] + j * sstride] = o[i][j];
+                }
+            } else {  // values are on the binary16 grid: the conversion is exact
+                __half *y = static_cast<__half *>(a.y);
+                if (vec) {
+                    *reinterpret_cast<__half2 *>(y + off[i]) =
+                        __halves2half2(__float2half_rn(o[i][0]), __float2half_rn(o[i][SPL - 1]));
+                } else {
+#pragma unroll
+                    for (int j = 0; j < SPL; ++j)
+                        if (b0 + j < a.N) y[off[i] + j * sstride] = __float2half_rn(o[i][j]);
+                }
+            }
+        }
+    }
+
+}
+
 template <int KIND, int PC, int PR, int DW, int SW, int NWC, int SPL>
 __global__ void __launch_bounds__((NWC + 1) * 32, 1) k_bi(const __grid_constant__ BiArgs a) {
     using O = Ops<KIND, SPL>;
@@ -479,140 +620,7 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1) k_bi(const __grid_constant_
             }
         }
 
-        // epilogue: epi_value (ReLU, nn.py:96-98; binary16 hook for F16/CB4) then, if
-        // fused, the 2x2/2 max-pool (nn.py:124-135); element (b, d, row, col) of the
-        // output layout is
-        // obase + d*dstride + row*rstride + col*cstride (+ j*sstride for the lane's
-        // j-th sample)
-        if (!active || r >= a.Yh) continue;
-        const int *pm = a.perm + g * a.DT + wc * DW;  // this warp's output channels (balanced)
-        const bool pool = PR == 2 && a.ep.pool;
-        const int orow = pool ? r / 2 : r, ocol = pool ? col0 / 2 : col0;
-        const int b0 = sb * IL + lane * SPL;  // first sample of this lane
-        const int oil = a.ep.out_padded ? a.ep.oil : 0;
-        long long obase, dstride, sstride;
-        int rstride, cstride;
-        if (!a.ep.out_padded) {
-            const int oh = pool ? a.Yh / 2 : a.Yh, ow = pool ? a.Yw / 2 : a.Yw;
-            obase = ((long long)b0 * a.D * oh + orow) * ow + ocol;
-            dstride = (long long)oh * ow;
-            sstride = (long long)a.D * oh * ow;
-            rstride = ow;
-            cstride = 1;
-        } else if (oil) {
-            obase = (long long)(b0 / oil) * a.ep.o_sample_stride +
-                    (((long long)orow + a.ep.oph) * a.ep.oWs + ocol + a.ep.opw) * oil + b0 % oil;
-            dstride = (long long)a.ep.oHp * a.ep.oWs * oil;
-            sstride = 1;
-            rstride = a.ep.oWs * oil;
-            cstride = oil;
-        } else {
-            obase = (long long)b0 * a.ep.o_sample_stride + ((long long)orow + a.ep.oph) * a.ep.oWs + ocol + a.ep.opw;
-            dstride = (long long)a.ep.oHp * a.ep.oWs;
-            sstride = a.ep.o_sample_stride;
-            rstride = a.ep.oWs;
-            cstride = 1;
-        }
-        const bool vec = SPL == 2 && oil == IL;  // the lane's two samples adjacent: one vector store
-        const int ncol = min(PC, a.Yw - col0);
-        const int nrow = min(PR, a.Yh - r);
-#pragma unroll
-        for (int dw = 0; dw < DW; ++dw) {
-            if (part >= 0 && dw % a.split != part) continue;
-            const int d = __ldg(pm + dw);
-            if (d < 0) continue;
-            const long long od = obase + d * dstride;
-            float v[P][SPL];
-#pragma unroll
-            for (int p = 0; p < P; ++p) {
-                O::unpack(acc[dw][p], v[p]);
-#pragma unroll
-                for (int j = 0; j < SPL; ++j) v[p][j] = epi_value<KIND>(v[p][j], a.ep);
-            }
-            // the thread's outputs: PC/2 pooled values of one row, or its P pixels
-            float o[P][SPL];
-            long long off[P];
-            bool ok[P];
-            int no = 0;
-            if constexpr (PR == 2 && PC % 2 == 0) {
-                if (pool) {
-#pragma unroll
-                    for (int c2 = 0; c2 < PC / 2; ++c2) {
-#pragma unroll
-                        for (int j = 0; j < SPL; ++j)
-                            o[c2][j] = pool4(v[2 * c2][j], v[2 * c2 + 1][j], v[PC + 2 * c2][j],
-                                             v[PC + 2 * c2 + 1][j]);
-                        off[c2] = od + c2 * cstride;
-                        ok[c2] = 2 * c2 < ncol;
-                    }
-                    no = PC / 2;
-                }
-            }
-            if (no == 0) {
-#pragma unroll
-                for (int p = 0; p < P; ++p) {
-#pragma unroll
-                    for (int j = 0; j < SPL; ++j) o[p][j] = v[p][j];
-                    off[p] = od + (p / PC) * rstride + (p % PC) * cstride;
-                    ok[p] = (p / PC) < nrow && (p % PC) < ncol;
-                }
-                no = P;
-            }
-            const bool f32out = KIND == USC_F32 || (KIND == USC_I8 && !a.ep.requant);
-            // sample-major layouts (plain NCHW / padded NCHW): a lane's pixels of one row are
-            // contiguous, so full 4-pixel groups go out as one 16-byte (fp32) or 8-byte
-            // (binary16) store per sample instead of four scalar ones
-            if constexpr (PC % 4 == 0) {
-                if (!vec && cstride == 1 && (sstride & 3) == 0 && (reinterpret_cast<uintptr_t>(a.y) & 15) == 0) {
-                    const int rows = no / PC > 0 ? no / PC : 1, per = no < PC ? no : PC;  // pooled: 1 row
-#pragma unroll
-                    for (int rr = 0; rr < PR; ++rr) {
-                        if (rr >= rows) break;
-#pragma unroll
-                        for (int q = 0; q < PC / 4; ++q) {
-                            const int i = rr * per + 4 * q;
-                            if (4 * q + 3 >= per || !ok[i] || !ok[i + 3] || (off[i] & 3)) continue;
-#pragma unroll
-                            for (int j = 0; j < SPL; ++j) {
-                                if (b0 + j >= a.N) continue;
-                                if (f32out)
-                                    *reinterpret_cast<float4 *>(static_cast<float *>(a.y) + off[i] + j * sstride) =
-                                        make_float4(o[i][j], o[i + 1][j], o[i + 2][j], o[i + 3][j]);
-                                else
-                                    *reinterpret_cast<uint2 *>(static_cast<__half *>(a.y) + off[i] + j * sstride) =
-                                        make_uint2(pack_h2(o[i][j], o[i + 1][j]), pack_h2(o[i + 2][j], o[i + 3][j]));
-                            }
-#pragma unroll
-                            for (int u = 0; u < 4; ++u) ok[i + u] = false;  // stored
-                        }
-                    }
-                }
-            }
-#pragma unroll
-            for (int i = 0; i < P; ++i) {
-                if (i >= no || !ok[i]) continue;
-                if (f32out) {
-                    float *y = static_cast<float *>(a.y);
-                    if (vec) {
-                        *reinterpret_cast<float2 *>(y + off[i]) = make_float2(o[i][0], o[i][SPL - 1]);
-                    } else {
-#pragma unroll
-                        for (int j = 0; j < SPL; ++j)
-                            if (b0 + j < a.N) y[off[i] + j * sstride] = o[i][j];
-                    }
-                } else {  // values are on the binary16 grid: the conversion is exact
-                    __half *y = static_cast<__half *>(a.y);
-                    if (vec) {
-                        *reinterpret_cast<__half2 *>(y + off[i]) =
-                            __halves2half2(__float2half_rn(o[i][0]), __float2half_rn(o[i][SPL - 1]));
-                    } else {
-#pragma unroll
-                        for (int j = 0; j < SPL; ++j)
-                            if (b0 + j < a.N) y[off[i] + j * sstride] = __float2half_rn(o[i][j]);
-                    }
-                }
-            }
-        }
+        if (active && r < a.Yh) store_tile<KIND, PC, PR, DW, SPL>(a, acc, g, wc, sb, r, col0, part, lane);
     }
 }
 

@@ -268,6 +268,14 @@ static bool bi_instance(int PC, int PR, int DW, int NW, int SW, int SPL, int dty
     return false;
 }
 
+static bool bt_instance(int PC, int PR, int DW, int NW) {
+#define XT(NW_, PC_, PR_, DW_) \
+    if (NW == NW_ && PC == PC_ && PR == PR_ && DW == DW_) return true;
+    USC_BT(XT)
+#undef XT
+    return false;
+}
+
 int usc_bi_instances(int32_t *out, int32_t max_count) {
     int n = 0;
 #define X7(NW_, PC_, PR_, DW_, SW_, SPL_, K_)                   \
@@ -297,6 +305,9 @@ int usc_bi_instances(int32_t *out, int32_t max_count) {
         USC_BI_W16(X)
     }
     USC_BI_H(XH)
+#define XT(NWT_, PC_, PR_, DW_) X7(NWT_, PC_, PR_, DW_, 1, 2, 2)
+    USC_BT(XT)
+#undef XT
 #undef X
 #undef XH
 #undef X7
@@ -339,20 +350,23 @@ int usc_plan_make(const usc_geometry *g0, int32_t n, int32_t dtype, const usc_ex
     // staged element size: the BI kernel holds int8 codes as binary16 (exact, |code| <= 127)
     int kernel = c.kernel ? c.kernel : 3;
     if (g.stride_w > 2) kernel = 2;
+    if (kernel == 4 && (dtype != USC_F32 || g.stride_w != 1 || g.stride_h != 1))
+        return fail(USC_ERR_UNSUPPORTED, "the tensor-memory kernel is fp32, stride 1 only");
+    const bool bi = kernel == 3 || kernel == 4;  // batch-interleaved families
     const int eb = (kernel == 3 && dtype == USC_I8) ? 2 : elem_bytes(dtype);
 
     // kernel 3 sample interleave: samples_per_cta 32 (BI32) or 64 (BI64, two samples per
     // lane); default BI64 once the batch fills two 32-sample blocks
     int IL = 0;
-    if (kernel == 3) {
+    if (bi) {
         IL = (c.samples_per_cta == 32 || c.samples_per_cta == 64) ? c.samples_per_cta : (n > 32 ? 64 : 32);
-        if (dtype != USC_F32) IL = 64;  // binary16-staged kinds: BI64 only
+        if (dtype != USC_F32 || kernel == 4) IL = 64;  // binary16-staged kinds and TMEM: BI64 only
     }
     rc = usc_act_layout_make(g.in_channels, g.input_h, g.input_w, g.pad_h, g.pad_w, eb, IL, &pl->in);
     if (rc) return rc;
     const int Yh = pl->out_h, Yw = pl->out_w, Ws = pl->in.ws;
     const int threads = (c.threads == 128 || c.threads == 256) ? c.threads : 256;
-    if (kernel == 3) {
+    if (bi) {
         // batch-interleaved: a CTA = 32 samples x (WS strips of PR x PC pixels) x (WC*DW
         // channels), NW compute warps (threads = NW*32) + 1 producer warp; warp w owns
         // strip w % WS for channel subgroup w / WS; lane = sample.
@@ -374,7 +388,9 @@ int usc_plan_make(const usc_geometry *g0, int32_t n, int32_t dtype, const usc_ex
             auto any_inst = [&](int pr, int pc) {
                 for (int nw : {8, 12, 16})
                     for (int dw : {2, 4, 8, 16})
-                        if (bi_instance(pc, pr, dw, nw, g.stride_w, IL / 32, dtype)) return true;
+                        if (kernel == 4 ? bt_instance(pc, pr, dw, nw)
+                                        : bi_instance(pc, pr, dw, nw, g.stride_w, IL / 32, dtype))
+                            return true;
                 return false;
             };
             if (!any_inst(PR, PC)) {
@@ -420,7 +436,7 @@ int usc_plan_make(const usc_geometry *g0, int32_t n, int32_t dtype, const usc_ex
                 return fail(USC_ERR_VALUE, "ch_per_cta %d not a multiple of %d channel warps", c.ch_per_cta, wc);
             for (int dw : {8, 16, 4, 2}) {
                 if (c.ch_per_cta) dw = c.ch_per_cta / wc;
-                if (bi_instance(PC, PR, dw, nw, g.stride_w, IL / 32, dtype)) {
+                if (kernel == 4 ? bt_instance(PC, PR, dw, nw) : bi_instance(PC, PR, dw, nw, g.stride_w, IL / 32, dtype)) {
                     NW = nw, WS = ws, WC = wc, DW = dw;
                     break;
                 }
@@ -482,6 +498,10 @@ int usc_plan_make(const usc_geometry *g0, int32_t n, int32_t dtype, const usc_ex
         const int NCLS = ncr * ncc;
         int CC = c.chunk_channels ? c.chunk_channels : 64;
         CC = std::min(std::min(CC, g.in_channels), 256);
+        if (kernel == 4) {  // a chunk's positions fill one 256-column TMEM buffer (2 columns each)
+            if (HS * TWs > 128) return fail(USC_ERR_VALUE, "tile of %d positions exceeds tensor memory", HS * TWs);
+            CC = std::min(CC, 128 / (HS * TWs));
+        }
         const int S = c.stages ? std::max(2, std::min(4, c.stages)) : 2;
         const int64_t budget = 200 * 1024;
         // per-stage entry block: hdr DT*8 + runs padded to even (16-B aligned starts) +
@@ -499,7 +519,7 @@ int usc_plan_make(const usc_geometry *g0, int32_t n, int32_t dtype, const usc_ex
         const int64_t ent_stage = ent_bytes(CC);
         if (S * (stage + ent_stage) + 128 > 224 * 1024)
             return fail(USC_ERR_VALUE, "BI tile does not fit shared memory");
-        pl->kernel = 3;
+        pl->kernel = kernel;
         pl->ncls_r = ncr;
         pl->ncls_c = ncc;
         pl->P = P;
@@ -693,7 +713,7 @@ static int32_t theta_word(int dtype, const void *payload, const float *table, in
 
 int usc_pack_size(const usc_plan *pl, int64_t n_nz, int64_t *bytes) {
     const int64_t nb = (int64_t)pl->groups * pl->n_chunks;
-    if (pl->kernel == 3) {
+    if (pl->kernel == 3 || pl->kernel == 4) {
         // [64 B][int32 blk[nb+1]][int32 perm[G*DT]][blocks: hdr int2[DT], runs padded to
         // even, 16-B rounded]
         const int64_t ncls = std::max(1, pl->ncls_r * pl->ncls_c);
@@ -773,6 +793,8 @@ int usc_pack(const usc_plan *pl, const int64_t *row_ptr, const int64_t *col, con
         const int64_t cl = c - (c / CC) * CC;
         if (pl->kernel == 1)
             *off = cl * cs_tiled + kh * Ws + kw;
+        else if (pl->kernel == 4)  // TMEM column of the position (two samples per lane)
+            *off = ((cl * pl->HS + kh) * pl->TWs + kw) * 2;
         else if (pl->kernel == 3)  // byte offset in the [CC][HS][TWs][IL] f32 stage
             *off = ((cl * pl->HS + kh) * pl->TWs + kw) * (pl->dtype == USC_F32 ? 4 : 2) * pl->in.interleave;
         else
@@ -781,7 +803,7 @@ int usc_pack(const usc_plan *pl, const int64_t *row_ptr, const int64_t *col, con
             return fail(USC_ERR_UNSUPPORTED, "packed offset %lld too large", (long long)*off);
         return USC_OK;
     };
-    if (pl->kernel == 3) {
+    if (pl->kernel == 3 || pl->kernel == 4) {
         // blob = [64 B][int32 blk[nb+1]][int32 perm[G*DT]][blocks].  Block (group, chunk):
         // int2 hdr[DT] = {first, end} entry index of each slot's run (relative to the
         // entries after hdr), runs start at even indices (16-B aligned pairs).

@@ -115,7 +115,7 @@ def fit_plan(filt: CsrFilter, n: int, dtype: int, config: ExecConfig | None, pay
     """The planning half of plan_for (host only)."""
     config = config or ExecConfig()
     plan = make_plan(filt.geometry, n, dtype, config)
-    if plan.kernel == 3 and not config.ent_reserve:
+    if plan.kernel in (3, 4) and not config.ent_reserve:
         fields = {f: getattr(config, f) for f in config.__dataclass_fields__}
         cc, best = plan.CC, None
         while cc >= 1 and best is None:
@@ -179,7 +179,7 @@ def padded_input(x_dev, plan: _lib.Plan, stream=None):
     import torch
     lay = plan.in_
     # the batch-interleaved kernel stages int8 codes as binary16 (exact)
-    dt = torch.float16 if (plan.kernel == 3 and plan.dtype == _lib.USC_I8) else x_dev.dtype
+    dt = torch.float16 if (plan.kernel in (3, 4) and plan.dtype == _lib.USC_I8) else x_dev.dtype
     out = torch.empty(lay.elems(plan.n), dtype=dt, device=x_dev.device)
     _lib.check(_lib.lib().usc_pad_input(_lib.ref(lay), plan.dtype, plan.n, _lib.t_ptr(x_dev),
                                         _lib.t_ptr(out), _lib.stream_ptr(stream)), "pad")
@@ -328,6 +328,22 @@ def tile_candidates(geometry: ConvGeometry, n: int, sb_values, precision=Precisi
                                               ch_per_cta=dw * (nw // ws), kernel=3, threads=nw * 32,
                                               pixel_warps=ws, stages=st, samples_per_cta=32 * spl,
                                               pixel_classes=pcl))
+    if 4 in kernels and precision is PrecisionMode.BINARY32 and n > 32 and geometry.stride == (1, 1):
+        # tensor-memory-fed fp32 BI64 (kernel 4, opt-in: measured slower than kernel 3 on the
+        # VGG layers -- short TMEM-bounded chunks, fill and per-load R2UR cost more issue
+        # slots than the shared-memory port saves)
+        yh = geometry.out_h if geometry.input_w != 1 else geometry.out_w
+        for nw, pc, pr, dw, _, _ in _lib.bi_instances(tmem=True):
+            if pc > max(1, yw) and pc > 1 or pr > yh:
+                continue
+            strips = -(-yh // pr) * -(-yw // pc)
+            for ws in (w for w in range(1, nw + 1) if nw % w == 0):
+                if ws > strips:
+                    break
+                for st in (3, 4):
+                    out.append(ExecConfig(sub_batch=min(sb_values), pix_per_thread=pc, rows_per_thread=pr,
+                                          ch_per_cta=dw * (nw // ws), kernel=4, threads=nw * 32,
+                                          pixel_warps=ws, stages=st, samples_per_cta=64))
     if 1 in kernels:
         ps = [p for p in (2, 4, 8) if p <= max(2, yw)]
         for sb in sb_values:

@@ -54,7 +54,7 @@ def _cfg_of(plan, cfg: ExecConfig, il: int = 0) -> ExecConfig:
     batch-interleaved kernel, the network's sample interleave pinned)."""
     fields = {f: getattr(cfg, f) for f in cfg.__dataclass_fields__}
     fields["kernel"] = plan.kernel
-    if plan.kernel == 3 and il:
+    if plan.kernel in (3, 4) and il:
         fields["samples_per_cta"] = il
     return ExecConfig(**fields)
 
@@ -193,8 +193,8 @@ class SparseVGG16:
         plans = [make_plan(g, n, self.dtype, c) for g, c in zip(self.geoms, self.configs)]
         # every layer reads the layout its plan wants: one interleave for the network
         # (BI32 or BI64, that of the first layer's plan)
-        il = plans[0].in_.interleave if all(p.kernel == 3 for p in plans) else 0
-        if il == 0 and any(p.kernel == 3 for p in plans):
+        il = plans[0].in_.interleave if all(p.kernel in (3, 4) for p in plans) else 0
+        if il == 0 and any(p.kernel in (3, 4) for p in plans):
             plans = [make_plan(g, n, self.dtype, ExecConfig(c.sub_batch, c.worker_count, c.pix_per_thread,
                                                             c.ch_per_cta, c.samples_per_cta,
                                                             c.chunk_channels,
@@ -227,7 +227,7 @@ class SparseVGG16:
                     out_dtype = torch.float32
             elif self.mode == "cb4":  # _half_hook of the conv and of the ReLU
                 epi.saturate, epi.cap, epi.saturate2, epi.cap2 = 1, lp["cap"], 1, lp["cap2"]
-            fuse = nxt == "M" and plan.kernel == 3 and plan.PR == 2 and plan.PC % 2 == 0
+            fuse = nxt == "M" and plan.kernel in (3, 4) and plan.PR == 2 and plan.PC % 2 == 0
             last = i + 2 >= len(VGG16_CIFAR)
             if fuse:  # conv + ReLU + 2x2 max-pool in one kernel, pooled output padded for the next conv
                 ph = 0 if last else 1

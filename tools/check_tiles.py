@@ -33,7 +33,7 @@ def main():
         torch.cuda.synchronize()
         ref = yout.clone()
         g = model.geoms[li]
-        cands = [c for c in tile_candidates(g, batch, [1], model.precision, (3,))
+        cands = [c for c in tile_candidates(g, batch, [1], model.precision, (3, 4))
                  if c.samples_per_cta == model.interleave]
         if epi.pool:
             cands = [c for c in cands if c.rows_per_thread == 2 and c.pix_per_thread % 2 == 0]

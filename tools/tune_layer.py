@@ -26,7 +26,7 @@ def main():
     for st in [s for s in model.steps if s[0] == "conv" and s[1] in args.layers]:
         _, li, plan0, _, xin, yout, epi = st
         g = model.geoms[li]
-        cands = [c for c in tile_candidates(g, args.batch, [1], model.precision, (3,))
+        cands = [c for c in tile_candidates(g, args.batch, [1], model.precision, (3, 4))
                  if c.samples_per_cta == model.interleave]
         if epi.pool:
             cands = [c for c in cands if c.rows_per_thread == 2 and c.pix_per_thread % 2 == 0]
@@ -41,8 +41,12 @@ def main():
             res.append((ms, plan.describe()))
         res.sort(key=lambda r: r[0])
         print(f"layer {li} ({g.in_channels}->{g.out_channels}, {g.input_h}x{g.input_w}): {len(res)} candidates")
-        for ms, d in res[:args.top]:
-            keep = {k: d[k] for k in ("P", "PR", "PC", "DT", "DW", "WS", "threads", "CC", "stages", "grid",
+        best_by_kernel = {}
+        for ms, d in res:
+            best_by_kernel.setdefault(d["kernel"], (ms, d))
+        shown = res[:args.top] + [v for v in best_by_kernel.values() if v not in res[:args.top]]
+        for ms, d in shown:
+            keep = {k: d[k] for k in ("kernel", "P", "PR", "PC", "DT", "DW", "WS", "threads", "CC", "stages", "grid",
                                       "pixel_classes")}
             print(f"  {ms * 1e3:8.1f} us  {keep}")
 
