@@ -328,7 +328,7 @@ def tile_candidates(geometry: ConvGeometry, n: int, sb_values, precision=Precisi
                                               ch_per_cta=dw * (nw // ws), kernel=3, threads=nw * 32,
                                               pixel_warps=ws, stages=st, samples_per_cta=32 * spl,
                                               pixel_classes=pcl))
-    if 4 in kernels and precision is PrecisionMode.BINARY32 and n > 32 and geometry.stride == (1, 1):
+    if 4 in kernels and precision is PrecisionMode.BINARY32 and geometry.stride == (1, 1):
         # tensor-memory-fed fp32 BI64 (kernel 4, opt-in: measured slower than kernel 3 on the
         # VGG layers -- short TMEM-bounded chunks, fill and per-load R2UR cost more issue
         # slots than the shared-memory port saves)

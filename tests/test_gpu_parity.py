@@ -100,6 +100,8 @@ def test_layer_configs_bitwise_all_tiles(name):
     xd = _dev(x, prec)
     cfgs = [U.ExecConfig(), U.ExecConfig(kernel=2), U.ExecConfig(kernel=1)] + \
         U.engine.tile_candidates(gg, rec["batch"], [1, 2], prec)
+    # the opt-in tensor-memory kernel (kernel 4): a spread of its tiles
+    cfgs += U.engine.tile_candidates(gg, rec["batch"], [1, 2], prec, kernels=(4,))[::7]
     for cfg in cfgs:
         out = U.sparse_conv_forward(xd, f, cfg)
         assert sha(out.data) == rec["out"], cfg
