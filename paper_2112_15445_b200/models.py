@@ -305,6 +305,64 @@ class SparseVGG16:
             self.run()
         return self.output()
 
+    def stream_forward(self, x_hosts, out_hosts):
+        """Inference over a stream of host batches with the transfers overlapped: the
+        H2D copy of batch i+1 (copy stream) and the D2H copy of batch i-1 (drain
+        stream) run while batch i computes (current stream, CUDA graph when captured).
+        x_hosts / out_hosts: pinned host tensors, (n,3,32,32) in / (n,512,1,1) out.
+        Returns after enqueueing everything; synchronise the current stream (or the
+        returned event) before reading out_hosts."""
+        import torch
+        cur = torch.cuda.current_stream(self.device)
+        if not hasattr(self, "_sf"):
+            lay = self.out_layout
+            self._sf = dict(
+                xin=[torch.empty(x_hosts[0].shape, dtype=x_hosts[0].dtype, device=self.device) for _ in range(2)],
+                outd=[torch.empty((self.batch, lay.channels, lay.height, lay.width), dtype=self.out_buf.dtype,
+                                  device=self.device) for _ in range(2)],
+                h2d=torch.cuda.Stream(self.device), d2h=torch.cuda.Stream(self.device))
+        sf = self._sf
+        h2d_done = [torch.cuda.Event() for _ in range(2)]
+        in_free = [torch.cuda.Event() for _ in range(2)]
+        out_ready = [torch.cuda.Event() for _ in range(2)]
+        out_free = [torch.cuda.Event() for _ in range(2)]
+        for e in in_free + out_free:
+            e.record(cur)
+        odt = _lib.USC_F32 if self.out_buf.element_size() == 4 else _lib.USC_F16
+
+        def h2d(i):
+            b = i % 2
+            sf["h2d"].wait_event(in_free[b])
+            with torch.cuda.stream(sf["h2d"]):
+                sf["xin"][b].copy_(x_hosts[i], non_blocking=True)
+                h2d_done[b].record(sf["h2d"])
+
+        h2d(0)
+        for i in range(len(x_hosts)):
+            b = i % 2
+            if i + 1 < len(x_hosts):
+                h2d(i + 1)
+            cur.wait_event(h2d_done[b])
+            self.load_input(sf["xin"][b])
+            in_free[b].record(cur)
+            if self.graph is not None:
+                self.graph.replay()
+            else:
+                self.run()
+            cur.wait_event(out_free[b])
+            _lib.check(_lib.lib().usc_unpad_output(_lib.ref(self.out_layout), odt, self.batch,
+                                                   _lib.t_ptr(self.out_buf), _lib.t_ptr(sf["outd"][b]),
+                                                   _lib.stream_ptr(cur)), "unpad")
+            out_ready[b].record(cur)
+            sf["d2h"].wait_event(out_ready[b])
+            with torch.cuda.stream(sf["d2h"]):
+                out_hosts[i].copy_(sf["outd"][b], non_blocking=True)
+                out_free[b].record(sf["d2h"])
+        done = torch.cuda.Event()
+        cur.wait_stream(sf["d2h"])
+        done.record(cur)
+        return done
+
     def capture(self):
         """Capture run() as one CUDA graph (launch-bound small layers)."""
         import torch

@@ -305,3 +305,17 @@ def test_device_encoder_bitwise(name):
         assert sha(getattr(dev, k)) == rec["csr"][k]
     zero = np.zeros_like(w)
     assert U.build_csr_device(torch.from_numpy(zero).cuda(), gg).n_nz == 1  # max(1, 0)
+
+
+def test_stream_forward_matches_forward():
+    """The overlapped streaming API returns exactly forward()'s features, in order."""
+    import torch
+    from paper_2112_15445_b200.models import SparseVGG16, vgg16_rng, vgg16_weights
+    rng = vgg16_rng(0.93, seed=3)
+    m = SparseVGG16(vgg16_weights(rng, 0.93), 64)
+    xs = [torch.from_numpy(rng.standard_normal((64, 3, 32, 32)).astype(np.float32)).pin_memory() for _ in range(5)]
+    outs = [torch.empty((64, 512, 1, 1)).pin_memory() for _ in range(5)]
+    m.capture()
+    m.stream_forward(xs, outs).synchronize()
+    for x, o in zip(xs, outs):
+        assert torch.equal(m.forward(x.cuda()).cpu(), o)
