@@ -4,6 +4,7 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 
 #include "usc_internal.h"
@@ -50,6 +51,19 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
         "}\n" ::"r"(smem_u32(bar)),
         "r"(parity), "r"(1000000)
         : "memory");
+}
+
+// Opt a kernel into the large dynamic shared-memory carve-out once per (kernel,
+// device): the attribute is per device, and launches may come from several threads.
+template <typename F>
+inline cudaError_t ensure_smem_attr(F fn, std::atomic<uint64_t> &done, int bytes) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const uint64_t bit = 1ull << (dev & 63);
+    if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_acq_rel);
+    return e;
 }
 
 // --------------------------------------------------------------------------

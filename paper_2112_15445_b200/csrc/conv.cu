@@ -386,11 +386,9 @@ int cuda_check(const char *what) {
 template <int KIND, int P, int DT, int SW>
 int launch_tiled_inst(const usc_plan *pl, const TiledArgs &a, cudaStream_t st) {
     auto fn = k_tiled<KIND, P, DT, SW, 256>;
-    static bool attr_set = false;  // per instantiation
-    if (!attr_set || pl->smem_bytes > 48 * 1024) {
-        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-        attr_set = true;
-    }
+    static std::atomic<uint64_t> attr{0};  // per instantiation and device
+    cudaError_t ae = usc_dev::ensure_smem_attr(fn, attr, 220 * 1024);
+    if (ae != cudaSuccess) return fail(USC_ERR_CUDA, "smem attribute: %s", cudaGetErrorString(ae));
     dim3 grid(static_cast<unsigned>(pl->grid_x), static_cast<unsigned>(pl->grid_y));
     fn<<<grid, 256, pl->smem_bytes, st>>>(a);
     return cuda_check("k_tiled launch");

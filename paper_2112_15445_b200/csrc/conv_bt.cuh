@@ -249,11 +249,9 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1) k_bt(const __grid_constant_
 template <int PC, int PR, int DW, int NWC>
 int launch_bt_inst(const usc_plan *pl, const BiArgs &a, cudaStream_t st) {
     auto fn = k_bt<PC, PR, DW, NWC>;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 224 * 1024);
-        attr = true;
-    }
+    static std::atomic<uint64_t> attr{0};
+    cudaError_t ae = ensure_smem_attr(fn, attr, 224 * 1024);
+    if (ae != cudaSuccess) return usc::fail(USC_ERR_CUDA, "smem attribute: %s", cudaGetErrorString(ae));
     fn<<<static_cast<unsigned>(pl->grid_x), (NWC + 1) * 32, pl->smem_bytes, st>>>(a);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return usc::fail(USC_ERR_CUDA, "k_bt launch: %s", cudaGetErrorString(e));

@@ -157,7 +157,7 @@ def resnet50_fp16(batch=256, sparsity=0.9):
     from paper_2112_15445_b200.pruning import synthesize_masked_weights
     from paper_2112_15445_b200.tensor import ConvGeometry
     F16 = PrecisionMode.BINARY16
-    rows, tot_s, tot_c, n_convs = [], 0.0, 0.0, 0
+    rows, tot_s, tot_c, tot_d, n_convs = [], 0.0, 0.0, 0.0, 0
     torch.backends.cudnn.benchmark = True
     for name, kw, count in resnet50_cifar_convs():
         c, d, k, hw, s, p = kw["c"], kw["d"], kw["k"], kw["hw"], kw["s"], kw["p"]
@@ -178,16 +178,23 @@ def resnet50_fp16(batch=256, sparsity=0.9):
         xt = torch.randn(batch, c, hw, hw, device="cuda").half().contiguous(memory_format=torch.channels_last)
         wt = torch.from_numpy(np.array(w.data)).cuda().half().contiguous(memory_format=torch.channels_last)
         cd = time_median_cuda(lambda: torch.nn.functional.conv2d(xt, wt, stride=s, padding=p), 9, 2)
+        backend = "sparse" if ms < cd else "dense"  # layer_bench.backend_config: ties -> dense
         rows.append({"layer": name, "count": count, "us": round(ms * 1e3, 1), "cudnn_fp16_us": round(cd * 1e3, 1),
-                     "kernel": plan.describe()["kernel"]})
+                     "kernel": plan.describe()["kernel"], "backend": backend})
         tot_s += ms * count
         tot_c += cd * count
+        tot_d += min(ms, cd) * count
         n_convs += count
     return {"config": f"pruned ResNet-50 CIFAR {int(sparsity * 100)}% BINARY16, batch {batch}, 53-conv layer sum",
             "convs": n_convs, "sparse_ms": round(tot_s, 4), "cudnn_fp16_ms": round(tot_c, 4),
             "images_per_s_conv_only": round(batch / (tot_s / 1e3), 1),
             "cudnn_images_per_s_conv_only": round(batch / (tot_c / 1e3), 1),
-            "speedup_vs_cudnn": round(tot_c / tot_s, 3), "layers": rows}
+            "speedup_vs_cudnn": round(tot_c / tot_s, 3),
+            "dispatch": {"ms": round(tot_d, 4), "images_per_s_conv_only": round(batch / (tot_d / 1e3), 1),
+                         "rule": "per-layer argmin of sparse vs cuDNN, ties to dense (backend_config, "
+                                 "ref bench.py:212-227)",
+                         "sparse_layers": sum(r["count"] for r in rows if r["backend"] == "sparse")},
+            "layers": rows}
 
 
 SWEEP_SHAPES = {"r50-3x3-64x32": (64, 64, 3, 32), "r50-3x3-256x8": (256, 256, 3, 8),
