@@ -164,6 +164,7 @@ def time_per_launch(model, steps=20):
         evs = []
         for _ in range(steps):
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda._sleep(200_000)  # device busy while the launch is enqueued (no host gap)
             a.record()
             if st[0] == "conv":
                 _, li, plan, blob, xin, yout, epi = st

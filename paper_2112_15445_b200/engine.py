@@ -279,8 +279,11 @@ def time_median(fn, repeats: int = 9, warmup: int = 2) -> float:
     return float(np.median(times) * 1e3)
 
 
-def time_median_cuda(fn, repeats: int = 9, warmup: int = 2) -> float:
-    """Median device time of fn() in ms, CUDA events on the current stream."""
+def time_median_cuda(fn, repeats: int = 9, warmup: int = 2, inner: int = 2) -> float:
+    """Median device time of fn() in ms, CUDA events on the current stream.  A
+    device-side spin is queued ahead of the start event so the timed launches are
+    already enqueued when the GPU reaches it: the host's per-launch cost (ctypes,
+    tensor-map encoding) never shows up as idle time between the events."""
     import torch
     for _ in range(warmup):
         fn()
@@ -288,11 +291,13 @@ def time_median_cuda(fn, repeats: int = 9, warmup: int = 2) -> float:
     times = []
     for _ in range(repeats):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda._sleep(300_000)  # ~150 us of device time to enqueue behind
         a.record()
-        fn()
+        for _ in range(inner):
+            fn()
         b.record()
         b.synchronize()
-        times.append(a.elapsed_time(b))
+        times.append(a.elapsed_time(b) / inner)
     return float(np.median(times))
 
 
