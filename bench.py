@@ -303,15 +303,12 @@ def main():
 
     model, ws = build_model(BATCH, device)
     if args.configs:
-        from paper_2112_15445_b200 import ExecConfig
-        model.configs = [ExecConfig(**c) for c in json.load(open(args.configs))]
-        model._build()
+        model.load_tuned_state(json.load(open(args.configs)))
     elif not args.no_autotune:
         model.autotune(repeats=3, warmup=1)
     if args.dump_configs and rank == 0:
-        import dataclasses
         with open(args.dump_configs, "w") as fh:
-            json.dump([dataclasses.asdict(c) for c in model.configs], fh)
+            json.dump(model.tuned_state(), fh)
     model.capture()
     x_host = torch.from_numpy(np.random.default_rng([1, rank]).standard_normal(
         (BATCH, 3, 32, 32)).astype(np.float32)).pin_memory()

@@ -14,6 +14,7 @@ synchronisation, capturable as one CUDA graph.
 
 from __future__ import annotations
 
+import ctypes
 import zlib
 
 import numpy as np
@@ -113,6 +114,7 @@ class SparseVGG16:
             self.payloads = [q.indices for q in self.qfilters]
             self.tables = [q.table for q in self.qfilters]
         self.pre_pool = self._pre_pool_layers()
+        self.fuse_pool = {}  # per pool-feeding conv: fuse the pool into its epilogue (autotuned)
         self.saturation = saturation
         self.layer_params = [dict() for _ in self.geoms]
         if mode in ("int8", "cb4"):
@@ -227,7 +229,8 @@ class SparseVGG16:
                     out_dtype = torch.float32
             elif self.mode == "cb4":  # _half_hook of the conv and of the ReLU
                 epi.saturate, epi.cap, epi.saturate2, epi.cap2 = 1, lp["cap"], 1, lp["cap2"]
-            fuse = nxt == "M" and plan.kernel in (3, 4) and plan.PR == 2 and plan.PC % 2 == 0
+            fuse = (nxt == "M" and plan.kernel in (3, 4) and plan.PR == 2 and plan.PC % 2 == 0
+                    and self.fuse_pool.get(li, True))
             last = i + 2 >= len(VGG16_CIFAR)
             if fuse:  # conv + ReLU + 2x2 max-pool in one kernel, pooled output padded for the next conv
                 ph = 0 if last else 1
@@ -385,13 +388,34 @@ class SparseVGG16:
     def conv_launch_list(self):
         return [(st[1], st[2]) for st in self.steps if st[0] == "conv"]
 
+    # -- tuned state (per-layer tiles + pool fusion) ---------------------------------
+    def tuned_state(self) -> dict:
+        import dataclasses
+        return {"configs": [dataclasses.asdict(c) for c in self.configs],
+                "fuse_pool": {str(k): bool(v) for k, v in self.fuse_pool.items()}}
+
+    def load_tuned_state(self, state) -> None:
+        """Accepts tuned_state() output (or a bare list of ExecConfig dicts)."""
+        if isinstance(state, list):
+            state = {"configs": state, "fuse_pool": {}}
+        self.configs = [ExecConfig(**c) for c in state["configs"]]
+        self.fuse_pool = {int(k): bool(v) for k, v in state.get("fuse_pool", {}).items()}
+        self.graph = None
+        self._build()
+
     # -- per-layer autotuning ----------------------------------------------------
     def autotune(self, repeats: int = 5, warmup: int = 2, noise_floor: float = 0.02):
         """Per-layer tile search (autotune_sb semantics, engine.py:139-170), timed
-        with CUDA events on the model's real buffers; rebuilds the plans."""
+        with CUDA events on the model's real buffers; rebuilds the plans.  For a conv
+        that feeds a max-pool both forms compete: the pool fused into the conv epilogue
+        (2-row, even-width pixel blocks) and a plain conv (any tile, e.g. halo-skipping
+        pixel classes) followed by the pool kernel."""
         import torch
         best_cfgs = []
-        for st in [s for s in self.steps if s[0] == "conv"]:
+        steps = self.steps
+        for si, st in enumerate(steps):
+            if st[0] != "conv":
+                continue
             _, li, plan0, _, xin, yout, epi = st
             g = self.geoms[li]
             usable = [sb for sb in (1, 2, 4, 8, 16, 32) if self.batch % sb == 0]
@@ -400,17 +424,40 @@ class SparseVGG16:
             cands = [_cfg_of(plan0, self.configs[li], self.interleave)] + [
                 c for c in tile_candidates(g, self.batch, usable, self.precision, kern)
                 if not self.interleave or c.samples_per_cta == self.interleave]
-            if epi.pool:  # keep the pool fused: 2-row, even-width pixel blocks only
-                cands = [c for c in cands if c.rows_per_thread == 2 and c.pix_per_thread % 2 == 0]
+            variants = [(epi, yout, 0.0, None)]  # (epilogue, output buffer, extra ms, filter)
+            if li in self.pre_pool and self.interleave:
+                if epi.pool:  # fused now: pooled layout/buffer are the step's own
+                    pooled_lay, pooled_buf = epi.out, yout
+                else:  # unfused now: the next step is the pool
+                    _, _, _, pooled_lay, _, pooled_buf = steps[si + 1]
+                flat = _lib.act_layout(g.out_channels, g.out_h, g.out_w, 0, 0, self.eb, self.interleave)
+                flat_buf = self._buf(flat, yout.dtype)
+                e_f, e_u = _lib.Epilogue(), _lib.Epilogue()
+                ctypes.pointer(e_f)[0] = epi
+                ctypes.pointer(e_u)[0] = epi
+                e_f.pool, e_f.out = 1, pooled_lay
+                e_u.pool, e_u.out = 0, flat
+                pdt = _lib.USC_F32 if yout.element_size() == 4 else _lib.USC_F16
+                t_pool = time_median_cuda(lambda: _lib.check(_lib.lib().usc_maxpool2(
+                    _lib.ref(flat), _lib.ref(pooled_lay), pdt, self.batch, _lib.t_ptr(flat_buf),
+                    _lib.t_ptr(pooled_buf), _lib.stream_ptr()), "pool"), repeats, warmup)
+                variants = [(e_f, pooled_buf, 0.0, lambda c: c.rows_per_thread == 2 and c.pix_per_thread % 2 == 0),
+                            (e_u, flat_buf, t_pool, None)]
             for cfg in cands:
                 try:
                     plan, blob = self._plan_for(li, cfg)
                 except ValueError:
                     continue
-                ms = time_median_cuda(lambda: launch(plan, blob, xin, yout, epi), repeats, warmup)
-                results.append((ms, cfg))
-            best = min(ms for ms, _ in results)
-            pick = next(cfg for ms, cfg in results if ms <= best * (1.0 + noise_floor))
+                for e, buf, extra, ok in variants:
+                    if ok is not None and not (plan.PR == 2 and plan.PC % 2 == 0):
+                        continue
+                    ms = time_median_cuda(lambda: launch(plan, blob, xin, buf, e), repeats, warmup) + extra
+                    fused = bool(e.pool)
+                    results.append((ms, cfg, fused))
+            best = min(ms for ms, _, _ in results)
+            pick, fused = next((cfg, f) for ms, cfg, f in results if ms <= best * (1.0 + noise_floor))
+            if li in self.pre_pool:
+                self.fuse_pool[li] = fused
             best_cfgs.append(pick)
         torch.cuda.synchronize()
         self.configs = best_cfgs

@@ -4,17 +4,16 @@
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
-from paper_2112_15445_b200 import ExecConfig
+
 from paper_2112_15445_b200.engine import launch
 from paper_2112_15445_b200.models import SparseVGG16, vgg16_rng, vgg16_weights
 L = int(sys.argv[1]) if len(sys.argv) > 1 else 5
 B = int(os.environ.get("B", 256))
 rng = vgg16_rng(0.93)
-cfgs = None
+m = SparseVGG16(vgg16_weights(rng, 0.93), B)
 if len(sys.argv) > 2:  # per-layer tiles dumped by bench.py --dump-configs
     import json
-    cfgs = [ExecConfig(**c) for c in json.load(open(sys.argv[2]))]
-m = SparseVGG16(vgg16_weights(rng, 0.93), B, configs=cfgs)
+    m.load_tuned_state(json.load(open(sys.argv[2])))
 m.forward(torch.randn(B, 3, 32, 32, device="cuda"))
 st = [s for s in m.steps if s[0] == "conv"][L]
 _, li, plan, blob, xin, yout, epi = st
