@@ -398,6 +398,7 @@ def autotune_sb(input: DenseTensor4, filt: CsrFilter, candidates=SB_CANDIDATES, 
         ms = time_median_cuda(lambda: launch(plan, blob, pads[lk], y), repeats, warmup)
         results.append((ms, cfg))
     best = min(ms for ms, _ in results)
+    filt._packs.clear()  # the candidates' device packs (the caller re-packs its pick)
     for sb in usable:  # ascending, so the smallest near-tie wins
         for ms, cfg in results:
             if cfg.sub_batch == sb and ms <= best * (1.0 + noise_floor):

@@ -456,6 +456,7 @@ class SparseVGG16:
                     results.append((ms, cfg, fused))
             best = min(ms for ms, _, _ in results)
             pick, fused = next((cfg, f) for ms, cfg, f in results if ms <= best * (1.0 + noise_floor))
+            self.filters[li]._packs.clear()  # drop the candidates' device packs (rebuilt for the pick)
             if li in self.pre_pool:
                 self.fuse_pool[li] = fused
             best_cfgs.append(pick)
