@@ -140,6 +140,11 @@ typedef struct usc_epilogue {
                                   * binary16 codes (the BI kernel's int8 staging) */
     float rq_scale;              /* 1/sigma of the next layer's input (a power of two) */
     int32_t rq_limit;            /* 2^(bits-1) - 1 */
+    int32_t residual;            /* BI kernel, F32/F16: 1 = add the shortcut tensor `res` (same logical
+                                  * shape as the output, layout `res_layout`) before the ReLU:
+                                  * F32 v = acc + r; F16 v = round16(round16(acc) + r) */
+    usc_act_layout res_layout;
+    uint64_t res;                /* device address of the shortcut tensor */
 } usc_epilogue;
 
 /* ---- library ---------------------------------------------------------- */
@@ -225,6 +230,14 @@ int usc_unpad_output(const usc_act_layout *layout, int32_t dtype, int32_t n, con
  * or the epilogue's padded layout. */
 int usc_conv_forward(const usc_plan *plan, const void *blob_dev, const void *x_dev, void *y_dev,
                      const usc_epilogue *epi, void *stream);
+/* usc_conv_forward on a window of a larger resident buffer: the plan's (hp x ws) input
+ * is read from x_dev with the strides of `x_layout` (same channels and interleave, at
+ * least as large).  Exact-geometry views of ResNet's stride-2 layers (ConvGeometry
+ * rejects 32 -> 16 with pad 1, tensor.py:186-190): a 3x3 stride-2 conv reads the
+ * top/left 33x33 of the 34x34 halo buffer with pad 0; a 1x1 stride-2 projection reads
+ * the 31x31 interior window (x_dev advanced to element (1,1)).  BI plans only. */
+int usc_conv_forward_view(const usc_plan *plan, const void *blob_dev, const void *x_dev,
+                          const usc_act_layout *x_layout, void *y_dev, const usc_epilogue *epi, void *stream);
 /* Reference-shaped kernel entry, the exact analogue of the numba FFI
  * kernels.sparse_conv_blocks(xflat, row_ptr, col_offsets, theta, out, blocks, sb,
  * x_size, s_h, s_w, padded_w) (kernels.py:57-58), all arrays on the device:

@@ -71,7 +71,7 @@ class Epilogue(ctypes.Structure):
     _fields_ = [("relu", c_i32), ("saturate", c_i32), ("cap", ctypes.c_float), ("saturate2", c_i32),
                 ("cap2", ctypes.c_float), ("scale", ctypes.c_float), ("out_padded", c_i32),
                 ("out", ActLayout), ("pool", c_i32), ("requant", c_i32), ("rq_scale", ctypes.c_float),
-                ("rq_limit", c_i32)]
+                ("rq_limit", c_i32), ("residual", c_i32), ("res_layout", ActLayout), ("res", ctypes.c_uint64)]
 
 
 class CsrCorruptionError(ValueError):
@@ -101,6 +101,7 @@ _SIGS = {
     "usc_pad_input": (c_i32, [c_ptr, c_i32, c_i32, c_ptr, c_ptr, c_ptr]),
     "usc_unpad_output": (c_i32, [c_ptr, c_i32, c_i32, c_ptr, c_ptr, c_ptr]),
     "usc_conv_forward": (c_i32, [c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr]),
+    "usc_conv_forward_view": (c_i32, [c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr]),
     "usc_sparse_conv_blocks": (c_i32, [c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_i64, c_i32, c_i64,
                                        c_i32, c_i32, c_i32, c_i32, c_i32, c_i32, c_ptr]),
     "usc_round_binary16": (c_i32, [c_ptr, c_ptr, c_i64, c_i32, c_ptr]),

@@ -90,6 +90,10 @@ struct Epi {
     int requant, rq_limit;
     float rq_scale;
     long long o_sample_stride;  // elements per sample (il 0) / interleave block (il 32, 64)
+    int residual;               // add the shortcut tensor before the ReLU
+    const void *res;
+    int rC, rHp, rWs, rph, rpw, ril;
+    long long r_sample_stride;
 };
 
 // Apply the stored entries [e0, e1) of one output channel to P pixels.

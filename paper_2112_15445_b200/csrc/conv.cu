@@ -433,6 +433,17 @@ Epi make_epi(const usc_epilogue *e) {
     ep.requant = e->requant;
     ep.rq_scale = e->rq_scale;
     ep.rq_limit = e->rq_limit;
+    ep.residual = e->residual;
+    if (e->residual) {
+        ep.res = reinterpret_cast<const void *>(e->res);
+        ep.rC = e->res_layout.channels;
+        ep.rHp = e->res_layout.hp;
+        ep.rWs = e->res_layout.ws;
+        ep.rph = e->res_layout.pad_h;
+        ep.rpw = e->res_layout.pad_w;
+        ep.ril = e->res_layout.interleave;
+        ep.r_sample_stride = e->res_layout.sample_stride;
+    }
     if (e->out_padded) {
         ep.oHp = e->out.hp;
         ep.oWs = e->out.ws;
@@ -485,8 +496,23 @@ int usc_peak_fp32_muladd(int32_t device, double *tflops) {
     return cuda_check("peak probe");
 }
 
+static int conv_forward_impl(const usc_plan *pl, const void *blob, const void *x, const usc_act_layout *xv, void *y,
+                             const usc_epilogue *epi, void *stream);
+
 int usc_conv_forward(const usc_plan *pl, const void *blob, const void *x, void *y,
                      const usc_epilogue *epi, void *stream) {
+    return conv_forward_impl(pl, blob, x, nullptr, y, epi, stream);
+}
+
+int usc_conv_forward_view(const usc_plan *pl, const void *blob, const void *x, const usc_act_layout *x_layout,
+                          void *y, const usc_epilogue *epi, void *stream) {
+    if (!x_layout) return fail(USC_ERR_VALUE, "null input layout");
+    if (pl && pl->kernel < 3) return fail(USC_ERR_UNSUPPORTED, "input views need a batch-interleaved plan");
+    return conv_forward_impl(pl, blob, x, x_layout, y, epi, stream);
+}
+
+static int conv_forward_impl(const usc_plan *pl, const void *blob, const void *x, const usc_act_layout *xv, void *y,
+                             const usc_epilogue *epi, void *stream) {
     if (!pl || !blob || !x || !y) return fail(USC_ERR_VALUE, "null argument");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const usc_geometry &g = pl->g;
@@ -502,9 +528,15 @@ int usc_conv_forward(const usc_plan *pl, const void *blob, const void *x, void *
         if (!ep.out_padded || epi->out.height != pl->out_h / 2 || epi->out.width != pl->out_w / 2)
             return fail(USC_ERR_VALUE, "fused max-pool needs the pooled output layout");
     }
+    if (ep.residual && (pl->kernel < 3 || (pl->dtype != USC_F32 && pl->dtype != USC_F16) || !epi->res ||
+                        epi->res_layout.interleave == 0 || epi->res_layout.channels != g.out_channels ||
+                        epi->res_layout.height != pl->out_h || epi->res_layout.width != pl->out_w ||
+                        epi->pool))
+        return fail(USC_ERR_VALUE, "residual epilogue needs an F32/F16 BI plan, an interleaved shortcut of the "
+                                   "output's shape and no fused pool");
     if (ep.requant && (pl->kernel < 3 || pl->dtype != USC_I8))
         return fail(USC_ERR_UNSUPPORTED, "requantising epilogue needs an int8 BI plan");
-    if (pl->kernel == 3 || pl->kernel == 4) return usc::launch_bi(pl, blob, x, y, ep, st);
+    if (pl->kernel == 3 || pl->kernel == 4) return usc::launch_bi(pl, blob, x, y, ep, st, xv);
     if (ep.out_padded && ep.oil != 0)
         return fail(USC_ERR_UNSUPPORTED, "kernels 1/2 write interleave-0 layouts only");
     // blob = [16 x f32 centroid table][int32 cpg, 16-B aligned][entries]

@@ -20,7 +20,7 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_tiled() {
 }
 
 int launch_bi(const usc_plan *pl, const void *blob, const void *x, void *y, const usc_dev::Epi &ep,
-              cudaStream_t st) {
+              cudaStream_t st, const usc_act_layout *xv) {
     // blob = [64 B][int32 blk[G*n_chunks + 1]][int32 perm[G*DT]][int32 rowcls[Yh], colcls[Yw]]
     // [blocks], each part 16-B aligned (usc_pack, kernel 3)
     const char *cb = static_cast<const char *>(blob);
@@ -37,8 +37,12 @@ int launch_bi(const usc_plan *pl, const void *blob, const void *x, void *y, cons
                                 (cuuint64_t)pl->g.in_channels, (cuuint64_t)((pl->n + IL - 1) / IL)};
     const bool h16 = pl->dtype != USC_F32;  // binary16-staged activations (F16, CB4, I8 codes)
     const cuuint64_t px = (cuuint64_t)IL * (h16 ? 2 : 4);
-    const cuuint64_t strides[4] = {px, px * pl->in.ws, px * pl->in.ws * pl->in.hp,
-                                   px * pl->in.ws * pl->in.hp * pl->g.in_channels};
+    // strides of the buffer x lives in: the plan's own layout, or a larger buffer the plan's
+    // (hp x ws) input is a window of (usc_conv_forward_view)
+    const usc_act_layout &bl = xv ? *xv : pl->in;
+    if (xv && (xv->interleave != IL || xv->hp < pl->in.hp || xv->ws < pl->in.ws || xv->channels != pl->g.in_channels))
+        return fail(USC_ERR_VALUE, "input view does not fit its buffer layout");
+    const cuuint64_t strides[4] = {px, px * bl.ws, px * bl.ws * bl.hp, (cuuint64_t)bl.sample_stride * (px / IL)};
     const cuuint32_t box[5] = {(cuuint32_t)IL, (cuuint32_t)pl->TWs, (cuuint32_t)pl->HS, (cuuint32_t)pl->CC, 1};
     const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
     CUresult r = enc(&a.xmap, h16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, const_cast<void *>(x), dims, strides, box, estr,

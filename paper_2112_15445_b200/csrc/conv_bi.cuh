@@ -302,6 +302,17 @@ __device__ __forceinline__ void run_pairs(typename Ops<KIND, SPL>::A (&acc)[PC *
 // output value of one accumulator (store_one semantics, common.cuh): F32 -> ReLU;
 // F16/CB4 -> the _half_hook order of quantization.py:238-244 (saturate, binary16
 // rounding, ReLU, saturate2 + rounding)
+// shortcut value of the lane's j-th sample at (b, d, row, col) (residual epilogue)
+template <int KIND>
+__device__ __forceinline__ float res_value(const Epi &ep, long long b, int d, int row, int col) {
+    const long long i = (b / ep.ril) * ep.r_sample_stride +
+                        ((((long long)d * ep.rHp + row + ep.rph) * ep.rWs + col + ep.rpw) * ep.ril) + b % ep.ril;
+    if constexpr (KIND == USC_F32)
+        return static_cast<const float *>(ep.res)[i];
+    else
+        return __half2float(static_cast<const __half *>(ep.res)[i]);
+}
+
 template <int KIND>
 __device__ __forceinline__ float epi_value(float v, const Epi &ep) {
     // ReLU is np.where(v > 0, v, 0) (nn.py:96-98): NaN -> 0
@@ -327,6 +338,19 @@ __device__ __forceinline__ float epi_value(float v, const Epi &ep) {
         }
         return v;
     }
+}
+
+// residual form (ResNet block output): F32 v = relu(acc + r); F16 v =
+// relu(round16(round16(acc) + r)) -- the conv's binary16 hook, the add, the add's hook
+template <int KIND>
+__device__ __forceinline__ float epi_value_res(float v, const Epi &ep, float r) {
+    if constexpr (KIND == USC_F32) {
+        v = __fadd_rn(v, r);
+    } else {
+        v = __fadd_rn(round16f(v), r);
+        v = round16f(v);
+    }
+    return ep.relu ? (v > 0.0f ? v : 0.0f) : v;
 }
 
 __device__ __forceinline__ uint32_t pack_h2(float lo, float hi) {  // exact: values on the binary16 grid
@@ -416,6 +440,17 @@ __device__ __forceinline__ void store_tile(const BiArgs &a, typename Ops<KIND, S
 #pragma unroll
         for (int p = 0; p < P; ++p) {
             O::unpack(acc[dw][p], v[p]);
+            if constexpr (KIND == USC_F32 || KIND == USC_F16) {
+                if (a.ep.residual) {
+                    const int rr = r + p / PC, cc = col0 + p % PC;
+#pragma unroll
+                    for (int j = 0; j < SPL; ++j)
+                        v[p][j] = (b0 + j < a.N && rr < a.Yh && cc < a.Yw)
+                                      ? epi_value_res<KIND>(v[p][j], a.ep, res_value<KIND>(a.ep, b0 + j, d, rr, cc))
+                                      : 0.0f;
+                    continue;
+                }
+            }
 #pragma unroll
             for (int j = 0; j < SPL; ++j) v[p][j] = epi_value<KIND>(v[p][j], a.ep);
         }

@@ -17,6 +17,6 @@ struct Epi;
 }
 namespace usc {
 int launch_bi(const usc_plan *pl, const void *blob, const void *x, void *y, const usc_dev::Epi &ep,
-              cudaStream_t st);
+              cudaStream_t st, const usc_act_layout *x_view = nullptr);
 }
 #endif

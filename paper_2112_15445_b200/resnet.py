@@ -1,0 +1,226 @@
+"""Pruned ResNet-50 for CIFAR-scale inputs on the sparse engine (BASELINE configs[2]).
+
+The reference has no ResNet; SURVEY.md §8d (cfg3) defines the network from its
+pieces: a 3x3 stem (stride 1, no max-pool), bottleneck stages at 32/16/8/4 with
+widths 64/128/256/512 (3/4/6/3 blocks, expansion 4, stride on the 3x3 and the
+projection), 53 sparse convs.  Two precisions, as the reference's modes:
+  fp32 -- every conv bit-identical to sparse_conv_forward; block output
+          relu(conv3 + shortcut);
+  fp16 -- 16b/16b (quantization.py:257-301): binary16 weights and activations,
+          every layer output rounded to binary16 (the conv hook), the residual add
+          rounded again, then ReLU.
+Stride-2 layers use the reference's exact geometries (ConvGeometry rejects 32 -> 16
+with pad 1, tensor.py:186-190): the 3x3 reads the top/left 33x33 window of its
+34x34 zero-haloed input (pad 0), the 1x1 projection the top/left 31x31 window --
+through usc_conv_forward_view, no copies.  Every activation stays resident in the
+BI64 layout; the residual add and ReLU are fused into conv3's epilogue.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import zlib
+
+import numpy as np
+
+from . import _lib
+from .csr import build_csr
+from .engine import ExecConfig, launch, plan_for, tile_candidates, time_median_cuda
+from .pruning import synthesize_masked_weights
+from .tensor import ConvGeometry, PrecisionMode
+
+STAGES = ((64, 3, 1), (128, 4, 2), (256, 6, 2), (512, 3, 2))  # (width, blocks, stride)
+
+
+def resnet50_layers(hw: int = 32):
+    """[(name, ConvGeometry, role, stride)] in execution order; role in {stem, c1, c2,
+    c3, proj}."""
+    out = [("stem", ConvGeometry(3, 64, 3, 3, hw, hw, padding=(1, 1)), "stem", 1)]
+    c_in = 64
+    for si, (width, blocks, stride) in enumerate(STAGES):
+        for b in range(blocks):
+            s = stride if b == 0 else 1
+            tag = f"s{si}b{b}"
+            out.append((f"{tag}.c1", ConvGeometry(c_in, width, 1, 1, hw, hw), "c1", 1))
+            if s == 2:
+                out.append((f"{tag}.c2", ConvGeometry(width, width, 3, 3, hw + 1, hw + 1, stride=(2, 2)), "c2", 2))
+            else:
+                out.append((f"{tag}.c2", ConvGeometry(width, width, 3, 3, hw, hw, padding=(1, 1)), "c2", 1))
+            hw_out = hw // s
+            if b == 0:
+                if s == 2:
+                    g = ConvGeometry(c_in, 4 * width, 1, 1, hw - 1, hw - 1, stride=(2, 2))
+                else:
+                    g = ConvGeometry(c_in, 4 * width, 1, 1, hw, hw)
+                out.append((f"{tag}.proj", g, "proj", s))
+            out.append((f"{tag}.c3", ConvGeometry(width, 4 * width, 1, 1, hw_out, hw_out), "c3", 1))
+            c_in, hw = 4 * width, hw_out
+    return out
+
+
+def resnet50_weights(sparsity: float, seed: int = 0, precision=PrecisionMode.BINARY32):
+    rng = np.random.default_rng([seed, zlib.crc32(b"resnet50-cifar"), int(round(sparsity * 1000))])
+    return [synthesize_masked_weights(g, sparsity, rng, precision) for _, g, _, _ in resnet50_layers()]
+
+
+class SparseResNet50:
+    """ResNet-50 CIFAR conv trunk (53 sparse convs) on one GPU for a fixed batch.
+    forward(x): plain NCHW (n,3,32,32) -> (n,2048,4,4) features."""
+
+    def __init__(self, weights, batch: int, precision=PrecisionMode.BINARY32, device=None):
+        import torch
+        self.precision = precision
+        self.dtype = _lib.USC_F16 if precision is PrecisionMode.BINARY16 else _lib.USC_F32
+        self.tdtype = torch.float16 if self.dtype == _lib.USC_F16 else torch.float32
+        self.eb = 2 if self.dtype == _lib.USC_F16 else 4
+        self.batch = batch
+        self.device = torch.device(device or "cuda")
+        self.layers = resnet50_layers()
+        self.filters = [build_csr(w, g) for w, (_, g, _, _) in zip(weights, self.layers)]
+        self.configs = [ExecConfig(samples_per_cta=64) for _ in self.layers]
+        self.graph = None
+        self._build()
+
+    # -- buffers -------------------------------------------------------------------
+    def _lay(self, c, hw, halo):
+        return _lib.act_layout(c, hw, hw, halo, halo, self.eb, 64)
+
+    def _buf(self, lay):
+        import torch
+        return torch.zeros(lay.elems(self.batch), dtype=self.tdtype, device=self.device)
+
+    def _build(self):
+        n = self.batch
+        self.steps = []  # (li, plan, blob, x, x_view_layout | None, y, epilogue)
+        self.in_layout = self._lay(3, 32, 1)
+        self.x_buf = self._buf(self.in_layout)
+
+        def conv(li, x, x_lay, y_lay, relu=True, residual=None):
+            name, g, role, s = self.layers[li]
+            plan, blob = plan_for(self.filters[li], n, self.dtype, self.configs[li], self.filters[li].weights,
+                                  device=self.device)
+            if plan.in_.interleave != 64:
+                raise RuntimeError(f"{name}: the network needs BI64 plans")
+            y = self._buf(y_lay)
+            e = _lib.Epilogue()
+            e.relu, e.scale, e.out_padded, e.out = int(relu), 1.0, 1, y_lay
+            if residual is not None:
+                r, r_lay = residual
+                e.residual, e.res_layout, e.res = 1, r_lay, r.data_ptr()
+            # a window of a larger buffer (the stride-2 exact geometries) goes through the view entry
+            view = None
+            if (plan.in_.hp, plan.in_.ws) != (x_lay.hp, x_lay.ws):
+                view = x_lay
+            self.steps.append((li, plan, blob, x, view, y, e))
+            return y
+
+        cur, cur_lay = self.x_buf, self.in_layout
+        li = 0
+        cur = conv(li, cur, cur_lay, self._lay(64, 32, 0))  # stem (its output feeds 1x1 convs)
+        cur_lay = self._lay(64, 32, 0)
+        li += 1
+        hw, c_in = 32, 64
+        for width, blocks, stride in STAGES:
+            for b in range(blocks):
+                s = stride if b == 0 else 1
+                hw_out = hw // s
+                blk_in, blk_lay = cur, cur_lay
+                h1_lay = self._lay(width, hw, 1)
+                h1 = conv(li, blk_in, blk_lay, h1_lay)
+                li += 1
+                h2_lay = self._lay(width, hw_out, 0)
+                h2 = conv(li, h1, h1_lay, h2_lay)
+                li += 1
+                if b == 0:
+                    sc_lay = self._lay(4 * width, hw_out, 0)
+                    sc = conv(li, blk_in, blk_lay, sc_lay, relu=False)
+                    li += 1
+                else:
+                    sc, sc_lay = blk_in, blk_lay
+                out_lay = self._lay(4 * width, hw_out, 0)
+                cur = conv(li, h2, h2_lay, out_lay, relu=True, residual=(sc, sc_lay))
+                cur_lay = out_lay
+                li += 1
+                hw, c_in = hw_out, 4 * width
+        self.out_buf, self.out_layout = cur, cur_lay
+
+    # -- execution -------------------------------------------------------------------
+    def _launch(self, st, stream=None):
+        li, plan, blob, x, view, y, e = st
+        L = _lib.lib()
+        sp = _lib.stream_ptr(stream)
+        if view is None:
+            _lib.check(L.usc_conv_forward(_lib.ref(plan), _lib.t_ptr(blob), _lib.t_ptr(x), _lib.t_ptr(y),
+                                          _lib.ref(e), sp), self.layers[li][0])
+        else:
+            _lib.check(L.usc_conv_forward_view(_lib.ref(plan), _lib.t_ptr(blob), _lib.t_ptr(x), _lib.ref(view),
+                                               _lib.t_ptr(y), _lib.ref(e), sp), self.layers[li][0])
+
+    def load_input(self, x, stream=None):
+        _lib.check(_lib.lib().usc_pad_input(_lib.ref(self.in_layout), self.dtype, self.batch, _lib.t_ptr(x),
+                                            _lib.t_ptr(self.x_buf), _lib.stream_ptr(stream)), "pad")
+
+    def run(self, stream=None):
+        for st in self.steps:
+            self._launch(st, stream)
+
+    def output(self, stream=None):
+        import torch
+        lay = self.out_layout
+        out = torch.empty((self.batch, lay.channels, lay.height, lay.width), dtype=self.tdtype, device=self.device)
+        _lib.check(_lib.lib().usc_unpad_output(_lib.ref(lay), self.dtype, self.batch, _lib.t_ptr(self.out_buf),
+                                               _lib.t_ptr(out), _lib.stream_ptr(stream)), "unpad")
+        return out
+
+    def forward(self, x):
+        self.load_input(x)
+        if self.graph is not None:
+            self.graph.replay()
+        else:
+            self.run()
+        return self.output()
+
+    def capture(self):
+        import torch
+        s = torch.cuda.Stream(device=self.device)
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            self.run()
+        torch.cuda.current_stream().wait_stream(s)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self.run()
+        self.graph = g
+        return g
+
+    def autotune(self, repeats: int = 3, warmup: int = 1, noise_floor: float = 0.02):
+        """Per-conv tile search on the network's own buffers and epilogues."""
+        import torch
+        picks = []
+        for st in self.steps:
+            li, plan0, _, x, view, y, e = st
+            g = self.layers[li][1]
+            cands = [self.configs[li]] + [c for c in tile_candidates(g, self.batch, [1], self.precision, (3,))
+                                          if c.samples_per_cta == 64]
+            res = []
+            for cfg in cands:
+                try:
+                    plan, blob = plan_for(self.filters[li], self.batch, self.dtype, cfg, self.filters[li].weights,
+                                          device=self.device)
+                except ValueError:
+                    continue
+                trial = (li, plan, blob, x, view, y, e)
+                try:
+                    ms = time_median_cuda(lambda: self._launch(trial), repeats, warmup)
+                except RuntimeError:
+                    continue
+                res.append((ms, cfg))
+            best = min(ms for ms, _ in res)
+            picks.append(next(cfg for ms, cfg in res if ms <= best * (1.0 + noise_floor)))
+            self.filters[li]._packs.clear()
+        torch.cuda.synchronize()
+        self.configs = picks
+        self.graph = None
+        self._build()
+        return picks

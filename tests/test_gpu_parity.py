@@ -319,3 +319,52 @@ def test_stream_forward_matches_forward():
     m.stream_forward(xs, outs).synchronize()
     for x, o in zip(xs, outs):
         assert torch.equal(m.forward(x.cuda()).cpu(), o)
+
+
+@pytest.mark.parametrize("prec", [F32, F16])
+def test_resnet50_network_vs_oracle(prec):
+    """ResNet-50 CIFAR (53 sparse convs, stride-2 exact-geometry views, residual add +
+    ReLU fused into conv3) against the composition of the reference's pieces: per conv
+    sparse_conv_forward (binary16 hook for fp16), ReLU, and the block output
+    relu(conv3 + shortcut) (fp16: relu(round16(round16(conv3) + shortcut)))."""
+    import torch
+    from paper_2112_15445_b200.resnet import SparseResNet50, resnet50_layers, resnet50_weights
+    ws = resnet50_weights(0.9, seed=2, precision=prec)
+    rng = np.random.default_rng(9)
+    x = rng.standard_normal((64, 3, 32, 32)).astype(np.float32)
+    if prec is F16:
+        x = oracle.round_to_binary16(x)
+    m = SparseResNet50(ws, 64, precision=prec)
+    xd = torch.from_numpy(x).cuda()
+    got = m.forward(xd.half() if prec is F16 else xd).float().cpu().numpy()
+
+    layers = resnet50_layers()
+    hook = oracle.round_to_binary16 if prec is F16 else (lambda a: a)
+
+    def conv(li, a):
+        name, g, role, s = layers[li]
+        if role == "c2" and s == 2:
+            a = np.pad(a, ((0, 0), (0, 0), (1, 0), (1, 0)))
+        if role == "proj" and s == 2:
+            a = np.ascontiguousarray(a[:, :, :g.input_h, :g.input_w])
+        gt = (g.in_channels, g.out_channels, g.filter_h, g.filter_w, g.input_h, g.input_w, g.stride, g.padding)
+        csr = oracle.build_csr(np.ascontiguousarray(ws[li].data), gt)
+        return hook(oracle.sparse_conv_forward(a, csr, gt, threads=oracle.max_threads()))
+
+    a = oracle.relu(conv(0, x))
+    li = 1
+    from paper_2112_15445_b200.resnet import STAGES
+    for width, blocks, stride in STAGES:
+        for b in range(blocks):
+            h1 = oracle.relu(conv(li, a))
+            h2 = oracle.relu(conv(li + 1, h1))
+            li += 2
+            if b == 0:
+                sc = conv(li, a)
+                li += 1
+            else:
+                sc = a
+            y = conv(li, h2)
+            li += 1
+            a = oracle.relu(hook((y + sc).astype(np.float32)))
+    assert np.array_equal(got, a)
