@@ -201,6 +201,56 @@ SWEEP_SHAPES = {"r50-3x3-64x32": (64, 64, 3, 32), "r50-3x3-256x8": (256, 256, 3,
                 "r50-1x1-64x256-32": (64, 256, 1, 32), "r50-1x1-256x64-32": (256, 64, 1, 32)}
 
 
+def resnet50_network(prec_name, steps, batch=256, sparsity=0.9):
+    """configs[2] as a network: the 53-conv ResNet-50 CIFAR trunk (residual adds and ReLU
+    fused) on the engine, autotuned + CUDA graph, vs the same network on cuDNN (torch,
+    channels_last; fp16 on tensor cores, fp32 with TF32 off)."""
+    from paper_2112_15445_b200 import PrecisionMode
+    from paper_2112_15445_b200.resnet import STAGES, SparseResNet50, resnet50_layers, resnet50_weights
+    prec = PrecisionMode.BINARY16 if prec_name == "fp16" else PrecisionMode.BINARY32
+    tdt = torch.float16 if prec_name == "fp16" else torch.float32
+    ws = resnet50_weights(sparsity, 0, prec)
+    m = SparseResNet50(ws, batch, precision=prec)
+    m.autotune()
+    m.capture()
+    m.load_input(torch.randn(batch, 3, 32, 32, device="cuda").to(tdt))
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
+    ms = timed(lambda: m.graph.replay(), steps, flush)
+    # cuDNN: torch semantics (stride-2 3x3 pad 1, stride-2 1x1) on the same masked weights
+    torch.backends.cudnn.benchmark = True
+    torch.backends.cudnn.allow_tf32 = False
+    cl = torch.channels_last
+    wt = [torch.from_numpy(np.array(w.data)).cuda().to(tdt).contiguous(memory_format=cl) for w in ws]
+    layers = resnet50_layers()
+    xt = torch.randn(batch, 3, 32, 32, device="cuda", dtype=tdt).contiguous(memory_format=cl)
+    F = torch.nn.functional
+
+    def fwd():
+        a = F.relu(F.conv2d(xt, wt[0], padding=1))
+        li = 1
+        for width, blocks, stride in STAGES:
+            for b in range(blocks):
+                s = stride if b == 0 else 1
+                h = F.relu(F.conv2d(a, wt[li]))
+                h = F.relu(F.conv2d(h, wt[li + 1], stride=s, padding=1))
+                li += 2
+                if b == 0:
+                    sc = F.conv2d(a, wt[li], stride=s)
+                    li += 1
+                else:
+                    sc = a
+                a = F.relu(F.conv2d(h, wt[li]) + sc)
+                li += 1
+        return a
+    cd = timed(fwd, steps, flush)
+    return {"config": f"pruned ResNet-50 CIFAR {int(sparsity * 100)}% {prec_name}, batch {batch}, full network "
+                      f"(53 sparse convs, residual adds)",
+            "images_per_s": round(batch / (ms / 1e3), 1), "ms_per_step": round(ms, 4),
+            "cudnn": {"images_per_s": round(batch / (cd / 1e3), 1), "ms_per_step": round(cd, 4),
+                      "kind": "fp16 tensor cores" if prec_name == "fp16" else "fp32, TF32 off"},
+            "speedup_vs_cudnn": round(cd / ms, 3)}
+
+
 def sweep(steps, shapes=None, sparsities=(0.5, 0.7, 0.9, 0.95, 0.98)):
     from paper_2112_15445_b200 import DenseTensor4, autotune_sb, build_csr, sparse_conv_forward
     from paper_2112_15445_b200.engine import launch, padded_input, plan_for, time_median_cuda
@@ -252,6 +302,9 @@ def main():
     for mode in ("int8", "cb4"):
         if args.only in (None, f"vgg16-{mode}"):
             print(json.dumps({"variant": f"vgg16-{mode}", **vgg16_quantised(mode, args.steps)}), flush=True)
+    for pn in ("fp16", "fp32"):
+        if args.only in (None, f"resnet50-net-{pn}"):
+            print(json.dumps({"variant": f"resnet50-net-{pn}", **resnet50_network(pn, args.steps)}), flush=True)
     if args.only in (None, "resnet50-fp16"):
         print(json.dumps({"variant": "resnet50-fp16", **resnet50_fp16()}), flush=True)
     if args.only in (None, "sweep") or (args.only or "").startswith("sweep:"):
