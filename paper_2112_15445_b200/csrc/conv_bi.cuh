@@ -428,6 +428,14 @@ __device__ __forceinline__ void store_tile(const BiArgs &a, typename Ops<KIND, S
         cstride = 1;
     }
     const bool vec = SPL == 2 && oil == IL;  // the lane's two samples adjacent: one vector store
+    // residual shortcut (BI layout): element (b0, d, r + pr, col0 + pc) = rbase + d*rdst + pr*rrow + pc*ril
+    long long rbase = 0, rdst = 0, rrow = 0;
+    if (a.ep.residual) {
+        rbase = (long long)(b0 / a.ep.ril) * a.ep.r_sample_stride +
+                (((long long)r + a.ep.rph) * a.ep.rWs + col0 + a.ep.rpw) * a.ep.ril + b0 % a.ep.ril;
+        rdst = (long long)a.ep.rHp * a.ep.rWs * a.ep.ril;
+        rrow = (long long)a.ep.rWs * a.ep.ril;
+    }
     const int ncol = min(PC, a.Yw - col0);
     const int nrow = min(PR, a.Yh - r);
 #pragma unroll
@@ -443,11 +451,27 @@ __device__ __forceinline__ void store_tile(const BiArgs &a, typename Ops<KIND, S
             if constexpr (KIND == USC_F32 || KIND == USC_F16) {
                 if (a.ep.residual) {
                     const int rr = r + p / PC, cc = col0 + p % PC;
+                    if (rr < a.Yh && cc < a.Yw) {
+                        float rv[SPL];
+                        if (SPL == 2 && a.ep.ril == IL) {  // the lane's two samples adjacent: one load
+                            const long long ri = rbase + (long long)d * rdst + (p / PC) * rrow + (p % PC) * IL;
+                            if constexpr (KIND == USC_F32) {
+                                const float2 q = *reinterpret_cast<const float2 *>(static_cast<const float *>(a.ep.res) + ri);
+                                rv[0] = q.x;
+                                rv[SPL - 1] = q.y;
+                            } else {
+                                const float2 q = __half22float2(
+                                    *reinterpret_cast<const __half2 *>(static_cast<const __half *>(a.ep.res) + ri));
+                                rv[0] = q.x;
+                                rv[SPL - 1] = q.y;
+                            }
+                        } else {
 #pragma unroll
-                    for (int j = 0; j < SPL; ++j)
-                        v[p][j] = (b0 + j < a.N && rr < a.Yh && cc < a.Yw)
-                                      ? epi_value_res<KIND>(v[p][j], a.ep, res_value<KIND>(a.ep, b0 + j, d, rr, cc))
-                                      : 0.0f;
+                            for (int j = 0; j < SPL; ++j) rv[j] = b0 + j < a.N ? res_value<KIND>(a.ep, b0 + j, d, rr, cc) : 0.0f;
+                        }
+#pragma unroll
+                        for (int j = 0; j < SPL; ++j) v[p][j] = epi_value_res<KIND>(v[p][j], a.ep, rv[j]);
+                    }
                     continue;
                 }
             }
