@@ -23,7 +23,7 @@
 //     output-channel slots of subgroup w / WS; DW*P accumulators per lane (SPL
 //     samples each) live for the whole input-channel loop; after a stage each warp
 //     arrives on empty[s] -- no CTA-wide barrier inside the loop;
-//   * entry block of one (group, chunk): int2 hdr[NCLS][DT] = {first, end} entry
+//   * entry block of one (group, chunk): int2 hdr[NCLS][DT] (padded to 16 B) = {first, end} entry
 //     index of every (pixel class, slot) run, then the runs, each starting 16-byte
 //     aligned so two entries are one LDS.128 broadcast.  Slots map to output
 //     channels through perm[] (the packer balances the warps' per-chunk work).  With
@@ -575,7 +575,7 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1) k_bi(const __grid_constant_
     // software-pipeline the pair loop when the second value set fits the register cap
     constexpr int REGCAP = NWC <= 8 ? 168 : (NWC <= 12 ? 128 : 96);
     constexpr int VR = (KIND == USC_F32) ? SPL : 1;  // registers per staged value
-    constexpr bool PIPE = SPL * DW * P + 4 * P * VR + 40 <= REGCAP;
+    constexpr bool PIPE = SPL * DW * P + 4 * P * VR + (KIND == USC_F32 ? 40 : 56) <= REGCAP;
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t *full = reinterpret_cast<uint64_t *>(smem);
     uint64_t *empty = full + 8;
@@ -633,7 +633,7 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1) k_bi(const __grid_constant_
     const int tr = wsi / a.SPRt, tcs = wsi - tr * a.SPRt;  // strip-row, strip within the tile
     const uint32_t base = ((tr * PR * a.s_h) * a.TWs + tcs * PC * SW) * PXB + lane * O::EB * SPL;
     const uint32_t rs = a.s_h * a.TWs * PXB;  // bytes between a thread's two pixel rows
-    const int hdr_bytes = a.ncls * a.DT * 8;
+    const int hdr_bytes = (a.ncls * a.DT * 8 + 15) & ~15;  // entries start 16-B aligned
     int s = 0;
     uint32_t ph = 0;
     for (int it = blockIdx.x; it < a.items; it += gridDim.x) {

@@ -158,7 +158,7 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1) k_bt(const __grid_constant_
     const int npos = a.CC * a.HS * a.TWs;  // positions of one chunk (<= 128)
     const int share = ((npos + MATES - 1) / MATES + 7) / 8 * 8;
     const int j0 = min(npos, mate * share), j1 = min(npos, j0 + share);
-    const int hdr_bytes = a.ncls * a.DT * 8;
+    const int hdr_bytes = (a.ncls * a.DT * 8 + 15) & ~15;  // entries start 16-B aligned
     int s = 0, kk = 0;
     uint32_t ph = 0;
     for (int it = blockIdx.x; it < a.items; it += gridDim.x) {

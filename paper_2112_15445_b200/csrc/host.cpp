@@ -511,7 +511,7 @@ int usc_plan_make(const usc_geometry *g0, int32_t n, int32_t dtype, const usc_ex
         const int64_t R = c.ent_reserve ? c.ent_reserve : 24 * 1024;
         auto ent_bytes = [&](int cc) {
             const int64_t worst =
-                (int64_t)NCLS * DT * 8 + NCLS * ((int64_t)DT * cc * g.filter_h * g.filter_w + DT) * 8 + 16;
+                (int64_t)NCLS * DT * 8 + 8 + NCLS * ((int64_t)DT * cc * g.filter_h * g.filter_w + DT) * 8 + 16;
             return (std::min(worst, R) + 127) / 128 * 128;
         };
         while (CC > 1 && S * ((CC * per_ch + 127) / 128 * 128 + ent_bytes(CC)) > budget) --CC;
@@ -912,13 +912,13 @@ int usc_pack(const usc_plan *pl, const int64_t *row_ptr, const int64_t *col, con
                         runs[2 * h + 1] = (int32_t)e;
                     }
                 }
-                const int64_t hdr = (int64_t)NCLS * DT * 8;
+                const int64_t hdr_raw = (int64_t)NCLS * DT * 8, hdr = align16(hdr_raw);  // entries 16-B aligned
                 const int64_t bytes = align16(hdr + e * 8);
                 if (!dry && pos + bytes + 16 > cap) return fail(USC_ERR_VALUE, "pack buffer too small");
                 if (!dry) {
-                    std::memcpy(b, runs.data(), (size_t)hdr);
+                    std::memset(b, 0, (size_t)bytes);
+                    std::memcpy(b, runs.data(), (size_t)hdr_raw);
                     char *ents = b + hdr;
-                    std::memset(ents, 0, (size_t)(bytes - hdr));
                     for (int64_t i = 0; i < (int64_t)out.size(); ++i) {
                         if (out[i].first < 0) continue;
                         int32_t v[2];

@@ -18,14 +18,23 @@ from paper_2112_15445_b200.engine import launch, plan_for, tile_candidates  # no
 
 def main():
     batch = int(sys.argv[1]) if len(sys.argv) > 1 else 64
+    fp16 = "--fp16" in sys.argv
+    only = [int(a) for a in sys.argv[2:] if a.isdigit()]
     dev = torch.device("cuda", 0)
-    model, _ = build_model(batch, dev)
-    x = torch.randn(batch, 3, 32, 32, device=dev)
+    if fp16:
+        from paper_2112_15445_b200 import PrecisionMode
+        from paper_2112_15445_b200.models import SparseVGG16, vgg16_rng, vgg16_weights
+        F16 = PrecisionMode.BINARY16
+        model = SparseVGG16(vgg16_weights(vgg16_rng(0.93, 0), 0.93, precision=F16), batch, precision=F16)
+        x = torch.randn(batch, 3, 32, 32, device=dev).half()
+    else:
+        model, _ = build_model(batch, dev)
+        x = torch.randn(batch, 3, 32, 32, device=dev)
     model.load_input(x)
     model.run()
     torch.cuda.synchronize()
     bad = 0
-    for st in [s for s in model.steps if s[0] == "conv"]:
+    for st in [s for s in model.steps if s[0] == "conv" and (not only or s[1] in only)]:
         _, li, plan0, blob0, xin, yout, epi = st
         keep = yout.clone()
         yout.fill_(float("nan"))  # the halo stays NaN in every run; only the interior is written
@@ -40,8 +49,7 @@ def main():
         n = 0
         for cfg in cands:
             try:
-                plan, blob = plan_for(model.filters[li], batch, model.dtype, cfg, model.filters[li].weights,
-                                      device=dev)
+                plan, blob = model._plan_for(li, cfg)
             except ValueError:
                 continue
             yout.fill_(float("nan"))

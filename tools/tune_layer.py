@@ -20,9 +20,16 @@ def main():
     ap.add_argument("layers", type=int, nargs="+")
     ap.add_argument("--top", type=int, default=12)
     ap.add_argument("--batch", type=int, default=BATCH)
+    ap.add_argument("--fp16", action="store_true", help="the BINARY16 network")
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
-    model, _ = build_model(args.batch, dev)
+    if args.fp16:
+        from paper_2112_15445_b200 import PrecisionMode
+        from paper_2112_15445_b200.models import SparseVGG16, vgg16_rng, vgg16_weights
+        F16 = PrecisionMode.BINARY16
+        model = SparseVGG16(vgg16_weights(vgg16_rng(0.93, 0), 0.93, precision=F16), args.batch, precision=F16)
+    else:
+        model, _ = build_model(args.batch, dev)
     for st in [s for s in model.steps if s[0] == "conv" and s[1] in args.layers]:
         _, li, plan0, _, xin, yout, epi = st
         g = model.geoms[li]
@@ -33,8 +40,7 @@ def main():
         res = []
         for cfg in cands:
             try:
-                plan, blob = plan_for(model.filters[li], args.batch, model.dtype, cfg,
-                                      model.filters[li].weights, device=dev)
+                plan, blob = model._plan_for(li, cfg)
             except ValueError:
                 continue
             ms = time_median_cuda(lambda: launch(plan, blob, xin, yout, epi), 7, 2)
