@@ -59,6 +59,7 @@ struct BiArgs {
     int WS, WC, SPRt, TH, row_tiles, col_tiles, G, tiles, S;
     int items, tfull, split;  // work items: tiles [0, tfull) whole, the rest split in `split` slot subsets
     int x_stage_bytes, stage_bytes;
+    int fast;                 // store_tile_fast applies (see there)
     Epi ep;
 };
 
@@ -565,6 +566,102 @@ __device__ __forceinline__ void store_tile(const BiArgs &a, typename Ops<KIND, S
 
 }
 
+// The common epilogue, compiled without runtime flags: ReLU output in the padded BI
+// layout of the same interleave (launch_bi sets a.fast for F32/F16 with relu, no
+// cap saturation/requant/residual).  The accumulator is never -0 (it starts at +0 and
+// x + (-x) rounds to +0), so fmaxf(v, 0) is np.where(v > 0, v, 0) including NaN -> 0;
+// ReLU commutes with the binary16 rounding, and the ReLU'd values are NaN-free, so
+// the 2x2 pool is a plain max (packed f16x2 for F16).
+template <int KIND, int PC, int PR, int DW, int SPL>
+__device__ __forceinline__ void store_tile_fast(const BiArgs &a, typename Ops<KIND, SPL>::A (&acc)[DW][PC * PR],
+                                                int g, int wc, int sb, int r, int col0, int part, int lane) {
+    constexpr int P = PC * PR;
+    constexpr int IL = 32 * SPL;
+    constexpr bool POOLABLE = PR == 2 && PC % 2 == 0;
+    const int *pm = a.perm + g * a.DT + wc * DW;
+    const bool pool = POOLABLE && a.ep.pool;
+    const int orow = pool ? r / 2 : r, ocol = pool ? col0 / 2 : col0;
+    const long long obase = (long long)sb * a.ep.o_sample_stride +
+                            (((long long)orow + a.ep.oph) * a.ep.oWs + ocol + a.ep.opw) * IL + lane * SPL;
+    const long long dstride = (long long)a.ep.oHp * a.ep.oWs * IL;
+    const int rstride = a.ep.oWs * IL;
+    const int ncol = min(PC, a.Yw - col0), nrow = min(PR, a.Yh - r);
+#pragma unroll
+    for (int dw = 0; dw < DW; ++dw) {
+        if (part >= 0 && dw % a.split != part) continue;
+        const int d = __ldg(pm + dw);
+        if (d < 0) continue;
+        const long long od = obase + d * dstride;
+        if constexpr (KIND == USC_F32) {
+            float *y = static_cast<float *>(a.y) + od;
+            float v[P][SPL];
+#pragma unroll
+            for (int p = 0; p < P; ++p) {
+                if constexpr (SPL == 1) {
+                    v[p][0] = fmaxf(acc[dw][p], 0.0f);
+                } else {
+                    float t[2];
+                    Ops<KIND, SPL>::unpack(acc[dw][p], t);
+                    v[p][0] = fmaxf(t[0], 0.0f);
+                    v[p][1] = fmaxf(t[1], 0.0f);
+                }
+            }
+            if (pool) {
+                if constexpr (POOLABLE) {
+#pragma unroll
+                    for (int c2 = 0; c2 < PC / 2; ++c2) {
+                        if (2 * c2 >= ncol) continue;
+                        float o[SPL];
+#pragma unroll
+                        for (int j = 0; j < SPL; ++j)
+                            o[j] = fmaxf(fmaxf(v[2 * c2][j], v[2 * c2 + 1][j]), fmaxf(v[PC + 2 * c2][j], v[PC + 2 * c2 + 1][j]));
+                        if constexpr (SPL == 1)
+                            y[c2 * IL] = o[0];
+                        else
+                            *reinterpret_cast<float2 *>(y + c2 * IL) = make_float2(o[0], o[SPL - 1]);
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int p = 0; p < P; ++p) {
+                    if (p / PC >= nrow || p % PC >= ncol) continue;
+                    float *q = y + (p / PC) * rstride + (p % PC) * IL;
+                    if constexpr (SPL == 1)
+                        *q = v[p][0];
+                    else
+                        *reinterpret_cast<float2 *>(q) = make_float2(v[p][0], v[p][SPL - 1]);
+                }
+            }
+        } else {  // F16, SPL 2: fp32 ReLU and finite saturation (sat_half), one cvt.rn.f16x2 per pixel
+            __half *y = static_cast<__half *>(a.y) + od;
+            auto rs = [](float v) {
+                v = fmaxf(v, 0.0f);
+                const float c = fminf(v, 65504.0f);  // finite overflow -> 65504, inf stays inf
+                return v == INFINITY ? v : c;
+            };
+            __half2 h[P];
+#pragma unroll
+            for (int p = 0; p < P; ++p) h[p] = __floats2half2_rn(rs(acc[dw][p].x), rs(acc[dw][p].y));
+            if (pool) {
+                if constexpr (POOLABLE) {
+#pragma unroll
+                    for (int c2 = 0; c2 < PC / 2; ++c2) {
+                        if (2 * c2 >= ncol) continue;
+                        *reinterpret_cast<__half2 *>(y + c2 * IL) =
+                            __hmax2(__hmax2(h[2 * c2], h[2 * c2 + 1]), __hmax2(h[PC + 2 * c2], h[PC + 2 * c2 + 1]));
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int p = 0; p < P; ++p) {
+                    if (p / PC >= nrow || p % PC >= ncol) continue;
+                    *reinterpret_cast<__half2 *>(y + (p / PC) * rstride + (p % PC) * IL) = h[p];
+                }
+            }
+        }
+    }
+}
+
 template <int KIND, int PC, int PR, int DW, int SW, int NWC, int SPL>
 __global__ void __launch_bounds__((NWC + 1) * 32, 1) k_bi(const __grid_constant__ BiArgs a) {
     using O = Ops<KIND, SPL>;
@@ -679,7 +776,15 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1) k_bi(const __grid_constant_
             }
         }
 
-        if (active && r < a.Yh) store_tile<KIND, PC, PR, DW, SPL>(a, acc, g, wc, sb, r, col0, part, lane);
+        if (active && r < a.Yh) {
+            if constexpr (KIND == USC_F32 || KIND == USC_F16) {
+                if (a.fast) {
+                    store_tile_fast<KIND, PC, PR, DW, SPL>(a, acc, g, wc, sb, r, col0, part, lane);
+                    continue;
+                }
+            }
+            store_tile<KIND, PC, PR, DW, SPL>(a, acc, g, wc, sb, r, col0, part, lane);
+        }
     }
 }
 
