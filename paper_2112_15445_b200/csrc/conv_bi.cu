@@ -85,8 +85,9 @@ int launch_bi(const usc_plan *pl, const void *blob, const void *x, void *y, cons
     a.x_stage_bytes = static_cast<int>(pl->smem_stage_bytes);
     a.stage_bytes = static_cast<int>(pl->smem_stage_bytes + pl->ent_stage_bytes);
     a.ep = ep;
-    a.fast = (pl->dtype == USC_F32 || pl->dtype == USC_F16) && ep.relu && !ep.saturate && !ep.saturate2 &&
-             !ep.requant && !ep.residual && ep.out_padded && ep.oil == pl->in.interleave;
+    a.fast = (pl->dtype == USC_F32 || pl->dtype == USC_F16) && !ep.saturate && !ep.saturate2 && !ep.requant &&
+             ep.out_padded && ep.oil == pl->in.interleave && (!ep.residual || ep.ril == pl->in.interleave) &&
+             (ep.relu || !ep.pool);
     if (pl->kernel == 4) return usc_bi::launch_bt(pl, a, st);
     if (pl->dtype == USC_F16) return usc_bi::launch_h16(pl, a, st);
     if (pl->dtype == USC_CB4) return usc_bi::launch_hcb(pl, a, st);

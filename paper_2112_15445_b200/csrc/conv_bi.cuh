@@ -566,12 +566,25 @@ __device__ __forceinline__ void store_tile(const BiArgs &a, typename Ops<KIND, S
 
 }
 
-// The common epilogue, compiled without runtime flags: ReLU output in the padded BI
-// layout of the same interleave (launch_bi sets a.fast for F32/F16 with relu, no
-// cap saturation/requant/residual).  The accumulator is never -0 (it starts at +0 and
-// x + (-x) rounds to +0), so fmaxf(v, 0) is np.where(v > 0, v, 0) including NaN -> 0;
-// ReLU commutes with the binary16 rounding, and the ReLU'd values are NaN-free, so
-// the 2x2 pool is a plain max (packed f16x2 for F16).
+// The common epilogue without the generic path's per-value flag tests: output (and
+// residual shortcut, if any) in the padded BI layout of the kernel's interleave, no
+// cap saturation / requantisation (launch_bi sets a.fast).  Per value:
+//   F32: v = acc (+ r); ReLU
+//   F16: v = sat16(acc) (+ r, sat16 again); ReLU; binary16 store
+// The accumulator is never -0 (it starts at +0 and x + (-x) rounds to +0), so
+// fmaxf(v, 0) is np.where(v > 0, v, 0) including NaN -> 0; ReLU commutes with the
+// saturating binary16 rounding; ReLU'd values are NaN-free, so the fused 2x2 pool
+// (only with ReLU) is a plain max (packed f16x2 for F16).
+__device__ __forceinline__ float sat16_pre(float v) {  // finite |v| > 65504 -> +-65504 (sat_half)
+    const float m = fabsf(v);
+    return (m > 65504.0f && m != INFINITY) ? copysignf(65504.0f, v) : v;
+}
+__device__ __forceinline__ float relu_sat16_pre(float v) {  // sat16_pre(ReLU(v))
+    v = fmaxf(v, 0.0f);
+    const float c = fminf(v, 65504.0f);
+    return v == INFINITY ? v : c;
+}
+
 template <int KIND, int PC, int PR, int DW, int SPL>
 __device__ __forceinline__ void store_tile_fast(const BiArgs &a, typename Ops<KIND, SPL>::A (&acc)[DW][PC * PR],
                                                 int g, int wc, int sb, int r, int col0, int part, int lane) {
@@ -579,31 +592,50 @@ __device__ __forceinline__ void store_tile_fast(const BiArgs &a, typename Ops<KI
     constexpr int IL = 32 * SPL;
     constexpr bool POOLABLE = PR == 2 && PC % 2 == 0;
     const int *pm = a.perm + g * a.DT + wc * DW;
-    const bool pool = POOLABLE && a.ep.pool;
+    const bool pool = POOLABLE && a.ep.pool, relu = a.ep.relu, res = a.ep.residual;
     const int orow = pool ? r / 2 : r, ocol = pool ? col0 / 2 : col0;
     const long long obase = (long long)sb * a.ep.o_sample_stride +
                             (((long long)orow + a.ep.oph) * a.ep.oWs + ocol + a.ep.opw) * IL + lane * SPL;
     const long long dstride = (long long)a.ep.oHp * a.ep.oWs * IL;
     const int rstride = a.ep.oWs * IL;
+    long long rbase = 0, rdst = 0;
+    int rrow = 0;
+    if (res) {
+        rbase = (long long)sb * a.ep.r_sample_stride +
+                (((long long)r + a.ep.rph) * a.ep.rWs + col0 + a.ep.rpw) * IL + lane * SPL;
+        rdst = (long long)a.ep.rHp * a.ep.rWs * IL;
+        rrow = a.ep.rWs * IL;
+    }
     const int ncol = min(PC, a.Yw - col0), nrow = min(PR, a.Yh - r);
 #pragma unroll
     for (int dw = 0; dw < DW; ++dw) {
         if (part >= 0 && dw % a.split != part) continue;
         const int d = __ldg(pm + dw);
         if (d < 0) continue;
-        const long long od = obase + d * dstride;
+        const long long od = obase + d * dstride, rd = rbase + d * rdst;
         if constexpr (KIND == USC_F32) {
             float *y = static_cast<float *>(a.y) + od;
             float v[P][SPL];
 #pragma unroll
             for (int p = 0; p < P; ++p) {
                 if constexpr (SPL == 1) {
-                    v[p][0] = fmaxf(acc[dw][p], 0.0f);
+                    v[p][0] = acc[dw][p];
                 } else {
-                    float t[2];
-                    Ops<KIND, SPL>::unpack(acc[dw][p], t);
-                    v[p][0] = fmaxf(t[0], 0.0f);
-                    v[p][1] = fmaxf(t[1], 0.0f);
+                    Ops<KIND, SPL>::unpack(acc[dw][p], v[p]);
+                }
+                if (res && p / PC < nrow && p % PC < ncol) {
+                    const float *q = static_cast<const float *>(a.ep.res) + rd + (p / PC) * rrow + (p % PC) * IL;
+                    if constexpr (SPL == 1) {
+                        v[p][0] = __fadd_rn(v[p][0], __ldg(q));
+                    } else {
+                        const float2 t = __ldg(reinterpret_cast<const float2 *>(q));
+                        v[p][0] = __fadd_rn(v[p][0], t.x);
+                        v[p][1] = __fadd_rn(v[p][1], t.y);
+                    }
+                }
+                if (relu) {
+#pragma unroll
+                    for (int j = 0; j < SPL; ++j) v[p][j] = fmaxf(v[p][j], 0.0f);
                 }
             }
             if (pool) {
@@ -632,16 +664,24 @@ __device__ __forceinline__ void store_tile_fast(const BiArgs &a, typename Ops<KI
                         *reinterpret_cast<float2 *>(q) = make_float2(v[p][0], v[p][SPL - 1]);
                 }
             }
-        } else {  // F16, SPL 2: fp32 ReLU and finite saturation (sat_half), one cvt.rn.f16x2 per pixel
+        } else {  // F16, SPL 2: one cvt.rn.f16x2 per pixel
             __half *y = static_cast<__half *>(a.y) + od;
-            auto rs = [](float v) {
-                v = fmaxf(v, 0.0f);
-                const float c = fminf(v, 65504.0f);  // finite overflow -> 65504, inf stays inf
-                return v == INFINITY ? v : c;
-            };
             __half2 h[P];
 #pragma unroll
-            for (int p = 0; p < P; ++p) h[p] = __floats2half2_rn(rs(acc[dw][p].x), rs(acc[dw][p].y));
+            for (int p = 0; p < P; ++p) {
+                float2 v = acc[dw][p];
+                if (res) {
+                    if (p / PC < nrow && p % PC < ncol) {
+                        const __half *q = static_cast<const __half *>(a.ep.res) + rd + (p / PC) * rrow + (p % PC) * IL;
+                        const float2 t = __half22float2(__ldg(reinterpret_cast<const __half2 *>(q)));
+                        v = __half22float2(__floats2half2_rn(sat16_pre(v.x), sat16_pre(v.y)));  // the conv's hook
+                        v.x = __fadd_rn(v.x, t.x);
+                        v.y = __fadd_rn(v.y, t.y);
+                    }
+                }
+                h[p] = relu ? __floats2half2_rn(relu_sat16_pre(v.x), relu_sat16_pre(v.y))
+                            : __floats2half2_rn(sat16_pre(v.x), sat16_pre(v.y));
+            }
             if (pool) {
                 if constexpr (POOLABLE) {
 #pragma unroll

@@ -160,13 +160,17 @@ def test_vgg16_network_matches_reference_composition():
     assert sha(out2.cpu().numpy()) == rec["out"]
 
 
-def test_vgg16_batch64_vs_oracle():
-    """Larger batch against the oracle (the reference's algorithm restated in C)."""
+@pytest.mark.parametrize("special", [False, True])
+def test_vgg16_batch64_vs_oracle(special):
+    """Larger batch against the oracle (the reference's algorithm restated in C);
+    `special` adds NaN / +-inf input pixels (ReLU maps NaN to 0, nn.py:96-98)."""
     import torch
     from paper_2112_15445_b200.models import VGG16_CIFAR, SparseVGG16, vgg16_rng, vgg16_weights
     rng = vgg16_rng(0.93, seed=5)
     ws = vgg16_weights(rng, 0.93)
     x = rng.standard_normal((64, 3, 32, 32)).astype(np.float32)
+    if special:
+        x[0, 0, 5, 5], x[1, 1, 7, 7], x[2, 2, 9, 9] = np.nan, np.inf, -np.inf
     m = SparseVGG16(ws, 64)
     got = m.forward(torch.from_numpy(x).cuda()).cpu().numpy()
     a, li = x, 0
@@ -203,15 +207,21 @@ def test_round_to_binary16_device():
     assert np.array_equal(got, oracle.round_to_binary16(x))
 
 
-def test_vgg16_binary16_network_vs_oracle():
+@pytest.mark.parametrize("special", [False, True])
+def test_vgg16_binary16_network_vs_oracle(special):
     """BINARY16 VGG-16 on the BI64 kernel (FHFMA, binary16 epilogue + fused pool)
     against the reference composition: binary16 conv (fp32 accumulate, saturating
-    RNE output, engine.py:109-110), ReLU, max-pool."""
+    RNE output, engine.py:109-110), ReLU, max-pool.  `special`: inputs scaled so
+    layer outputs overflow binary16 (saturation to 65504) plus NaN / +-inf pixels."""
     import torch
     from paper_2112_15445_b200.models import VGG16_CIFAR, SparseVGG16, vgg16_rng, vgg16_weights
     rng = vgg16_rng(0.93, seed=7)
     ws = vgg16_weights(rng, 0.93, precision=F16)
-    x = oracle.round_to_binary16(rng.standard_normal((64, 3, 32, 32)).astype(np.float32))
+    x = rng.standard_normal((64, 3, 32, 32)).astype(np.float32)
+    if special:
+        x *= 4096.0
+        x[0, 0, 5, 5], x[1, 1, 7, 7], x[2, 2, 9, 9] = np.nan, np.inf, -np.inf
+    x = oracle.round_to_binary16(x)
     m = SparseVGG16(ws, 64, precision=F16)
     assert m.interleave == 64
     got = m.forward(torch.from_numpy(x).cuda().half()).float().cpu().numpy()
@@ -321,8 +331,8 @@ def test_stream_forward_matches_forward():
         assert torch.equal(m.forward(x.cuda()).cpu(), o)
 
 
-@pytest.mark.parametrize("prec", [F32, F16])
-def test_resnet50_network_vs_oracle(prec):
+@pytest.mark.parametrize("prec,scale", [(F32, 1.0), (F16, 1.0), (F16, 256.0)])
+def test_resnet50_network_vs_oracle(prec, scale):
     """ResNet-50 CIFAR (53 sparse convs, stride-2 exact-geometry views, residual add +
     ReLU fused into conv3) against the composition of the reference's pieces: per conv
     sparse_conv_forward (binary16 hook for fp16), ReLU, and the block output
@@ -331,7 +341,7 @@ def test_resnet50_network_vs_oracle(prec):
     from paper_2112_15445_b200.resnet import SparseResNet50, resnet50_layers, resnet50_weights
     ws = resnet50_weights(0.9, seed=2, precision=prec)
     rng = np.random.default_rng(9)
-    x = rng.standard_normal((64, 3, 32, 32)).astype(np.float32)
+    x = rng.standard_normal((64, 3, 32, 32)).astype(np.float32) * np.float32(scale)
     if prec is F16:
         x = oracle.round_to_binary16(x)
     m = SparseResNet50(ws, 64, precision=prec)
