@@ -39,6 +39,7 @@
 #pragma once
 #include <cuda.h>
 
+#include <type_traits>
 #include <utility>
 
 #include "common.cuh"
@@ -585,34 +586,58 @@ __device__ __forceinline__ float relu_sat16_pre(float v) {  // sat16_pre(ReLU(v)
     return v == INFINITY ? v : c;
 }
 
-template <int KIND, int PC, int PR, int DW, int SPL>
+// shortcut value type of one lane and pixel (SPL samples)
+template <int KIND, int SPL>
+using ResV = typename std::conditional<KIND == USC_F32, typename std::conditional<SPL == 1, float, float2>::type,
+                                       __half2>::type;
+
+// The fast epilogue's global loads -- the warp's output channels and, with a residual,
+// the shortcut values of its DW x P outputs -- issued together so their latencies
+// overlap (k_bi issues them before the input-channel loop when registers allow).
+template <int KIND, int PC, int PR, int DW, int SPL, bool RES>
+__device__ __forceinline__ void fast_loads(const BiArgs &a, int g, int wc, int sb, int r, int col0, int part,
+                                           int lane, int (&dch)[DW], ResV<KIND, SPL> (&rv)[DW][PC * PR]) {
+    constexpr int P = PC * PR;
+    constexpr int IL = 32 * SPL;
+    const int *pm = a.perm + g * a.DT + wc * DW;
+#pragma unroll
+    for (int dw = 0; dw < DW; ++dw) dch[dw] = (part >= 0 && dw % a.split != part) ? -1 : __ldg(pm + dw);
+    if (!RES || !a.ep.residual) return;
+    const int ncol = min(PC, a.Yw - col0), nrow = min(PR, a.Yh - r);
+    const long long rbase = (long long)sb * a.ep.r_sample_stride +
+                            (((long long)r + a.ep.rph) * a.ep.rWs + col0 + a.ep.rpw) * IL + lane * SPL;
+    const long long rdst = (long long)a.ep.rHp * a.ep.rWs * IL;
+    const int rrow = a.ep.rWs * IL;
+    using RV = ResV<KIND, SPL>;
+#pragma unroll
+    for (int dw = 0; dw < DW; ++dw)
+#pragma unroll
+        for (int p = 0; p < P; ++p)
+            if (dch[dw] >= 0 && p / PC < nrow && p % PC < ncol)
+                rv[dw][p] = __ldg(reinterpret_cast<const RV *>(
+                    static_cast<const char *>(a.ep.res) +
+                    (rbase + dch[dw] * rdst + (p / PC) * rrow + (p % PC) * IL) * (KIND == USC_F32 ? 4 : 2)));
+}
+
+template <int KIND, int PC, int PR, int DW, int SPL, bool RES>
 __device__ __forceinline__ void store_tile_fast(const BiArgs &a, typename Ops<KIND, SPL>::A (&acc)[DW][PC * PR],
-                                                int g, int wc, int sb, int r, int col0, int part, int lane) {
+                                                int sb, int r, int col0, int lane, const int (&dch)[DW],
+                                                const ResV<KIND, SPL> (&rv)[DW][PC * PR]) {
     constexpr int P = PC * PR;
     constexpr int IL = 32 * SPL;
     constexpr bool POOLABLE = PR == 2 && PC % 2 == 0;
-    const int *pm = a.perm + g * a.DT + wc * DW;
-    const bool pool = POOLABLE && a.ep.pool, relu = a.ep.relu, res = a.ep.residual;
+    const bool pool = POOLABLE && a.ep.pool, relu = a.ep.relu, res = RES && a.ep.residual;
     const int orow = pool ? r / 2 : r, ocol = pool ? col0 / 2 : col0;
     const long long obase = (long long)sb * a.ep.o_sample_stride +
                             (((long long)orow + a.ep.oph) * a.ep.oWs + ocol + a.ep.opw) * IL + lane * SPL;
     const long long dstride = (long long)a.ep.oHp * a.ep.oWs * IL;
     const int rstride = a.ep.oWs * IL;
-    long long rbase = 0, rdst = 0;
-    int rrow = 0;
-    if (res) {
-        rbase = (long long)sb * a.ep.r_sample_stride +
-                (((long long)r + a.ep.rph) * a.ep.rWs + col0 + a.ep.rpw) * IL + lane * SPL;
-        rdst = (long long)a.ep.rHp * a.ep.rWs * IL;
-        rrow = a.ep.rWs * IL;
-    }
     const int ncol = min(PC, a.Yw - col0), nrow = min(PR, a.Yh - r);
 #pragma unroll
     for (int dw = 0; dw < DW; ++dw) {
-        if (part >= 0 && dw % a.split != part) continue;
-        const int d = __ldg(pm + dw);
+        const int d = dch[dw];
         if (d < 0) continue;
-        const long long od = obase + d * dstride, rd = rbase + d * rdst;
+        const long long od = obase + d * dstride;
         if constexpr (KIND == USC_F32) {
             float *y = static_cast<float *>(a.y) + od;
             float v[P][SPL];
@@ -624,13 +649,11 @@ __device__ __forceinline__ void store_tile_fast(const BiArgs &a, typename Ops<KI
                     Ops<KIND, SPL>::unpack(acc[dw][p], v[p]);
                 }
                 if (res && p / PC < nrow && p % PC < ncol) {
-                    const float *q = static_cast<const float *>(a.ep.res) + rd + (p / PC) * rrow + (p % PC) * IL;
                     if constexpr (SPL == 1) {
-                        v[p][0] = __fadd_rn(v[p][0], __ldg(q));
+                        v[p][0] = __fadd_rn(v[p][0], rv[dw][p]);
                     } else {
-                        const float2 t = __ldg(reinterpret_cast<const float2 *>(q));
-                        v[p][0] = __fadd_rn(v[p][0], t.x);
-                        v[p][1] = __fadd_rn(v[p][1], t.y);
+                        v[p][0] = __fadd_rn(v[p][0], rv[dw][p].x);
+                        v[p][1] = __fadd_rn(v[p][1], rv[dw][p].y);
                     }
                 }
                 if (relu) {
@@ -672,8 +695,7 @@ __device__ __forceinline__ void store_tile_fast(const BiArgs &a, typename Ops<KI
                 float2 v = acc[dw][p];
                 if (res) {
                     if (p / PC < nrow && p % PC < ncol) {
-                        const __half *q = static_cast<const __half *>(a.ep.res) + rd + (p / PC) * rrow + (p % PC) * IL;
-                        const float2 t = __half22float2(__ldg(reinterpret_cast<const __half2 *>(q)));
+                        const float2 t = __half22float2(rv[dw][p]);
                         v = __half22float2(__floats2half2_rn(sat16_pre(v.x), sat16_pre(v.y)));  // the conv's hook
                         v.x = __fadd_rn(v.x, t.x);
                         v.y = __fadd_rn(v.y, t.y);
@@ -702,7 +724,9 @@ __device__ __forceinline__ void store_tile_fast(const BiArgs &a, typename Ops<KI
     }
 }
 
-template <int KIND, int PC, int PR, int DW, int SW, int NWC, int SPL>
+// RES: the residual-epilogue variant (shortcut values prefetched before the channel
+// loop when their registers fit); launch_inst selects it for fast residual epilogues
+template <int KIND, int PC, int PR, int DW, int SW, int NWC, int SPL, bool RES>
 __global__ void __launch_bounds__((NWC + 1) * 32, 1) k_bi(const __grid_constant__ BiArgs a) {
     using O = Ops<KIND, SPL>;
     using A = typename O::A;
@@ -713,6 +737,9 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1) k_bi(const __grid_constant_
     constexpr int REGCAP = NWC <= 8 ? 168 : (NWC <= 12 ? 128 : 96);
     constexpr int VR = (KIND == USC_F32) ? SPL : 1;  // registers per staged value
     constexpr bool PIPE = SPL * DW * P + 4 * P * VR + (KIND == USC_F32 ? 40 : 56) <= REGCAP;
+    constexpr int RVR = (KIND == USC_F32) ? SPL : 1;  // registers per shortcut value
+    constexpr bool RPRE = RES && (KIND == USC_F32 || KIND == USC_F16) &&
+                          SPL * DW * P + (PIPE ? 4 : 2) * P * VR + DW * P * RVR + 40 <= REGCAP;
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t *full = reinterpret_cast<uint64_t *>(smem);
     uint64_t *empty = full + 8;
@@ -788,6 +815,14 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1) k_bi(const __grid_constant_
         const int cls = (a.ncls > 1 && r < a.Yh && col0 < a.Yw)
                             ? __ldg(a.rowcls + r) * a.ncls_c + __ldg(a.colcls + col0) : 0;
 
+        // fast epilogue loads issued before the channel loop (latency hidden by it) when
+        // the shortcut registers fit the cap, else right before the epilogue
+        int dch[DW];
+        ResV<KIND, SPL> rv[DW][P];
+        if constexpr (RPRE) {
+            if (a.fast && active && r < a.Yh) fast_loads<KIND, PC, PR, DW, SPL, RES>(a, g, wc, sb, r, col0, part, lane, dch, rv);
+        }
+
         A acc[DW][P];
 #pragma unroll
         for (int i = 0; i < DW; ++i)
@@ -819,7 +854,8 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1) k_bi(const __grid_constant_
         if (active && r < a.Yh) {
             if constexpr (KIND == USC_F32 || KIND == USC_F16) {
                 if (a.fast) {
-                    store_tile_fast<KIND, PC, PR, DW, SPL>(a, acc, g, wc, sb, r, col0, part, lane);
+                    if constexpr (!RPRE) fast_loads<KIND, PC, PR, DW, SPL, RES>(a, g, wc, sb, r, col0, part, lane, dch, rv);
+                    store_tile_fast<KIND, PC, PR, DW, SPL, RES>(a, acc, sb, r, col0, lane, dch, rv);
                     continue;
                 }
             }
@@ -830,8 +866,11 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1) k_bi(const __grid_constant_
 
 template <int KIND, int PC, int PR, int DW, int SW, int NWC, int SPL>
 int launch_inst(const usc_plan *pl, const BiArgs &a, cudaStream_t st) {
-    auto fn = k_bi<KIND, PC, PR, DW, SW, NWC, SPL>;
-    static std::atomic<uint64_t> attr{0};
+    constexpr bool HAS_RES = KIND == USC_F32 || KIND == USC_F16;
+    const bool res = HAS_RES && a.fast && a.ep.residual;
+    auto fn = res ? k_bi<KIND, PC, PR, DW, SW, NWC, SPL, HAS_RES> : k_bi<KIND, PC, PR, DW, SW, NWC, SPL, false>;
+    static std::atomic<uint64_t> attr_res{0}, attr_plain{0};
+    std::atomic<uint64_t> &attr = res ? attr_res : attr_plain;
     cudaError_t ae = ensure_smem_attr(fn, attr, 224 * 1024);
     if (ae != cudaSuccess) return usc::fail(USC_ERR_CUDA, "smem attribute: %s", cudaGetErrorString(ae));
     fn<<<static_cast<unsigned>(pl->grid_x), (NWC + 1) * 32, pl->smem_bytes, st>>>(a);
