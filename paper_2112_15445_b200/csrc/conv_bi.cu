@@ -82,6 +82,9 @@ int launch_bi(const usc_plan *pl, const void *blob, const void *x, void *y, cons
     a.split = pl->tail_split > 1 ? pl->tail_split : 1;
     a.tfull = a.split > 1 ? pl->tail_full : a.tiles;
     a.items = a.tfull + a.split * (a.tiles - a.tfull);
+    a.fG = usc_bi::fdiv_make(static_cast<uint32_t>(a.G));
+    a.fCT = usc_bi::fdiv_make(static_cast<uint32_t>(a.col_tiles));
+    a.fRT = usc_bi::fdiv_make(static_cast<uint32_t>(a.row_tiles));
     a.x_stage_bytes = static_cast<int>(pl->smem_stage_bytes);
     a.stage_bytes = static_cast<int>(pl->smem_stage_bytes + pl->ent_stage_bytes);
     a.ep = ep;
