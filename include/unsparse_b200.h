@@ -284,6 +284,19 @@ int usc_kmeans_codebook(const double *w, int64_t count, int32_t omega, int32_t p
                         double *centroids, double *quantized, int64_t *assignments,
                         int32_t *k_out, int32_t *zero_pinned);
 
+/* Training kernels of the dense Conv2D layer (nn.py:62-72), bit-identical to the
+ * reference (pruning with retraining).  All fp32, device pointers:
+ *   usc_conv_grad_weights -- kernels.conv_grad_weights (kernels.py:103-130):
+ *     xpad [n][C][Hp][Wp] (the zero-padded forward input), dout [n][D][Yh][Yw] ->
+ *     dw [D][C][Kh][Kw] (overwritten); fp64 accumulation in (b, r, cc) order.
+ *   usc_conv_grad_input -- kernels.conv_grad_input (kernels.py:133-162) into a zeroed
+ *     dxpad (nn.py:67): w [D][C][Kh][Kw], dout -> dxpad [n][C][Hp][Wp] (overwritten,
+ *     every element; crop the halo for dx, nn.py:69-71). */
+int usc_conv_grad_weights(const usc_geometry *g, int32_t n, const float *xpad_dev, const float *dout_dev,
+                          float *dw_dev, void *stream);
+int usc_conv_grad_input(const usc_geometry *g, int32_t n, const float *w_dev, const float *dout_dev,
+                        float *dxpad_dev, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -174,6 +174,32 @@ def dense_conv(x, w, geom, binary16=False, threads: int = 1):
     return round_to_binary16(out) if binary16 else out
 
 
+def conv_grad_weights(xpad, dout, s_h: int, s_w: int, kh: int, kw: int, threads: int = 1):
+    """kernels.py:103-130: dw (D, C, Kh, Kw) from the padded input and the output gradient."""
+    xpad = np.ascontiguousarray(xpad, np.float32)
+    dout = np.ascontiguousarray(dout, np.float32)
+    n, C, Hp, Wp = xpad.shape
+    D, Yh, Yw = dout.shape[1:]
+    dw = np.zeros((D, C, kh, kw), np.float32)
+    lib().orc_conv_grad_weights(_p(xpad), _p(dout), _p(dw), _i64(n), _i64(C), _i64(Hp), _i64(Wp), _i64(D),
+                                _i64(kh), _i64(kw), _i64(Yh), _i64(Yw), _i64(s_h), _i64(s_w), ctypes.c_int(threads))
+    return dw
+
+
+def conv_grad_input(w, dout, xpad_shape, s_h: int, s_w: int, threads: int = 1):
+    """kernels.py:133-162: dxpad (zero-initialised, nn.py:67) from the weights and the
+    output gradient."""
+    w = np.ascontiguousarray(w, np.float32)
+    dout = np.ascontiguousarray(dout, np.float32)
+    n, C, Hp, Wp = xpad_shape
+    D, _, Kh, Kw = w.shape
+    Yh, Yw = dout.shape[2:]
+    dxpad = np.zeros(xpad_shape, np.float32)
+    lib().orc_conv_grad_input(_p(w), _p(dout), _p(dxpad), _i64(n), _i64(C), _i64(Hp), _i64(Wp), _i64(D),
+                              _i64(Kh), _i64(Kw), _i64(Yh), _i64(Yw), _i64(s_h), _i64(s_w), ctypes.c_int(threads))
+    return dxpad
+
+
 def relu(x):
     """nn.py:96-98."""
     x = np.ascontiguousarray(x, np.float32)

@@ -93,6 +93,8 @@ _SIGS = {
     "usc_csr_count_device": (c_i32, [c_ptr, c_ptr, c_ptr, c_ptr, c_ptr]),
     "usc_build_csr_device": (c_i32, [c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr]),
     "usc_csr_validate": (c_i32, [c_ptr, c_ptr, c_i64, c_ptr, c_i64, c_i64, c_i64, c_ptr]),
+    "usc_conv_grad_weights": (c_i32, [c_ptr, c_i32, c_ptr, c_ptr, c_ptr, c_ptr]),
+    "usc_conv_grad_input": (c_i32, [c_ptr, c_i32, c_ptr, c_ptr, c_ptr, c_ptr]),
     "usc_csr_to_dense": (c_i32, [c_ptr, c_ptr, c_ptr, c_ptr, c_i64, c_ptr]),
     "usc_plan_make": (c_i32, [c_ptr, c_i32, c_i32, c_ptr, c_ptr]),
     "usc_bi_instances": (c_i32, [c_ptr, c_i32]),

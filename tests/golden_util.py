@@ -43,3 +43,16 @@ def layer_inputs(name, g, sparsity, batch, binary16=False, seed=0):
     if binary16:
         x = oracle.round_to_binary16(x)
     return x, w
+
+
+def grad_cases():
+    """tests/golden/grad_cases.npz (make_golden_grad.py): [(geometry dims, arrays)] of the
+    reference's conv_grad_weights / conv_grad_input / Conv2D.backward."""
+    z = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "grad_cases.npz"))
+    out, k = [], 0
+    while f"g{k}_x" in z:
+        c, d, kh, kw, h, w, sh, sw, ph, pw = [int(v) for v in z[f"g{k}_geom"]]
+        out.append((dict(C=c, D=d, Kh=kh, Kw=kw, H=h, W=w, sh=sh, sw=sw, ph=ph, pw=pw),
+                    {n: z[f"g{k}_{n}"] for n in ("x", "w", "dout", "dw", "dx", "dxpad")}))
+        k += 1
+    return out

@@ -378,3 +378,46 @@ def test_resnet50_network_vs_oracle(prec, scale):
             li += 1
             a = oracle.relu(hook((y + sc).astype(np.float32)))
     assert np.array_equal(got, a)
+
+
+def test_conv_gradients_bitwise_vs_reference():
+    """Training kernels: usc_conv_grad_weights / usc_conv_grad_input
+    and Conv2D.backward equal the reference's kernels.py:103-162 / nn.py:62-72 outputs
+    (golden vectors) bit for bit; the forward equals the oracle's dense conv."""
+    import torch
+    from golden_util import grad_cases
+    from paper_2112_15445_b200 import training as T
+    for g, a in grad_cases():
+        geom = U.ConvGeometry(g["C"], g["D"], g["Kh"], g["Kw"], g["H"], g["W"], stride=(g["sh"], g["sw"]),
+                              padding=(g["ph"], g["pw"]))
+        layer = T.Conv2D(geom, np.random.default_rng(0))
+        layer.w = a["w"].copy()
+        y = layer.forward(torch.from_numpy(a["x"]).cuda())
+        gt = (g["C"], g["D"], g["Kh"], g["Kw"], g["H"], g["W"], (g["sh"], g["sw"]), (g["ph"], g["pw"]))
+        assert np.array_equal(y.cpu().numpy(), oracle.dense_conv(a["x"], a["w"], gt)), g
+        dx = layer.backward(torch.from_numpy(a["dout"]).cuda())
+        assert np.array_equal(layer.grad_w, a["dw"]), g
+        assert np.array_equal(dx.cpu().numpy(), a["dx"]), g
+        dxpad = torch.full(a["dxpad"].shape, float("nan"), device="cuda")  # every element is written
+        T.conv_grad_input(torch.from_numpy(a["w"]).cuda(), torch.from_numpy(a["dout"]).cuda(), dxpad,
+                          g["sh"], g["sw"])
+        assert np.array_equal(dxpad.cpu().numpy(), a["dxpad"]), g
+
+
+def test_conv_gradients_vgg_layer_vs_oracle():
+    """A VGG-sized pruned layer (64->64 3x3 at 16x16, batch 8) against the oracle's
+    restatement (pinned to the reference by the golden cases above)."""
+    import torch
+    from paper_2112_15445_b200 import training as T
+    rng = np.random.default_rng(5)
+    n, C, D, H = 8, 64, 64, 16
+    xpad = np.pad(rng.standard_normal((n, C, H, H)).astype(np.float32), ((0, 0), (0, 0), (1, 1), (1, 1)))
+    w = rng.standard_normal((D, C, 3, 3)).astype(np.float32)
+    w.reshape(-1)[rng.choice(w.size, int(w.size * 0.9), replace=False)] = 0.0
+    dout = rng.standard_normal((n, D, H, H)).astype(np.float32)
+    dw = torch.empty((D, C, 3, 3), device="cuda")
+    T.conv_grad_weights(torch.from_numpy(xpad).cuda(), torch.from_numpy(dout).cuda(), dw, 1, 1)
+    assert np.array_equal(dw.cpu().numpy(), oracle.conv_grad_weights(xpad, dout, 1, 1, 3, 3, threads=4))
+    dxpad = torch.empty(xpad.shape, device="cuda")
+    T.conv_grad_input(torch.from_numpy(w).cuda(), torch.from_numpy(dout).cuda(), dxpad, 1, 1)
+    assert np.array_equal(dxpad.cpu().numpy(), oracle.conv_grad_input(w, dout, xpad.shape, 1, 1, threads=4))

@@ -167,3 +167,18 @@ def test_vgg16_trunk_composition():
             c = v
         assert sha(a) == lr["out"]
     assert sha(a) == rec["out"]
+
+
+def test_conv_gradients_match_reference():
+    """kernels.py:103-162: the oracle's conv_grad_weights (fp64
+    accumulator, b/r/cc order) and conv_grad_input (fp32 scatter order) equal the
+    reference's outputs bit for bit, including the Yw == 1 loops and stride 2."""
+    from golden_util import grad_cases
+    for g, a in grad_cases():
+        xpad = np.pad(a["x"], ((0, 0), (0, 0), (g["ph"], g["ph"]), (g["pw"], g["pw"])))
+        dw = oracle.conv_grad_weights(xpad, a["dout"], g["sh"], g["sw"], g["Kh"], g["Kw"], threads=4)
+        dxpad = oracle.conv_grad_input(a["w"], a["dout"], xpad.shape, g["sh"], g["sw"], threads=4)
+        assert np.array_equal(dw, a["dw"]), g
+        assert np.array_equal(dxpad, a["dxpad"]), g
+        dx = dxpad[:, :, g["ph"]:g["ph"] + g["H"], g["pw"]:g["pw"] + g["W"]]
+        assert np.array_equal(dx, a["dx"]), g
