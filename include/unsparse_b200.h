@@ -238,6 +238,14 @@ int usc_conv_forward(const usc_plan *plan, const void *blob_dev, const void *x_d
  * the 31x31 interior window (x_dev advanced to element (1,1)).  BI plans only. */
 int usc_conv_forward_view(const usc_plan *plan, const void *blob_dev, const void *x_dev,
                           const usc_act_layout *x_layout, void *y_dev, const usc_epilogue *epi, void *stream);
+/* A 1x1 stride-s convolution (ResNet's stride-2 projections) run as a stride-1,
+ * unpadded 1x1 plan over every (step_h, step_w)-th pixel of the buffer `x_layout`
+ * describes: the TMA map strides over the skipped pixels, so only the pixels the
+ * convolution uses are read.  Same result as the stride-s plan (a 1x1 conv is
+ * pointwise); the filter must be encoded for the plan's stride-1 geometry. */
+int usc_conv_forward_strided(const usc_plan *plan, const void *blob_dev, const void *x_dev,
+                             const usc_act_layout *x_layout, int32_t step_h, int32_t step_w, void *y_dev,
+                             const usc_epilogue *epi, void *stream);
 /* Reference-shaped kernel entry, the exact analogue of the numba FFI
  * kernels.sparse_conv_blocks(xflat, row_ptr, col_offsets, theta, out, blocks, sb,
  * x_size, s_h, s_w, padded_w) (kernels.py:57-58), all arrays on the device:

@@ -104,6 +104,7 @@ _SIGS = {
     "usc_unpad_output": (c_i32, [c_ptr, c_i32, c_i32, c_ptr, c_ptr, c_ptr]),
     "usc_conv_forward": (c_i32, [c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr]),
     "usc_conv_forward_view": (c_i32, [c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr]),
+    "usc_conv_forward_strided": (c_i32, [c_ptr, c_ptr, c_ptr, c_ptr, c_i32, c_i32, c_ptr, c_ptr, c_ptr]),
     "usc_sparse_conv_blocks": (c_i32, [c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_i64, c_i32, c_i64,
                                        c_i32, c_i32, c_i32, c_i32, c_i32, c_i32, c_ptr]),
     "usc_round_binary16": (c_i32, [c_ptr, c_ptr, c_i64, c_i32, c_ptr]),

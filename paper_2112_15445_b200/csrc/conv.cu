@@ -497,7 +497,7 @@ int usc_peak_fp32_muladd(int32_t device, double *tflops) {
 }
 
 static int conv_forward_impl(const usc_plan *pl, const void *blob, const void *x, const usc_act_layout *xv, void *y,
-                             const usc_epilogue *epi, void *stream);
+                             const usc_epilogue *epi, void *stream, int step_h = 1, int step_w = 1);
 
 int usc_conv_forward(const usc_plan *pl, const void *blob, const void *x, void *y,
                      const usc_epilogue *epi, void *stream) {
@@ -511,8 +511,19 @@ int usc_conv_forward_view(const usc_plan *pl, const void *blob, const void *x, c
     return conv_forward_impl(pl, blob, x, x_layout, y, epi, stream);
 }
 
+int usc_conv_forward_strided(const usc_plan *pl, const void *blob, const void *x, const usc_act_layout *x_layout,
+                             int32_t step_h, int32_t step_w, void *y, const usc_epilogue *epi, void *stream) {
+    if (!x_layout) return fail(USC_ERR_VALUE, "null input layout");
+    if (step_h < 1 || step_w < 1 || step_h > 8 || step_w > 8) return fail(USC_ERR_VALUE, "steps must be 1..8");
+    if (pl && pl->kernel < 3) return fail(USC_ERR_UNSUPPORTED, "input views need a batch-interleaved plan");
+    if (pl && (pl->g.filter_h != 1 || pl->g.filter_w != 1 || pl->g.stride_h != 1 || pl->g.stride_w != 1 ||
+               pl->g.pad_h || pl->g.pad_w))
+        return fail(USC_ERR_VALUE, "a strided view runs a 1x1, stride-1, unpadded plan");
+    return conv_forward_impl(pl, blob, x, x_layout, y, epi, stream, step_h, step_w);
+}
+
 static int conv_forward_impl(const usc_plan *pl, const void *blob, const void *x, const usc_act_layout *xv, void *y,
-                             const usc_epilogue *epi, void *stream) {
+                             const usc_epilogue *epi, void *stream, int step_h, int step_w) {
     if (!pl || !blob || !x || !y) return fail(USC_ERR_VALUE, "null argument");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const usc_geometry &g = pl->g;
@@ -536,7 +547,7 @@ static int conv_forward_impl(const usc_plan *pl, const void *blob, const void *x
                                    "output's shape and no fused pool");
     if (ep.requant && (pl->kernel < 3 || pl->dtype != USC_I8))
         return fail(USC_ERR_UNSUPPORTED, "requantising epilogue needs an int8 BI plan");
-    if (pl->kernel == 3 || pl->kernel == 4) return usc::launch_bi(pl, blob, x, y, ep, st, xv);
+    if (pl->kernel == 3 || pl->kernel == 4) return usc::launch_bi(pl, blob, x, y, ep, st, xv, step_h, step_w);
     if (ep.out_padded && ep.oil != 0)
         return fail(USC_ERR_UNSUPPORTED, "kernels 1/2 write interleave-0 layouts only");
     // blob = [16 x f32 centroid table][int32 cpg, 16-B aligned][entries]

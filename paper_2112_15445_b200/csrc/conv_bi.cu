@@ -20,7 +20,7 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_tiled() {
 }
 
 int launch_bi(const usc_plan *pl, const void *blob, const void *x, void *y, const usc_dev::Epi &ep,
-              cudaStream_t st, const usc_act_layout *xv) {
+              cudaStream_t st, const usc_act_layout *xv, int step_h, int step_w) {
     // blob = [64 B][int32 blk[G*n_chunks + 1]][int32 perm[G*DT]][int32 rowcls[Yh], colcls[Yw]]
     // [blocks], each part 16-B aligned (usc_pack, kernel 3)
     const char *cb = static_cast<const char *>(blob);
@@ -40,9 +40,12 @@ int launch_bi(const usc_plan *pl, const void *blob, const void *x, void *y, cons
     // strides of the buffer x lives in: the plan's own layout, or a larger buffer the plan's
     // (hp x ws) input is a window of (usc_conv_forward_view)
     const usc_act_layout &bl = xv ? *xv : pl->in;
-    if (xv && (xv->interleave != IL || xv->hp < pl->in.hp || xv->ws < pl->in.ws || xv->channels != pl->g.in_channels))
+    // a strided view (usc_conv_forward_strided) reads every step-th pixel of the buffer
+    if (xv && (xv->interleave != IL || (pl->in.hp - 1) * step_h + 1 > xv->hp ||
+               (pl->in.ws - 1) * step_w + 1 > xv->ws || xv->channels != pl->g.in_channels))
         return fail(USC_ERR_VALUE, "input view does not fit its buffer layout");
-    const cuuint64_t strides[4] = {px, px * bl.ws, px * bl.ws * bl.hp, (cuuint64_t)bl.sample_stride * (px / IL)};
+    const cuuint64_t strides[4] = {px * step_w, px * bl.ws * step_h, px * bl.ws * bl.hp,
+                                   (cuuint64_t)bl.sample_stride * (px / IL)};
     const cuuint32_t box[5] = {(cuuint32_t)IL, (cuuint32_t)pl->TWs, (cuuint32_t)pl->HS, (cuuint32_t)pl->CC, 1};
     const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
     CUresult r = enc(&a.xmap, h16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, const_cast<void *>(x), dims, strides, box, estr,

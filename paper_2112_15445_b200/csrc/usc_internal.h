@@ -17,6 +17,6 @@ struct Epi;
 }
 namespace usc {
 int launch_bi(const usc_plan *pl, const void *blob, const void *x, void *y, const usc_dev::Epi &ep,
-              cudaStream_t st, const usc_act_layout *x_view = nullptr);
+              cudaStream_t st, const usc_act_layout *x_view = nullptr, int step_h = 1, int step_w = 1);
 }
 #endif

@@ -12,7 +12,8 @@ projection), 53 sparse convs.  Two precisions, as the reference's modes:
 Stride-2 layers use the reference's exact geometries (ConvGeometry rejects 32 -> 16
 with pad 1, tensor.py:186-190): the 3x3 reads the top/left 33x33 window of its
 34x34 zero-haloed input (pad 0), the 1x1 projection the top/left 31x31 window --
-through usc_conv_forward_view, no copies.  Every activation stays resident in the
+through usc_conv_forward_view, no copies; the 1x1 projection runs as a stride-1 plan over
+every 2nd pixel (usc_conv_forward_strided).  Every activation stays resident in the
 BI64 layout; the residual add and ReLU are fused into conv3's epilogue.
 """
 
@@ -76,7 +77,16 @@ class SparseResNet50:
         self.batch = batch
         self.device = torch.device(device or "cuda")
         self.layers = resnet50_layers()
-        self.filters = [build_csr(w, g) for w, (_, g, _, _) in zip(weights, self.layers)]
+        # (plan geometry, pixel step): a stride-2 1x1 projection runs as a stride-1 1x1
+        # plan over every 2nd pixel (usc_conv_forward_strided: the TMA map skips the
+        # pixels the projection never reads); same entries, same order, same bits
+        self.eff = []
+        for _, g, role, s in self.layers:
+            if role == "proj" and s > 1:
+                self.eff.append((ConvGeometry(g.in_channels, g.out_channels, 1, 1, g.out_h, g.out_w), s))
+            else:
+                self.eff.append((g, 1))
+        self.filters = [build_csr(w, eg) for w, (eg, _) in zip(weights, self.eff)]
         self.configs = [ExecConfig(samples_per_cta=64) for _ in self.layers]
         self.graph = None
         self._build()
@@ -107,10 +117,16 @@ class SparseResNet50:
             if residual is not None:
                 r, r_lay = residual
                 e.residual, e.res_layout, e.res = 1, r_lay, r.data_ptr()
-            # a window of a larger buffer (the stride-2 exact geometries) goes through the view entry
+            # a window of a larger buffer (the stride-2 exact geometries) goes through the view
+            # entry; a stride-2 projection through the strided view
+            step = self.eff[li][1]
             view = None
-            if (plan.in_.hp, plan.in_.ws) != (x_lay.hp, x_lay.ws):
-                view = x_lay
+            if step > 1:
+                if x_lay.pad_h or x_lay.pad_w:
+                    raise RuntimeError(f"{name}: strided projection needs a halo-free input buffer")
+                view = (x_lay, step)
+            elif (plan.in_.hp, plan.in_.ws) != (x_lay.hp, x_lay.ws):
+                view = (x_lay, 1)
             self.steps.append((li, plan, blob, x, view, y, e))
             return y
 
@@ -152,9 +168,13 @@ class SparseResNet50:
         if view is None:
             _lib.check(L.usc_conv_forward(_lib.ref(plan), _lib.t_ptr(blob), _lib.t_ptr(x), _lib.t_ptr(y),
                                           _lib.ref(e), sp), self.layers[li][0])
-        else:
-            _lib.check(L.usc_conv_forward_view(_lib.ref(plan), _lib.t_ptr(blob), _lib.t_ptr(x), _lib.ref(view),
+        elif view[1] == 1:
+            _lib.check(L.usc_conv_forward_view(_lib.ref(plan), _lib.t_ptr(blob), _lib.t_ptr(x), _lib.ref(view[0]),
                                                _lib.t_ptr(y), _lib.ref(e), sp), self.layers[li][0])
+        else:
+            _lib.check(L.usc_conv_forward_strided(_lib.ref(plan), _lib.t_ptr(blob), _lib.t_ptr(x), _lib.ref(view[0]),
+                                                  view[1], view[1], _lib.t_ptr(y), _lib.ref(e), sp),
+                       self.layers[li][0])
 
     def load_input(self, x, stream=None):
         _lib.check(_lib.lib().usc_pad_input(_lib.ref(self.in_layout), self.dtype, self.batch, _lib.t_ptr(x),
@@ -200,7 +220,7 @@ class SparseResNet50:
         picks = []
         for st in self.steps:
             li, plan0, _, x, view, y, e = st
-            g = self.layers[li][1]
+            g = self.eff[li][0]
             cands = [self.configs[li]] + [c for c in tile_candidates(g, self.batch, [1], self.precision, (3,))
                                           if c.samples_per_cta == 64]
             res = []
