@@ -299,12 +299,23 @@ __device__ __forceinline__ void run_pairs(typename Ops<KIND, SPL>::A (&acc)[PC *
             }
         }
     } else {
+        // two pairs per iteration: the entry registers alternate instead of being moved
 #pragma unroll 1
-        for (; ep + 16 <= ee; ep += 16) {
+        for (; ep + 32 <= ee; ep += 32) {
+            V v0[P], v1[P];
+            load_pair<KIND, PC, PR, SW, SPL>(v0, v1, xs, rs, nn);
+            const int4 n = lds_v4(ep + 16);
+            mac_pair<KIND, SPL, P>(acc, v0, v1, nn);
+            load_pair<KIND, PC, PR, SW, SPL>(v0, v1, xs, rs, n);
+            nn = lds_v4(ep + 32);
+            mac_pair<KIND, SPL, P>(acc, v0, v1, n);
+        }
+        if (ep + 16 <= ee) {
             V v0[P], v1[P];
             load_pair<KIND, PC, PR, SW, SPL>(v0, v1, xs, rs, nn);
             const int4 n = nn;
-            nn = lds_v4(ep + 16);
+            ep += 16;
+            nn = lds_v4(ep);
             mac_pair<KIND, SPL, P>(acc, v0, v1, n);
         }
     }
