@@ -2,6 +2,8 @@
 // builds the TMA tensor map of the input and the kernel arguments.
 #include <cudaTypedefs.h>
 
+#include <cmath>
+
 #include "conv_bt.cuh"
 
 namespace usc {
@@ -94,6 +96,16 @@ int launch_bi(const usc_plan *pl, const void *blob, const void *x, void *y, cons
     a.fast = (pl->dtype == USC_F32 || pl->dtype == USC_F16) && !ep.saturate && !ep.saturate2 && !ep.requant &&
              ep.out_padded && ep.oil == pl->in.interleave && (!ep.residual || ep.ril == pl->in.interleave) &&
              (ep.relu || !ep.pool);
+    if (pl->dtype == USC_I8 && ep.requant && ep.relu && !ep.saturate && !ep.saturate2 && !ep.residual &&
+        ep.out_padded && ep.oil == pl->in.interleave) {
+        // the integer requantisation needs both scales to be powers of two (fixed-point sigmas)
+        int e1, e2;
+        const float m1 = std::frexp(ep.scale, &e1), m2 = std::frexp(ep.rq_scale, &e2);
+        if (m1 == 0.5f && m2 == 0.5f) {
+            a.fast = 1;
+            a.i8shift = -((e1 - 1) + (e2 - 1));
+        }
+    }
     if (pl->kernel == 4) return usc_bi::launch_bt(pl, a, st);
     if (pl->dtype == USC_F16) return usc_bi::launch_h16(pl, a, st);
     if (pl->dtype == USC_CB4) return usc_bi::launch_hcb(pl, a, st);

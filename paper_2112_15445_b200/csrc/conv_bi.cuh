@@ -75,6 +75,7 @@ struct BiArgs {
     int items, tfull, split;  // work items: tiles [0, tfull) whole, the rest split in `split` slot subsets
     int x_stage_bytes, stage_bytes;
     int fast;                 // store_tile_fast applies (see there)
+    int i8shift;              // I8 fast requantisation: code = round(acc * 2^-i8shift) (see there)
     FDiv fG, fCT, fRT;        // divisions by G, col_tiles, row_tiles (tile decode)
     Epi ep;
 };
@@ -713,6 +714,44 @@ __device__ __forceinline__ void store_tile_fast(const BiArgs &a, typename Ops<KI
                         *reinterpret_cast<float2 *>(q) = make_float2(v[p][0], v[p][SPL - 1]);
                 }
             }
+        } else if constexpr (KIND == USC_I8) {
+            // int8 requantising epilogue with ReLU (quantization.py:61-76 on acc*sigma_w*sigma_x):
+            // both scales are powers of two and acc is an exact integer, so the fp64
+            // round-half-away-from-zero of acc*2^-s is (|acc| + 2^(s-1)) >> s, clamped
+            // to +-limit -- integer ops, same codes (ReLU leaves no negative zero)
+            __half *y = static_cast<__half *>(a.y) + od;
+            const int sh = a.i8shift, lim = a.ep.rq_limit;
+            auto code = [&](float v) -> int {
+                const int m = max(__float2int_rn(v), 0);  // ReLU on the exact integer accumulator
+                if (sh > 0) return min((m + (1 << (sh - 1))) >> sh, lim);
+                return -sh >= 8 ? (m ? lim : 0) : min(m << -sh, lim);
+            };
+            int c[P][2];
+#pragma unroll
+            for (int p = 0; p < P; ++p) {
+                c[p][0] = code(acc[dw][p].x);
+                c[p][1] = code(acc[dw][p].y);
+            }
+            if (pool) {
+                if constexpr (POOLABLE) {
+#pragma unroll
+                    for (int c2 = 0; c2 < PC / 2; ++c2) {
+                        if (2 * c2 >= ncol) continue;
+                        int o[2];
+#pragma unroll
+                        for (int j = 0; j < 2; ++j)
+                            o[j] = max(max(c[2 * c2][j], c[2 * c2 + 1][j]), max(c[PC + 2 * c2][j], c[PC + 2 * c2 + 1][j]));
+                        *reinterpret_cast<__half2 *>(y + c2 * IL) = __halves2half2(__int2half_rn(o[0]), __int2half_rn(o[1]));
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int p = 0; p < P; ++p) {
+                    if (p / PC >= nrow || p % PC >= ncol) continue;
+                    *reinterpret_cast<__half2 *>(y + (p / PC) * rstride + (p % PC) * IL) =
+                        __halves2half2(__int2half_rn(c[p][0]), __int2half_rn(c[p][1]));
+                }
+            }
         } else {  // F16, SPL 2: one cvt.rn.f16x2 per pixel
             __half *y = static_cast<__half *>(a.y) + od;
             __half2 h[P];
@@ -911,7 +950,7 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1) k_bi(const __grid_constant_
         }
 
         if (active && r < a.Yh) {
-            if constexpr (KIND == USC_F32 || KIND == USC_F16) {
+            if constexpr (KIND == USC_F32 || KIND == USC_F16 || KIND == USC_I8) {
                 if (a.fast) {
                     if constexpr (!RPRE) fast_loads<KIND, PC, PR, DW, SPL, RES>(a, g, wc, sb, r, col0, part, lane, dch, rv);
                     store_tile_fast<KIND, PC, PR, DW, SPL, RES>(a, acc, sb, r, col0, lane, dch, rv);
