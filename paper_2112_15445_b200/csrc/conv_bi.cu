@@ -106,6 +106,9 @@ int launch_bi(const usc_plan *pl, const void *blob, const void *x, void *y, cons
             a.i8shift = -((e1 - 1) + (e2 - 1));
         }
     }
+    if (pl->dtype == USC_CB4 && !ep.requant && !ep.residual && ep.out_padded && ep.oil == pl->in.interleave &&
+        (ep.relu || !ep.pool))
+        a.fast = 1;  // the 4b/16b hook with its saturations (store_tile_fast)
     if (pl->kernel == 4) return usc_bi::launch_bt(pl, a, st);
     if (pl->dtype == USC_F16) return usc_bi::launch_h16(pl, a, st);
     if (pl->dtype == USC_CB4) return usc_bi::launch_hcb(pl, a, st);

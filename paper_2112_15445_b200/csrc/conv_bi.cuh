@@ -752,6 +752,55 @@ __device__ __forceinline__ void store_tile_fast(const BiArgs &a, typename Ops<KI
                         __halves2half2(__int2half_rn(c[p][0]), __int2half_rn(c[p][1]));
                 }
             }
+        } else if constexpr (KIND == USC_CB4) {
+            // 4b/16b hook (quantization.py:238-244): round16(min(ReLU(round16(min(v, cap))), cap2)).
+            // Tame tiles (every |v| < 65520, no NaN): one cvt per pixel, ReLU by sign bits,
+            // and min with round16(cap2) -- equal to round16(min(x, cap2)) for x on the
+            // binary16 grid (rounding is monotonic); otherwise the per-value epi_value.
+            __half *y = static_cast<__half *>(a.y) + od;
+            float v[P][2];
+            uint32_t mx = 0;
+#pragma unroll
+            for (int p = 0; p < P; ++p) {
+                Ops<KIND, SPL>::unpack(acc[dw][p], v[p]);
+                mx = max(mx, max(__float_as_uint(v[p][0]) & 0x7fffffffu, __float_as_uint(v[p][1]) & 0x7fffffffu));
+            }
+            __half2 h[P];
+            if (__all_sync(0xffffffffu, mx < 0x477FF000u)) {
+                const float cap = a.ep.saturate ? a.ep.cap : INFINITY;
+                const __half2 cap2 = a.ep.saturate2 ? __half2half2(sat_half(a.ep.cap2)) : __float2half2_rn(INFINITY);
+#pragma unroll
+                for (int p = 0; p < P; ++p) {
+                    __half2 t = __floats2half2_rn(fminf(v[p][0], cap), fminf(v[p][1], cap));
+                    if (relu) {
+                        uint32_t b = *reinterpret_cast<uint32_t *>(&t), sg;
+                        asm("prmt.b32 %0, %1, 0, 0xBB99;" : "=r"(sg) : "r"(b));
+                        b &= ~sg;
+                        t = *reinterpret_cast<__half2 *>(&b);
+                    }
+                    h[p] = __hmin2(t, cap2);
+                }
+            } else {
+#pragma unroll
+                for (int p = 0; p < P; ++p)
+                    h[p] = __floats2half2_rn(epi_value<KIND>(v[p][0], a.ep), epi_value<KIND>(v[p][1], a.ep));
+            }
+            if (pool) {
+                if constexpr (POOLABLE) {
+#pragma unroll
+                    for (int c2 = 0; c2 < PC / 2; ++c2) {
+                        if (2 * c2 >= ncol) continue;
+                        *reinterpret_cast<__half2 *>(y + c2 * IL) =
+                            __hmax2(__hmax2(h[2 * c2], h[2 * c2 + 1]), __hmax2(h[PC + 2 * c2], h[PC + 2 * c2 + 1]));
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int p = 0; p < P; ++p) {
+                    if (p / PC >= nrow || p % PC >= ncol) continue;
+                    *reinterpret_cast<__half2 *>(y + (p / PC) * rstride + (p % PC) * IL) = h[p];
+                }
+            }
         } else {  // F16, SPL 2: one cvt.rn.f16x2 per pixel
             __half *y = static_cast<__half *>(a.y) + od;
             __half2 h[P];
@@ -950,7 +999,7 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1) k_bi(const __grid_constant_
         }
 
         if (active && r < a.Yh) {
-            if constexpr (KIND == USC_F32 || KIND == USC_F16 || KIND == USC_I8) {
+            if constexpr (KIND == USC_F32 || KIND == USC_F16 || KIND == USC_I8 || KIND == USC_CB4) {
                 if (a.fast) {
                     if constexpr (!RPRE) fast_loads<KIND, PC, PR, DW, SPL, RES>(a, g, wc, sb, r, col0, part, lane, dch, rv);
                     store_tile_fast<KIND, PC, PR, DW, SPL, RES>(a, acc, sb, r, col0, lane, dch, rv);
