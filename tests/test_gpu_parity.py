@@ -276,6 +276,38 @@ def test_vgg16_int8_network_vs_oracle():
     assert np.array_equal(got, _vgg_oracle(m, x, conv))
 
 
+def test_vgg16_int8_requant_shift_range_vs_oracle():
+    """The integer requantisation (round-half-away by shift, clamp to +-127) across its
+    shift range: every later layer's input sigma is made 2^6 finer than calibrated, so
+    every epilogue shift is 6 smaller (many codes clamp at +-127) while the reference
+    composition requantises with the same sigmas in fp64."""
+    import dataclasses
+    import torch
+    from paper_2112_15445_b200.models import SparseVGG16, vgg16_rng, vgg16_weights
+    rng = vgg16_rng(0.93, seed=12)
+    ws = vgg16_weights(rng, 0.93)
+    x = rng.standard_normal((64, 3, 32, 32)).astype(np.float32)
+    m = SparseVGG16(ws, 64, mode="int8", calibration=torch.from_numpy(x).cuda())
+    for li in range(1, len(m.geoms)):
+        s = m.sigmas[li]
+        m.sigmas[li] = dataclasses.replace(s, int_bits=s.int_bits - 6, frac_bits=s.frac_bits + 6, sigma=s.sigma / 64)
+    for li in range(len(m.geoms)):
+        p = m.layer_params[li]
+        p["scale"] = float(np.float32(m.qfilters[li].params.sigma * m.sigmas[li].sigma))
+        if li + 1 < len(m.geoms):
+            p["rq_scale"] = float(np.float32(1.0 / m.sigmas[li + 1].sigma))
+    m._build()
+    got = m.forward(torch.from_numpy(x).cuda()).cpu().numpy()
+
+    def conv(li, a, gt):
+        s = m.sigmas[li]
+        xq = oracle.linear_quantize(a.astype(np.float32), dict(total_bits=s.total_bits, sigma=s.sigma, mu=0.0))
+        f = m.filters[li]
+        return oracle.relu(oracle.sparse_conv_forward(xq, (f.row_ptr, f.col_offsets, f.weights, f.n_nz), gt,
+                                                      threads=oracle.max_threads()))
+    assert np.array_equal(got, _vgg_oracle(m, x, conv))
+
+
 def test_vgg16_codebook_network_vs_oracle():
     """4b/16b VGG-16: codebook weights, binary16 activations with the _half_hook
     saturation at 0.99 x the calibrated conv / ReLU maxima (quantization.py:223-301)."""
