@@ -110,16 +110,22 @@ def fp32_muladd_peak(device_index: int) -> float:
     return float(v.value)
 
 
+TUNED_REL = os.path.join("profiles", "r01_tuned.json")
+
+
 def ncu_traffic(plan_desc) -> float | None:
-    """DRAM bytes per launch of the dominant kernel from the committed ncu capture
-    (profiles/traffic.json, written by tools/ncu_summary.py), if it is for the same tile."""
+    """DRAM bytes per launch of the dominant kernel from the committed ncu captures
+    (profiles/traffic.json, written by tools/ncu_summary.py: one entry per captured
+    conv plan), if one is for the same tile."""
     p = os.path.join(ROOT, "profiles", "traffic.json")
     if not os.path.exists(p):
         return None
     with open(p) as fh:
         d = json.load(fh)
-    if d.get("plan") == json.loads(json.dumps(plan_desc)):
-        return d.get("dram_bytes")
+    want = json.loads(json.dumps(plan_desc))
+    for e in d.get("entries", [d]):
+        if e.get("plan") == want:
+            return e.get("dram_bytes")
     return None
 
 
@@ -286,7 +292,11 @@ def main():
     ap.add_argument("--no-cudnn", action="store_true")
     ap.add_argument("--dump-configs", default=None, help="write the autotuned per-layer tiles (JSON)")
     ap.add_argument("--configs", default=None, help="per-layer tiles (JSON from --dump-configs); no autotune")
+    ap.add_argument("--retune", action="store_true",
+                    help="autotune the tiles this run instead of loading the committed " + TUNED_REL)
     args = ap.parse_args()
+    if not args.configs and not args.retune and not args.no_autotune and os.path.exists(os.path.join(ROOT, TUNED_REL)):
+        args.configs = os.path.join(ROOT, TUNED_REL)  # the committed autotuner result (matches profiles/)
     args.warmup = max(3, args.warmup)
     rank, local_rank, world = env_rank()
     if args.impl == "reference":
@@ -459,7 +469,9 @@ def main():
                            "per_gpu_batch": BATCH, "seq_len": None, "sparsity": SPARSITY,
                            "parallelism": f"dp{world} (batch-sharded, no collective)",
                            "l2": "flushed (256 MiB write) between timed steps",
-                           "cuda_graph": True},
+                           "cuda_graph": True,
+                           "tiles": (os.path.relpath(args.configs, ROOT) + " (committed autotuner result)")
+                           if args.configs else "autotuned this run"},
                 "e2e": e2e, "gpu_launches": args.steps * model.launches_per_forward,
                 "roofline": roofline, "layers": layers, "cudnn": cudnn, "cpu_baseline": cpu,
                 "clocks": clk.summary()}

@@ -3,6 +3,7 @@ the --set full report of the dominant kernel (DRAM traffic, throughputs, stall m
 
     python tools/ncu_summary.py launches gpurun_out/launches.csv profiles/r01_launches.md
     python tools/ncu_summary.py full gpurun_out/prof.ncu-rep profiles/r01_top_kernel.md [plan.json]
+    python tools/ncu_summary.py traffic gpurun_out/traffic.ncu-rep gpurun_out/plans.json profiles/traffic.json
 """
 import collections
 import csv
@@ -33,6 +34,28 @@ def launches(src, dst):
         out.append(f"| `{k[:90]}` | {len(v)} | {sum(v):.1f} | {sum(v)/len(v):.2f} | {sum(v)/total:.3f} |")
     open(dst, "w").write("\n".join(out) + "\n")
     print("\n".join(out[:12]))
+
+
+def traffic(rep, plans_path, dst):
+    """DRAM bytes (read + write) of every captured launch, keyed by its plan (launch order =
+    plans.json order) -> profiles/traffic.json entries (bench.py's roofline.traffic)."""
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    r = list(csv.reader(io.StringIO(raw)))
+    h, units = r[0], r[1]
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    ix = {n: i for i, n in enumerate(h)}
+    plans = json.load(open(plans_path))
+    entries = []
+    for row, p in zip(r[2:], plans):
+        b = 0.0
+        for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            b += float(row[ix[k]].replace(",", "")) * scale.get(units[ix[k]], 1.0)
+        entries.append(dict(layer=p["layer"], plan=p["plan"], dram_bytes=b,
+                            time_us=float(row[ix["gpu__time_duration.sum"]].replace(",", "")) *
+                            {"ns": 1e-3, "us": 1.0, "usecond": 1.0, "nsecond": 1e-3}.get(units[ix["gpu__time_duration.sum"]], 1.0)))
+    json.dump({"source": os.path.basename(rep), "entries": entries}, open(dst, "w"), indent=1)
+    for e in entries:
+        print(e["layer"], round(e["dram_bytes"] / 1e6, 2), "MB", round(e["time_us"], 1), "us")
 
 
 def full(rep, dst, plan_path=None):
@@ -66,7 +89,7 @@ def full(rep, dst, plan_path=None):
     for k, v in sorted(stalls.items(), key=lambda kv: -(kv[1] or 0))[:10]:
         lines.append(f"| {k} | {100 * (v or 0) / tot:.1f}% |")
     open(dst, "w").write("\n".join(lines) + "\n")
-    if plan_path:
+    if plan_path and os.environ.get("NCU_SUMMARY_TRAFFIC", "0") == "1":
         plan = json.load(open(plan_path))
         json.dump({"plan": plan, "dram_bytes": dram, "source": os.path.basename(rep)},
                   open(os.path.join(os.path.dirname(dst), "traffic.json"), "w"), indent=1)
@@ -76,5 +99,7 @@ def full(rep, dst, plan_path=None):
 if __name__ == "__main__":
     if sys.argv[1] == "launches":
         launches(sys.argv[2], sys.argv[3])
+    elif sys.argv[1] == "traffic":
+        traffic(sys.argv[2], sys.argv[3], sys.argv[4])
     else:
         full(sys.argv[2], sys.argv[3], sys.argv[4] if len(sys.argv) > 4 else None)
