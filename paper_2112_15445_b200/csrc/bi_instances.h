@@ -12,18 +12,20 @@
     X(2, 2, 16, 1, 1) X(8, 1, 16, 1, 1) X(2, 2, 8, 1, 1) X(1, 1, 16, 1, 1) X(2, 2, 4, 1, 1)                \
     X(2, 2, 2, 1, 1) X(2, 1, 4, 1, 1) X(1, 1, 4, 1, 1) X(4, 1, 8, 2, 1) X(8, 1, 8, 2, 1)                  \
     X(4, 2, 4, 1, 2) X(8, 1, 4, 1, 2) X(2, 2, 8, 1, 2) X(4, 2, 8, 1, 2) X(8, 2, 4, 1, 2) X(2, 2, 4, 1, 2)   \
-    X(4, 1, 8, 1, 2) X(2, 1, 8, 1, 2) X(1, 1, 8, 1, 2) X(1, 1, 4, 1, 2) X(2, 2, 2, 1, 2) X(4, 1, 4, 2, 2)
+    X(4, 1, 8, 1, 2) X(2, 1, 8, 1, 2) X(1, 1, 8, 1, 2) X(1, 1, 4, 1, 2) X(2, 2, 2, 1, 2) X(4, 1, 4, 2, 2)   \
+    X(4, 2, 4, 2, 2) X(8, 1, 4, 2, 2)
 
 #define USC_BI_W12(X)                                                                                     \
     X(4, 2, 8, 1, 1) X(8, 2, 4, 1, 1) X(8, 1, 8, 1, 1) X(2, 2, 16, 1, 1) X(4, 1, 16, 1, 1) X(2, 2, 8, 1, 1) \
     X(4, 2, 4, 1, 1) X(8, 1, 4, 1, 1) X(2, 1, 16, 1, 1) X(4, 1, 8, 2, 1)                                   \
-    X(4, 2, 4, 1, 2) X(2, 2, 8, 1, 2) X(8, 1, 4, 1, 2) X(2, 2, 4, 1, 2) X(4, 1, 4, 1, 2)
+    X(4, 2, 4, 1, 2) X(2, 2, 8, 1, 2) X(8, 1, 4, 1, 2) X(2, 2, 4, 1, 2) X(4, 1, 4, 1, 2)                   \
+    X(4, 2, 4, 2, 2) X(4, 1, 4, 2, 2)
 
 #define USC_BI_W16(X)                                                                                     \
     X(2, 2, 8, 1, 1) X(4, 2, 4, 1, 1) X(2, 2, 4, 1, 1) X(4, 1, 8, 1, 1) X(8, 1, 4, 1, 1) X(1, 1, 16, 1, 1) \
     X(2, 1, 16, 1, 1) X(1, 2, 16, 1, 1) X(2, 2, 2, 1, 1) X(4, 1, 4, 2, 1) X(2, 1, 8, 2, 1) X(1, 1, 8, 2, 1) \
     X(2, 2, 4, 1, 2) X(4, 1, 4, 1, 2) X(2, 2, 2, 1, 2) X(4, 2, 2, 1, 2) X(1, 1, 8, 1, 2) X(1, 1, 4, 1, 2)  \
-    X(1, 1, 2, 1, 2)
+    X(1, 1, 2, 1, 2) X(4, 2, 2, 2, 2) X(4, 1, 4, 2, 2) X(8, 1, 2, 2, 2)
 
 // binary16-input kinds (F16: FHFMA; CB4: FMUL + FADD2), BI64 only (two samples per
 // lane as one 32-bit half2 load).  X(NW, PC, PR, DW, SW), each built for F16 and CB4.
@@ -32,7 +34,8 @@
     X(8, 1, 1, 8, 1) X(8, 4, 1, 8, 2) X(12, 4, 2, 4, 1) X(12, 8, 1, 4, 1)            \
     X(12, 2, 2, 4, 1) X(16, 2, 2, 4, 1) X(16, 4, 1, 4, 1) X(16, 2, 2, 2, 1) X(16, 4, 2, 2, 1)          \
     X(16, 1, 1, 8, 1) X(16, 4, 1, 4, 2) X(12, 4, 2, 2, 1) X(12, 8, 1, 2, 1) X(12, 4, 1, 4, 1)           \
-    X(8, 8, 2, 2, 1) X(16, 8, 1, 2, 1) X(16, 1, 1, 4, 1) X(8, 1, 1, 4, 1) X(16, 8, 2, 1, 1) X(12, 8, 2, 1, 1)
+    X(8, 8, 2, 2, 1) X(16, 8, 1, 2, 1) X(16, 1, 1, 4, 1) X(8, 1, 1, 4, 1) X(16, 8, 2, 1, 1) X(12, 8, 2, 1, 1) \
+    X(16, 4, 2, 2, 2) X(12, 4, 2, 4, 2) X(16, 8, 1, 2, 2)
 
 // tensor-memory-fed fp32 BI64 kernel (kernel 4, conv_bt.cuh).  X(NW, PC, PR, DW),
 // NW a multiple of 4 (the compute warps of each lane quarter fill its TMEM copy).
