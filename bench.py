@@ -4,10 +4,16 @@ BASELINE.json configs[1] -- on N B200s, batch-sharded (weak scaling, no
 collective on the hot path).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--global-batch B]
 
-Prints ONE JSON line (rank 0).  ``--impl reference`` times the reference's CPU
-algorithm (the oracle port in oracle/, all host threads) on a bounded sample of
-the same workload.
+Prints ONE JSON line (rank 0).  ``--gpus N`` without a torchrun environment
+re-launches itself under torch.distributed.run with N ranks (one per GPU);
+under torchrun the world size must equal N.  Default: weak scaling, 256 images
+per rank; ``--global-batch B`` splits B images over the ranks instead (strong
+scaling, sharding.ShardedRun).  The e2e leg ends every step with the final
+gather of the features (the one collective of the batch-sharded job).
+``--impl reference`` times the reference's CPU algorithm (the oracle port in
+oracle/, all host threads) on a bounded sample of the same workload.
 """
 
 from __future__ import annotations
@@ -100,13 +106,17 @@ def measured_peaks():
     return 6650.0, "fallback"
 
 
-def fp32_muladd_peak(device_index: int) -> float:
-    """Live FMUL+FADD (the exact path's instruction mix) peak in TFLOP/s on this
-    GPU, from the library's diagnostic probe (usc_peak_fp32_muladd)."""
+MIX_NAMES = {0: "FMUL+FADD", 1: "FMUL,FMUL+FADD2 (two samples per lane)", 2: "FHFMA"}
+
+
+def mix_peak(device_index: int, mix: int) -> float:
+    """Live CUDA-core peak (nonzero TFLOP/s) of an exact instruction mix on this GPU,
+    from the library's probe (usc_peak_mix): 0 = FMUL+FADD, 1 = the fp32 BI64 inner
+    loop's FMUL,FMUL+FADD2, 2 = binary16 FHFMA."""
     import ctypes
     from paper_2112_15445_b200 import _lib
     v = ctypes.c_double(0.0)
-    _lib.check(_lib.lib().usc_peak_fp32_muladd(device_index, ctypes.byref(v)), "peak")
+    _lib.check(_lib.lib().usc_peak_mix(device_index, mix, ctypes.byref(v)), "peak")
     return float(v.value)
 
 
@@ -223,8 +233,9 @@ def cudnn_reference(ws, batch, device, steps=10, tf32=False):
     return {"ms_per_step": ms, "images_per_s": batch / ms * 1e3}
 
 
-def cpu_reference_run(batch_sample, threads, ws_data, seed=1):
-    """The reference's algorithm (oracle port, C) for the same network on a sample."""
+def cpu_reference_run(batch_sample, threads, ws_data, seed=1, x=None):
+    """The reference's algorithm (oracle port, C) for the same network on a sample
+    (seeded N(0,1) images, or the given `x`)."""
     import oracle
     from paper_2112_15445_b200.models import VGG16_CIFAR, vgg16_geometries
     geoms = vgg16_geometries()
@@ -232,7 +243,8 @@ def cpu_reference_run(batch_sample, threads, ws_data, seed=1):
     for w, g in zip(ws_data, geoms):
         gt = (g.in_channels, g.out_channels, 3, 3, g.input_h, g.input_w, (1, 1), (1, 1))
         csrs.append((gt, oracle.build_csr(w, gt)))
-    x = np.random.default_rng(seed).standard_normal((batch_sample, 3, 32, 32)).astype(np.float32)
+    if x is None:
+        x = np.random.default_rng(seed).standard_normal((batch_sample, 3, 32, 32)).astype(np.float32)
 
     def fwd():
         a, li = x, 0
@@ -281,37 +293,187 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def free_port() -> int:
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def launch_ranks(args):
+    """`--gpus N` outside torchrun: re-exec this script under torch.distributed.run
+    with N local ranks (127.0.0.1 rendezvous); rank 0 prints the JSON line."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    sys.stdout.flush()
+    os.execv(sys.executable, cmd)
+
+
+def self_check(model, x_np, ws, samples=8):
+    """The first `samples` images of the timed batch through the oracle (the
+    reference's algorithm restated in C, the checker only) vs the timed graph's
+    output: bitwise equality required (fp32 path)."""
+    import oracle
+    oracle.build()
+    ref = cpu_reference_run(samples, oracle.max_threads(), [w.data for w in ws], x=x_np[:samples])()
+    got = model.output().cpu().numpy()[:samples]
+    return {"samples": samples, "bitwise": bool(np.array_equal(got, ref)),
+            "checker": "oracle/oracle.c (C restatement of kernels.py:57-100, pinned to the reference's golden vectors)"}
+
+
+def cfg1_leg(device, steps=50, cpu=True):
+    """BASELINE configs[0]: one pruned VGG-16 256->256 3x3 layer, 8x8 map, batch 32,
+    90% sparsity, fp32 -- the reference's bench_layer comparison (bench.py:98-130):
+    device us of the kernel (L2 flushed), the drop-in API with host numpy buffers
+    (H2D + pad + kernel + D2H inside the timing), cuDNN dense at equal precision,
+    and the reference's CPU algorithm on the host cores."""
+    import zlib
+
+    import torch
+    import paper_2112_15445_b200 as U
+    from paper_2112_15445_b200.engine import _storage_dtype, dtype_of, launch, padded_input, plan_for
+    from paper_2112_15445_b200.pruning import synthesize_masked_weights
+    g = U.ConvGeometry(256, 256, 3, 3, 8, 8, padding=(1, 1))
+    n, sparsity = 32, 0.9
+    rng = np.random.default_rng([0, zlib.crc32(b"cfg1-vgg16-256x8"), int(round(sparsity * 1000))])
+    w = synthesize_masked_weights(g, sparsity, rng)
+    x_np = rng.standard_normal((n, 256, 8, 8)).astype(np.float32)
+    filt = U.build_csr(w, g)
+    xd = U.DenseTensor4(torch.from_numpy(x_np).to(device))
+    cfg = U.autotune_sb(xd, filt, repeats=5, warmup=2)
+    plan, blob = plan_for(filt, n, dtype_of(xd.precision), cfg, filt.weights)
+    x_pad = padded_input(xd.device(), plan)
+    y = torch.empty((n, 256, 8, 8), dtype=_storage_dtype(plan.dtype), device=device)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=device)
+
+    def dev_time(fn, flush_l2):
+        for _ in range(3):
+            fn()
+        ts = []
+        for _ in range(steps):
+            if flush_l2:
+                flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda._sleep(100_000)
+            a.record()
+            fn()
+            b.record()
+            ts.append((a, b))
+        torch.cuda.synchronize()
+        return float(np.median([a.elapsed_time(b) for a, b in ts])) * 1e3
+
+    kern_us = dev_time(lambda: launch(plan, blob, x_pad, y), True)
+    kern_warm_us = dev_time(lambda: launch(plan, blob, x_pad, y), False)
+    api_dev_us = dev_time(lambda: U.sparse_conv_forward(xd, filt, cfg), True)
+    # host cost of one drop-in call (plans cached on the filter): enqueue time per call
+    for _ in range(5):
+        U.sparse_conv_forward(xd, filt, cfg)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        U.sparse_conv_forward(xd, filt, cfg)
+    host_us = (time.perf_counter() - t0) / steps * 1e6
+    torch.cuda.synchronize()
+    # e2e through the reference-facing API: host numpy in, host numpy out
+    e2e = []
+    for i in range(steps + 3):
+        t0 = time.perf_counter()
+        out = U.sparse_conv_forward(U.DenseTensor4(x_np), filt, cfg).data
+        if i >= 3:
+            e2e.append(time.perf_counter() - t0)
+    e2e_us = float(np.median(e2e)) * 1e6
+    # cuDNN dense on the same masked weights, equal precision (TF32 off) and TF32
+    wt = torch.from_numpy(np.array(w.data)).to(device)
+    xt = xd.device()
+    torch.backends.cudnn.benchmark = True
+    cud = {}
+    for name, tf32 in (("fp32_tf32_off", False), ("tf32", True)):
+        torch.backends.cudnn.allow_tf32 = tf32
+        cud[name] = round(dev_time(lambda: torch.nn.functional.conv2d(xt, wt, padding=1), True), 2)
+    torch.backends.cudnn.allow_tf32 = True
+    genuine = int(np.count_nonzero(filt.weights))
+    flops = 2.0 * genuine * 64 * n
+    byts = n * 256 * 64 * 4 * 2 + filt.n_nz * 256 * 8 + 4 * 257
+    res = {"workload": "VGG-16 256->256 3x3, 8x8 map, pad 1, batch 32, 90% layer-global sparsity, fp32 "
+                       "(BASELINE configs[0])",
+           "tile": {k: v for k, v in plan.describe().items()},
+           "kernel_us": round(kern_us, 2), "kernel_us_l2_warm": round(kern_warm_us, 2),
+           "api_device_us": round(api_dev_us, 2), "api_host_us_per_call": round(host_us, 1),
+           "e2e_us": round(e2e_us, 1),
+           "e2e_path": "sparse_conv_forward(DenseTensor4(host numpy), build_csr(...)).data: pageable H2D, "
+                       "pad, kernel, D2H to numpy (wall clock, median)",
+           "images_per_s": {"kernel": round(n / kern_us * 1e6, 1), "e2e": round(n / e2e_us * 1e6, 1)},
+           "nonzero_tflops": round(flops / kern_us / 1e6, 2), "hbm_gbs": round(byts / kern_us / 1e3, 1),
+           "cudnn_us": cud, "speedup_vs_cudnn_fp32": round(cud["fp32_tf32_off"] / kern_us, 2)}
+    import oracle
+    oracle.build()
+    csr = (filt.row_ptr, filt.col_offsets, filt.weights, filt.n_nz)
+    gt = (256, 256, 3, 3, 8, 8, (1, 1), (1, 1))
+    ref = oracle.sparse_conv_forward(x_np, csr, gt, threads=oracle.max_threads())
+    res["parity"] = {"samples": n, "bitwise": bool(np.array_equal(out, ref))}
+    if cpu:
+        th = oracle.max_threads()
+        t0, reps = time.perf_counter(), 0
+        while time.perf_counter() - t0 < 5.0 or reps < 2:
+            oracle.sparse_conv_forward(x_np, csr, gt, threads=th)
+            reps += 1
+        cpu_us = (time.perf_counter() - t0) / reps * 1e6
+        res["cpu_reference"] = {"us": round(cpu_us, 1), "cores": th, "kind": "port",
+                                "sample": f"{reps} full cfg1 calls (32 images), ~5 s"}
+    return res
+
+
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--gpus", type=int, default=None,
+                    help="ranks (one per GPU); without torchrun env, re-launches under torchrun")
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--global-batch", type=int, default=None,
+                    help="strong scaling: split this many images over the ranks (default: 256 per rank)")
     ap.add_argument("--no-autotune", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-cudnn", action="store_true")
+    ap.add_argument("--no-cfg1", action="store_true")
     ap.add_argument("--dump-configs", default=None, help="write the autotuned per-layer tiles (JSON)")
     ap.add_argument("--configs", default=None, help="per-layer tiles (JSON from --dump-configs); no autotune")
     ap.add_argument("--retune", action="store_true",
                     help="autotune the tiles this run instead of loading the committed " + TUNED_REL)
     args = ap.parse_args()
-    if not args.configs and not args.retune and not args.no_autotune and os.path.exists(os.path.join(ROOT, TUNED_REL)):
-        args.configs = os.path.join(ROOT, TUNED_REL)  # the committed autotuner result (matches profiles/)
-    args.warmup = max(3, args.warmup)
+    if "WORLD_SIZE" not in os.environ and (args.gpus or 1) > 1:
+        launch_ranks(args)
     rank, local_rank, world = env_rank()
+    if args.gpus is not None and args.gpus != world:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but the launcher started {world} rank(s)")
+    args.warmup = max(3, args.warmup)
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
 
     import torch
     import torch.distributed as dist
-    from paper_2112_15445_b200 import _lib
+    from paper_2112_15445_b200.sharding import ShardedRun
     torch.cuda.set_device(local_rank)
     device = torch.device("cuda", local_rank)
     if world > 1:
         dist.init_process_group("nccl", device_id=device)
+    if args.global_batch:
+        job = ShardedRun(args.global_batch, rank, world, align=64)
+        scaling = "strong"
+    else:
+        job = ShardedRun.weak(BATCH, rank, world)
+        scaling = "weak"
+    batch = job.local_batch
+    if batch < 1:
+        raise SystemExit(f"bench.py: rank {rank} has no images (global batch {job.global_batch})")
+    if (not args.configs and not args.retune and not args.no_autotune and batch == BATCH
+            and os.path.exists(os.path.join(ROOT, TUNED_REL))):
+        args.configs = os.path.join(ROOT, TUNED_REL)  # the committed autotuner result (matches profiles/)
 
-    model, ws = build_model(BATCH, device)
+    model, ws = build_model(batch, device)
     if args.configs:
         model.load_tuned_state(json.load(open(args.configs)))
     elif not args.no_autotune:
@@ -320,10 +482,9 @@ def main():
         with open(args.dump_configs, "w") as fh:
             json.dump(model.tuned_state(), fh)
     model.capture()
-    x_host = torch.from_numpy(np.random.default_rng([1, rank]).standard_normal(
-        (BATCH, 3, 32, 32)).astype(np.float32)).pin_memory()
+    x_np = np.random.default_rng([1, rank]).standard_normal((batch, 3, 32, 32)).astype(np.float32)
+    x_host = torch.from_numpy(x_np).pin_memory()
     x_dev = x_host.to(device)
-    out_host = torch.empty((BATCH, 512, 1, 1), dtype=torch.float32).pin_memory()
     model.load_input(x_dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=device)  # 2x L2
 
@@ -352,34 +513,49 @@ def main():
         total_ms = float(t.item())
         dist.barrier()
     ms_per_step = total_ms / args.steps
-    value = world * BATCH * args.steps / (total_ms / 1e3)
+    value = job.global_batch * args.steps / (total_ms / 1e3)
+    # the timed graph's own output checked against the oracle on its first images
+    parity = self_check(model, x_np, ws) if rank == 0 else None
 
     # ---- e2e through the public API with host buffers ---------------------------
     e2e_steps = max(10, args.steps // 2)
+    gathered = job.world > 1
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    # (a) one batch at a time: H2D, forward, D2H serialised on one stream
+    out_rows = job.global_batch if gathered else batch
+    # (a) one batch at a time: H2D, forward, final gather, D2H serialised on one stream
+    out_host = torch.empty((out_rows, 512, 1, 1), dtype=torch.float32).pin_memory()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record()
     for _ in range(e2e_steps):
         x_dev.copy_(x_host, non_blocking=True)
-        out = model.forward(x_dev)
-        out_host.copy_(out, non_blocking=True)
+        out = job.gather(model.forward(x_dev)) if gathered else model.forward(x_dev)
+        if rank == 0:
+            out_host.copy_(out, non_blocking=True)
     b.record()
     b.synchronize()
     e2e_serial_ms = a.elapsed_time(b)
     # (b) the streaming API: every step still moves its input H2D and its features D2H,
-    # overlapped with the neighbouring steps' compute (SparseVGG16.stream_forward)
+    # overlapped with the neighbouring steps' compute (SparseVGG16.stream_forward); at N>1
+    # each step's features are gathered to rank 0 before the D2H
     x_hosts = [torch.from_numpy(np.random.default_rng([2, rank, i]).standard_normal(
-        (BATCH, 3, 32, 32)).astype(np.float32)).pin_memory() for i in range(4)]
+        (batch, 3, 32, 32)).astype(np.float32)).pin_memory() for i in range(4)]
     x_seq = [x_hosts[i % 4] for i in range(e2e_steps)]
-    out_seq = [torch.empty((BATCH, 512, 1, 1), dtype=torch.float32).pin_memory() for _ in range(e2e_steps)]
-    model.stream_forward(x_seq[:2], out_seq[:2]).synchronize()  # warm the streams / buffers
+    out_seq = [torch.empty((out_rows, 512, 1, 1), dtype=torch.float32).pin_memory()
+               for _ in range(e2e_steps)]
+    collect = None
+    if gathered:
+        def collect(t):
+            full = job.gather(t)
+            return full if rank == 0 else None
+    model.stream_forward(x_seq[:2], out_seq[:2], collect=collect).synchronize()  # warm streams / buffers
     torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record()
-    model.stream_forward(x_seq, out_seq)
+    model.stream_forward(x_seq, out_seq, collect=collect)
     b.record()
     b.synchronize()
     e2e_ms = a.elapsed_time(b)
@@ -387,12 +563,15 @@ def main():
         t = torch.tensor([e2e_ms, e2e_serial_ms], device=device)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms, e2e_serial_ms = float(t[0].item()), float(t[1].item())
-    e2e = {"value": round(world * BATCH * e2e_steps / (e2e_ms / 1e3), 1), "unit": "images/s",
-           "h2d_bytes_per_step": int(x_host.numel() * 4), "d2h_bytes_per_step": int(out_host.numel() * 4),
+    e2e = {"value": round(job.global_batch * e2e_steps / (e2e_ms / 1e3), 1), "unit": "images/s",
+           "h2d_bytes_per_step": int(job.global_batch * 3 * 32 * 32 * 4),
+           "d2h_bytes_per_step": int(out_rows * 512 * 4),
            "path": "SparseVGG16.stream_forward: per step pinned H2D of the input, pad + CUDA graph, "
-                   "D2H of the features, transfers overlapped with neighbouring steps on two copy streams",
-           "serial": {"value": round(world * BATCH * e2e_steps / (e2e_serial_ms / 1e3), 1),
-                      "path": "SparseVGG16.forward with H2D/D2H serialised on one stream"}}
+                   + ("all_gather of the features to rank 0 (sharding.ShardedRun.gather), " if gathered else "")
+                   + "D2H of the features, transfers overlapped with neighbouring steps on two copy streams",
+           "serial": {"value": round(job.global_batch * e2e_steps / (e2e_serial_ms / 1e3), 1),
+                      "path": "SparseVGG16.forward with H2D" + (", gather" if gathered else "")
+                              + " and D2H serialised on one stream"}}
 
     # ---- per-launch breakdown, roofline of the dominant kernel --------------------
     per = time_per_launch(model)
@@ -401,21 +580,23 @@ def main():
     dom = max(conv_ms, key=conv_ms.get)
     dom_ms = conv_ms[dom]
     hbm_peak, peak_kind = measured_peaks()
-    core_peak = fp32_muladd_peak(local_rank)
+    plan = next(st[2] for st in model.steps if st[0] == "conv" and st[1] == dom)
+    mix = 1 if plan.kernel in (3, 4) and plan.NS == 64 else 0
+    core_peak = mix_peak(local_rank, mix)
     s = stats[dom]
     achieved_gbs = s["bytes"] / (dom_ms / 1e3) / 1e9
     achieved_tf = s["flops"] / (dom_ms / 1e3) / 1e12
     g = model.geoms[dom]
-    plan = next(st[2] for st in model.steps if st[0] == "conv" and st[1] == dom)
     ai = s["flops"] / s["bytes"]
     # attainable roof = min(core peak, AI * HBM): every 3x3 layer here is far right of the
-    # ridge, so the bound is the CUDA-core FMUL+FADD rate (no tensor cores: the
-    # contraction is unstructured-sparse and must round like the reference)
+    # ridge, so the bound is the CUDA-core issue rate of the kernel's own exact mix (no
+    # tensor cores: the contraction is unstructured-sparse and must round like the reference)
     roofline = {"bound": "fp32-cuda-core" if ai * hbm_peak / 1e3 > core_peak else "hbm",
                 "achieved": round(achieved_tf, 3), "peak": round(core_peak, 2), "unit": "TFLOP/s",
                 "frac": round(achieved_tf / core_peak, 4),
                 "traffic": ncu_traffic(plan.describe()),
-                "peak_source": "live FMUL+FADD probe on this GPU (usc_peak_fp32_muladd)",
+                "peak_source": f"live {MIX_NAMES[mix]} probe on this GPU (usc_peak_mix {mix}: the dominant "
+                               f"kernel's own multiply/add instruction mix)",
                 "kernel": f"k_bi conv layer {dom} ({g.in_channels}->{g.out_channels}, {g.input_h}x{g.input_w})",
                 "kernel_share_of_step": round(dom_ms / sum(per.values()), 3),
                 "launch_us": round(dom_ms * 1e3, 2),
@@ -442,8 +623,9 @@ def main():
     if rank == 0:
         cudnn = None
         if not args.no_cudnn:
-            cudnn = {"fp32_tf32_off": cudnn_reference(ws, BATCH, device),
-                     "tf32": cudnn_reference(ws, BATCH, device, tf32=True)}
+            cudnn = {"fp32_tf32_off": cudnn_reference(ws, batch, device),
+                     "tf32": cudnn_reference(ws, batch, device, tf32=True)}
+        cfg1 = None if args.no_cfg1 else cfg1_leg(device, cpu=not args.no_cpu_baseline and world == 1)
         cpu = None
         if not args.no_cpu_baseline and world == 1:
             import oracle
@@ -463,18 +645,20 @@ def main():
                                              f"(oracle/oracle.c), ~10 s of host work"}
         line = {"impl": "ours", "metric": METRIC, "value": round(value, 1), "unit": "images/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+                "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f32",
                 "data": "synthetic (seeded N(0,1) inputs, random-init pruned weights)",
-                "config": {"workload": WORKLOAD, "model": "vgg16-cifar10", "global_batch": world * BATCH,
-                           "per_gpu_batch": BATCH, "seq_len": None, "sparsity": SPARSITY,
-                           "parallelism": f"dp{world} (batch-sharded, no collective)",
+                "config": {"workload": WORKLOAD, "model": "vgg16-cifar10", "global_batch": job.global_batch,
+                           "per_gpu_batch": batch, "seq_len": None, "sparsity": SPARSITY,
+                           "parallelism": f"dp{world} (batch-sharded, no collective in the timed step; "
+                                          f"final all_gather in the e2e leg)",
                            "l2": "flushed (256 MiB write) between timed steps",
                            "cuda_graph": True,
                            "tiles": (os.path.relpath(args.configs, ROOT) + " (committed autotuner result)")
                            if args.configs else "autotuned this run"},
                 "e2e": e2e, "gpu_launches": args.steps * model.launches_per_forward,
+                "parity": parity,
                 "roofline": roofline, "layers": layers, "cudnn": cudnn, "cpu_baseline": cpu,
-                "clocks": clk.summary()}
+                "cfg1": cfg1, "clocks": clk.summary()}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()

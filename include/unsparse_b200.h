@@ -211,6 +211,20 @@ int usc_plan_make(const usc_geometry *g, int32_t n, int32_t dtype, const usc_exe
  * warps*32, samples_per_cta = 32*samples per lane). */
 int usc_bi_instances(int32_t *out, int32_t max_count);
 int usc_pack_size(const usc_plan *plan, int64_t n_nz, int64_t *bytes);
+/* autotune_sb (engine.py:139-170) behind the C ABI: plans, packs and times every
+ * tile candidate of the layer (the batch-interleaved kernel's compiled instances x
+ * warp splits x ring depths x pixel classes, and kernel 1's sub-batch x pixels x
+ * channels -- engine.tile_candidates) on `x_dev` (plain NCHW, n x C x H x W in the
+ * dtype's storage: f32, binary16, int8 codes, binary16) with CUDA events on
+ * `stream` (median of `repeats` after `warmup` launches) and writes the fastest
+ * config to *best (candidates within noise_floor of it resolve to the earliest, in
+ * ascending sub-batch order, as the reference's rule).  Allocates and frees its
+ * own scratch buffers; synchronises `stream`.  row_ptr/col_offsets/payload/table
+ * as usc_pack.  *best_ms (may be NULL) receives the winner's median time. */
+int usc_autotune(const usc_geometry *g, int32_t n, int32_t dtype, const int64_t *row_ptr,
+                 const int64_t *col_offsets, const void *payload, int64_t n_nz, const float *table,
+                 const void *x_dev, int32_t repeats, int32_t warmup, float noise_floor, usc_exec_cfg *best,
+                 float *best_ms, void *stream);
 int usc_pack(const usc_plan *plan, const int64_t *row_ptr, const int64_t *col_offsets,
              const void *payload, int64_t n_nz, const float *table, void *host_blob,
              int64_t blob_bytes, int64_t *n_entries);
@@ -276,6 +290,11 @@ int usc_quantize_i8(const float *src, int8_t *dst, int64_t count, double sigma, 
  * then add, never contracted) on `device`, in TFLOP/s (2 flops per pair); the
  * roofline denominator bench.py reports the sparse conv kernel against. */
 int usc_peak_fp32_muladd(int32_t device, double *tflops);
+/* Same probe for a chosen mix, in nonzero TFLOP/s (2 flops per MAC):
+ *   0 = FMUL + FADD (one sample per lane, kernels 1/2 and BI32),
+ *   1 = FMUL, FMUL + one packed FADD2 per two samples (the fp32 BI64 inner loop),
+ *   2 = FHFMA (fma.rn.f32.f16, the binary16 BI64 inner loop). */
+int usc_peak_mix(int32_t device, int32_t mix, double *tflops);
 
 /* ---- quantisation primitives (host) -- quantization.py ------------------ */
 /* fit_fixed_point (quantization.py:41-58): from max|x| */

@@ -99,6 +99,8 @@ _SIGS = {
     "usc_plan_make": (c_i32, [c_ptr, c_i32, c_i32, c_ptr, c_ptr]),
     "usc_bi_instances": (c_i32, [c_ptr, c_i32]),
     "usc_pack_size": (c_i32, [c_ptr, c_i64, c_ptr]),
+    "usc_autotune": (c_i32, [c_ptr, c_i32, c_i32, c_ptr, c_ptr, c_ptr, c_i64, c_ptr, c_ptr, c_i32, c_i32,
+                             ctypes.c_float, c_ptr, c_ptr, c_ptr]),
     "usc_pack": (c_i32, [c_ptr, c_ptr, c_ptr, c_ptr, c_i64, c_ptr, c_ptr, c_i64, c_ptr]),
     "usc_pad_input": (c_i32, [c_ptr, c_i32, c_i32, c_ptr, c_ptr, c_ptr]),
     "usc_unpad_output": (c_i32, [c_ptr, c_i32, c_i32, c_ptr, c_ptr, c_ptr]),
@@ -112,6 +114,7 @@ _SIGS = {
     "usc_maxpool2": (c_i32, [c_ptr, c_ptr, c_i32, c_i32, c_ptr, c_ptr, c_ptr]),
     "usc_quantize_i8": (c_i32, [c_ptr, c_ptr, c_i64, ctypes.c_double, c_i32, c_ptr]),
     "usc_peak_fp32_muladd": (c_i32, [c_i32, c_ptr]),
+    "usc_peak_mix": (c_i32, [c_i32, c_i32, c_ptr]),
     "usc_fit_fixed_point": (c_i32, [ctypes.c_double, c_i32, c_ptr, c_ptr, c_ptr]),
     "usc_linear_codes": (c_i32, [c_ptr, c_i64, ctypes.c_double, c_i32, c_ptr]),
     "usc_kmeans_codebook": (c_i32, [c_ptr, c_i64, c_i32, c_i32, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr]),
@@ -173,6 +176,10 @@ def np_ptr(a):
 
 
 def t_ptr(t):
+    """Device pointer of a CUDA tensor (kernel arguments; a host tensor here would
+    fault inside the kernel and poison the context, so it is rejected)."""
+    if not t.is_cuda:
+        raise ValueError(f"expected a CUDA tensor, got one on {t.device}")
     return ctypes.c_void_p(t.data_ptr())
 
 

@@ -369,6 +369,52 @@ __global__ void k_peak_muladd(float *out, float a, float b, int iters) {
     if (s == 1.2345f) out[0] = s;
 }
 
+// The BI64 fp32 inner-loop mix: per lane two samples, FMUL x2 then one packed FADD2
+// (add.rn.f32x2) per MAC pair (8 independent chains per thread).
+__global__ void k_peak_fadd2(float *out, float a, float b, int iters) {
+    unsigned long long acc[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        float lo = threadIdx.x * 0.001f + i, hi = lo + 0.5f;
+        asm("mov.b64 %0, {%1, %2};" : "=l"(acc[i]) : "f"(lo), "f"(hi));
+    }
+    for (int it = 0; it < iters; ++it)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            float lo, hi, p0, p1;
+            asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(acc[i]));
+            asm volatile("mul.rn.f32 %0, %1, %2;" : "=f"(p0) : "f"(lo), "f"(a));
+            asm volatile("mul.rn.f32 %0, %1, %2;" : "=f"(p1) : "f"(hi), "f"(b));
+            unsigned long long q;
+            asm("mov.b64 %0, {%1, %2};" : "=l"(q) : "f"(p0), "f"(p1));
+            asm volatile("add.rn.f32x2 %0, %0, %1;" : "+l"(acc[i]) : "l"(q));
+        }
+    float s = 0.0f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        float lo, hi;
+        asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(acc[i]));
+        s += lo + hi;
+    }
+    if (s == 1.2345f) out[0] = s;
+}
+
+// The binary16 path's FHFMA (fma.rn.f32.f16: fp32 += f16 * f16), 8 chains per thread.
+__global__ void k_peak_fhfma(float *out, float a, float b, int iters) {
+    float acc[8];
+    const unsigned short th = __half_as_ushort(__float2half(a));
+    const unsigned short xv = (unsigned short)(0x3800 + (threadIdx.x & 255));
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[i] = b + i;
+    for (int it = 0; it < iters; ++it)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) asm volatile("fma.rn.f32.f16 %0, %1, %2, %0;" : "+f"(acc[i]) : "h"(th), "h"(xv));
+    float s = 0.0f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s += acc[i];
+    if (s == 1.2345f) out[0] = s;
+}
+
 int grid_for(long long total, int threads = 256) {
     long long g = (total + threads - 1) / threads;
     return static_cast<int>(std::max<long long>(1, std::min<long long>(g, 148LL * 32)));
@@ -468,7 +514,10 @@ int usc_device_sm_count(int device) {
     return v;
 }
 
-int usc_peak_fp32_muladd(int32_t device, double *tflops) {
+int usc_peak_fp32_muladd(int32_t device, double *tflops) { return usc_peak_mix(device, 0, tflops); }
+
+int usc_peak_mix(int32_t device, int32_t mix, double *tflops) {
+    if (mix < 0 || mix > 2) return fail(USC_ERR_VALUE, "unknown instruction mix %d", mix);
     int sms = usc_device_sm_count(device);
     if (sms <= 0) return fail(USC_ERR_CUDA, "no CUDA device %d", device);
     cudaSetDevice(device);
@@ -478,11 +527,13 @@ int usc_peak_fp32_muladd(int32_t device, double *tflops) {
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     const int blocks = sms * 8, threads = 256, iters = 8192;
-    k_peak_muladd<<<blocks, threads>>>(out, 1.0001f, 0.5f, iters);
+    auto fn = mix == 0 ? k_peak_muladd : (mix == 1 ? k_peak_fadd2 : k_peak_fhfma);
+    const double macs_per_iter = mix == 1 ? 16.0 : 8.0;  // per thread: 8 chains (x2 samples for FADD2)
+    fn<<<blocks, threads>>>(out, 1.0001f, 0.5f, iters);
     float best = 1e30f;
     for (int r = 0; r < 5; ++r) {
         cudaEventRecord(e0);
-        k_peak_muladd<<<blocks, threads>>>(out, 1.0001f, 0.5f, iters);
+        fn<<<blocks, threads>>>(out, 1.0001f, 0.5f, iters);
         cudaEventRecord(e1);
         cudaEventSynchronize(e1);
         float ms;
@@ -492,7 +543,7 @@ int usc_peak_fp32_muladd(int32_t device, double *tflops) {
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     cudaFree(out);
-    *tflops = (double)blocks * threads * iters * 8 * 2 / (best * 1e-3) / 1e12;
+    *tflops = (double)blocks * threads * iters * macs_per_iter * 2 / (best * 1e-3) / 1e12;
     return cuda_check("peak probe");
 }
 

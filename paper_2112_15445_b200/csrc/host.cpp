@@ -763,7 +763,7 @@ int usc_pack(const usc_plan *pl, const int64_t *row_ptr, const int64_t *col, con
     // one stored entry j of channel d -> (input channel, offset in the kernel's staged
     // tile), or off = -1 to drop it (a repeated zero-weight offset)
     const int64_t max_off = pl->dtype == USC_I8 ? (1 << 24) : (1 << 28);
-    std::vector<int64_t> zero_seen;
+    std::unordered_set<int64_t> zero_seen;  // distinct zero-weight offsets of the channel
     int64_t dec_kh = 0, dec_kw = 0;  // tap of the last decoded entry (plan orientation)
     auto decode = [&](int64_t j, int64_t *cpos, int64_t *off) -> int {
         const int64_t lam = col[j];
@@ -781,11 +781,10 @@ int usc_pack(const usc_plan *pl, const int64_t *row_ptr, const int64_t *col, con
         if (zero) {
             // a zero-weight entry only matters when x is non-finite, where one copy
             // per distinct offset already yields the NaN
-            if (std::find(zero_seen.begin(), zero_seen.end(), lam) != zero_seen.end()) {
+            if (!zero_seen.insert(lam).second) {
                 *off = -1;
                 return USC_OK;
             }
-            zero_seen.push_back(lam);
         }
         if (pl->transposed) std::swap(kh, kw);  // (c, kh, 0) -> (c, 0, kh)
         dec_kh = kh;
@@ -998,6 +997,8 @@ int usc_pack(const usc_plan *pl, const int64_t *row_ptr, const int64_t *col, con
 int usc_fit_fixed_point(double amax, int32_t total_bits, int32_t *int_bits, int32_t *frac_bits,
                         double *sigma) {
     if (total_bits < 2) return fail(USC_ERR_VALUE, "total_bits must be >= 2");
+    // the reference's math.ceil(log2(inf or nan)) raises (OverflowError / ValueError)
+    if (!std::isfinite(amax)) return fail(USC_ERR_VALUE, "cannot fit a fixed-point format to a non-finite maximum");
     int ib = amax == 0.0 ? 0 : (int)std::ceil(std::log2(amax));
     *int_bits = ib;
     *frac_bits = total_bits - ib - 1;

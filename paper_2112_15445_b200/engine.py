@@ -106,7 +106,15 @@ def plan_for(filt: CsrFilter, n: int, dtype: int, config: ExecConfig | None, pay
     sized from the filter itself: a plan at chunk length CC is packed dry to measure
     its densest (group, chunk) block, then re-planned with exactly that reserve; when
     input tile + entries no longer fit, CC shrinks until they do."""
-    plan = fit_plan(filt, n, dtype, config, payload, table)
+    config = config or ExecConfig()
+    # fitted plans are cached on the (immutable) filter, so a repeated call costs a
+    # dict lookup instead of two make_plan calls and a dry pack of the whole filter
+    key = (n, dtype, config, id(payload), None if table is None else np.asarray(table, np.float32).tobytes())
+    cache = filt._extra.setdefault("plans", {})
+    hit = cache.get(key)
+    if hit is None or hit[1] is not payload:
+        hit = cache[key] = (fit_plan(filt, n, dtype, config, payload, table), payload)
+    plan = hit[0]
     blob, _ = device_pack(filt, plan, payload, table, device)
     return plan, blob
 
@@ -230,7 +238,7 @@ def sparse_conv_forward(input: DenseTensor4, filt: CsrFilter,
     y = torch.empty((input.n, g.out_channels, g.out_h, g.out_w), dtype=_storage_dtype(dtype),
                     device=x.device)
     launch(plan, blob, x_pad, y)
-    return DenseTensor4(y, input.precision)
+    return DenseTensor4._adopt(y, input.precision)
 
 
 def sparse_conv_1d(input: DenseTensor4, filt: CsrFilter,
@@ -407,3 +415,24 @@ def autotune_sb(input: DenseTensor4, filt: CsrFilter, candidates=SB_CANDIDATES, 
                                   cfg.pixel_warps, cfg.stages, cfg.rows_per_thread, cfg.ent_reserve,
                                   cfg.pixel_classes)
     return ExecConfig(usable[0], worker_count)
+
+
+def autotune_native(input: DenseTensor4, filt: CsrFilter, repeats: int = 9, warmup: int = 2,
+                    noise_floor: float = 0.02, payload=None, table=None, dtype: int | None = None) -> ExecConfig:
+    """The tile search through the C ABI (usc_autotune): what a non-Python caller of
+    libunsparse_b200.so runs.  Same candidates and rule as autotune_sb
+    on the fp32 / binary16 path."""
+    dtype = dtype_of(input.precision) if dtype is None else dtype
+    x = input.device()
+    payload = filt.weights if payload is None else np.ascontiguousarray(payload)
+    tbl = None if table is None else np.ascontiguousarray(table, np.float32)
+    g = _lib.make_geometry(filt.geometry)
+    best = _lib.ExecCfg()
+    ms = ctypes.c_float(0.0)
+    _lib.check(_lib.lib().usc_autotune(_lib.ref(g), input.n, dtype, _lib.np_ptr(filt.row_ptr),
+                                       _lib.np_ptr(filt.col_offsets), _lib.np_ptr(payload), filt.n_nz,
+                                       None if tbl is None else _lib.np_ptr(tbl), _lib.t_ptr(x), repeats, warmup,
+                                       noise_floor, _lib.ref(best), _lib.ref(ms), _lib.stream_ptr()), "autotune")
+    return ExecConfig(best.sub_batch, best.worker_count, best.pix_per_thread, best.ch_per_cta,
+                      best.samples_per_cta, best.chunk_channels, best.kernel, best.threads, best.pixel_warps,
+                      best.stages, best.rows_per_thread, best.ent_reserve, best.pixel_classes)

@@ -63,6 +63,22 @@ def _cfg_of(plan, cfg: ExecConfig, il: int = 0) -> ExecConfig:
 MODES = ("fp32", "fp16", "int8", "cb4")
 
 
+def vgg16_layer_sequence(cfg=VGG16_CIFAR):
+    """The trunk as the reference's nn.Model layer list would index it (nn.py:150-200):
+    Conv2D, ReLU per conv, MaxPool2 per "M" -- act_hook(i, a) fires after layer i."""
+    out = []
+    for v in cfg:
+        out += [("pool",)] if v == "M" else [("conv",), ("relu",)]
+    return out
+
+
+def vgg16_hook_indices(cfg=VGG16_CIFAR):
+    """[(conv hook index, relu hook index)] per conv, in the reference's layer numbering."""
+    seq = vgg16_layer_sequence(cfg)
+    convs = [i for i, (k,) in enumerate(seq) if k == "conv"]
+    return [(i, i + 1) for i in convs]
+
+
 class SparseVGG16:
     """Pruned VGG-16 CIFAR-10 conv trunk on one GPU, for a fixed batch.
 
@@ -83,7 +99,8 @@ class SparseVGG16:
     """
 
     def __init__(self, weights, batch: int, precision=PrecisionMode.BINARY32, configs=None,
-                 device=None, mode: str | None = None, calibration=None, saturation: float = 0.99):
+                 device=None, mode: str | None = None, calibration=None, saturation: float = 0.99,
+                 maxima: dict | None = None, codebooks=None):
         import torch
         mode = mode or ("fp16" if precision is PrecisionMode.BINARY16 else "fp32")
         if mode not in MODES:
@@ -109,7 +126,8 @@ class SparseVGG16:
             self.payloads = [q.codes for q in self.qfilters]
         else:
             from .quantization import build_csr_codebook
-            self.qfilters = [build_csr_codebook(w, g) for w, g in zip(weights, self.geoms)]
+            cbs = codebooks if codebooks is not None else [None] * len(self.geoms)
+            self.qfilters = [build_csr_codebook(w, g, codebook=cb) for w, g, cb in zip(weights, self.geoms, cbs)]
             self.filters = [q.filt for q in self.qfilters]
             self.payloads = [q.indices for q in self.qfilters]
             self.tables = [q.table for q in self.qfilters]
@@ -117,7 +135,11 @@ class SparseVGG16:
         self.fuse_pool = {}  # per pool-feeding conv: fuse the pool into its epilogue (autotuned)
         self.saturation = saturation
         self.layer_params = [dict() for _ in self.geoms]
-        if mode in ("int8", "cb4"):
+        if mode == "cb4" and maxima is not None:  # calibrate_activation_maxima output
+            for li, (ci, ri) in enumerate(vgg16_hook_indices()):
+                self.layer_params[li].update(cap=float(np.float32(saturation * maxima[ci])),
+                                             cap2=float(np.float32(saturation * maxima[ri])))
+        elif mode in ("int8", "cb4"):
             if calibration is None:
                 raise ValueError(f"{mode} needs calibration inputs")
             self.calibrate(calibration)
@@ -146,12 +168,12 @@ class SparseVGG16:
         self.sigmas = []
         for li, g in enumerate(self.geoms):
             if self.mode == "int8":
-                xq = quantize_input_int8(DenseTensor4(a))
+                xq = quantize_input_int8(DenseTensor4._adopt(a))
                 self.sigmas.append(xq.params)
                 y = sparse_conv_forward_int8(xq, self.qfilters[li], relu=True).device()
                 a = y
             else:
-                conv = sparse_conv_forward(DenseTensor4(a), self.filters[li]).device()
+                conv = sparse_conv_forward(DenseTensor4._adopt(a), self.filters[li]).device()
                 relu = torch.where(conv > 0, conv, torch.zeros_like(conv))
                 cmax, rmax = float(conv.max().item()), float(relu.max().item())
                 self.layer_params[li].update(
@@ -308,13 +330,16 @@ class SparseVGG16:
             self.run()
         return self.output()
 
-    def stream_forward(self, x_hosts, out_hosts):
+    def stream_forward(self, x_hosts, out_hosts, collect=None):
         """Inference over a stream of host batches with the transfers overlapped: the
         H2D copy of batch i+1 (copy stream) and the D2H copy of batch i-1 (drain
         stream) run while batch i computes (current stream, CUDA graph when captured).
         x_hosts / out_hosts: pinned host tensors, (n,3,32,32) in / (n,512,1,1) out.
-        Returns after enqueueing everything; synchronise the current stream (or the
-        returned event) before reading out_hosts."""
+        ``collect`` (batch-sharded jobs): maps each batch's device features to the
+        tensor to copy out -- e.g. ShardedRun.gather, the final all_gather -- or to
+        None on ranks that keep nothing.  Returns after enqueueing everything;
+        synchronise the current stream (or the returned event) before reading
+        out_hosts."""
         import torch
         cur = torch.cuda.current_stream(self.device)
         if not hasattr(self, "_sf"):
@@ -356,10 +381,16 @@ class SparseVGG16:
             _lib.check(_lib.lib().usc_unpad_output(_lib.ref(self.out_layout), odt, self.batch,
                                                    _lib.t_ptr(self.out_buf), _lib.t_ptr(sf["outd"][b]),
                                                    _lib.stream_ptr(cur)), "unpad")
+            src = sf["outd"][b]
+            if collect is not None:
+                src = collect(src)
+                if src is not None:  # allocated on this stream, read by the drain stream
+                    src.record_stream(sf["d2h"])
             out_ready[b].record(cur)
             sf["d2h"].wait_event(out_ready[b])
             with torch.cuda.stream(sf["d2h"]):
-                out_hosts[i].copy_(sf["outd"][b], non_blocking=True)
+                if src is not None:
+                    out_hosts[i].copy_(src, non_blocking=True)
                 out_free[b].record(sf["d2h"])
         done = torch.cuda.Event()
         cur.wait_stream(sf["d2h"])

@@ -10,8 +10,10 @@ The quantised sparse conv variants the reference only defines by composition
 
 * int8: ``build_csr_int8`` + ``quantize_input_int8`` + ``sparse_conv_forward_int8``
   equal the reference composition ``sparse_conv_forward(linear_quantize(x),
-  build_csr(linear_quantize(w)))`` bitwise (int32 accumulation of the codes,
-  one exact power-of-two rescale), whenever max_d sum|k_w| * max|k_x| < 2**24;
+  build_csr(linear_quantize(w)))`` bitwise: the batch-interleaved kernel (the
+  default) accumulates the code products in fp32 in the reference's order and
+  rescales once by a power of two; kernel 1 accumulates in int32, which equals
+  the composition whenever max_d sum|k_w| * max|k_x| < 2**24;
 * 4b/16b: ``build_csr_codebook`` + ``sparse_conv_forward_codebook`` store a
   4-bit centroid index per entry, decode through a 16-entry fp32 table in shared
   memory, accumulate fp32 in reference order and apply the 4b/16b activation hook
@@ -24,13 +26,13 @@ import ctypes
 import json
 import math
 import warnings
-from dataclasses import dataclass
+from dataclasses import dataclass, field
 
 import numpy as np
 
 from . import _lib
 from .csr import CsrFilter, build_csr
-from .engine import ExecConfig, launch, padded_input, plan_for
+from .engine import ExecConfig, launch, padded_input, plan_for, sparse_conv_forward
 from .tensor import ConvGeometry, DenseTensor4, PrecisionMode, round_to_binary16
 
 MODES = ("passthrough", "16b/16b", "4b/16b")
@@ -181,6 +183,7 @@ class Int8CsrFilter:
     filt: CsrFilter
     codes: np.ndarray
     params: FixedPointParams
+    weight_bound: int = field(default=-1, repr=False)  # max_d sum|k_w| (cached)
 
     @property
     def geometry(self) -> ConvGeometry:
@@ -205,10 +208,10 @@ class Int8Tensor:
 
 def build_csr_int8(dense_weights: DenseTensor4, geometry: ConvGeometry, total_bits: int = 8,
                    params: FixedPointParams | None = None) -> Int8CsrFilter:
-    if total_bits > 8:
-        raise ValueError("int8 path needs total_bits <= 8")
     w = dense_weights.data
     params = params or fit_fixed_point(w, total_bits)
+    if params.total_bits > 8:  # codes above 127 would wrap in the int8 payload
+        raise ValueError(f"int8 path needs total_bits <= 8, got params with {params.total_bits}")
     wq = linear_quantize(w, params)
     filt = build_csr(DenseTensor4.from_array(wq), geometry)
     codes = np.rint(filt.weights.astype(np.float64) / params.sigma)
@@ -222,22 +225,30 @@ def quantize_input_int8(x: DenseTensor4, total_bits: int = 8,
     """Fixed-point codes of the activations (fit_fixed_point + linear_quantize,
     quantization.py:41-76), quantised on the device."""
     import torch
-    if total_bits > 8:
-        raise ValueError("int8 path needs total_bits <= 8")
     src = x.device() if isinstance(x, DenseTensor4) else x
     src = src.to(torch.float32).contiguous()
     params = params or fit_fixed_point(src, total_bits)
+    if params.total_bits > 8:
+        raise ValueError(f"int8 path needs total_bits <= 8, got params with {params.total_bits}")
     codes = torch.empty(src.shape, dtype=torch.int8, device=src.device)
+    # clip to the params' own code range, exactly as linear_quantize(x, params)
     _lib.check(_lib.lib().usc_quantize_i8(_lib.t_ptr(src), _lib.t_ptr(codes), src.numel(),
-                                          params.sigma, total_bits, _lib.stream_ptr()), "quantize")
+                                          params.sigma, params.total_bits, _lib.stream_ptr()), "quantize")
     return Int8Tensor(codes, params)
 
 
-def int8_exact_bound(fq: Int8CsrFilter, xq: Int8Tensor) -> int:
+def int8_exact_bound(fq: Int8CsrFilter, xq: Int8Tensor, exact: bool = False) -> int:
     """max_d sum_j |k_w| * max|k_x|: below 2**24 every partial sum of the fp32
-    reference composition is exact, so the int8 kernel equals it bitwise."""
-    per = np.abs(fq.codes.astype(np.int64)).reshape(fq.geometry.out_channels, -1).sum(axis=1)
-    return int(per.max()) * int(xq.codes.abs().max().item())
+    reference composition is an exact integer.  Without ``exact`` the activation
+    factor is the code limit 2**(bits-1)-1 (no device read); with it, the
+    measured max|k_x| (one device->host sync)."""
+    if fq.weight_bound < 0:
+        fq.weight_bound = int(np.abs(fq.codes.astype(np.int64)).reshape(fq.geometry.out_channels, -1)
+                              .sum(axis=1).max())
+    per = fq.weight_bound
+    if exact:
+        return per * int(xq.codes.abs().max().item())
+    return per * (2 ** (xq.params.total_bits - 1) - 1)
 
 
 def sparse_conv_forward_int8(xq: Int8Tensor, fq: Int8CsrFilter, config: ExecConfig | None = None,
@@ -251,17 +262,19 @@ def sparse_conv_forward_int8(xq: Int8Tensor, fq: Int8CsrFilter, config: ExecConf
     n = xq.n
     if n % config.sub_batch:
         raise ValueError(f"sub_batch {config.sub_batch} does not divide batch {n}")
-    if int8_exact_bound(fq, xq) >= 2 ** 24:
-        warnings.warn("int8 partial sums exceed 2**24: the fp32 reference composition rounds, "
-                      "this kernel is exact", RuntimeWarning)
     plan, blob = plan_for(fq.filt, n, _lib.USC_I8, config, fq.codes)
+    if plan.kernel == 1 and int8_exact_bound(fq, xq) >= 2 ** 24 and int8_exact_bound(fq, xq, True) >= 2 ** 24:
+        # kernel 3 accumulates the code products in fp32 in the reference's order (equal to
+        # the composition at any magnitude); kernel 1 accumulates in exact int32
+        warnings.warn("int8 partial sums exceed 2**24: the fp32 reference composition rounds, "
+                      "kernel 1 accumulates exactly in int32 and may differ from it", RuntimeWarning)
     x_pad = padded_input(xq.codes, plan)
     y = torch.empty((n, g.out_channels, g.out_h, g.out_w), dtype=torch.float32, device=x_pad.device)
     epi = _lib.Epilogue()
     epi.relu = 1 if relu else 0
     epi.scale = float(np.float32(fq.params.sigma * xq.params.sigma))
     launch(plan, blob, x_pad, y, epi)
-    return DenseTensor4(y, PrecisionMode.BINARY32)
+    return DenseTensor4._adopt(y, PrecisionMode.BINARY32)
 
 
 # ---------------------------------------------------------------------------
@@ -325,4 +338,101 @@ def sparse_conv_forward_codebook(x: DenseTensor4, fc: CodebookCsrFilter,
         epi.saturate = 1
         epi.cap = float(np.float32(saturation * float(calibrated_max)))
     launch(plan, blob, x_pad, y, epi)
-    return DenseTensor4(y, PrecisionMode.BINARY16)
+    return DenseTensor4._adopt(y, PrecisionMode.BINARY16)
+
+
+# ---------------------------------------------------------------------------
+# whole-model quantisation (quantization.py:221-301) for the VGG-16 trunk
+
+def calibrate_activation_maxima(model, X_val, batch_size: int = 64) -> dict:
+    """quantization.py:223-235: per-layer activation maxima over one validation pass,
+    keyed by the reference's layer index (Conv2D, ReLU, MaxPool2 each count,
+    models.vgg16_layer_sequence).  ``model``: a QuantizedModel, a SparseVGG16 or the
+    list of pruned conv weights; the pass runs the layers eagerly on the GPU through
+    sparse_conv_forward in binary32 without hooks (the reference records, it does not
+    modify)."""
+    import torch
+    from .models import VGG16_CIFAR, vgg16_geometries, vgg16_layer_sequence
+    if isinstance(model, QuantizedModel):
+        weights = model.weights
+    elif hasattr(model, "filters") and hasattr(model, "geoms"):
+        weights = None
+        filters = [getattr(q, "filt", q) for q in getattr(model, "qfilters", model.filters)]
+    else:
+        weights = model
+    if weights is not None:
+        filters = [build_csr(w if isinstance(w, DenseTensor4) else DenseTensor4.from_array(w), g)
+                   for w, g in zip(weights, vgg16_geometries())]
+    filters = [f if f.precision is PrecisionMode.BINARY32 else
+               CsrFilter(f.row_ptr, f.col_offsets, f.weights, f.n_nz, f.geometry) for f in filters]
+    seq = vgg16_layer_sequence(VGG16_CIFAR)
+    xs = X_val if type(X_val).__module__.startswith("torch") else torch.from_numpy(np.asarray(X_val, np.float32))
+    maxima = {}
+    for start in range(0, xs.shape[0], batch_size):
+        a = xs[start:start + batch_size].to("cuda", torch.float32)
+        li = 0
+        for i, (kind,) in enumerate(seq):
+            if kind == "conv":
+                a = sparse_conv_forward(DenseTensor4._adopt(a.contiguous()), filters[li]).device()
+                li += 1
+            elif kind == "relu":
+                a = torch.where(a > 0, a, torch.zeros_like(a))
+            else:
+                a = torch.nn.functional.max_pool2d(a, 2)
+            m = float(a.max().item()) if a.numel() else 0.0
+            maxima[i] = max(maxima.get(i, -np.inf), m)
+    return maxima
+
+
+@dataclass
+class QuantizedModel:
+    """quantization.py:247-254: the quantised pruned weights plus what the activation
+    hook needs (calibrated maxima, saturation), and the codebooks of 4b/16b."""
+
+    weights: list
+    mode: str
+    maxima: dict | None = None
+    codebooks: list | None = None
+    saturation: float = 0.99
+
+    def network(self, batch: int, device=None, configs=None, calibration=None):
+        """The fused sparse VGG-16 trunk for this model (passthrough -> fp32,
+        16b/16b -> binary16, 4b/16b -> codebook weights + _half_hook epilogues)."""
+        from .models import SparseVGG16
+        net_mode = {"passthrough": "fp32", "16b/16b": "fp16", "4b/16b": "cb4"}[self.mode]
+        prec = PrecisionMode.BINARY16 if net_mode == "fp16" else PrecisionMode.BINARY32
+        return SparseVGG16(self.weights, batch, precision=prec, configs=configs, device=device, mode=net_mode,
+                           calibration=calibration, saturation=self.saturation, maxima=self.maxima,
+                           codebooks=self.codebooks)
+
+
+def quantize_model(pruned, mode: str, calibration=None, omega: int = 16, psi: int = 16,
+                   saturation: float = 0.99) -> QuantizedModel:
+    """quantization.py:257-301 for the pruned VGG-16 trunk (``pruned``: its conv
+    weights, DenseTensor4 or arrays, in network order).
+
+    passthrough: binary32 copy.  16b/16b: weights rounded to binary16 (every
+    activation is then rounded after each layer by the network's epilogue).
+    4b/16b: each prunable weight tensor shared across ``omega`` zero-pinned
+    centroids (psi-bit fixed point, kept in binary32), activations binary16 with
+    saturation at ``saturation`` x the calibrated per-layer maximum; ``calibration``
+    supplies the inputs of the calibration pass.  Masked positions stay zero."""
+    if mode not in MODES:
+        raise ValueError(f"unknown mode {mode!r}; expected one of {MODES}")
+    ws = [np.array(w.data if isinstance(w, DenseTensor4) else w, dtype=np.float32) for w in pruned]
+    masks = [w != 0 for w in ws]
+    if mode == "passthrough":
+        return QuantizedModel([DenseTensor4.from_array(w) for w in ws], mode, saturation=saturation)
+    if mode == "16b/16b":
+        return QuantizedModel([DenseTensor4.from_array(w * m, PrecisionMode.BINARY16) for w, m in zip(ws, masks)],
+                              mode, saturation=saturation)
+    if calibration is None:
+        raise ValueError("4b/16b needs calibration inputs")
+    codebooks, qws = [], []
+    for w, m in zip(ws, masks):
+        cb = kmeans_codebook(w, omega, psi)
+        codebooks.append(cb)
+        qws.append(DenseTensor4.from_array(cb.reconstruct(w.shape) * m))
+    qm = QuantizedModel(qws, mode, codebooks=codebooks, saturation=saturation)
+    qm.maxima = calibrate_activation_maxima(qm, calibration)
+    return qm

@@ -214,6 +214,21 @@ class SparseResNet50:
         self.graph = g
         return g
 
+    # -- tuned state (per-conv tiles) -------------------------------------------------
+    def tuned_state(self) -> dict:
+        import dataclasses
+        return {"configs": [dataclasses.asdict(c) for c in self.configs]}
+
+    def load_tuned_state(self, state) -> None:
+        """Accepts tuned_state() output (or a bare list of ExecConfig dicts)."""
+        if isinstance(state, dict):
+            state = state["configs"]
+        if len(state) != len(self.layers):
+            raise ValueError(f"tuned state has {len(state)} configs for {len(self.layers)} convs")
+        self.configs = [ExecConfig(**c) for c in state]
+        self.graph = None
+        self._build()
+
     def autotune(self, repeats: int = 3, warmup: int = 1, noise_floor: float = 0.02):
         """Per-conv tile search on the network's own buffers and epilogues."""
         import torch

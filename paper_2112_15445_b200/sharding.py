@@ -46,3 +46,57 @@ def gather_shards(local, n: int, group=None, align: int = 1):
     bufs = [torch.empty_like(pad) for _ in range(world)]
     dist.all_gather(bufs, pad, group=group)
     return torch.cat([b[:s] for b, s in zip(bufs, sizes)], dim=0)
+
+
+class ShardedRun:
+    """One rank's view of a batch-sharded inference job.
+
+    ``global_batch`` samples are split into contiguous per-rank slices
+    (``shard_range``); each rank runs ``forward`` (its own replica of the
+    network: CSR packs replicated, no exchange on the hot path) over its slice
+    and the per-rank outputs are concatenated in rank order by one final
+    ``gather_shards``.  ``weak`` mode fixes the per-rank batch instead
+    (``global_batch = world * per_rank``).  Mirrors the reference's partition of
+    the work into independent virtual blocks (engine.py:53-61): sample groups
+    never interact, so the gathered result equals the single-process one bit for
+    bit."""
+
+    def __init__(self, global_batch: int, rank: int = 0, world: int = 1, align: int = 1,
+                 group=None):
+        self.global_batch, self.rank, self.world, self.align = global_batch, rank, world, align
+        self.group = group
+        self.start, self.stop = shard_range(global_batch, rank, world, align)
+
+    @classmethod
+    def from_env(cls, global_batch: int, align: int = 1, group=None) -> "ShardedRun":
+        """Rank and world size from torch.distributed when it is initialised (else 1 rank)."""
+        import torch.distributed as dist
+        if dist.is_available() and dist.is_initialized():
+            return cls(global_batch, dist.get_rank(group), dist.get_world_size(group), align, group)
+        return cls(global_batch, 0, 1, align, group)
+
+    @classmethod
+    def weak(cls, per_rank: int, rank: int = 0, world: int = 1, group=None) -> "ShardedRun":
+        return cls(per_rank * world, rank, world, per_rank, group)
+
+    @property
+    def local_batch(self) -> int:
+        return self.stop - self.start
+
+    def local(self, x):
+        """This rank's rows of a global batch (dim 0)."""
+        if x.shape[0] != self.global_batch:
+            raise ValueError(f"global input has {x.shape[0]} rows, expected {self.global_batch}")
+        return x[self.start:self.stop]
+
+    def gather(self, local_out):
+        """The final (and only) collective: every rank's output rows, in rank order."""
+        if self.world == 1:
+            if local_out.shape[0] != self.global_batch:
+                raise ValueError("local output does not cover the batch")
+            return local_out
+        return gather_shards(local_out, self.global_batch, self.group, self.align)
+
+    def run(self, x_global, forward):
+        """gather(forward(local(x_global)))."""
+        return self.gather(forward(self.local(x_global)))

@@ -146,6 +146,19 @@ def layer_case(name, geometry, sparsity, batch, precision=F32, seed=0):
     return x, weights
 
 
+def csr_file_digests(filt):
+    """sha256 of the bytes the reference's save_csr writes (binary + JSON sidecar)."""
+    import tempfile
+    with tempfile.TemporaryDirectory() as d:
+        path = os.path.join(d, "filt.csr")
+        RC.save_csr(filt, path)
+        with open(path, "rb") as fh:
+            binary = hashlib.sha256(fh.read()).hexdigest()
+        with open(path + ".json", "rb") as fh:
+            sidecar = hashlib.sha256(fh.read()).hexdigest()
+    return dict(binary=binary, sidecar=sidecar)
+
+
 def layer_records():
     recs = {}
     specs = [
@@ -166,7 +179,8 @@ def layer_records():
         filt = U.build_csr(w, g)
         out = U.sparse_conv_forward(x, filt, U.ExecConfig(1)).data
         recs[name] = dict(geometry=geom_tuple(g), sparsity=s, batch=n, binary16=prec is F16,
-                          x=sha(x.data), w=sha(w.data), csr=csr_record(filt), out=sha(out))
+                          x=sha(x.data), w=sha(w.data), csr=csr_record(filt), out=sha(out),
+                          csr_file=csr_file_digests(filt))
     return recs
 
 

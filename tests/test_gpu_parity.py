@@ -453,3 +453,19 @@ def test_conv_gradients_vgg_layer_vs_oracle():
     dxpad = torch.empty(xpad.shape, device="cuda")
     T.conv_grad_input(torch.from_numpy(w).cuda(), torch.from_numpy(dout).cuda(), dxpad, 1, 1)
     assert np.array_equal(dxpad.cpu().numpy(), oracle.conv_grad_input(w, dout, xpad.shape, 1, 1, threads=4))
+
+
+@pytest.mark.parametrize("name", ["cfg1-vgg16-256x8", "cfg1-vgg16-256x8-f16", "resnet50-1x1-64x256"])
+def test_native_autotune_c_abi(name):
+    """usc_autotune (the C-ABI tile search, engine.py:139-170): its pick runs and is
+    bitwise equal to the reference's output."""
+    from paper_2112_15445_b200.engine import autotune_native
+    rec = golden()["layers"][name]
+    g = geom(rec["geometry"])
+    prec = F16 if rec["binary16"] else F32
+    x, w = layer_inputs(name, g, rec["sparsity"], rec["batch"], binary16=rec["binary16"])
+    f = U.build_csr(U.DenseTensor4.from_array(w, prec), G(rec["geometry"]))
+    xd = _dev(x, prec)
+    cfg = autotune_native(xd, f, repeats=3, warmup=1)
+    assert cfg.kernel in (1, 3)
+    assert sha(U.sparse_conv_forward(xd, f, cfg).data) == rec["out"]

@@ -5,6 +5,8 @@ import os
 import re
 import subprocess
 
+import hashlib
+
 import numpy as np
 import pytest
 
@@ -104,16 +106,42 @@ def test_geometry_errors():
         U.ExecConfig(3).block_count(8, 4)
 
 
-def test_save_load_csr_byte_compatible(tmp_path):
-    rec = golden()["layers"]["cfg1-vgg16-256x8"]
+@pytest.mark.parametrize("name", sorted(golden()["layers"]))
+def test_save_load_csr_byte_compatible(tmp_path, name):
+    """save_csr writes exactly the bytes the reference's save_csr writes (binary and
+    JSON sidecar; sha256 recorded by make_golden.py), and load_csr reads them back."""
+    rec = golden()["layers"][name]
     g = geom(rec["geometry"])
-    _, w = layer_inputs("cfg1-vgg16-256x8", g, rec["sparsity"], rec["batch"])
-    f = U.build_csr(U.DenseTensor4.from_array(w), G(rec["geometry"]))
+    prec = U.PrecisionMode.BINARY16 if rec["binary16"] else U.PrecisionMode.BINARY32
+    _, w = layer_inputs(name, g, rec["sparsity"], rec["batch"], binary16=rec["binary16"])
+    f = U.build_csr(U.DenseTensor4.from_array(w, prec), G(rec["geometry"]))
     U.save_csr(f, tmp_path / "f.csr")
+    assert hashlib.sha256((tmp_path / "f.csr").read_bytes()).hexdigest() == rec["csr_file"]["binary"]
+    assert hashlib.sha256((tmp_path / "f.csr.json").read_bytes()).hexdigest() == rec["csr_file"]["sidecar"]
     f2 = U.load_csr(tmp_path / "f.csr")
     assert f2.n_nz == f.n_nz and np.array_equal(f2.col_offsets, f.col_offsets)
     assert np.array_equal(f2.weights, f.weights) and f2.geometry == f.geometry
-    assert abs(U.effective_sparsity(f) - 0.9) < 1e-3
+    assert f2.precision is prec
+
+
+def test_save_csr_lossless_codebook_weights(tmp_path):
+    """4b/16b weights (16-bit fixed-point centroids) survive a BINARY16 filter's
+    save/load only with lossless=True (f4 payload, tag 2)."""
+    rng = np.random.default_rng(5)
+    g = U.ConvGeometry(16, 8, 3, 3, 6, 6, padding=(1, 1))
+    w = rng.standard_normal((8, 16, 3, 3)).astype(np.float32)
+    w[rng.random(w.shape) < 0.8] = 0.0
+    cb = U.kmeans_codebook(w, 16, 16)
+    wc = cb.reconstruct(w.shape)
+    f = U.CsrFilter(*(lambda t: (t.row_ptr, t.col_offsets, t.weights, t.n_nz))(
+        U.build_csr(U.DenseTensor4.from_array(wc), g)), g, U.PrecisionMode.BINARY16)
+    assert not np.array_equal(f.weights.astype(np.float16).astype(np.float32), f.weights)
+    U.save_csr(f, tmp_path / "lossy.csr")
+    U.save_csr(f, tmp_path / "lossless.csr", lossless=True)
+    lossy, lossless = U.load_csr(tmp_path / "lossy.csr"), U.load_csr(tmp_path / "lossless.csr")
+    assert not np.array_equal(lossy.weights, f.weights)
+    assert np.array_equal(lossless.weights, f.weights)
+    assert lossless.precision is U.PrecisionMode.BINARY16
 
 
 def test_quantisation_primitives_match_golden():

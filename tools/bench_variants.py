@@ -35,6 +35,26 @@ def measured_hbm_peak() -> float:
     return 6650.0
 
 
+OUT_DIR = os.environ.get("TUNED_OUT", "gpurun_out")
+
+
+def dump_state(name, state):
+    """Tuned tiles of a variant -> <TUNED_OUT>/r02_tuned_<name>.json (committed under
+    profiles/ so the -m gpu parity tests run exactly the benchmarked plans)."""
+    os.makedirs(OUT_DIR, exist_ok=True)
+    with open(os.path.join(OUT_DIR, f"r02_tuned_{name}.json"), "w") as fh:
+        json.dump(state, fh)
+
+
+def load_state(name):
+    p = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles",
+                     f"r02_tuned_{name}.json")
+    if os.environ.get("RETUNE") or not os.path.exists(p):
+        return None
+    with open(p) as fh:
+        return json.load(fh)
+
+
 def timed(fn, steps, flush=None):
     for _ in range(3):
         fn()
@@ -78,7 +98,12 @@ def vgg16_fp16(steps):
     batch = 256
     ws = vgg16_weights(vgg16_rng(0.93, 0), 0.93, precision=PrecisionMode.BINARY16)
     m = SparseVGG16(ws, batch, precision=PrecisionMode.BINARY16)
-    m.autotune(repeats=3, warmup=1)
+    st = load_state("vgg16_fp16")
+    if st:
+        m.load_tuned_state(st)
+    else:
+        m.autotune(repeats=3, warmup=1)
+        dump_state("vgg16_fp16", m.tuned_state())
     m.capture()
     m.load_input(torch.randn(batch, 3, 32, 32, device="cuda").half())
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
@@ -100,7 +125,12 @@ def vgg16_quantised(mode, steps):
     if mode == "cb4":
         x = round_to_binary16(x)
     m = SparseVGG16(ws, batch, mode=mode, calibration=x)
-    m.autotune(repeats=3, warmup=1)
+    st = load_state(f"vgg16_{mode}")
+    if st:
+        m.load_tuned_state(st)
+    else:
+        m.autotune(repeats=3, warmup=1)
+        dump_state(f"vgg16_{mode}", m.tuned_state())
     m.capture()
     m.load_input(x if mode == "int8" else x.half())
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
@@ -212,7 +242,12 @@ def resnet50_network(prec_name, steps, batch=256, sparsity=0.9):
     tdt = torch.float16 if prec_name == "fp16" else torch.float32
     ws = resnet50_weights(sparsity, 0, prec)
     m = SparseResNet50(ws, batch, precision=prec)
-    m.autotune()
+    st = load_state(f"resnet50_{prec_name}")
+    if st:
+        m.load_tuned_state(st)
+    else:
+        m.autotune()
+        dump_state(f"resnet50_{prec_name}", m.tuned_state())
     m.capture()
     m.load_input(torch.randn(batch, 3, 32, 32, device="cuda").to(tdt))
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
@@ -258,7 +293,8 @@ def sweep(steps, shapes=None, sparsities=(0.5, 0.7, 0.9, 0.95, 0.98)):
     from paper_2112_15445_b200.engine import launch, padded_input, plan_for, tile_candidates, time_median_cuda
     from paper_2112_15445_b200.pruning import synthesize_masked_weights
     from paper_2112_15445_b200.tensor import ConvGeometry
-    out = []
+    import dataclasses
+    out, tiles = [], {}
     batch = 1024
     for name, (c, d, k, hw) in SWEEP_SHAPES.items():
         if shapes and name not in shapes:
@@ -287,7 +323,9 @@ def sweep(steps, shapes=None, sparsities=(0.5, 0.7, 0.9, 0.95, 0.98)):
                 if best is None or t < best[0]:
                     best = (t, cand)
                 f._packs.clear()
-            plan, blob = plan_for(f, batch, 0, best[1] if best else cfg, f.weights)
+            pick = best[1] if best else cfg
+            tiles[f"{name}@{s}"] = dataclasses.asdict(pick)
+            plan, blob = plan_for(f, batch, 0, pick, f.weights)
             xp = pads.get((plan.in_.interleave, plan.in_.hp, plan.in_.ws)) if plan.kernel in (3, 4) else None
             xp = xp if xp is not None else padded_input(x, plan)
             ms = time_median_cuda(_resident_launch(plan, blob, xp, d, g, batch, torch.float32), 9, 2)
@@ -308,6 +346,8 @@ def sweep(steps, shapes=None, sparsities=(0.5, 0.7, 0.9, 0.95, 0.98)):
                         "hbm_frac": round(nbytes / (ms / 1e3) / 1e9 / measured_hbm_peak(), 3),
                         "cudnn_fp32_us": round(cd * 1e3, 1), "speedup_vs_cudnn": round(cd / ms, 3),
                         "plan": plan.describe()})
+    if not shapes:
+        dump_state("sweep", tiles)
     return out
 
 
