@@ -92,6 +92,10 @@ typedef struct usc_exec_cfg {
     int32_t ent_reserve;      /* kernel 3: shared-memory bytes reserved per stage for CSR entries (0 auto) */
     int32_t pixel_classes;    /* kernel 3, 1x1 pixel blocks: 1 = per-pixel-class entry runs that drop
                                * the taps landing on the zero halo (exact for finite weights) */
+    int32_t window;           /* kernel 3: 1 = register-window variant (k_bw): one output row of
+                               * pix_per_thread pixels per thread, the warp's ch_per_cta/warps slots
+                               * share one entry stream ordered by input row, each x window loaded
+                               * into registers once per (c, kh); stride 1, F32/F16, filter_w 1 or 3 */
 } usc_exec_cfg;
 
 /* Resolved plan for one (geometry, batch, dtype, cfg): tile shape, packing
@@ -117,6 +121,7 @@ typedef struct usc_plan {
                                   * 1 x 1 = no classes */
     int32_t tail_full, tail_split;  /* BI kernel: tiles [0, tail_full) run whole, each later tile as
                                      * tail_split slot-subset items (balances the last wave) */
+    int32_t window;              /* BI kernel: register-window variant (usc_exec_cfg.window) */
     int64_t smem_stage_bytes, smem_bytes;
     int64_t grid_x, grid_y;
 } usc_plan;
@@ -210,6 +215,10 @@ int usc_plan_make(const usc_geometry *g, int32_t n, int32_t dtype, const usc_exe
  * returns the total count.  The autotuner's kernel-3 search space (threads =
  * warps*32, samples_per_cta = 32*samples per lane). */
 int usc_bi_instances(int32_t *out, int32_t max_count);
+/* The register-window variant's compiled tiles (usc_exec_cfg.window = 1): up to
+ * max_count records of 5 int32 (family 0 fp32 / 1 binary16, compute warps, PC, DW,
+ * filter width); returns the total count. */
+int usc_bw_instances(int32_t *out, int32_t max_count);
 int usc_pack_size(const usc_plan *plan, int64_t n_nz, int64_t *bytes);
 /* autotune_sb (engine.py:139-170) behind the C ABI: plans, packs and times every
  * tile candidate of the layer (the batch-interleaved kernel's compiled instances x
@@ -269,6 +278,16 @@ int usc_sparse_conv_blocks(const float *xflat, const int64_t *row_ptr, const int
                            const float *theta, float *out, const int64_t *blocks, int64_t n_blocks,
                            int32_t sb, int64_t x_size, int32_t s_h, int32_t s_w, int32_t padded_w,
                            int32_t D, int32_t out_h, int32_t out_w, void *stream);
+/* Layout transposes for the per-layer sparse/dense backend dispatcher (bench.py:212-227,
+ * pipeline.py:381-389): a layer run on cuDNN reads the network's resident BI64 binary16
+ * layout `l` as NHWC [n][H][W][C] (usc_bi_to_nhwc) and its NHWC binary16 output is
+ * written back into `l`'s interior (usc_nhwc_to_bi) with the epilogue fused:
+ * v = sat16(y); with a shortcut (`res` in `res_layout`, same logical shape)
+ * v = sat16(v + r) (binary16 add); ReLU where(v > 0, v, 0) when relu != 0.
+ * BI64 layouts with channels % 16 == 0 only. */
+int usc_bi_to_nhwc(const usc_act_layout *l, int32_t n, const void *src, void *dst, void *stream);
+int usc_nhwc_to_bi(const usc_act_layout *l, int32_t n, const void *src, void *dst, const usc_act_layout *res_layout,
+                   const void *res, int32_t relu, void *stream);
 /* round_to_binary16 (tensor.py:48-63) on device: f32 in -> f32 on the binary16 grid
  * (to_half == 0) or binary16 storage (to_half == 1). */
 int usc_round_binary16(const float *src, void *dst, int64_t count, int32_t to_half, void *stream);

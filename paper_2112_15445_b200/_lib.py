@@ -43,7 +43,7 @@ class ExecCfg(ctypes.Structure):
     _fields_ = [(n, c_i32) for n in ("sub_batch", "worker_count", "pix_per_thread", "ch_per_cta",
                                      "samples_per_cta", "chunk_channels", "threads", "kernel",
                                      "pixel_warps", "stages", "rows_per_thread", "ent_reserve",
-                                     "pixel_classes")]
+                                     "pixel_classes", "window")]
 
 
 class Plan(ctypes.Structure):
@@ -54,12 +54,13 @@ class Plan(ctypes.Structure):
                 ("groups", c_i32), ("n_chunks", c_i32), ("WS", c_i32), ("WC", c_i32), ("DW", c_i32),
                 ("SPRt", c_i32), ("col_tiles", c_i32), ("TWs", c_i32), ("ent_stage_bytes", c_i32), ("stages", c_i32), ("PR", c_i32), ("PC", c_i32),
                 ("transposed", c_i32), ("ncls_r", c_i32), ("ncls_c", c_i32), ("tail_full", c_i32),
-                ("tail_split", c_i32),
+                ("tail_split", c_i32), ("window", c_i32),
                 ("smem_stage_bytes", c_i64), ("smem_bytes", c_i64), ("grid_x", c_i64),
                 ("grid_y", c_i64)]
 
     def describe(self) -> dict:
-        return dict(kernel={1: "tiled", 2: "generic", 3: f"bi{self.NS}", 4: "bt64"}[self.kernel], P=self.P, DT=self.DT,
+        kern = {1: "tiled", 2: "generic", 3: f"bw{self.NS}" if self.window else f"bi{self.NS}", 4: "bt64"}[self.kernel]
+        return dict(kernel=kern, P=self.P, DT=self.DT,
                     NS=self.NS, CC=self.CC, TH=self.TH, threads=self.threads, WS=self.WS,
                     WC=self.WC, DW=self.DW, PR=self.PR, PC=self.PC, stages=self.stages,
                     grid=(self.grid_x, self.grid_y), smem_bytes=self.smem_bytes,
@@ -98,12 +99,15 @@ _SIGS = {
     "usc_csr_to_dense": (c_i32, [c_ptr, c_ptr, c_ptr, c_ptr, c_i64, c_ptr]),
     "usc_plan_make": (c_i32, [c_ptr, c_i32, c_i32, c_ptr, c_ptr]),
     "usc_bi_instances": (c_i32, [c_ptr, c_i32]),
+    "usc_bw_instances": (c_i32, [c_ptr, c_i32]),
     "usc_pack_size": (c_i32, [c_ptr, c_i64, c_ptr]),
     "usc_autotune": (c_i32, [c_ptr, c_i32, c_i32, c_ptr, c_ptr, c_ptr, c_i64, c_ptr, c_ptr, c_i32, c_i32,
                              ctypes.c_float, c_ptr, c_ptr, c_ptr]),
     "usc_pack": (c_i32, [c_ptr, c_ptr, c_ptr, c_ptr, c_i64, c_ptr, c_ptr, c_i64, c_ptr]),
     "usc_pad_input": (c_i32, [c_ptr, c_i32, c_i32, c_ptr, c_ptr, c_ptr]),
     "usc_unpad_output": (c_i32, [c_ptr, c_i32, c_i32, c_ptr, c_ptr, c_ptr]),
+    "usc_bi_to_nhwc": (c_i32, [c_ptr, c_i32, c_ptr, c_ptr, c_ptr]),
+    "usc_nhwc_to_bi": (c_i32, [c_ptr, c_i32, c_ptr, c_ptr, c_ptr, c_ptr, c_i32, c_ptr]),
     "usc_conv_forward": (c_i32, [c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr]),
     "usc_conv_forward_view": (c_i32, [c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr]),
     "usc_conv_forward_strided": (c_i32, [c_ptr, c_ptr, c_ptr, c_ptr, c_i32, c_i32, c_ptr, c_ptr, c_ptr]),
@@ -152,6 +156,16 @@ def bi_instances(binary16: bool = False, tmem: bool = False) -> list[tuple[int, 
     L.usc_bi_instances(buf, n)
     kind = 2 if tmem else int(binary16)
     return [tuple(buf[7 * i:7 * i + 6]) for i in range(n) if buf[7 * i + 6] == kind]
+
+
+def bw_instances() -> list[tuple[int, int, int, int, int]]:
+    """The register-window kernel's compiled tiles: (family 0 fp32 / 1 binary16, compute
+    warps, PC, DW, KW)."""
+    L = lib()
+    n = L.usc_bw_instances(None, 0)
+    buf = (c_i32 * (5 * n))()
+    L.usc_bw_instances(buf, n)
+    return [tuple(buf[5 * i:5 * i + 5]) for i in range(n)]
 
 
 def check(rc: int, what: str = ""):

@@ -42,3 +42,12 @@
 #define USC_BT(X)                                                                               \
     X(8, 2, 2, 8) X(8, 4, 2, 4) X(8, 4, 1, 8) X(8, 8, 1, 4) X(8, 2, 1, 16) X(12, 2, 2, 8) X(12, 4, 2, 4) \
     X(12, 4, 1, 8) X(12, 8, 1, 4) X(16, 2, 2, 4) X(16, 4, 1, 4) X(16, 2, 1, 8)
+
+// register-window kernel (k_bw, conv_bw.cuh): X(FAMILY, NW, PC, DW, KW) -- FAMILY 0 =
+// fp32 (F32), 1 = binary16 input (F16); a thread's block is one row of PC pixels, DW
+// slots share the merged entry stream, KW = filter width (3 or 1), BI64, stride 1.
+// Registers: 2*DW*PC accumulators + (PC+KW-1)*(FAMILY ? 1 : 2) window values under the
+// cap of the warp count (168 for 8 compute warps, 128 for 12); DW*PC = 64 spills.
+#define USC_BW(X)                                                                                    \
+    X(0, 8, 4, 12, 3) X(0, 8, 4, 8, 3) X(0, 12, 4, 8, 3) X(0, 8, 4, 12, 1) X(0, 12, 4, 8, 1)           \
+    X(1, 8, 4, 12, 3) X(1, 8, 4, 8, 3) X(1, 12, 4, 8, 3) X(1, 8, 4, 12, 1) X(1, 12, 4, 8, 1)

@@ -5,6 +5,7 @@
 #include <cmath>
 
 #include "conv_bt.cuh"
+#include "conv_bw.cuh"
 
 namespace usc {
 
@@ -110,6 +111,7 @@ int launch_bi(const usc_plan *pl, const void *blob, const void *x, void *y, cons
         (ep.relu || !ep.pool))
         a.fast = 1;  // the 4b/16b hook with its saturations (store_tile_fast)
     if (pl->kernel == 4) return usc_bi::launch_bt(pl, a, st);
+    if (pl->window) return usc_bi::launch_bw(pl, a, st);
     if (pl->dtype == USC_F16) return usc_bi::launch_h16(pl, a, st);
     if (pl->dtype == USC_CB4) return usc_bi::launch_hcb(pl, a, st);
     if (pl->dtype == USC_I8) return usc_bi::launch_hi8(pl, a, st);

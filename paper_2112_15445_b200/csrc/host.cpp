@@ -268,6 +268,33 @@ static bool bi_instance(int PC, int PR, int DW, int NW, int SW, int SPL, int dty
     return false;
 }
 
+// the k_bw (register-window) instances compiled into the library (bi_instances.h)
+static bool bw_instance(int PC, int DW, int NW, int KW, int dtype) {
+    const int fam = dtype == USC_F32 ? 0 : (dtype == USC_F16 ? 1 : -1);
+#define XW(F_, NW_, PC_, DW_, KW_) \
+    if (fam == F_ && NW == NW_ && PC == PC_ && DW == DW_ && KW == KW_) return true;
+    USC_BW(XW)
+#undef XW
+    return false;
+}
+
+int usc_bw_instances(int32_t *out, int32_t max_count) {
+    int n = 0;
+#define XW(F_, NW_, PC_, DW_, KW_)        \
+    if (n < max_count && out) {           \
+        int32_t *o = out + 5 * n;         \
+        o[0] = F_;                        \
+        o[1] = NW_;                       \
+        o[2] = PC_;                       \
+        o[3] = DW_;                       \
+        o[4] = KW_;                       \
+    }                                     \
+    ++n;
+    USC_BW(XW)
+#undef XW
+    return n;
+}
+
 static bool bt_instance(int PC, int PR, int DW, int NW) {
 #define XT(NW_, PC_, PR_, DW_) \
     if (NW == NW_ && PC == PC_ && PR == PR_ && DW == DW_) return true;
@@ -353,6 +380,10 @@ int usc_plan_make(const usc_geometry *g0, int32_t n, int32_t dtype, const usc_ex
     if (kernel == 4 && (dtype != USC_F32 || g.stride_w != 1 || g.stride_h != 1))
         return fail(USC_ERR_UNSUPPORTED, "the tensor-memory kernel is fp32, stride 1 only");
     const bool bi = kernel == 3 || kernel == 4;  // batch-interleaved families
+    const bool win = bi && c.window != 0;        // register-window variant (k_bw)
+    if (win && (kernel != 3 || (dtype != USC_F32 && dtype != USC_F16) || g.stride_w != 1 ||
+                (g.filter_w != 1 && g.filter_w != 3)))
+        return fail(USC_ERR_UNSUPPORTED, "the register-window kernel is F32/F16, stride_w 1, filter_w 1 or 3");
     const int eb = (kernel == 3 && dtype == USC_I8) ? 2 : elem_bytes(dtype);
 
     // kernel 3 sample interleave: samples_per_cta 32 (BI32) or 64 (BI64, two samples per
@@ -360,7 +391,7 @@ int usc_plan_make(const usc_geometry *g0, int32_t n, int32_t dtype, const usc_ex
     int IL = 0;
     if (bi) {
         IL = (c.samples_per_cta == 32 || c.samples_per_cta == 64) ? c.samples_per_cta : (n > 32 ? 64 : 32);
-        if (dtype != USC_F32 || kernel == 4) IL = 64;  // binary16-staged kinds and TMEM: BI64 only
+        if (dtype != USC_F32 || kernel == 4 || win) IL = 64;  // binary16-staged kinds, TMEM, k_bw: BI64 only
     }
     rc = usc_act_layout_make(g.in_channels, g.input_h, g.input_w, g.pad_h, g.pad_w, eb, IL, &pl->in);
     if (rc) return rc;
@@ -373,8 +404,9 @@ int usc_plan_make(const usc_geometry *g0, int32_t n, int32_t dtype, const usc_ex
         const bool even = Yh % 2 == 0 && Yw % 2 == 0 && g.stride_w == 1;
         int PR = c.rows_per_thread ? c.rows_per_thread : (even && Yh >= 2 ? 2 : 1);
         if (PR != 1 && PR != 2) return fail(USC_ERR_VALUE, "BI rows_per_thread must be 1 or 2");
-        if (PR > Yh) PR = 1;
+        if (PR > Yh || win) PR = 1;
         int PC = c.pix_per_thread;
+        if (win && !PC) PC = 4;
         if (!PC) {  // widest block that divides the row, else 4 with a partial last strip
             PC = Yw >= 4 ? 4 : (Yw >= 2 ? 2 : 1);
             for (int q : {8, 4, 2})
@@ -383,7 +415,7 @@ int usc_plan_make(const usc_geometry *g0, int32_t n, int32_t dtype, const usc_ex
                     break;
                 }
         }
-        if (!c.pix_per_thread || !c.rows_per_thread) {
+        if (!win && (!c.pix_per_thread || !c.rows_per_thread)) {
             // no compiled instance for the preferred block: the first (PR, PC) that has one
             auto any_inst = [&](int pr, int pc) {
                 for (int nw : {8, 12, 16})
@@ -434,9 +466,12 @@ int usc_plan_make(const usc_geometry *g0, int32_t n, int32_t dtype, const usc_ex
             const int wc = nw / ws;
             if (c.ch_per_cta && c.ch_per_cta % wc)
                 return fail(USC_ERR_VALUE, "ch_per_cta %d not a multiple of %d channel warps", c.ch_per_cta, wc);
-            for (int dw : {8, 16, 4, 2}) {
+            for (int dw : {8, 16, 4, 2, 12}) {
                 if (c.ch_per_cta) dw = c.ch_per_cta / wc;
-                if (kernel == 4 ? bt_instance(PC, PR, dw, nw) : bi_instance(PC, PR, dw, nw, g.stride_w, IL / 32, dtype)) {
+                const bool inst = win ? bw_instance(PC, dw, nw, g.filter_w, dtype)
+                                      : (kernel == 4 ? bt_instance(PC, PR, dw, nw)
+                                                     : bi_instance(PC, PR, dw, nw, g.stride_w, IL / 32, dtype));
+                if (inst) {
                     NW = nw, WS = ws, WC = wc, DW = dw;
                     break;
                 }
@@ -483,7 +518,7 @@ int usc_plan_make(const usc_geometry *g0, int32_t n, int32_t dtype, const usc_ex
         int ncr = 1, ncc = 1;
         // (row classes need 1-row blocks, column classes 1-column blocks: every pixel of a
         // thread's block must share the valid-tap set along a classed axis)
-        if (c.pixel_classes && (PC == 1 || PR == 1) && g.filter_h <= 32 && g.filter_w <= 32) {
+        if (c.pixel_classes && !win && (PC == 1 || PR == 1) && g.filter_h <= 32 && g.filter_w <= 32) {
             std::vector<int> cl;
             std::vector<uint32_t> mk;
             if (PR == 1) {
@@ -510,8 +545,12 @@ int usc_plan_make(const usc_geometry *g0, int32_t n, int32_t dtype, const usc_ex
         // exceeds it (the caller re-plans with the measured size).
         const int64_t R = c.ent_reserve ? c.ent_reserve : 24 * 1024;
         auto ent_bytes = [&](int cc) {
+            // k_bw: hdr int2[WC], per channel subgroup its MAC entries + one ROW entry per (c, kh)
+            // + an even-count pad
             const int64_t worst =
-                (int64_t)NCLS * DT * 8 + 8 + NCLS * ((int64_t)DT * cc * g.filter_h * g.filter_w + DT) * 8 + 16;
+                win ? (int64_t)WC * 8 + 16 + ((int64_t)DT * cc * g.filter_h * g.filter_w +
+                                             (int64_t)WC * (cc * g.filter_h + 2)) * 8 + 16
+                    : (int64_t)NCLS * DT * 8 + 8 + NCLS * ((int64_t)DT * cc * g.filter_h * g.filter_w + DT) * 8 + 16;
             return (std::min(worst, R) + 127) / 128 * 128;
         };
         while (CC > 1 && S * ((CC * per_ch + 127) / 128 * 128 + ent_bytes(CC)) > budget) --CC;
@@ -520,6 +559,7 @@ int usc_plan_make(const usc_geometry *g0, int32_t n, int32_t dtype, const usc_ex
         if (S * (stage + ent_stage) + 128 > 224 * 1024)
             return fail(USC_ERR_VALUE, "BI tile does not fit shared memory");
         pl->kernel = kernel;
+        pl->window = win ? 1 : 0;
         pl->ncls_r = ncr;
         pl->ncls_c = ncc;
         pl->P = P;
@@ -556,7 +596,7 @@ int usc_plan_make(const usc_geometry *g0, int32_t n, int32_t dtype, const usc_ex
         // (F | DW) when that shortens the round-robin makespan (whole tile = 1 unit)
         pl->tail_full = (int32_t)tiles;
         pl->tail_split = 1;
-        {
+        if (!win) {  // (k_bw runs whole tiles: its merged run covers every slot of the warp)
             const int64_t C = sms;
             auto makespan = [&](int64_t R, int F) {
                 const int64_t full = tiles - R, nsplit = F * R;
@@ -717,6 +757,13 @@ int usc_pack_size(const usc_plan *pl, int64_t n_nz, int64_t *bytes) {
         // [64 B][int32 blk[nb+1]][int32 perm[G*DT]][blocks: hdr int2[DT], runs padded to
         // even, 16-B rounded]
         const int64_t ncls = std::max(1, pl->ncls_r * pl->ncls_c);
+        if (pl->window) {  // k_bw: per (block, channel subgroup) up to CC*Kh ROW entries + END
+            *bytes = 64 + align16(4 * (nb + 1)) + align16(4 * (int64_t)pl->groups * pl->DT) +
+                     align16(4 * ((int64_t)pl->out_h + pl->out_w)) + nb * ((int64_t)pl->WC * 8 + 32) +
+                     ((int64_t)pl->g.out_channels * n_nz + nb * pl->WC * ((int64_t)pl->CC * pl->g.filter_h + 1)) * 8 +
+                     64;
+            return USC_OK;
+        }
         *bytes = 64 + align16(4 * (nb + 1)) + align16(4 * (int64_t)pl->groups * pl->DT) +
                  align16(4 * ((int64_t)pl->out_h + pl->out_w)) + nb * (ncls * pl->DT * 8 + 16) +
                  ncls * ((int64_t)pl->g.out_channels * n_nz + nb * pl->DT) * 8 + 64;
@@ -839,6 +886,7 @@ int usc_pack(const usc_plan *pl, const int64_t *row_ptr, const int64_t *col, con
         std::vector<std::vector<std::pair<int64_t, int64_t>>> per(D);  // (chunk, off) per d
         std::vector<std::vector<int64_t>> src(D);
         std::vector<std::vector<uint16_t>> tap(D);  // kh << 8 | kw per entry
+        std::vector<std::vector<int32_t>> chan(D);  // input channel per entry
         std::vector<int64_t> cnt((size_t)D * NC, 0);
         for (int d = 0; d < D; ++d) {
             zero_seen.clear();
@@ -850,6 +898,7 @@ int usc_pack(const usc_plan *pl, const int64_t *row_ptr, const int64_t *col, con
                 per[d].push_back({cpos / CC, off});
                 src[d].push_back(j);
                 tap[d].push_back((uint16_t)(dec_kh << 8 | dec_kw));
+                chan[d].push_back((int32_t)cpos);
                 ++cnt[(size_t)d * NC + cpos / CC];
             }
         }
@@ -880,7 +929,74 @@ int usc_pack(const usc_plan *pl, const int64_t *row_ptr, const int64_t *col, con
             slot[(size_t)(best / WC) * DT + (best % WC) * DW + used[best]++] = d;
         }
         int64_t pos = 0, worst = 0, total = 0;
-        for (int gi = 0; gi < G; ++gi)
+        if (pl->window) {
+            // k_bw block (group, chunk): int2 hdr[WC] = {first, end} of every channel subgroup's
+            // merged run; a run lists, per input row (c, kh) in ascending order, one ROW entry
+            // (window offset) then the MAC entries (code = slot * KW + kw, theta) of the
+            // subgroup's slots -- per slot still in stored (c, kh, kw) order -- and ends with an
+            // END entry (the kernel prefetches one entry ahead: 16 B of slack follow the block)
+            const int KW = g.filter_w;
+            const int64_t pxb = (pl->dtype == USC_F32 ? 4 : 2) * (int64_t)pl->in.interleave;
+            const uint32_t ROW = 62u << 24, END = 63u << 24;
+            for (int gi = 0; gi < G; ++gi)
+                for (int k = 0; k < NC; ++k) {
+                    blk[(int64_t)gi * NC + k] = (int32_t)pos;
+                    char *b = base + pos;
+                    std::vector<int32_t> runs(2 * (size_t)WC);
+                    std::vector<std::pair<uint32_t, int64_t>> out;  // (word0, stored entry j or -1)
+                    for (int wc = 0; wc < WC; ++wc) {
+                        runs[2 * wc] = (int32_t)out.size();
+                        struct E {
+                            int cl, kh, dw, kw;
+                            int64_t j;
+                        };
+                        std::vector<E> ents;
+                        for (int dw = 0; dw < DW; ++dw) {
+                            const int d = slot[(size_t)gi * DT + wc * DW + dw];
+                            if (d < 0) continue;
+                            for (size_t i = 0; i < per[d].size(); ++i)
+                                if (per[d][i].first == k)
+                                    ents.push_back({chan[d][i] - k * CC, tap[d][i] >> 8, dw, tap[d][i] & 255, src[d][i]});
+                        }
+                        std::stable_sort(ents.begin(), ents.end(), [](const E &x, const E &y) {
+                            if (x.cl != y.cl) return x.cl < y.cl;
+                            if (x.kh != y.kh) return x.kh < y.kh;
+                            if (x.dw != y.dw) return x.dw < y.dw;
+                            return x.kw < y.kw;
+                        });
+                        int lc = -1, lk = -1;
+                        for (const E &en : ents) {
+                            if (en.cl != lc || en.kh != lk) {
+                                const int64_t off = ((int64_t)en.cl * pl->HS + en.kh) * pl->TWs * pxb;
+                                if (off >= (1 << 24)) return fail(USC_ERR_UNSUPPORTED, "window offset too large");
+                                out.push_back({ROW | (uint32_t)off, -1});
+                                lc = en.cl;
+                                lk = en.kh;
+                            }
+                            out.push_back({(uint32_t)(en.dw * KW + en.kw) << 24, en.j});
+                        }
+                        out.push_back({END, -1});
+                        runs[2 * wc + 1] = (int32_t)out.size();
+                    }
+                    const int64_t hdr_raw = (int64_t)WC * 8, hdr = align16(hdr_raw);
+                    const int64_t bytes = align16(hdr + (int64_t)out.size() * 8);
+                    if (!dry && pos + bytes + 16 > cap) return fail(USC_ERR_VALUE, "pack buffer too small");
+                    if (!dry) {
+                        std::memset(b, 0, (size_t)bytes);
+                        std::memcpy(b, runs.data(), (size_t)hdr_raw);
+                        char *ents = b + hdr;
+                        for (size_t i = 0; i < out.size(); ++i) {
+                            int32_t v[2] = {(int32_t)out[i].first,
+                                            out[i].second < 0 ? 0 : theta_word(pl->dtype, payload, table, out[i].second)};
+                            std::memcpy(ents + i * 8, v, 8);
+                        }
+                    }
+                    total += (int64_t)out.size();
+                    worst = std::max(worst, bytes + 16);
+                    pos += bytes;
+                }
+        }
+        for (int gi = 0; gi < (pl->window ? 0 : G); ++gi)
             for (int k = 0; k < NC; ++k) {
                 blk[(int64_t)gi * NC + k] = (int32_t)pos;
                 char *b = base + pos;

@@ -48,6 +48,7 @@ class ExecConfig:
     rows_per_thread: int = 0
     ent_reserve: int = 0
     pixel_classes: int = 0
+    window: int = 0
 
     def __post_init__(self):
         if self.sub_batch < 1:
@@ -64,7 +65,7 @@ class ExecConfig:
         return _lib.ExecCfg(self.sub_batch, self.worker_count, self.pix_per_thread, self.ch_per_cta,
                             self.samples_per_cta, self.chunk_channels, self.threads, self.kernel,
                             self.pixel_warps, self.stages, self.rows_per_thread, self.ent_reserve,
-                            self.pixel_classes)
+                            self.pixel_classes, self.window)
 
 
 @dataclass(frozen=True)
@@ -156,7 +157,7 @@ def _max_block(filt, plan, payload, table=None) -> int:
 def _pack_key(plan: _lib.Plan, device) -> tuple:
     return (plan.dtype, plan.kernel, plan.DT, plan.CC, plan.HS, plan.TWs, plan.in_.ws, plan.in_.hp,
             plan.transposed, plan.groups, plan.n_chunks, plan.ent_stage_bytes, plan.WC, plan.DW,
-            plan.ncls_r, plan.ncls_c, plan.in_.interleave, str(device))
+            plan.ncls_r, plan.ncls_c, plan.in_.interleave, plan.window, str(device))
 
 
 def device_pack(filt: CsrFilter, plan: _lib.Plan, payload: np.ndarray, table=None, device=None):
@@ -341,6 +342,24 @@ def tile_candidates(geometry: ConvGeometry, n: int, sb_values, precision=Precisi
                                               ch_per_cta=dw * (nw // ws), kernel=3, threads=nw * 32,
                                               pixel_warps=ws, stages=st, samples_per_cta=32 * spl,
                                               pixel_classes=pcl))
+    if 5 in kernels and geometry.stride == (1, 1) and geometry.filter_w in (1, 3) and geometry.input_w != 1:
+        # register-window variant of kernel 3 (k_bw, opt-in "kernel 5" of the search): one row
+        # of PC pixels per thread, the warp's DW slots sharing one entry stream and each
+        # (c, kh) input-row window loaded into registers once.  Measured 2-2.6x slower than
+        # k_bi on the VGG layers: the per-entry jump-table dispatch (LDC + BRX)
+        # is a latency chain 8-12 warps per SM cannot hide, so it is not in the default search.
+        yh, fam = geometry.out_h, 1 if precision is PrecisionMode.BINARY16 else 0
+        for f, nw, pc, dw, kw in _lib.bw_instances():
+            if f != fam or kw != geometry.filter_w or pc > max(1, yw) and pc > 1:
+                continue
+            strips = yh * -(-yw // pc)
+            for ws in (w for w in range(1, nw + 1) if nw % w == 0):
+                if ws > strips:
+                    break
+                for st in (2, 3):
+                    out.append(ExecConfig(sub_batch=min(sb_values), pix_per_thread=pc, rows_per_thread=1,
+                                          ch_per_cta=dw * (nw // ws), kernel=3, threads=nw * 32, pixel_warps=ws,
+                                          stages=st, samples_per_cta=64, window=1))
     if 4 in kernels and precision is PrecisionMode.BINARY32 and geometry.stride == (1, 1):
         # tensor-memory-fed fp32 BI64 (kernel 4, opt-in: measured slower than kernel 3 on the
         # VGG layers -- short TMEM-bounded chunks, fill and per-load R2UR cost more issue
@@ -371,7 +390,7 @@ def tile_candidates(geometry: ConvGeometry, n: int, sb_values, precision=Precisi
         except ValueError:
             continue
         key = (plan.kernel, plan.P, plan.PR, plan.PC, plan.DT, plan.DW, plan.WS, plan.NS, plan.CC,
-               plan.threads, plan.stages, plan.ncls_r, plan.ncls_c)
+               plan.threads, plan.stages, plan.ncls_r, plan.ncls_c, plan.window)
         if key not in seen:
             seen.add(key)
             feasible.append(cfg)
@@ -413,7 +432,7 @@ def autotune_sb(input: DenseTensor4, filt: CsrFilter, candidates=SB_CANDIDATES, 
                 return ExecConfig(cfg.sub_batch, worker_count, cfg.pix_per_thread, cfg.ch_per_cta,
                                   cfg.samples_per_cta, cfg.chunk_channels, cfg.kernel, cfg.threads,
                                   cfg.pixel_warps, cfg.stages, cfg.rows_per_thread, cfg.ent_reserve,
-                                  cfg.pixel_classes)
+                                  cfg.pixel_classes, cfg.window)
     return ExecConfig(usable[0], worker_count)
 
 
@@ -435,4 +454,4 @@ def autotune_native(input: DenseTensor4, filt: CsrFilter, repeats: int = 9, warm
                                        noise_floor, _lib.ref(best), _lib.ref(ms), _lib.stream_ptr()), "autotune")
     return ExecConfig(best.sub_batch, best.worker_count, best.pix_per_thread, best.ch_per_cta,
                       best.samples_per_cta, best.chunk_channels, best.kernel, best.threads, best.pixel_warps,
-                      best.stages, best.rows_per_thread, best.ent_reserve, best.pixel_classes)
+                      best.stages, best.rows_per_thread, best.ent_reserve, best.pixel_classes, best.window)

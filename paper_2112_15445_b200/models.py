@@ -100,7 +100,7 @@ class SparseVGG16:
 
     def __init__(self, weights, batch: int, precision=PrecisionMode.BINARY32, configs=None,
                  device=None, mode: str | None = None, calibration=None, saturation: float = 0.99,
-                 maxima: dict | None = None, codebooks=None):
+                 maxima: dict | None = None, codebooks=None, backends=None):
         import torch
         mode = mode or ("fp16" if precision is PrecisionMode.BINARY16 else "fp32")
         if mode not in MODES:
@@ -131,6 +131,9 @@ class SparseVGG16:
             self.filters = [q.filt for q in self.qfilters]
             self.payloads = [q.indices for q in self.qfilters]
             self.tables = [q.table for q in self.qfilters]
+        self.weights = weights
+        self.backends = list(backends) if backends is not None else ["sparse"] * len(self.geoms)
+        self._check_backends()
         self.pre_pool = self._pre_pool_layers()
         self.fuse_pool = {}  # per pool-feeding conv: fuse the pool into its epilogue (autotuned)
         self.saturation = saturation
@@ -200,6 +203,85 @@ class SparseVGG16:
             li += 1
         return out
 
+    # -- per-layer backend (the reference's backend_config, bench.py:212-227) ----------
+    def dense_eligible(self, li: int) -> bool:
+        """cuDNN may run conv `li`: binary16 (16b/16b) networks only -- the north star's
+        1e-2 tolerance path; fp32 / int8 / 4b/16b stay sparse and bitwise -- with channel
+        counts the BI64 <-> NHWC transposes take."""
+        g = self.geoms[li]
+        return self.mode == "fp16" and g.in_channels % 16 == 0 and g.out_channels % 16 == 0
+
+    def _check_backends(self):
+        if len(self.backends) != len(self.geoms):
+            raise ValueError(f"{len(self.backends)} backends for {len(self.geoms)} convs")
+        for li, b in enumerate(self.backends):
+            if b not in ("sparse", "dense"):
+                raise ValueError(f"unknown backend {b!r}")
+            if b == "dense" and not self.dense_eligible(li):
+                raise ValueError(f"conv {li} cannot run dense (16b/16b networks with channels % 16 == 0 only)")
+
+    def _dense_step(self, li, x, x_lay, y, y_lay, pool):
+        """cuDNN (torch conv2d, binary16 tensor cores, channels_last) + ReLU (+ 2x2 max-pool)
+        for conv li: BI64 -> NHWC, conv, [pool], NHWC -> BI64 with saturation and ReLU."""
+        import torch
+        g, n = self.geoms[li], self.batch
+        if not hasattr(self, "_dense_w"):
+            self._dense_w = {}
+        if li not in self._dense_w:
+            w = torch.from_numpy(np.array(self.weights[li].data)).to(self.device, torch.float16)
+            self._dense_w[li] = w.contiguous(memory_format=torch.channels_last)
+        w = self._dense_w[li]
+        xin = torch.empty((n, g.in_channels, g.input_h, g.input_w), dtype=torch.float16, device=self.device,
+                          memory_format=torch.channels_last)
+        L = _lib.lib()
+
+        def fn(stream=None):
+            sp = _lib.stream_ptr(stream)
+            _lib.check(L.usc_bi_to_nhwc(_lib.ref(x_lay), n, _lib.t_ptr(x), _lib.t_ptr(xin), sp), "bi_to_nhwc")
+            yo = torch.nn.functional.conv2d(xin, w, padding=1)
+            if pool:  # ReLU commutes with max; the transpose applies it
+                yo = torch.nn.functional.max_pool2d(yo, 2)
+            if not yo.is_contiguous(memory_format=torch.channels_last):
+                yo = yo.contiguous(memory_format=torch.channels_last)
+            _lib.check(L.usc_nhwc_to_bi(_lib.ref(y_lay), n, _lib.t_ptr(yo), _lib.t_ptr(y), None, None, 1, sp),
+                       "nhwc_to_bi")
+        return fn
+
+    def autotune_backends(self, repeats: int = 5, warmup: int = 2) -> list:
+        """Per-conv sparse vs cuDNN on the network's own buffers (16b/16b only): argmin of
+        the sparse step (tuned tile; + its pool launch when unfused) and the dense step,
+        exact ties to dense (backend_config, bench.py:212-227)."""
+        import torch
+        if self.mode != "fp16":
+            raise ValueError("the backend dispatcher runs 16b/16b networks only (other modes stay bitwise)")
+        torch.backends.cudnn.benchmark = True
+
+        def per_conv_ms():
+            out, li_of = {}, None
+            for st in self.steps:
+                if st[0] == "pool":
+                    li_of_pool = st[1]
+                    out[li_of_pool] = out.get(li_of_pool, 0.0) + time_median_cuda(
+                        lambda: self._run_step(st), repeats, warmup)
+                    continue
+                out[st[1]] = out.get(st[1], 0.0) + time_median_cuda(lambda: self._run_step(st), repeats, warmup)
+            return out
+
+        self.backends = ["sparse"] * len(self.geoms)
+        self.graph = None
+        self._build()
+        sparse_ms = per_conv_ms()
+        self.backends = ["dense" if self.dense_eligible(li) else "sparse" for li in range(len(self.geoms))]
+        self._build()
+        dense_ms = per_conv_ms()
+        self.backends = ["dense" if self.dense_eligible(li) and dense_ms[li] <= sparse_ms[li] else "sparse"
+                         for li in range(len(self.geoms))]
+        self.backend_times = {li: {"sparse_ms": sparse_ms[li], "dense_ms": dense_ms[li]}
+                              for li in range(len(self.geoms))}
+        self._build()
+        torch.cuda.synchronize()
+        return self.backends
+
     # -- buffers and plans ---------------------------------------------------
     def _buf(self, lay, dtype=None):
         import torch
@@ -236,8 +318,22 @@ class SparseVGG16:
             if v == "M":
                 continue
             g = self.geoms[li]
-            plan, blob = self._plan_for(li, plan_cfgs[li])
             nxt = VGG16_CIFAR[i + 1] if i + 1 < len(VGG16_CIFAR) else None
+            if self.backends[li] == "dense":
+                last = i + 2 >= len(VGG16_CIFAR)
+                if nxt == "M":
+                    ph = 0 if last else 1
+                    out_lay = _lib.act_layout(g.out_channels, g.out_h // 2, g.out_w // 2, ph, ph, self.eb, il)
+                else:
+                    out_lay = _lib.act_layout(g.out_channels, g.out_h, g.out_w, 1, 1, self.eb, il)
+                out_buf = self._buf(out_lay)
+                self.steps.append(("dense", li, self._dense_step(li, cur_buf, cur_lay, out_buf, out_lay,
+                                                                 nxt == "M")))
+                self.nonzero_macs += int(np.count_nonzero(self.filters[li].weights)) * g.out_h * g.out_w * n
+                cur_buf, cur_lay = out_buf, out_lay
+                li += 1
+                continue
+            plan, blob = self._plan_for(li, plan_cfgs[li])
             epi = _lib.Epilogue()
             epi.relu = 1
             epi.scale = 1.0
@@ -294,12 +390,29 @@ class SparseVGG16:
                                             _lib.t_ptr(x), _lib.t_ptr(self.x_buf),
                                             _lib.stream_ptr(stream)), "pad")
 
+    def _run_step(self, st, stream=None):
+        L = _lib.lib()
+        sp = _lib.stream_ptr(stream)
+        if st[0] == "dense":
+            st[2](stream)
+        elif st[0] == "conv":
+            _, _, plan, blob, xin, yout, epi = st
+            _lib.check(L.usc_conv_forward(_lib.ref(plan), _lib.t_ptr(blob), _lib.t_ptr(xin),
+                                          _lib.t_ptr(yout), _lib.ref(epi), sp), "conv")
+        else:
+            _, _, lin, lout, xin, yout = st
+            pdt = _lib.USC_F32 if xin.element_size() == 4 else _lib.USC_F16
+            _lib.check(L.usc_maxpool2(_lib.ref(lin), _lib.ref(lout), pdt, self.batch,
+                                      _lib.t_ptr(xin), _lib.t_ptr(yout), sp), "pool")
+
     def run(self, stream=None):
         """All 18 launches on the current stream (no host synchronisation)."""
         L = _lib.lib()
         sp = _lib.stream_ptr(stream)
         for st in self.steps:
-            if st[0] == "conv":
+            if st[0] == "dense":
+                st[2](stream)
+            elif st[0] == "conv":
                 _, _, plan, blob, xin, yout, epi = st
                 _lib.check(L.usc_conv_forward(_lib.ref(plan), _lib.t_ptr(blob), _lib.t_ptr(xin),
                                               _lib.t_ptr(yout), _lib.ref(epi), sp), "conv")
@@ -423,7 +536,8 @@ class SparseVGG16:
     def tuned_state(self) -> dict:
         import dataclasses
         return {"configs": [dataclasses.asdict(c) for c in self.configs],
-                "fuse_pool": {str(k): bool(v) for k, v in self.fuse_pool.items()}}
+                "fuse_pool": {str(k): bool(v) for k, v in self.fuse_pool.items()},
+                "backends": list(self.backends)}
 
     def load_tuned_state(self, state) -> None:
         """Accepts tuned_state() output (or a bare list of ExecConfig dicts)."""
@@ -431,6 +545,9 @@ class SparseVGG16:
             state = {"configs": state, "fuse_pool": {}}
         self.configs = [ExecConfig(**c) for c in state["configs"]]
         self.fuse_pool = {int(k): bool(v) for k, v in state.get("fuse_pool", {}).items()}
+        if "backends" in state:
+            self.backends = list(state["backends"])
+            self._check_backends()
         self.graph = None
         self._build()
 
@@ -445,6 +562,9 @@ class SparseVGG16:
         best_cfgs = []
         steps = self.steps
         for si, st in enumerate(steps):
+            if st[0] == "dense":
+                best_cfgs.append(self.configs[st[1]])
+                continue
             if st[0] != "conv":
                 continue
             _, li, plan0, _, xin, yout, epi = st

@@ -68,7 +68,7 @@ class SparseResNet50:
     """ResNet-50 CIFAR conv trunk (53 sparse convs) on one GPU for a fixed batch.
     forward(x): plain NCHW (n,3,32,32) -> (n,2048,4,4) features."""
 
-    def __init__(self, weights, batch: int, precision=PrecisionMode.BINARY32, device=None):
+    def __init__(self, weights, batch: int, precision=PrecisionMode.BINARY32, device=None, backends=None):
         import torch
         self.precision = precision
         self.dtype = _lib.USC_F16 if precision is PrecisionMode.BINARY16 else _lib.USC_F32
@@ -87,9 +87,62 @@ class SparseResNet50:
             else:
                 self.eff.append((g, 1))
         self.filters = [build_csr(w, eg) for w, (eg, _) in zip(weights, self.eff)]
+        self.weights = weights
         self.configs = [ExecConfig(samples_per_cta=64) for _ in self.layers]
+        self.backends = list(backends) if backends is not None else ["sparse"] * len(self.layers)
+        self._check_backends()
         self.graph = None
         self._build()
+
+    # -- per-layer backend (the reference's backend_config, bench.py:212-227) ----------
+    def dense_eligible(self, li: int) -> bool:
+        """cuDNN may run conv `li`: binary16 network (the 1e-2 tolerance path; fp32 stays
+        all-sparse and bitwise) and channel counts the BI64<->NHWC transposes take."""
+        g = self.layers[li][1]
+        return (self.dtype == _lib.USC_F16 and g.in_channels % 16 == 0 and g.out_channels % 16 == 0)
+
+    def _check_backends(self):
+        if len(self.backends) != len(self.layers):
+            raise ValueError(f"{len(self.backends)} backends for {len(self.layers)} convs")
+        for li, b in enumerate(self.backends):
+            if b not in ("sparse", "dense"):
+                raise ValueError(f"unknown backend {b!r}")
+            if b == "dense" and not self.dense_eligible(li):
+                raise ValueError(f"conv {self.layers[li][0]} cannot run dense (binary16 networks with "
+                                 f"channels % 16 == 0 only)")
+
+    def _dense_weight(self, li):
+        import torch
+        if not hasattr(self, "_dense_w"):
+            self._dense_w = {}
+        if li not in self._dense_w:
+            w = torch.from_numpy(np.array(self.weights[li].data)).to(self.device, torch.float16)
+            self._dense_w[li] = w.contiguous(memory_format=torch.channels_last)
+        return self._dense_w[li]
+
+    def _dense_step(self, li, x, x_lay, y, y_lay, relu, residual):
+        """cuDNN (torch conv2d, binary16 on tensor cores, channels_last) for conv li:
+        BI64 -> NHWC, conv, NHWC -> BI64 with the epilogue (saturation, residual, ReLU)."""
+        import torch
+        _, g, role, s = self.layers[li]
+        n, C, D = self.batch, g.in_channels, g.out_channels
+        k = g.filter_h
+        xin = torch.empty((n, C, x_lay.height, x_lay.width), dtype=torch.float16, device=self.device,
+                          memory_format=torch.channels_last)
+        w = self._dense_weight(li)
+        res, res_lay = (None, None) if residual is None else residual
+        L = _lib.lib()
+
+        def fn(stream=None):
+            sp = _lib.stream_ptr(stream)
+            _lib.check(L.usc_bi_to_nhwc(_lib.ref(x_lay), n, _lib.t_ptr(x), _lib.t_ptr(xin), sp), "bi_to_nhwc")
+            yo = torch.nn.functional.conv2d(xin, w, stride=s, padding=k // 2)
+            if not yo.is_contiguous(memory_format=torch.channels_last):
+                yo = yo.contiguous(memory_format=torch.channels_last)
+            _lib.check(L.usc_nhwc_to_bi(_lib.ref(y_lay), n, _lib.t_ptr(yo), _lib.t_ptr(y),
+                                        None if res is None else _lib.ref(res_lay),
+                                        None if res is None else _lib.t_ptr(res), int(relu), sp), "nhwc_to_bi")
+        return fn
 
     # -- buffers -------------------------------------------------------------------
     def _lay(self, c, hw, halo):
@@ -107,6 +160,11 @@ class SparseResNet50:
 
         def conv(li, x, x_lay, y_lay, relu=True, residual=None):
             name, g, role, s = self.layers[li]
+            if self.backends[li] == "dense":
+                y = self._buf(y_lay)
+                self.steps.append((li, None, None, x, None, y, self._dense_step(li, x, x_lay, y, y_lay, relu,
+                                                                                residual)))
+                return y
             plan, blob = plan_for(self.filters[li], n, self.dtype, self.configs[li], self.filters[li].weights,
                                   device=self.device)
             if plan.in_.interleave != 64:
@@ -163,6 +221,9 @@ class SparseResNet50:
     # -- execution -------------------------------------------------------------------
     def _launch(self, st, stream=None):
         li, plan, blob, x, view, y, e = st
+        if plan is None:  # dense step (cuDNN)
+            e(stream)
+            return
         L = _lib.lib()
         sp = _lib.stream_ptr(stream)
         if view is None:
@@ -217,11 +278,14 @@ class SparseResNet50:
     # -- tuned state (per-conv tiles) -------------------------------------------------
     def tuned_state(self) -> dict:
         import dataclasses
-        return {"configs": [dataclasses.asdict(c) for c in self.configs]}
+        return {"configs": [dataclasses.asdict(c) for c in self.configs], "backends": list(self.backends)}
 
     def load_tuned_state(self, state) -> None:
         """Accepts tuned_state() output (or a bare list of ExecConfig dicts)."""
         if isinstance(state, dict):
+            if "backends" in state:
+                self.backends = list(state["backends"])
+                self._check_backends()
             state = state["configs"]
         if len(state) != len(self.layers):
             raise ValueError(f"tuned state has {len(state)} configs for {len(self.layers)} convs")
@@ -235,6 +299,9 @@ class SparseResNet50:
         picks = []
         for st in self.steps:
             li, plan0, _, x, view, y, e = st
+            if plan0 is None:  # dense step: keep its (unused) sparse config
+                picks.append(self.configs[li])
+                continue
             g = self.eff[li][0]
             cands = [self.configs[li]] + [c for c in tile_candidates(g, self.batch, [1], self.precision, (3,))
                                           if c.samples_per_cta == 64]
@@ -259,3 +326,27 @@ class SparseResNet50:
         self.graph = None
         self._build()
         return picks
+
+    def autotune_backends(self, repeats: int = 5, warmup: int = 2) -> list:
+        """Per-conv sparse vs cuDNN choice on the network's own buffers (binary16 only):
+        the sparse step with its tuned tile against the dense step (transposes + cuDNN +
+        fused epilogue); argmin, exact ties to dense (backend_config, bench.py:212-227)."""
+        import torch
+        if self.dtype != _lib.USC_F16:
+            raise ValueError("the backend dispatcher runs binary16 networks only (fp32 stays bitwise)")
+        torch.backends.cudnn.benchmark = True
+        self.backends = ["sparse"] * len(self.layers)
+        self.graph = None
+        self._build()
+        sparse_ms = {st[0]: time_median_cuda(lambda: self._launch(st), repeats, warmup) for st in self.steps}
+        self.backends = ["dense" if self.dense_eligible(li) else "sparse" for li in range(len(self.layers))]
+        self._build()
+        dense_ms = {st[0]: time_median_cuda(lambda: self._launch(st), repeats, warmup) for st in self.steps
+                    if st[1] is None}
+        self.backends = ["dense" if li in dense_ms and dense_ms[li] <= sparse_ms[li] else "sparse"
+                         for li in range(len(self.layers))]
+        self.backend_times = {self.layers[li][0]: {"sparse_ms": sparse_ms[li], "dense_ms": dense_ms.get(li)}
+                              for li in range(len(self.layers))}
+        self._build()
+        torch.cuda.synchronize()
+        return self.backends

@@ -102,6 +102,8 @@ def test_layer_configs_bitwise_all_tiles(name):
         U.engine.tile_candidates(gg, rec["batch"], [1, 2], prec)
     # the opt-in tensor-memory kernel (kernel 4): a spread of its tiles
     cfgs += U.engine.tile_candidates(gg, rec["batch"], [1, 2], prec, kernels=(4,))[::7]
+    # the opt-in register-window variant (k_bw): every tile
+    cfgs += U.engine.tile_candidates(gg, rec["batch"], [1, 2], prec, kernels=(5,))
     for cfg in cfgs:
         out = U.sparse_conv_forward(xd, f, cfg)
         assert sha(out.data) == rec["out"], cfg

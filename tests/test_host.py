@@ -276,3 +276,16 @@ def test_every_tile_candidate_fits_its_filter(name):
         if p.kernel == 3:
             assert U.engine._max_block(f, p, f.weights) <= p.ent_stage_bytes
             assert p.smem_bytes <= 224 * 1024
+
+
+def test_spearman_matches_scipy_with_ties():
+    from scipy.stats import spearmanr
+
+    from paper_2112_15445_b200 import layer_bench as LB
+    rng = np.random.default_rng(3)
+    for _ in range(20):
+        x = rng.integers(0, 5, 17).astype(float)
+        y = rng.integers(0, 4, 17).astype(float)
+        if np.ptp(x) == 0 or np.ptp(y) == 0:
+            continue
+        assert LB.spearman_rho(x, y) == pytest.approx(spearmanr(x, y).statistic, abs=1e-12)

@@ -85,7 +85,24 @@ def full(rep, dst, plan_path=None):
     lines = [f"# ncu --set full: {d.get('Kernel Name', '?')}", "", "| metric | value |", "|---|---|"]
     for k in keys:
         lines.append(f"| {k} | {d.get(k, 'n/a')} {u.get(k, '')} |")
-    lines += ["", f"DRAM traffic per launch: {dram:.0f} bytes", "", "| stall reason | share |", "|---|---|"]
+    lines += ["", f"DRAM traffic per launch: {dram:.0f} bytes "
+              f"(read {f('dram__bytes_read.sum') or 0:.0f}, write {f('dram__bytes_write.sum') or 0:.0f})"]
+    meta = json.load(open(plan_path)) if plan_path and os.path.exists(plan_path) else {}
+    if "nonzero_macs" in meta:  # tools/ncu_target.py: per-MAC ratios of the captured launch
+        macs, ab = meta["nonzero_macs"], meta["algorithmic_bytes"]
+        t_us = f("gpu__time_duration.sum") or 0
+        wf = f("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum") or 0
+        inst = f("smsp__inst_executed.sum") or 0
+        lines += ["", f"target: `{meta['spec']}`, plan `{json.dumps(meta['plan'])}`", "",
+                  "| derived (per launch) | value |", "|---|---|",
+                  f"| nonzero MACs | {macs} |",
+                  f"| shared-memory wavefronts per MAC | {wf / macs:.3f} |",
+                  f"| warp instructions per 1000 MACs | {1000 * inst / macs:.2f} |",
+                  f"| nonzero TFLOP/s (2 flop/MAC, ncu time) | {2 * macs / (t_us * 1e-6) / 1e12:.2f} |",
+                  f"| algorithmic bytes | {ab} |",
+                  f"| DRAM bytes / algorithmic bytes | {dram / ab:.3f} |",
+                  f"| algorithmic GB/s (ncu time) | {ab / (t_us * 1e-6) / 1e9:.1f} |"]
+    lines += ["", "| stall reason | share |", "|---|---|"]
     for k, v in sorted(stalls.items(), key=lambda kv: -(kv[1] or 0))[:10]:
         lines.append(f"| {k} | {100 * (v or 0) / tot:.1f}% |")
     open(dst, "w").write("\n".join(lines) + "\n")
