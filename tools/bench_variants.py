@@ -109,10 +109,34 @@ def vgg16_fp16(steps):
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
     ms = timed(lambda: m.graph.replay(), steps, flush)
     cd = timed(cudnn_vgg(ws, batch, torch.float16, channels_last=True), steps, flush)
+    disp = dispatched(m, "vgg16_fp16", steps, flush, cd)
     return {"config": "pruned VGG-16 CIFAR-10 93% BINARY16, batch 256", "dtype": "f16 storage, f32 accumulate",
             "images_per_s": round(batch / (ms / 1e3), 1), "ms_per_step": round(ms, 4),
             "cudnn_fp16_tensor_core": {"images_per_s": round(batch / (cd / 1e3), 1), "ms_per_step": round(cd, 4)},
-            "speedup_vs_cudnn": round(cd / ms, 3)}
+            "speedup_vs_cudnn": round(cd / ms, 3), "dispatch": disp}
+
+
+def dispatched(m, name, steps, flush, cudnn_ms):
+    """The per-layer sparse/cuDNN dispatcher (backend_config, ref bench.py:212-227) on a
+    binary16 network: argmin per conv on the network's buffers, then the mixed network
+    timed as one CUDA graph (fp16 tolerance path, tests/test_gpu_dispatch.py)."""
+    st = load_state(f"{name}_dispatch")
+    if st:
+        m.load_tuned_state(st)
+    else:
+        m.autotune_backends(repeats=5, warmup=2)
+        dump_state(f"{name}_dispatch", m.tuned_state())
+    m.capture()
+    ms = timed(lambda: m.graph.replay(), steps, flush)
+    backends = list(m.backends)
+    out = {"images_per_s": round(m.batch / (ms / 1e3), 1), "ms_per_step": round(ms, 4),
+           "speedup_vs_cudnn": round(cudnn_ms / ms, 3), "sparse_layers": backends.count("sparse"),
+           "dense_layers": backends.count("dense"), "backends": backends,
+           "rule": "per-conv argmin of the sparse step vs transpose + cuDNN + fused epilogue, ties to dense"}
+    if hasattr(m, "backend_times"):
+        out["per_conv_ms"] = {str(k): {a: (round(b, 4) if b is not None else None) for a, b in v.items()}
+                              for k, v in m.backend_times.items()}
+    return out
 
 
 def vgg16_quantised(mode, steps):
@@ -279,12 +303,15 @@ def resnet50_network(prec_name, steps, batch=256, sparsity=0.9):
                 li += 1
         return a
     cd = timed(fwd, steps, flush)
-    return {"config": f"pruned ResNet-50 CIFAR {int(sparsity * 100)}% {prec_name}, batch {batch}, full network "
-                      f"(53 sparse convs, residual adds)",
-            "images_per_s": round(batch / (ms / 1e3), 1), "ms_per_step": round(ms, 4),
-            "cudnn": {"images_per_s": round(batch / (cd / 1e3), 1), "ms_per_step": round(cd, 4),
-                      "kind": "fp16 tensor cores" if prec_name == "fp16" else "fp32, TF32 off"},
-            "speedup_vs_cudnn": round(cd / ms, 3)}
+    out = {"config": f"pruned ResNet-50 CIFAR {int(sparsity * 100)}% {prec_name}, batch {batch}, full network "
+                     f"(53 sparse convs, residual adds)",
+           "images_per_s": round(batch / (ms / 1e3), 1), "ms_per_step": round(ms, 4),
+           "cudnn": {"images_per_s": round(batch / (cd / 1e3), 1), "ms_per_step": round(cd, 4),
+                     "kind": "fp16 tensor cores" if prec_name == "fp16" else "fp32, TF32 off"},
+           "speedup_vs_cudnn": round(cd / ms, 3)}
+    if prec_name == "fp16":
+        out["dispatch"] = dispatched(m, "resnet50_fp16", steps, flush, cd)
+    return out
 
 
 def sweep(steps, shapes=None, sparsities=(0.5, 0.7, 0.9, 0.95, 0.98)):
