@@ -302,11 +302,12 @@ def free_port() -> int:
     return p
 
 
-def launch_ranks(args):
-    """`--gpus N` outside torchrun: re-exec this script under torch.distributed.run
-    with N local ranks (127.0.0.1 rendezvous); rank 0 prints the JSON line."""
+def launch_ranks(args, script=None):
+    """`--gpus N` outside torchrun: re-exec this script (or `script`) under
+    torch.distributed.run with N local ranks (127.0.0.1 rendezvous); rank 0 prints."""
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
-           "--master-addr", "127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+           "--master-addr", "127.0.0.1", f"--master-port={free_port()}",
+           os.path.abspath(script or __file__)] + sys.argv[1:]
     sys.stdout.flush()
     os.execv(sys.executable, cmd)
 
@@ -488,8 +489,13 @@ def main():
     model.load_input(x_dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=device)  # 2x L2
 
-    for _ in range(args.warmup):
+    def step():  # one pass: pad the resident input into the BI layout, the 18 launches, unpack
+        model.load_input(x_dev)
         model.graph.replay()
+        model.output()
+
+    for _ in range(args.warmup):
+        step()
     torch.cuda.synchronize()
 
     # ---- timed region: K steps, inputs resident, L2 flushed between steps -----
@@ -502,7 +508,7 @@ def main():
         for a, b in evs:
             flush.zero_()
             a.record()
-            model.graph.replay()
+            step()
             b.record()
         torch.cuda.synchronize()
     step_ms = [a.elapsed_time(b) for a, b in evs]
@@ -652,10 +658,12 @@ def main():
                            "parallelism": f"dp{world} (batch-sharded, no collective in the timed step; "
                                           f"final all_gather in the e2e leg)",
                            "l2": "flushed (256 MiB write) between timed steps",
+                           "timed_step": "input pad into the BI64 layout + CUDA graph (13 conv + pools) + "
+                                         "output unpack, device-resident input",
                            "cuda_graph": True,
                            "tiles": (os.path.relpath(args.configs, ROOT) + " (committed autotuner result)")
                            if args.configs else "autotuned this run"},
-                "e2e": e2e, "gpu_launches": args.steps * model.launches_per_forward,
+                "e2e": e2e, "gpu_launches": args.steps * (model.launches_per_forward + 2),
                 "parity": parity,
                 "roofline": roofline, "layers": layers, "cudnn": cudnn, "cpu_baseline": cpu,
                 "cfg1": cfg1, "clocks": clk.summary()}

@@ -220,65 +220,118 @@ class SparseVGG16:
             if b == "dense" and not self.dense_eligible(li):
                 raise ValueError(f"conv {li} cannot run dense (16b/16b networks with channels % 16 == 0 only)")
 
-    def _dense_step(self, li, x, x_lay, y, y_lay, pool):
-        """cuDNN (torch conv2d, binary16 tensor cores, channels_last) + ReLU (+ 2x2 max-pool)
-        for conv li: BI64 -> NHWC, conv, [pool], NHWC -> BI64 with saturation and ReLU."""
+    def _dense_fn(self, li, x_held, out_held, pool):
+        """cuDNN (torch conv2d: binary16 tensor cores, channels_last) + ReLU (+ 2x2 max-pool)
+        for conv li on the NHWC form of its input: sat16(conv) (the binary16 hook), ReLU
+        (where(v > 0, v, 0)), pool; the NHWC result is the next layer's input."""
         import torch
-        g, n = self.geoms[li], self.batch
         if not hasattr(self, "_dense_w"):
             self._dense_w = {}
         if li not in self._dense_w:
             w = torch.from_numpy(np.array(self.weights[li].data)).to(self.device, torch.float16)
             self._dense_w[li] = w.contiguous(memory_format=torch.channels_last)
         w = self._dense_w[li]
-        xin = torch.empty((n, g.in_channels, g.input_h, g.input_w), dtype=torch.float16, device=self.device,
-                          memory_format=torch.channels_last)
-        L = _lib.lib()
 
         def fn(stream=None):
-            sp = _lib.stream_ptr(stream)
-            _lib.check(L.usc_bi_to_nhwc(_lib.ref(x_lay), n, _lib.t_ptr(x), _lib.t_ptr(xin), sp), "bi_to_nhwc")
-            yo = torch.nn.functional.conv2d(xin, w, padding=1)
-            if pool:  # ReLU commutes with max; the transpose applies it
-                yo = torch.nn.functional.max_pool2d(yo, 2)
-            if not yo.is_contiguous(memory_format=torch.channels_last):
-                yo = yo.contiguous(memory_format=torch.channels_last)
-            _lib.check(L.usc_nhwc_to_bi(_lib.ref(y_lay), n, _lib.t_ptr(yo), _lib.t_ptr(y), None, None, 1, sp),
-                       "nhwc_to_bi")
+            y = torch.nn.functional.conv2d(x_held[0], w, padding=1).clamp_(-65504.0, 65504.0)
+            y = torch.where(y > 0, y, torch.zeros((), dtype=y.dtype, device=y.device))
+            if pool:
+                y = torch.nn.functional.max_pool2d(y, 2)
+            if not y.is_contiguous(memory_format=torch.channels_last):
+                y = y.contiguous(memory_format=torch.channels_last)
+            out_held[0] = y
         return fn
 
+    def _to_nhwc(self, buf, lay, held, shape):
+        import torch
+        t = torch.empty(shape, dtype=torch.float16, device=self.device, memory_format=torch.channels_last)
+        held[0] = t
+        n = self.batch
+
+        def fn(stream=None):
+            _lib.check(_lib.lib().usc_bi_to_nhwc(_lib.ref(lay), n, _lib.t_ptr(buf), _lib.t_ptr(t),
+                                                 _lib.stream_ptr(stream)), "bi_to_nhwc")
+            held[0] = t
+        return fn
+
+    def _to_bi(self, held, buf, lay):
+        n = self.batch
+
+        def fn(stream=None):
+            _lib.check(_lib.lib().usc_nhwc_to_bi(_lib.ref(lay), n, _lib.t_ptr(held[0]), _lib.t_ptr(buf), None,
+                                                 None, 0, _lib.stream_ptr(stream)), "nhwc_to_bi")
+        return fn
+
+    def network_ms(self, steps: int = 10) -> float:
+        """Median device time of one captured forward (CUDA graph replay)."""
+        import torch
+        self.capture()
+        for _ in range(3):
+            self.graph.replay()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(steps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            self.graph.replay()
+            b.record()
+            b.synchronize()
+            ts.append(a.elapsed_time(b))
+        return float(np.median(ts))
+
     def autotune_backends(self, repeats: int = 5, warmup: int = 2) -> list:
-        """Per-conv sparse vs cuDNN on the network's own buffers (16b/16b only): argmin of
-        the sparse step (tuned tile; + its pool launch when unfused) and the dense step,
-        exact ties to dense (backend_config, bench.py:212-227)."""
+        """Sparse vs cuDNN per conv (16b/16b only; backend_config's rule, bench.py:212-227:
+        argmin, exact ties to dense), decided on whole-network time because a dense conv's
+        cost depends on its neighbours (NHWC chains, transposes at sparse/dense borders):
+        the per-conv argmin of isolated costs (sparse step + its pool vs the cuDNN conv
+        alone), every "dense from conv k on" split, all sparse and all dense are built,
+        captured and timed; the fastest wins."""
         import torch
         if self.mode != "fp16":
             raise ValueError("the backend dispatcher runs 16b/16b networks only (other modes stay bitwise)")
         torch.backends.cudnn.benchmark = True
+        nl = len(self.geoms)
+        elig = [self.dense_eligible(li) for li in range(nl)]
 
-        def per_conv_ms():
-            out, li_of = {}, None
+        def build(bk):
+            self.backends = list(bk)
+            self.graph = None
+            self._build()
+
+        def per_conv_ms(kind):
+            out = {}
             for st in self.steps:
-                if st[0] == "pool":
-                    li_of_pool = st[1]
-                    out[li_of_pool] = out.get(li_of_pool, 0.0) + time_median_cuda(
-                        lambda: self._run_step(st), repeats, warmup)
+                if (kind == "sparse") != (st[0] != "dense"):
                     continue
                 out[st[1]] = out.get(st[1], 0.0) + time_median_cuda(lambda: self._run_step(st), repeats, warmup)
             return out
 
-        self.backends = ["sparse"] * len(self.geoms)
-        self.graph = None
-        self._build()
-        sparse_ms = per_conv_ms()
-        self.backends = ["dense" if self.dense_eligible(li) else "sparse" for li in range(len(self.geoms))]
-        self._build()
-        dense_ms = per_conv_ms()
-        self.backends = ["dense" if self.dense_eligible(li) and dense_ms[li] <= sparse_ms[li] else "sparse"
-                         for li in range(len(self.geoms))]
-        self.backend_times = {li: {"sparse_ms": sparse_ms[li], "dense_ms": dense_ms[li]}
-                              for li in range(len(self.geoms))}
-        self._build()
+        build(["sparse"] * nl)
+        sparse_ms = per_conv_ms("sparse")
+        build(["dense" if e else "sparse" for e in elig])
+        self.run()
+        torch.cuda.synchronize()
+        dense_ms = {}
+        for st in self.steps:  # the cuDNN conv alone (the chain's transposes are border costs)
+            if st[0] == "dense" and st[2].__name__ == "fn" and st[2].__qualname__.startswith("SparseVGG16._dense_fn"):
+                dense_ms[st[1]] = time_median_cuda(lambda: self._run_step(st), repeats, warmup)
+        argmin = ["dense" if elig[li] and dense_ms.get(li, 1e9) <= sparse_ms[li] else "sparse" for li in range(nl)]
+        cands = {"all-sparse": ["sparse"] * nl, "all-dense": ["dense" if e else "sparse" for e in elig],
+                 "argmin": argmin}
+        for k in range(1, nl):
+            cands[f"dense-from-{k}"] = ["dense" if elig[li] and li >= k else "sparse" for li in range(nl)]
+        times, seen = {}, set()
+        for name, bk in cands.items():
+            if tuple(bk) in seen:
+                continue
+            seen.add(tuple(bk))
+            build(bk)
+            times[name] = self.network_ms()
+        best = min(times, key=times.get)
+        self.backend_times = {li: {"sparse_ms": sparse_ms.get(li), "dense_ms": dense_ms.get(li)} for li in range(nl)}
+        self.backend_search = {k: round(v, 4) for k, v in times.items()}
+        self.backend_pick = best
+        build(cands[best])
         torch.cuda.synchronize()
         return self.backends
 
@@ -311,7 +364,7 @@ class SparseVGG16:
         g0 = self.geoms[0]
         self.in_layout = _lib.act_layout(g0.in_channels, g0.input_h, g0.input_w, 1, 1, self.eb, il)
         self.x_buf = self._buf(self.in_layout)
-        cur_buf, cur_lay = self.x_buf, self.in_layout
+        cur_buf, cur_lay, cur_held = self.x_buf, self.in_layout, None
         self.nonzero_macs = 0
         li = 0
         for i, v in enumerate(VGG16_CIFAR):
@@ -320,19 +373,27 @@ class SparseVGG16:
             g = self.geoms[li]
             nxt = VGG16_CIFAR[i + 1] if i + 1 < len(VGG16_CIFAR) else None
             if self.backends[li] == "dense":
+                # a dense chain stays NHWC; the BI64 form is only materialised before a sparse conv
                 last = i + 2 >= len(VGG16_CIFAR)
+                if cur_held is None:
+                    cur_held = [None]
+                    self.steps.append(("dense", li, self._to_nhwc(cur_buf, cur_lay, cur_held,
+                                                                  (n, g.in_channels, g.input_h, g.input_w))))
                 if nxt == "M":
                     ph = 0 if last else 1
                     out_lay = _lib.act_layout(g.out_channels, g.out_h // 2, g.out_w // 2, ph, ph, self.eb, il)
                 else:
                     out_lay = _lib.act_layout(g.out_channels, g.out_h, g.out_w, 1, 1, self.eb, il)
-                out_buf = self._buf(out_lay)
-                self.steps.append(("dense", li, self._dense_step(li, cur_buf, cur_lay, out_buf, out_lay,
-                                                                 nxt == "M")))
+                out_held = [None]
+                self.steps.append(("dense", li, self._dense_fn(li, cur_held, out_held, nxt == "M")))
                 self.nonzero_macs += int(np.count_nonzero(self.filters[li].weights)) * g.out_h * g.out_w * n
-                cur_buf, cur_lay = out_buf, out_lay
+                cur_buf, cur_lay, cur_held = None, out_lay, out_held
                 li += 1
                 continue
+            if cur_buf is None:  # NHWC -> the BI64 layout this sparse conv reads
+                cur_buf = self._buf(cur_lay)
+                self.steps.append(("dense", li, self._to_bi(cur_held, cur_buf, cur_lay)))
+            cur_held = None
             plan, blob = self._plan_for(li, plan_cfgs[li])
             epi = _lib.Epilogue()
             epi.relu = 1
@@ -372,6 +433,9 @@ class SparseVGG16:
                 self.steps.append(("pool", li, cur_lay, pool_lay, cur_buf, pool_buf))
                 cur_buf, cur_lay = pool_buf, pool_lay
             li += 1
+        if cur_buf is None:
+            cur_buf = self._buf(cur_lay)
+            self.steps.append(("dense", li - 1, self._to_bi(cur_held, cur_buf, cur_lay)))
         self.out_buf, self.out_layout = cur_buf, cur_lay
 
     # -- execution -------------------------------------------------------------
@@ -559,13 +623,10 @@ class SparseVGG16:
         (2-row, even-width pixel blocks) and a plain conv (any tile, e.g. halo-skipping
         pixel classes) followed by the pool kernel."""
         import torch
-        best_cfgs = []
+        best_cfgs = list(self.configs)
         steps = self.steps
         for si, st in enumerate(steps):
-            if st[0] == "dense":
-                best_cfgs.append(self.configs[st[1]])
-                continue
-            if st[0] != "conv":
+            if st[0] != "conv":  # dense convs, transposes and pools have no tile
                 continue
             _, li, plan0, _, xin, yout, epi = st
             g = self.geoms[li]
@@ -610,7 +671,7 @@ class SparseVGG16:
             self.filters[li]._packs.clear()  # drop the candidates' device packs (rebuilt for the pick)
             if li in self.pre_pool:
                 self.fuse_pool[li] = fused
-            best_cfgs.append(pick)
+            best_cfgs[li] = pick
         torch.cuda.synchronize()
         self.configs = best_cfgs
         self.graph = None

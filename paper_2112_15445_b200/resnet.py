@@ -120,28 +120,25 @@ class SparseResNet50:
             self._dense_w[li] = w.contiguous(memory_format=torch.channels_last)
         return self._dense_w[li]
 
-    def _dense_step(self, li, x, x_lay, y, y_lay, relu, residual):
-        """cuDNN (torch conv2d, binary16 on tensor cores, channels_last) for conv li:
-        BI64 -> NHWC, conv, NHWC -> BI64 with the epilogue (saturation, residual, ReLU)."""
+    def _dense_fn(self, li, x_act, relu, res_act, out_act):
+        """cuDNN (torch conv2d: binary16 on tensor cores, channels_last) for conv li on the
+        NHWC form of its input; the epilogue in binary16 as the hooks define it:
+        sat16(conv) (+ shortcut, sat16 again), ReLU; the NHWC result becomes out_act's."""
         import torch
         _, g, role, s = self.layers[li]
-        n, C, D = self.batch, g.in_channels, g.out_channels
-        k = g.filter_h
-        xin = torch.empty((n, C, x_lay.height, x_lay.width), dtype=torch.float16, device=self.device,
-                          memory_format=torch.channels_last)
         w = self._dense_weight(li)
-        res, res_lay = (None, None) if residual is None else residual
-        L = _lib.lib()
+        k = g.filter_h
 
         def fn(stream=None):
-            sp = _lib.stream_ptr(stream)
-            _lib.check(L.usc_bi_to_nhwc(_lib.ref(x_lay), n, _lib.t_ptr(x), _lib.t_ptr(xin), sp), "bi_to_nhwc")
-            yo = torch.nn.functional.conv2d(xin, w, stride=s, padding=k // 2)
-            if not yo.is_contiguous(memory_format=torch.channels_last):
-                yo = yo.contiguous(memory_format=torch.channels_last)
-            _lib.check(L.usc_nhwc_to_bi(_lib.ref(y_lay), n, _lib.t_ptr(yo), _lib.t_ptr(y),
-                                        None if res is None else _lib.ref(res_lay),
-                                        None if res is None else _lib.t_ptr(res), int(relu), sp), "nhwc_to_bi")
+            y = torch.nn.functional.conv2d(x_act.nhwc_now(), w, stride=s, padding=k // 2)
+            y = y.clamp_(-65504.0, 65504.0)  # binary16 hook: finite overflow saturates (tensor.py:55-60)
+            if res_act is not None:
+                y = y.add_(res_act.nhwc_now()).clamp_(-65504.0, 65504.0)
+            if relu:  # where(v > 0, v, 0): NaN -> 0
+                y = torch.where(y > 0, y, torch.zeros((), dtype=y.dtype, device=y.device))
+            if not y.is_contiguous(memory_format=torch.channels_last):
+                y = y.contiguous(memory_format=torch.channels_last)
+            out_act.held[0] = y
         return fn
 
     # -- buffers -------------------------------------------------------------------
@@ -153,28 +150,74 @@ class SparseResNet50:
         return torch.zeros(lay.elems(self.batch), dtype=self.tdtype, device=self.device)
 
     def _build(self):
+        """Steps in execution order.  Every activation has a canonical BI64 layout (the halo
+        its sparse consumers read) and, when a dense (cuDNN) conv touches it, an NHWC form;
+        a form is materialised by a transpose step the first time a consumer needs it, so a
+        chain of dense convs stays in NHWC and transposes only run at sparse/dense borders."""
+        import torch
         n = self.batch
-        self.steps = []  # (li, plan, blob, x, x_view_layout | None, y, epilogue)
+        net = self
+        self.steps = []  # (li, plan, blob, x, x_view_layout | None, y, epilogue) | (li, None, .., fn)
         self.in_layout = self._lay(3, 32, 1)
         self.x_buf = self._buf(self.in_layout)
+        L = _lib.lib()
 
-        def conv(li, x, x_lay, y_lay, relu=True, residual=None):
+        class Act:
+            def __init__(self, c, hw, lay, buf=None):
+                self.c, self.hw, self.lay, self.buf = c, hw, lay, buf
+                self.held = [None]  # NHWC tensor (written at run time by its producer)
+                self.has_nhwc = False
+
+            def bi(self):  # the BI64 buffer, adding an NHWC -> BI transpose the first time
+                if self.buf is None:
+                    self.buf = net._buf(self.lay)
+                    act = self
+
+                    def fn(stream=None):
+                        _lib.check(L.usc_nhwc_to_bi(_lib.ref(act.lay), n, _lib.t_ptr(act.held[0]),
+                                                    _lib.t_ptr(act.buf), None, None, 0,
+                                                    _lib.stream_ptr(stream)), "nhwc_to_bi")
+                    net.steps.append((-1, None, None, None, None, None, fn))
+                return self.buf
+
+            def nhwc(self):  # request the NHWC form, adding a BI -> NHWC transpose the first time
+                if not self.has_nhwc:
+                    self.has_nhwc = True
+                    t = torch.empty((n, self.c, self.hw, self.hw), dtype=torch.float16, device=net.device,
+                                    memory_format=torch.channels_last)
+                    self.held[0] = t
+                    act = self
+
+                    def fn(stream=None):
+                        _lib.check(L.usc_bi_to_nhwc(_lib.ref(act.lay), n, _lib.t_ptr(act.buf), _lib.t_ptr(t),
+                                                    _lib.stream_ptr(stream)), "bi_to_nhwc")
+                        act.held[0] = t
+                    net.steps.append((-1, None, None, None, None, None, fn))
+                return self
+
+            def nhwc_now(self):
+                return self.held[0]
+
+        def conv(li, xa, c_out, hw_out, halo, relu=True, residual=None):
             name, g, role, s = self.layers[li]
+            ya = Act(c_out, hw_out, self._lay(c_out, hw_out, halo))
             if self.backends[li] == "dense":
-                y = self._buf(y_lay)
-                self.steps.append((li, None, None, x, None, y, self._dense_step(li, x, x_lay, y, y_lay, relu,
-                                                                                residual)))
-                return y
+                xa.nhwc()
+                if residual is not None:
+                    residual.nhwc()
+                ya.has_nhwc = True
+                self.steps.append((li, None, None, None, None, None, self._dense_fn(li, xa, relu, residual, ya)))
+                return ya
+            x, x_lay = xa.bi(), xa.lay
             plan, blob = plan_for(self.filters[li], n, self.dtype, self.configs[li], self.filters[li].weights,
                                   device=self.device)
             if plan.in_.interleave != 64:
                 raise RuntimeError(f"{name}: the network needs BI64 plans")
-            y = self._buf(y_lay)
             e = _lib.Epilogue()
-            e.relu, e.scale, e.out_padded, e.out = int(relu), 1.0, 1, y_lay
+            e.relu, e.scale, e.out_padded, e.out = int(relu), 1.0, 1, ya.lay
             if residual is not None:
-                r, r_lay = residual
-                e.residual, e.res_layout, e.res = 1, r_lay, r.data_ptr()
+                e.residual, e.res_layout, e.res = 1, residual.lay, residual.bi().data_ptr()
+            y = ya.bi()
             # a window of a larger buffer (the stride-2 exact geometries) goes through the view
             # entry; a stride-2 projection through the strided view
             step = self.eff[li][1]
@@ -186,37 +229,31 @@ class SparseResNet50:
             elif (plan.in_.hp, plan.in_.ws) != (x_lay.hp, x_lay.ws):
                 view = (x_lay, 1)
             self.steps.append((li, plan, blob, x, view, y, e))
-            return y
+            return ya
 
-        cur, cur_lay = self.x_buf, self.in_layout
+        cur = Act(3, 32, self.in_layout, self.x_buf)
         li = 0
-        cur = conv(li, cur, cur_lay, self._lay(64, 32, 0))  # stem (its output feeds 1x1 convs)
-        cur_lay = self._lay(64, 32, 0)
+        cur = conv(li, cur, 64, 32, 0)  # stem (its output feeds 1x1 convs)
         li += 1
-        hw, c_in = 32, 64
+        hw = 32
         for width, blocks, stride in STAGES:
             for b in range(blocks):
                 s = stride if b == 0 else 1
                 hw_out = hw // s
-                blk_in, blk_lay = cur, cur_lay
-                h1_lay = self._lay(width, hw, 1)
-                h1 = conv(li, blk_in, blk_lay, h1_lay)
+                blk_in = cur
+                h1 = conv(li, blk_in, width, hw, 1)
                 li += 1
-                h2_lay = self._lay(width, hw_out, 0)
-                h2 = conv(li, h1, h1_lay, h2_lay)
+                h2 = conv(li, h1, width, hw_out, 0)
                 li += 1
                 if b == 0:
-                    sc_lay = self._lay(4 * width, hw_out, 0)
-                    sc = conv(li, blk_in, blk_lay, sc_lay, relu=False)
+                    sc = conv(li, blk_in, 4 * width, hw_out, 0, relu=False)
                     li += 1
                 else:
-                    sc, sc_lay = blk_in, blk_lay
-                out_lay = self._lay(4 * width, hw_out, 0)
-                cur = conv(li, h2, h2_lay, out_lay, relu=True, residual=(sc, sc_lay))
-                cur_lay = out_lay
+                    sc = blk_in
+                cur = conv(li, h2, 4 * width, hw_out, 0, relu=True, residual=sc)
                 li += 1
-                hw, c_in = hw_out, 4 * width
-        self.out_buf, self.out_layout = cur, cur_lay
+                hw = hw_out
+        self.out_buf, self.out_layout = cur.bi(), cur.lay
 
     # -- execution -------------------------------------------------------------------
     def _launch(self, st, stream=None):
@@ -296,11 +333,10 @@ class SparseResNet50:
     def autotune(self, repeats: int = 3, warmup: int = 1, noise_floor: float = 0.02):
         """Per-conv tile search on the network's own buffers and epilogues."""
         import torch
-        picks = []
+        picks = list(self.configs)
         for st in self.steps:
             li, plan0, _, x, view, y, e = st
-            if plan0 is None:  # dense step: keep its (unused) sparse config
-                picks.append(self.configs[li])
+            if plan0 is None:  # dense conv or transpose: no tile to search
                 continue
             g = self.eff[li][0]
             cands = [self.configs[li]] + [c for c in tile_candidates(g, self.batch, [1], self.precision, (3,))
@@ -319,7 +355,7 @@ class SparseResNet50:
                     continue
                 res.append((ms, cfg))
             best = min(ms for ms, _ in res)
-            picks.append(next(cfg for ms, cfg in res if ms <= best * (1.0 + noise_floor)))
+            picks[li] = next(cfg for ms, cfg in res if ms <= best * (1.0 + noise_floor))
             self.filters[li]._packs.clear()
         torch.cuda.synchronize()
         self.configs = picks
@@ -327,26 +363,71 @@ class SparseResNet50:
         self._build()
         return picks
 
+    def network_ms(self, steps: int = 10) -> float:
+        """Median device time of one captured forward (CUDA graph replay)."""
+        import torch
+        self.capture()
+        for _ in range(3):
+            self.graph.replay()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(steps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            self.graph.replay()
+            b.record()
+            b.synchronize()
+            ts.append(a.elapsed_time(b))
+        return float(np.median(ts))
+
     def autotune_backends(self, repeats: int = 5, warmup: int = 2) -> list:
-        """Per-conv sparse vs cuDNN choice on the network's own buffers (binary16 only):
-        the sparse step with its tuned tile against the dense step (transposes + cuDNN +
-        fused epilogue); argmin, exact ties to dense (backend_config, bench.py:212-227)."""
+        """Sparse vs cuDNN per conv (binary16 only; the reference's backend_config rule,
+        bench.py:212-227: argmin, exact ties to dense).  A dense conv's cost depends on
+        its neighbours (transposes only at sparse/dense borders), so the choice is made on
+        whole-network time: the per-conv argmin of the isolated costs (sparse step vs the
+        cuDNN conv alone), every "dense from block k on" split, all sparse and all dense
+        are each built, captured and timed, and the fastest assignment wins."""
         import torch
         if self.dtype != _lib.USC_F16:
             raise ValueError("the backend dispatcher runs binary16 networks only (fp32 stays bitwise)")
         torch.backends.cudnn.benchmark = True
-        self.backends = ["sparse"] * len(self.layers)
-        self.graph = None
-        self._build()
-        sparse_ms = {st[0]: time_median_cuda(lambda: self._launch(st), repeats, warmup) for st in self.steps}
-        self.backends = ["dense" if self.dense_eligible(li) else "sparse" for li in range(len(self.layers))]
-        self._build()
-        dense_ms = {st[0]: time_median_cuda(lambda: self._launch(st), repeats, warmup) for st in self.steps
-                    if st[1] is None}
-        self.backends = ["dense" if li in dense_ms and dense_ms[li] <= sparse_ms[li] else "sparse"
-                         for li in range(len(self.layers))]
-        self.backend_times = {self.layers[li][0]: {"sparse_ms": sparse_ms[li], "dense_ms": dense_ms.get(li)}
-                              for li in range(len(self.layers))}
-        self._build()
+        nl = len(self.layers)
+        elig = [self.dense_eligible(li) for li in range(nl)]
+
+        def build(backends):
+            self.backends = list(backends)
+            self.graph = None
+            self._build()
+
+        build(["sparse"] * nl)
+        sparse_ms = {st[0]: time_median_cuda(lambda: self._launch(st), repeats, warmup)
+                     for st in self.steps if st[1] is not None}
+        build(["dense" if e else "sparse" for e in elig])
+        self.run()  # materialise every NHWC form once
+        torch.cuda.synchronize()
+        dense_ms = {st[0]: time_median_cuda(lambda: self._launch(st), repeats, warmup)
+                    for st in self.steps if st[1] is None and st[0] >= 0}
+        argmin = ["dense" if elig[li] and dense_ms[li] <= sparse_ms[li] else "sparse" for li in range(nl)]
+        blocks = [li for li, (name, _, role, _) in enumerate(self.layers) if role == "c1"]
+        cands = {"all-sparse": ["sparse"] * nl, "all-dense": ["dense" if e else "sparse" for e in elig],
+                 "argmin": argmin}
+        for k in blocks:
+            cands[f"dense-from-{self.layers[k][0]}"] = ["dense" if elig[li] and li >= k else "sparse"
+                                                        for li in range(nl)]
+            cands[f"argmin-then-dense-from-{self.layers[k][0]}"] = [
+                "dense" if elig[li] and li >= k else argmin[li] for li in range(nl)]
+        times = {}
+        for name, bk in cands.items():
+            key = tuple(bk)
+            if key in {tuple(v) for n2, v in cands.items() if n2 in times}:
+                continue
+            build(bk)
+            times[name] = self.network_ms()
+        best = min(times, key=times.get)
+        self.backend_times = {self.layers[li][0]: {"sparse_ms": sparse_ms.get(li), "dense_ms": dense_ms.get(li)}
+                              for li in range(nl)}
+        self.backend_search = {k: round(v, 4) for k, v in times.items()}
+        self.backend_pick = best
+        build(cands[best])
         torch.cuda.synchronize()
         return self.backends

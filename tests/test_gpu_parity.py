@@ -471,3 +471,30 @@ def test_native_autotune_c_abi(name):
     cfg = autotune_native(xd, f, repeats=3, warmup=1)
     assert cfg.kernel in (1, 3)
     assert sha(U.sparse_conv_forward(xd, f, cfg).data) == rec["out"]
+
+
+def test_run_bench_harness_on_gpu():
+    """layer_bench.run_bench (bench.py:143-166) end to end on the GPU: presets x
+    precisions x sparsities with the reference's seeding, CSV round trip and the
+    per-layer backend choice (bench.py:212-227); the timed sparse layer equals the
+    reference's output on the same seeded inputs."""
+    import zlib
+    from paper_2112_15445_b200 import layer_bench as LB
+    rep = LB.run_bench({"layers": ["cnn1d-300x64-k2", "resnet50-1x1-256x64"], "sparsities": [0.9],
+                        "precisions": ["binary32", "binary16"], "batch": 8, "repeats": 3, "warmup": 1})
+    assert len(rep.rows) == 4 and rep.environment["gpu"]
+    for r in rep.rows:
+        assert r.sparse_ms > 0 and r.dense_ms > 0 and r.dense_backend == "cudnn"
+    rows = LB.rows_from_csv(LB.rows_to_csv(rep.rows))
+    cfg = LB.backend_config(rows, expected_layers=[r.layer_id for r in rep.rows])
+    assert set(v["backend"] for v in cfg.values()) <= {"sparse", "dense"}
+    # the seeded layer the harness timed, recomputed, against the oracle
+    g = LB.preset_geometry("resnet50-1x1-256x64")
+    rng = np.random.default_rng([0, zlib.crc32(b"resnet50-1x1-256x64"), 900])
+    w = U.pruning.synthesize_masked_weights(g, 0.9, rng)
+    x = rng.standard_normal((8, g.in_channels, g.input_h, g.input_w)).astype(np.float32)
+    f = U.build_csr(w, g)
+    out = U.sparse_conv_forward(_dev(x), f).data
+    gt = (g.in_channels, g.out_channels, 1, 1, g.input_h, g.input_w, (1, 1), (0, 0))
+    ref = oracle.sparse_conv_forward(x, (f.row_ptr, f.col_offsets, f.weights, f.n_nz), gt)
+    assert np.array_equal(out, ref)

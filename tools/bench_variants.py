@@ -133,6 +133,8 @@ def dispatched(m, name, steps, flush, cudnn_ms):
            "speedup_vs_cudnn": round(cudnn_ms / ms, 3), "sparse_layers": backends.count("sparse"),
            "dense_layers": backends.count("dense"), "backends": backends,
            "rule": "per-conv argmin of the sparse step vs transpose + cuDNN + fused epilogue, ties to dense"}
+    if hasattr(m, "backend_search"):
+        out["pick"], out["search"] = m.backend_pick, m.backend_search
     if hasattr(m, "backend_times"):
         out["per_conv_ms"] = {str(k): {a: (round(b, 4) if b is not None else None) for a, b in v.items()}
                               for k, v in m.backend_times.items()}
