@@ -288,6 +288,9 @@ int usc_sparse_conv_blocks(const float *xflat, const int64_t *row_ptr, const int
 int usc_bi_to_nhwc(const usc_act_layout *l, int32_t n, const void *src, void *dst, void *stream);
 int usc_nhwc_to_bi(const usc_act_layout *l, int32_t n, const void *src, void *dst, const usc_act_layout *res_layout,
                    const void *res, int32_t relu, void *stream);
+/* The same epilogue in place on `count` binary16 values of any layout (a cuDNN layer's
+ * NHWC output inside a dense chain): v = sat16(y); res: v = sat16(v + r); ReLU when relu. */
+int usc_f16_epilogue(void *y, const void *res, int64_t count, int32_t relu, void *stream);
 /* round_to_binary16 (tensor.py:48-63) on device: f32 in -> f32 on the binary16 grid
  * (to_half == 0) or binary16 storage (to_half == 1). */
 int usc_round_binary16(const float *src, void *dst, int64_t count, int32_t to_half, void *stream);

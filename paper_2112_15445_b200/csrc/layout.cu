@@ -126,6 +126,22 @@ __global__ void k_nhwc_to_bi(const __half *__restrict__ src, uint32_t *__restric
     }
 }
 
+// in place, any layout (elementwise): v = sat16(y); residual: v = sat16(v + r); ReLU
+__global__ void k_f16_epilogue(uint32_t *__restrict__ y, const uint32_t *__restrict__ res, long long words,
+                               int relu) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < words;
+         i += (long long)gridDim.x * blockDim.x) {
+        uint32_t w = sat16x2(y[i]);
+        if (res) {
+            const uint32_t rw = __ldg(res + i);
+            __half2 s = __hadd2(*reinterpret_cast<const __half2 *>(&w), *reinterpret_cast<const __half2 *>(&rw));
+            w = sat16x2(*reinterpret_cast<uint32_t *>(&s));
+        }
+        if (relu) w = relu16x2(w);
+        y[i] = w;
+    }
+}
+
 int check_bi(const usc_act_layout *l, int32_t n) {
     if (!l || n < 1) return usc::fail(USC_ERR_VALUE, "layout conversion: bad arguments");
     if (l->interleave != 64) return usc::fail(USC_ERR_UNSUPPORTED, "layout conversion needs the BI64 layout");
@@ -164,4 +180,16 @@ int usc_nhwc_to_bi(const usc_act_layout *l, int32_t n, const void *src, void *ds
         static_cast<const uint32_t *>(res), R, relu, units);
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? USC_OK : usc::fail(USC_ERR_CUDA, "k_nhwc_to_bi: %s", cudaGetErrorString(e));
+}
+
+int usc_f16_epilogue(void *y, const void *res, int64_t count, int32_t relu, void *stream) {
+    if (!y || count < 0 || (count & 1)) return usc::fail(USC_ERR_VALUE, "f16 epilogue: even element count needed");
+    const long long words = count / 2;
+    if (!words) return USC_OK;
+    const long long blocks = (words + 255) / 256;
+    k_f16_epilogue<<<static_cast<int>(blocks < 148LL * 32 ? blocks : 148LL * 32), 256, 0,
+                     static_cast<cudaStream_t>(stream)>>>(static_cast<uint32_t *>(y),
+                                                          static_cast<const uint32_t *>(res), words, relu);
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? USC_OK : usc::fail(USC_ERR_CUDA, "k_f16_epilogue: %s", cudaGetErrorString(e));
 }

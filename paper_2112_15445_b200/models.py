@@ -232,13 +232,19 @@ class SparseVGG16:
             self._dense_w[li] = w.contiguous(memory_format=torch.channels_last)
         w = self._dense_w[li]
 
+        L = _lib.lib()
+
         def fn(stream=None):
-            y = torch.nn.functional.conv2d(x_held[0], w, padding=1).clamp_(-65504.0, 65504.0)
-            y = torch.where(y > 0, y, torch.zeros((), dtype=y.dtype, device=y.device))
-            if pool:
-                y = torch.nn.functional.max_pool2d(y, 2)
+            y = torch.nn.functional.conv2d(x_held[0], w, padding=1)
             if not y.is_contiguous(memory_format=torch.channels_last):
                 y = y.contiguous(memory_format=torch.channels_last)
+            # one in-place pass: sat16 (the binary16 hook) and ReLU (NaN -> 0), then the pool
+            _lib.check(L.usc_f16_epilogue(_lib.t_ptr(y), None, y.numel(), 1, _lib.stream_ptr(stream)),
+                       "f16 epilogue")
+            if pool:
+                y = torch.nn.functional.max_pool2d(y, 2)
+                if not y.is_contiguous(memory_format=torch.channels_last):
+                    y = y.contiguous(memory_format=torch.channels_last)
             out_held[0] = y
         return fn
 

@@ -129,15 +129,16 @@ class SparseResNet50:
         w = self._dense_weight(li)
         k = g.filter_h
 
+        L = _lib.lib()
+
         def fn(stream=None):
             y = torch.nn.functional.conv2d(x_act.nhwc_now(), w, stride=s, padding=k // 2)
-            y = y.clamp_(-65504.0, 65504.0)  # binary16 hook: finite overflow saturates (tensor.py:55-60)
-            if res_act is not None:
-                y = y.add_(res_act.nhwc_now()).clamp_(-65504.0, 65504.0)
-            if relu:  # where(v > 0, v, 0): NaN -> 0
-                y = torch.where(y > 0, y, torch.zeros((), dtype=y.dtype, device=y.device))
             if not y.is_contiguous(memory_format=torch.channels_last):
                 y = y.contiguous(memory_format=torch.channels_last)
+            # one in-place pass: sat16 (binary16 hook, tensor.py:55-60), + shortcut, sat16, ReLU
+            r = None if res_act is None else res_act.nhwc_now()
+            _lib.check(L.usc_f16_epilogue(_lib.t_ptr(y), None if r is None else _lib.t_ptr(r), y.numel(),
+                                          int(relu), _lib.stream_ptr(stream)), "f16 epilogue")
             out_act.held[0] = y
         return fn
 
@@ -217,7 +218,7 @@ class SparseResNet50:
             e.relu, e.scale, e.out_padded, e.out = int(relu), 1.0, 1, ya.lay
             if residual is not None:
                 e.residual, e.res_layout, e.res = 1, residual.lay, residual.bi().data_ptr()
-            y = ya.bi()
+            y = ya.buf = self._buf(ya.lay)
             # a window of a larger buffer (the stride-2 exact geometries) goes through the view
             # entry; a stride-2 projection through the strided view
             step = self.eff[li][1]
