@@ -157,3 +157,71 @@ def test_autotune_backends_picks_and_runs():
     assert ok, err
     with pytest.raises(ValueError):
         SparseResNet50(resnet50_weights(0.9, seed=6), 64).autotune_backends()
+
+
+@pytest.mark.parametrize("net", ["vgg16", "resnet50"])
+def test_benchmarked_dispatch_states_within_tolerance(net):
+    """The committed dispatcher picks (profiles/r02_tuned_<net>_fp16_dispatch.json: tiles and
+    per-conv backends, as bench_variants times them) at batch 256 against the oracle
+    composition, on He-scaled weights (the fp16 tolerance is meaningless once the
+    raw-N(0,1) networks saturate)."""
+    import json
+    import os
+
+    import torch
+    state = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles",
+                                        f"r02_tuned_{net}_fp16_dispatch.json")))
+    assert "dense" in state["backends"] and "sparse" in state["backends"]
+    x = oracle.round_to_binary16(np.random.default_rng(31).standard_normal((256, 3, 32, 32)).astype(np.float32))
+    th = oracle.max_threads()
+    if net == "vgg16":
+        from paper_2112_15445_b200.models import VGG16_CIFAR, SparseVGG16, vgg16_rng, vgg16_weights
+        ws = _tame(vgg16_weights(vgg16_rng(0.93, 0), 0.93, precision=F16), 0.07)
+        m = SparseVGG16(ws, 256, precision=F16)
+        m.load_tuned_state(state)
+        m.capture()
+        got = m.forward(torch.from_numpy(x).cuda().half()).float().cpu().numpy()
+        a, li = x, 0
+        for v in VGG16_CIFAR:
+            if v == "M":
+                a = oracle.maxpool2(a)
+                continue
+            g = m.geoms[li]
+            gt = (g.in_channels, g.out_channels, 3, 3, g.input_h, g.input_w, (1, 1), (1, 1))
+            a = oracle.relu(oracle.sparse_conv_forward(a, oracle.build_csr(ws[li].data, gt), gt, binary16=True,
+                                                       threads=th))
+            li += 1
+    else:
+        from paper_2112_15445_b200.resnet import STAGES, SparseResNet50, resnet50_layers, resnet50_weights
+        ws = _tame(resnet50_weights(0.9, 0, F16), 0.1)
+        layers = resnet50_layers()
+        m = SparseResNet50(ws, 256, precision=F16)
+        m.load_tuned_state(state)
+        m.capture()
+        got = m.forward(torch.from_numpy(x).cuda().half()).float().cpu().numpy()
+
+        def conv(li, a):
+            _, g, role, s = layers[li]
+            if role == "c2" and s == 2:
+                a = np.pad(a, ((0, 0), (0, 0), (1, 0), (1, 0)))
+            if role == "proj" and s == 2:
+                a = np.ascontiguousarray(a[:, :, :g.input_h, :g.input_w])
+            gt = (g.in_channels, g.out_channels, g.filter_h, g.filter_w, g.input_h, g.input_w, g.stride, g.padding)
+            return oracle.round_to_binary16(oracle.sparse_conv_forward(
+                a, oracle.build_csr(np.ascontiguousarray(ws[li].data), gt), gt, threads=th))
+
+        a = oracle.relu(conv(0, x))
+        li = 1
+        for width, blocks, stride in STAGES:
+            for b in range(blocks):
+                h2 = oracle.relu(conv(li + 1, oracle.relu(conv(li, a))))
+                li += 2
+                if b == 0:
+                    sc = conv(li, a)
+                    li += 1
+                else:
+                    sc = a
+                a = oracle.relu(oracle.round_to_binary16((conv(li, h2) + sc).astype(np.float32)))
+                li += 1
+    ok, err = _close(got, a)
+    assert ok, err
