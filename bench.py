@@ -457,10 +457,18 @@ def main():
     import torch
     import torch.distributed as dist
     from paper_2112_15445_b200.sharding import ShardedRun
-    torch.cuda.set_device(local_rank)
-    device = torch.device("cuda", local_rank)
+    # BENCH_SHARE_GPU=1 + BENCH_DIST_BACKEND=gloo: every rank on cuda:0 -- a test hook that
+    # exercises the multi-rank path (launch, barriers, max over ranks, final gather) on a
+    # one-GPU box; the numbers of such a run are not a scaling measurement
+    gpu = 0 if os.environ.get("BENCH_SHARE_GPU") == "1" else local_rank
+    torch.cuda.set_device(gpu)
+    device = torch.device("cuda", gpu)
     if world > 1:
-        dist.init_process_group("nccl", device_id=device)
+        backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=device)
+        else:
+            dist.init_process_group(backend)
     if args.global_batch:
         job = ShardedRun(args.global_batch, rank, world, align=64)
         scaling = "strong"
@@ -504,7 +512,7 @@ def main():
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    with ClockSampler(local_rank) as clk:
+    with ClockSampler(gpu) as clk:
         for a, b in evs:
             flush.zero_()
             a.record()
@@ -588,7 +596,7 @@ def main():
     hbm_peak, peak_kind = measured_peaks()
     plan = next(st[2] for st in model.steps if st[0] == "conv" and st[1] == dom)
     mix = 1 if plan.kernel in (3, 4) and plan.NS == 64 else 0
-    core_peak = mix_peak(local_rank, mix)
+    core_peak = mix_peak(gpu, mix)
     s = stats[dom]
     achieved_gbs = s["bytes"] / (dom_ms / 1e3) / 1e9
     achieved_tf = s["flops"] / (dom_ms / 1e3) / 1e12

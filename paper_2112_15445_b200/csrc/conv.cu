@@ -264,6 +264,42 @@ __global__ void k_pad_any(const T *__restrict__ src, TD *__restrict__ dst, int n
     }
 }
 
+// plain NCHW -> a batch-interleaved layout, one CTA per (sample block, channel, padded
+// row): the IL samples x 32 pixels of a row segment go through a [IL][33] shared tile so
+// the NCHW reads (pixels contiguous per sample) and the BI writes (samples contiguous per
+// pixel) are both coalesced; halo rows / columns and samples past n are written as zeros.
+template <typename T, typename TD = T>
+__global__ void k_pad_bi(const T *__restrict__ src, TD *__restrict__ dst, int n, int H, int W, const LayoutD L) {
+    __shared__ T tile[64][33];
+    const int IL = L.il;
+    const int yp = blockIdx.x % L.Hp;
+    const int c = (blockIdx.x / L.Hp) % L.C;
+    const long long nb = blockIdx.x / ((long long)L.Hp * L.C);
+    TD *drow = dst + nb * L.ss + ((long long)c * L.Hp + yp) * L.Ws * IL;
+    const int iy = yp - L.ph;
+    const bool rowin = iy >= 0 && iy < H;
+    for (int x0 = 0; x0 < L.Ws; x0 += 32) {
+        for (int i = threadIdx.x; i < IL * 32; i += blockDim.x) {
+            const int sm = i >> 5, xx = i & 31, ix = x0 + xx - L.pw;
+            const long long b = nb * IL + sm;
+            T v{};
+            if (rowin && b < n && ix >= 0 && ix < W) v = src[((b * L.C + c) * H + iy) * W + ix];
+            tile[sm][xx] = v;
+        }
+        __syncthreads();
+        for (int i = threadIdx.x; i < IL * 32; i += blockDim.x) {
+            const int xx = i / IL, sm = i - xx * IL, xp = x0 + xx;
+            if (xp < L.Ws) {
+                if constexpr (std::is_same<T, TD>::value)
+                    drow[(long long)xp * IL + sm] = tile[sm][xx];
+                else  // int8 code -> binary16 (exact)
+                    drow[(long long)xp * IL + sm] = __short2half_rn(static_cast<short>(tile[sm][xx]));
+            }
+        }
+        __syncthreads();
+    }
+}
+
 // any layout -> plain NCHW (n x C x H x W)
 template <typename T>
 __global__ void k_unpad_any(const T *__restrict__ src, T *__restrict__ dst, int H, int W, const LayoutD L,
@@ -683,6 +719,28 @@ int usc_pad_input(const usc_act_layout *l, int32_t dtype, int32_t n, const void 
     const long long total = usc_act_layout_elems(l, n);
     const int grid = grid_for(total);
     const LayoutD L = to_dev(*l);
+    if (l->interleave) {  // batch-interleaved: the tiled transpose
+        const long long blocks = (long long)((n + l->interleave - 1) / l->interleave) * l->channels * l->hp;
+        if (blocks > 0x7fffffffLL) return fail(USC_ERR_UNSUPPORTED, "pad: too many rows");
+        switch (usc::elem_bytes(dtype)) {
+            case 4:
+                k_pad_bi<float><<<(unsigned)blocks, 256, 0, st>>>(static_cast<const float *>(src),
+                                                                   static_cast<float *>(dst), n, l->height, l->width, L);
+                break;
+            case 2:
+                k_pad_bi<uint16_t><<<(unsigned)blocks, 256, 0, st>>>(static_cast<const uint16_t *>(src),
+                                                                      static_cast<uint16_t *>(dst), n, l->height,
+                                                                      l->width, L);
+                break;
+            case 1:  // the BI kernel stages int8 codes as binary16
+                k_pad_bi<int8_t, __half><<<(unsigned)blocks, 256, 0, st>>>(static_cast<const int8_t *>(src),
+                                                                            static_cast<__half *>(dst), n, l->height,
+                                                                            l->width, L);
+                break;
+            default: return fail(USC_ERR_VALUE, "unknown dtype %d", dtype);
+        }
+        return cuda_check("k_pad_bi launch");
+    }
     switch (usc::elem_bytes(dtype)) {
         case 4:
             k_pad_any<float><<<grid, 256, 0, st>>>(static_cast<const float *>(src), static_cast<float *>(dst),
