@@ -497,10 +497,10 @@ def main():
     model.load_input(x_dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=device)  # 2x L2
 
+    io_graph = model.capture(io_src=x_dev)  # pad of the resident input + 18 launches + unpack
+
     def step():  # one pass: pad the resident input into the BI layout, the 18 launches, unpack
-        model.load_input(x_dev)
-        model.graph.replay()
-        model.output()
+        io_graph.replay()
 
     for _ in range(args.warmup):
         step()
@@ -666,7 +666,7 @@ def main():
                            "parallelism": f"dp{world} (batch-sharded, no collective in the timed step; "
                                           f"final all_gather in the e2e leg)",
                            "l2": "flushed (256 MiB write) between timed steps",
-                           "timed_step": "input pad into the BI64 layout + CUDA graph (13 conv + pools) + "
+                           "timed_step": "one CUDA graph: input pad into the BI64 layout + 13 conv + pools + "
                                          "output unpack, device-resident input",
                            "cuda_graph": True,
                            "tiles": (os.path.relpath(args.configs, ROOT) + " (committed autotuner result)")

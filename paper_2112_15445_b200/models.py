@@ -580,19 +580,30 @@ class SparseVGG16:
         done.record(cur)
         return done
 
-    def capture(self):
-        """Capture run() as one CUDA graph (launch-bound small layers)."""
+    def capture(self, io_src=None):
+        """Capture run() as one CUDA graph (launch-bound small layers), kept as self.graph.
+        With ``io_src`` (a resident NCHW input tensor) a separate graph is returned that also
+        holds the input pad into the BI layout and the output unpack (``output()``'s
+        buffer): one replay = one full pass over that input."""
         import torch
         s = torch.cuda.Stream(device=self.device)
         s.wait_stream(torch.cuda.current_stream())
+
+        def body():
+            if io_src is not None:
+                self.load_input(io_src)
+            self.run()
+            if io_src is not None:
+                self.output()
         with torch.cuda.stream(s):
-            self.run()  # warm (attributes, lazy init) outside capture
+            body()  # warm (attributes, lazy init, the output buffer) outside capture
         torch.cuda.current_stream().wait_stream(s)
         torch.cuda.synchronize()
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g):
-            self.run()
-        self.graph = g
+            body()
+        if io_src is None:  # forward() / stream_forward() replay the run()-only graph
+            self.graph = g
         return g
 
     @property
