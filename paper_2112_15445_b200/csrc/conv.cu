@@ -300,19 +300,21 @@ __global__ void k_pad_bi(const T *__restrict__ src, TD *__restrict__ dst, int n,
     }
 }
 
-// any layout -> plain NCHW (n x C x H x W)
-template <typename T>
+// any layout -> plain NCHW (n x C x H x W); index arithmetic in 32 bits when the
+// element count allows (64-bit division is a long emulated sequence)
+template <typename T, typename I>
 __global__ void k_unpad_any(const T *__restrict__ src, T *__restrict__ dst, int H, int W, const LayoutD L,
                             long long total) {
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
-         i += (long long)gridDim.x * blockDim.x) {
+    for (long long i0 = blockIdx.x * (long long)blockDim.x + threadIdx.x; i0 < total;
+         i0 += (long long)gridDim.x * blockDim.x) {
+        const I i = static_cast<I>(i0);
         const int x = static_cast<int>(i % W);
-        long long t = i / W;
+        I t = i / W;
         const int y = static_cast<int>(t % H);
         t /= H;
         const int c = static_cast<int>(t % L.C);
         const long long b = t / L.C;
-        dst[i] = src[lay_index(L, b, c, y, x)];
+        dst[i0] = src[lay_index(L, b, c, y, x)];
     }
 }
 
@@ -336,13 +338,14 @@ __global__ void k_h2f(const __half *__restrict__ src, float *__restrict__ dst, l
 // nn.MaxPool2.forward (nn.py:124-135): value at np.argmax of the 2x2 window in
 // order (0,0),(0,1),(1,0),(1,1) -- first NaN if any, else first maximum.
 // Works between any two layouts; output-ordered (sample fastest for BI layouts).
-template <typename T>
+template <typename T, typename I>
 __global__ void k_maxpool2(const T *__restrict__ src, T *__restrict__ dst, int n_total, int C, int OH,
                            int OW, const LayoutD Li, const LayoutD Lo) {
     const long long total = (long long)n_total * C * OH * OW;
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
-         i += (long long)gridDim.x * blockDim.x) {
-        long long t = i;
+    for (long long i0 = blockIdx.x * (long long)blockDim.x + threadIdx.x; i0 < total;
+         i0 += (long long)gridDim.x * blockDim.x) {
+        const long long i = i0;
+        I t = static_cast<I>(i0);  // 32-bit index arithmetic when the count allows
         int lane = 0;
         if (Lo.il) {
             lane = static_cast<int>(t % Lo.il);
@@ -772,19 +775,19 @@ int usc_unpad_output(const usc_act_layout *l, int32_t dtype, int32_t n, const vo
     const long long total = (long long)n * l->channels * l->height * l->width;
     const int grid = grid_for(total);
     const LayoutD L = to_dev(*l);
+    const bool small = total < 0x7fffffffLL;
     switch (usc::elem_bytes(dtype)) {
         case 4:
-            k_unpad_any<float><<<grid, 256, 0, st>>>(static_cast<const float *>(src), static_cast<float *>(dst),
-                                                     l->height, l->width, L, total);
+            (small ? k_unpad_any<float, unsigned> : k_unpad_any<float, long long>)<<<grid, 256, 0, st>>>(
+                static_cast<const float *>(src), static_cast<float *>(dst), l->height, l->width, L, total);
             break;
         case 2:
-            k_unpad_any<uint16_t><<<grid, 256, 0, st>>>(static_cast<const uint16_t *>(src),
-                                                        static_cast<uint16_t *>(dst), l->height, l->width, L,
-                                                        total);
+            (small ? k_unpad_any<uint16_t, unsigned> : k_unpad_any<uint16_t, long long>)<<<grid, 256, 0, st>>>(
+                static_cast<const uint16_t *>(src), static_cast<uint16_t *>(dst), l->height, l->width, L, total);
             break;
         case 1:
-            k_unpad_any<int8_t><<<grid, 256, 0, st>>>(static_cast<const int8_t *>(src),
-                                                      static_cast<int8_t *>(dst), l->height, l->width, L, total);
+            (small ? k_unpad_any<int8_t, unsigned> : k_unpad_any<int8_t, long long>)<<<grid, 256, 0, st>>>(
+                static_cast<const int8_t *>(src), static_cast<int8_t *>(dst), l->height, l->width, L, total);
             break;
         default: return fail(USC_ERR_VALUE, "unknown dtype %d", dtype);
     }
@@ -826,11 +829,11 @@ int usc_maxpool2(const usc_act_layout *in_l, const usc_act_layout *out_l, int32_
     const long long total = (long long)n_total * in_l->channels * OH * OW;
     const LayoutD Li = to_dev(*in_l), Lo = to_dev(*out_l);
     if (dtype == USC_F32) {
-        k_maxpool2<float><<<grid_for(total), 256, 0, st>>>(static_cast<const float *>(src),
+        (total < 0x7fffffffLL ? k_maxpool2<float, unsigned> : k_maxpool2<float, long long>)<<<grid_for(total), 256, 0, st>>>(static_cast<const float *>(src),
                                                            static_cast<float *>(dst), n_total,
                                                            in_l->channels, OH, OW, Li, Lo);
     } else if (dtype == USC_F16 || dtype == USC_CB4) {
-        k_maxpool2<__half><<<grid_for(total), 256, 0, st>>>(static_cast<const __half *>(src),
+        (total < 0x7fffffffLL ? k_maxpool2<__half, unsigned> : k_maxpool2<__half, long long>)<<<grid_for(total), 256, 0, st>>>(static_cast<const __half *>(src),
                                                             static_cast<__half *>(dst), n_total,
                                                             in_l->channels, OH, OW, Li, Lo);
     } else {
