@@ -232,6 +232,8 @@ def sparse_conv_forward(input: DenseTensor4, filt: CsrFilter,
     config = config or ExecConfig()
     _check_call(input, filt, config)
     g = filt.geometry
+    if input.n == 0:  # no virtual blocks (engine.py:85-88): the empty output, nothing launched
+        return DenseTensor4(np.zeros((0, g.out_channels, g.out_h, g.out_w), np.float32), input.precision)
     dtype = dtype_of(input.precision)
     plan, blob = plan_for(filt, input.n, dtype, config, filt.weights)
     x = input.device()
@@ -407,6 +409,8 @@ def autotune_sb(input: DenseTensor4, filt: CsrFilter, candidates=SB_CANDIDATES, 
     import torch
     n = input.n
     usable = sorted(c for c in set(candidates) if n % c == 0) or [1]
+    if n == 0:  # nothing to time: every candidate divides an empty batch
+        return ExecConfig(usable[0], worker_count)
     g = filt.geometry
     dtype = dtype_of(input.precision)
     x = input.device()

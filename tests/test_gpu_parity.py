@@ -498,3 +498,4 @@ def test_run_bench_harness_on_gpu():
     gt = (g.in_channels, g.out_channels, 1, 1, g.input_h, g.input_w, (1, 1), (0, 0))
     ref = oracle.sparse_conv_forward(x, (f.row_ptr, f.col_offsets, f.weights, f.n_nz), gt)
     assert np.array_equal(out, ref)
+

@@ -289,3 +289,18 @@ def test_spearman_matches_scipy_with_ties():
         if np.ptp(x) == 0 or np.ptp(y) == 0:
             continue
         assert LB.spearman_rho(x, y) == pytest.approx(spearmanr(x, y).statistic, abs=1e-12)
+
+
+def test_empty_batch_like_reference():
+    """An empty batch has no virtual blocks (engine.py:85-88): the reference returns a
+    (0, D, Yh, Yw) output; so does the engine, without a launch; sub_batch rules as the
+    reference (any sub_batch divides 0)."""
+    g = U.ConvGeometry(4, 2, 3, 3, 5, 5, padding=(1, 1))
+    w = np.random.default_rng(0).standard_normal((2, 4, 3, 3)).astype(np.float32)
+    f = U.build_csr(U.DenseTensor4.from_array(w), g)
+    x = U.DenseTensor4.from_array(np.zeros((0, 4, 5, 5), np.float32))
+    y = U.sparse_conv_forward(x, f, U.ExecConfig(2))
+    assert y.shape == (0, 2, 5, 5) and y.data.dtype == np.float32
+    assert U.autotune_sb(x, f).sub_batch == 2
+    with pytest.raises(ValueError):
+        U.sparse_conv_forward(U.DenseTensor4.from_array(np.zeros((3, 4, 5, 5), np.float32)), f, U.ExecConfig(2))
