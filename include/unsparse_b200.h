@@ -291,6 +291,18 @@ int usc_nhwc_to_bi(const usc_act_layout *l, int32_t n, const void *src, void *ds
 /* The same epilogue in place on `count` binary16 values of any layout (a cuDNN layer's
  * NHWC output inside a dense chain): v = sat16(y); res: v = sat16(v + r); ReLU when relu. */
 int usc_f16_epilogue(void *y, const void *res, int64_t count, int32_t relu, void *stream);
+/* The dense backend on the 5th-generation tensor cores (binary16 networks, fp16 tolerance
+ * path): an implicit-GEMM convolution (tcgen05.mma, fp32 accumulation in tensor memory,
+ * TMA-staged 128-byte-swizzled operands) reading the BI64 binary16 input `x` in
+ * `x_layout` and writing the BI64 output `y` in `y_layout` (interior only) with the
+ * epilogue fused: round to binary16 with saturation, + shortcut `res` (binary16, sat16),
+ * ReLU when relu != 0.  torch conv2d semantics: padding = filter/2 (read from the input
+ * halo, which must be at least that wide), stride g->stride_h (= stride_w, 1 or 2),
+ * filters 1x1 or 3x3; in_channels % 64 == 0, out_channels % 128 == 0.  `w_dev`: the dense
+ * weights as [out_channels][filter_h*filter_w][in_channels] binary16 (K-major). */
+int usc_dense_conv_f16(const usc_geometry *g, int32_t n, const void *w_dev, const usc_act_layout *x_layout,
+                       const void *x, const usc_act_layout *y_layout, void *y, const usc_act_layout *res_layout,
+                       const void *res, int32_t relu, void *stream);
 /* round_to_binary16 (tensor.py:48-63) on device: f32 in -> f32 on the binary16 grid
  * (to_half == 0) or binary16 storage (to_half == 1). */
 int usc_round_binary16(const float *src, void *dst, int64_t count, int32_t to_half, void *stream);

@@ -1,0 +1,354 @@
+// dense_tc.cu -- the dense backend of the per-layer dispatcher on the 5th-generation
+// tensor cores: an implicit-GEMM binary16 convolution that reads and writes the network's
+// resident BI64 layout directly (no NHWC transposes), tcgen05.mma with the accumulator in
+// tensor memory.  For binary16 networks only (the north star's 1e-2 tolerance path):
+// tensor-core sums are not the reference's sequential fp32 order.
+//
+// GEMM view of one CTA tile (one output row y, TWP output pixels x0.., one 64-sample
+// block, 128 output channels d0..):
+//   D[d][(x, s)] = sum_{t = (kh, kw), c} W[d][t][c] * X[c][s*y + kh][s*x + kw][sample s]
+//   M = 128 (d), N = TWP * 64 (pixels x samples), K = taps * C.
+// Operands (TMA, 128-byte swizzle, 1024-B aligned stages):
+//   A = weights [D][taps*C] binary16, K-major: box [64 k][128 d] (16 KB per stage);
+//   B = activations: per tile pixel one box [64 samples][1][1][64 channels] of the BI64
+//       tensor -> [64 c][64 s] (8 KB), i.e. MN-major (samples contiguous), one 128-B
+//       swizzle row per channel; the TWP boxes of a stage are the MN atoms of B.
+// Per stage: 4 MMAs of K = 16 (tcgen05.mma.cta_group::1.kind::f16, M128 x N, fp32 acc).
+// Warp roles: warps 0-3 epilogue (TMEM lane quarter = warp), warp 4 TMA producer and
+// TMEM owner, warp 5 MMA issuer.  Epilogue: tcgen05.ld 32 columns at a time, binary16
+// rounding with saturation, optional residual add (binary16) + saturation, ReLU
+// (NaN -> 0), 64-byte stores into the output layout (halo untouched).
+#include <cudaTypedefs.h>
+
+#include "common.cuh"
+#include "usc_internal.h"
+
+using namespace usc_dev;
+
+namespace {
+
+constexpr int kStages = 4;
+constexpr int kKC = 64;               // channels (K) per stage and tap
+constexpr int kABytes = 128 * kKC * 2;  // 16 KB
+constexpr int kBPix = kKC * 64 * 2;     // 8 KB per pixel box
+
+struct DtcArgs {
+    CUtensorMap xmap, wmap;
+    void *y;
+    const void *res;
+    LayoutD Lo, Lr;
+    int C, D, Kh, Kw, stride, offh, offw;  // input coord = stride*o + k + off
+    int Yh, Yw, NB, relu;
+    int m_blocks, x_tiles;
+    int k_iters, cb;  // k_iters = taps * cb, cb = C / 64
+};
+
+__device__ __forceinline__ void mbar_wait_bounded(uint64_t *bar, uint32_t parity) {
+    // a descriptor or transaction-count bug must fail the launch, not hang the GPU
+    uint32_t ok = 0;
+    for (long long it = 0; it < (1LL << 27) && !ok; ++it)
+        asm volatile(
+            "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(ok)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+    if (!ok) __trap();
+}
+
+__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, int c0, int c1, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_5d(void *dst, const CUtensorMap *map, int c0, int c1, int c2, int c3, int c4,
+                                            uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// UMMA shared-memory descriptors (sm_100 format, version 1), 128-byte swizzle:
+//   K-major A tile [rows][64 k]: rows 128 B apart, 8-row groups SBO = 1024 B;
+//   MN-major B tile: 128-B rows = 64 MN elements, K rows 128 B apart (8-row groups
+//   SBO = 1024 B), MN atoms (tile pixels) LBO = 8 KB apart.
+__device__ __forceinline__ uint64_t desc_sw128(uint32_t addr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
+    uint64_t d = 0;
+    d |= (uint64_t)((addr >> 4) & 0x3FFF);
+    d |= (uint64_t)((lbo_bytes >> 4) & 0x3FFF) << 16;
+    d |= (uint64_t)((sbo_bytes >> 4) & 0x3FFF) << 32;
+    d |= 1ull << 46;  // version 1 (Blackwell)
+    d |= 2ull << 61;  // SWIZZLE_128B
+    return d;
+}
+
+__device__ __forceinline__ void umma_f16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t accumulate) {
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void umma_commit(uint64_t *bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ uint32_t sat16x2(uint32_t w) {  // +-inf -> +-65504 per half
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        const uint32_t h = (w >> (16 * k)) & 0xffffu;
+        if ((h & 0x7fffu) == 0x7c00u) w = (w & ~(0xffffu << (16 * k))) | (((h & 0x8000u) | 0x7bffu) << (16 * k));
+    }
+    return w;
+}
+__device__ __forceinline__ uint32_t relu16x2(uint32_t w) {
+    uint32_t out = 0;
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        const uint32_t h = (w >> (16 * k)) & 0xffffu, m = h & 0x7fffu;
+        if (!(h & 0x8000u) && m != 0 && m <= 0x7c00u) out |= h << (16 * k);
+    }
+    return out;
+}
+
+template <int TWP>
+__global__ void __launch_bounds__(192, 1) k_dtc(const __grid_constant__ DtcArgs a) {
+    constexpr int N = TWP * 64;
+    constexpr int kStage = kABytes + TWP * kBPix;
+    constexpr uint32_t kCols = N;  // fp32 accumulator columns (power of 2: 128 or 256)
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char *smem = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + kStages * kStage);
+    uint64_t *empty = full + kStages;
+    uint64_t *tfull = empty + kStages;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tfull + 1);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // tile decode: (m block, x tile, y, sample block)
+    int t = blockIdx.x;
+    const int mb = t % a.m_blocks;
+    t /= a.m_blocks;
+    const int xt = t % a.x_tiles;
+    t /= a.x_tiles;
+    const int yo = t % a.Yh;
+    const int nb = t / a.Yh;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init(tfull, 1);
+        fence_mbar_init();
+    }
+    if (warp == 4) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "n"(kCols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 4) {
+        // ---------------- TMA producer ----------------
+        if (lane == 0) {
+            for (int i = 0; i < a.k_iters; ++i) {
+                const int s = i % kStages;
+                if (i >= kStages) mbar_wait_bounded(&empty[s], ((i / kStages) - 1) & 1);
+                unsigned char *st = smem + s * kStage;
+                const int tap = i / a.cb, cb = i - tap * a.cb;
+                const int kh = tap / a.Kw, kw = tap - kh * a.Kw;
+                mbar_expect_tx(&full[s], kStage);
+                tma_load_2d(st, &a.wmap, tap * a.C + cb * kKC, mb * 128, &full[s]);
+                const int yi = a.stride * yo + kh + a.offh;
+#pragma unroll
+                for (int j = 0; j < TWP; ++j) {
+                    const int xi = a.stride * (xt * TWP + j) + kw + a.offw;
+                    tma_load_5d(st + kABytes + j * kBPix, &a.xmap, 0, xi, yi, cb * kKC, nb, &full[s]);
+                }
+            }
+        }
+    } else if (warp == 5) {
+        // ---------------- MMA issuer ----------------
+        // instruction descriptor: fp32 accumulate, f16 x f16, A K-major, B MN-major, N, M = 128
+        const uint32_t idesc = (1u << 4) | (1u << 16) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+        for (int i = 0; i < a.k_iters; ++i) {
+            const int s = i % kStages;
+            mbar_wait_bounded(&full[s], (i / kStages) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            if (lane == 0) {
+                const uint32_t abase = smem_u32(smem + s * kStage), bbase = abase + kABytes;
+#pragma unroll
+                for (int k = 0; k < kKC / 16; ++k) {
+                    const uint64_t ad = desc_sw128(abase + k * 32, 16, 1024);
+                    const uint64_t bd = desc_sw128(bbase + k * 16 * 128, kBPix, 1024);
+                    umma_f16(tmem, ad, bd, idesc, (i > 0 || k > 0) ? 1u : 0u);
+                }
+                umma_commit(&empty[s]);  // frees the stage once these MMAs have read it
+                if (i == a.k_iters - 1) umma_commit(tfull);
+            }
+            __syncwarp();
+        }
+    } else {
+        // ---------------- epilogue (warps 0-3: TMEM lanes 32w .. 32w+31) ----------------
+        mbar_wait_bounded(tfull, 0);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const int d = mb * 128 + warp * 32 + lane;
+        const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16);
+#pragma unroll 1
+        for (int ch = 0; ch < N / 32; ++ch) {  // 32 columns = 32 samples of one pixel
+            uint32_t v[32];
+            asm volatile(
+                "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+                "%14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+                : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                  "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
+                  "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
+                  "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
+                  "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+                : "r"(taddr + ch * 32));
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            const int px = ch >> 1, s0 = (ch & 1) * 32;
+            const int xo = xt * TWP + px;
+            if (d >= a.D || xo >= a.Yw) continue;
+            uint32_t h[16];
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+                const __half2 p = __floats2half2_rn(__uint_as_float(v[2 * k]), __uint_as_float(v[2 * k + 1]));
+                h[k] = sat16x2(*reinterpret_cast<const uint32_t *>(&p));
+            }
+            if (a.res) {
+                const uint4 *rp = reinterpret_cast<const uint4 *>(static_cast<const __half *>(a.res) +
+                                                                  lay_index(a.Lr, (long long)nb * 64, d, yo, xo) + s0);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const uint4 r = __ldg(rp + q);
+                    const uint32_t rr[4] = {r.x, r.y, r.z, r.w};
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        __half2 sum = __hadd2(*reinterpret_cast<const __half2 *>(&h[4 * q + u]),
+                                              *reinterpret_cast<const __half2 *>(&rr[u]));
+                        h[4 * q + u] = sat16x2(*reinterpret_cast<uint32_t *>(&sum));
+                    }
+                }
+            }
+            if (a.relu) {
+#pragma unroll
+                for (int k = 0; k < 16; ++k) h[k] = relu16x2(h[k]);
+            }
+            uint4 *yp = reinterpret_cast<uint4 *>(static_cast<__half *>(a.y) +
+                                                  lay_index(a.Lo, (long long)nb * 64, d, yo, xo) + s0);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) yp[q] = make_uint4(h[4 * q], h[4 * q + 1], h[4 * q + 2], h[4 * q + 3]);
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 4) {
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kCols));
+    }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_tiled() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+}  // namespace
+
+int usc_dense_conv_f16(const usc_geometry *g, int32_t n, const void *w_dev, const usc_act_layout *xl, const void *x,
+                       const usc_act_layout *yl, void *y, const usc_act_layout *rl, const void *res, int32_t relu,
+                       void *stream) {
+    if (!g || !w_dev || !xl || !x || !yl || !y || n < 1) return usc::fail(USC_ERR_VALUE, "dense conv: null argument");
+    if (g->filter_h != g->filter_w || (g->filter_h != 1 && g->filter_h != 3) || g->stride_h != g->stride_w ||
+        (g->stride_h != 1 && g->stride_h != 2))
+        return usc::fail(USC_ERR_UNSUPPORTED, "dense conv: 1x1 / 3x3 filters, stride 1 or 2");
+    if (g->in_channels % kKC || g->out_channels % 128)
+        return usc::fail(USC_ERR_UNSUPPORTED, "dense conv: channels in %% 64 and out %% 128 needed");
+    if (xl->interleave != 64 || yl->interleave != 64 || (res && (!rl || rl->interleave != 64)))
+        return usc::fail(USC_ERR_UNSUPPORTED, "dense conv: BI64 layouts only");
+    const int s = g->stride_h, K = g->filter_h, pad = K / 2;
+    const int Yh = (xl->height + 2 * pad - K) / s + 1, Yw = (xl->width + 2 * pad - K) / s + 1;
+    if (yl->height != Yh || yl->width != Yw || yl->channels != g->out_channels || xl->channels != g->in_channels)
+        return usc::fail(USC_ERR_VALUE, "dense conv: layouts do not match the convolution");
+    if (xl->pad_h < pad || xl->pad_w < pad)
+        return usc::fail(USC_ERR_VALUE, "dense conv: input halo smaller than the padding");
+    if (res && (rl->height != Yh || rl->width != Yw || rl->channels != g->out_channels))
+        return usc::fail(USC_ERR_VALUE, "dense conv: shortcut layout does not match the output");
+    auto enc = encode_tiled();
+    if (!enc) return usc::fail(USC_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    DtcArgs a{};
+    const int NB = (n + 63) / 64;
+    {   // activations: [NB][C][Hp][Wp][64] binary16, box = one pixel x 64 channels x 64 samples
+        const cuuint64_t dims[5] = {64, (cuuint64_t)xl->ws, (cuuint64_t)xl->hp, (cuuint64_t)xl->channels, (cuuint64_t)NB};
+        const cuuint64_t strides[4] = {128, (cuuint64_t)xl->ws * 128, (cuuint64_t)xl->ws * xl->hp * 128,
+                                       (cuuint64_t)xl->sample_stride * 2};
+        const cuuint32_t box[5] = {64, 1, 1, (cuuint32_t)kKC, 1};
+        const cuuint32_t es[5] = {1, 1, 1, 1, 1};
+        CUresult r = enc(&a.xmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 5, const_cast<void *>(x), dims, strides, box, es,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return usc::fail(USC_ERR_CUDA, "dense conv: activation tensor map (%d)", (int)r);
+    }
+    const int taps = K * K, Kd = taps * g->in_channels;
+    {   // weights: [D][taps*C] binary16 K-major, box [64 k][128 d]
+        const cuuint64_t dims[2] = {(cuuint64_t)Kd, (cuuint64_t)g->out_channels};
+        const cuuint64_t strides[1] = {(cuuint64_t)Kd * 2};
+        const cuuint32_t box[2] = {(cuuint32_t)kKC, 128};
+        const cuuint32_t es[2] = {1, 1};
+        CUresult r = enc(&a.wmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void *>(w_dev), dims, strides, box, es,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return usc::fail(USC_ERR_CUDA, "dense conv: weight tensor map (%d)", (int)r);
+    }
+    a.y = y;
+    a.res = res;
+    a.Lo = to_dev(*yl);
+    a.Lr = res ? to_dev(*rl) : a.Lo;
+    a.C = g->in_channels;
+    a.D = g->out_channels;
+    a.Kh = K;
+    a.Kw = K;
+    a.stride = s;
+    a.offh = xl->pad_h - pad;
+    a.offw = xl->pad_w - pad;
+    a.Yh = Yh;
+    a.Yw = Yw;
+    a.NB = NB;
+    a.relu = relu;
+    a.m_blocks = g->out_channels / 128;
+    a.cb = g->in_channels / kKC;
+    a.k_iters = taps * a.cb;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int twp = Yw % 4 == 0 ? 4 : 2;
+    a.x_tiles = (Yw + twp - 1) / twp;
+    const long long tiles = (long long)a.m_blocks * a.x_tiles * Yh * NB;
+    if (tiles > 0x7fffffffLL) return usc::fail(USC_ERR_UNSUPPORTED, "dense conv: grid too large");
+    const int smem = kStages * (kABytes + twp * kBPix) + 1024 + 256;
+    cudaError_t e;
+    if (twp == 4) {
+        static std::atomic<uint64_t> attr{0};
+        e = ensure_smem_attr(k_dtc<4>, attr, smem);
+        if (e == cudaSuccess) k_dtc<4><<<(unsigned)tiles, 192, smem, st>>>(a);
+    } else {
+        static std::atomic<uint64_t> attr{0};
+        e = ensure_smem_attr(k_dtc<2>, attr, smem);
+        if (e == cudaSuccess) k_dtc<2><<<(unsigned)tiles, 192, smem, st>>>(a);
+    }
+    if (e == cudaSuccess) e = cudaGetLastError();
+    return e == cudaSuccess ? USC_OK : usc::fail(USC_ERR_CUDA, "k_dtc: %s", cudaGetErrorString(e));
+}

@@ -211,14 +211,23 @@ class SparseVGG16:
         g = self.geoms[li]
         return self.mode == "fp16" and g.in_channels % 16 == 0 and g.out_channels % 16 == 0
 
+    def tc_eligible(self, li: int) -> bool:
+        """The tensor-core backend (dense.py) may run conv li: 16b/16b, channels in % 64 and
+        out % 128."""
+        from .dense import tc_eligible
+        g = self.geoms[li]
+        return self.mode == "fp16" and tc_eligible(g.in_channels, g.out_channels, 3, 1)
+
     def _check_backends(self):
         if len(self.backends) != len(self.geoms):
             raise ValueError(f"{len(self.backends)} backends for {len(self.geoms)} convs")
         for li, b in enumerate(self.backends):
-            if b not in ("sparse", "dense"):
+            if b not in ("sparse", "dense", "tc"):
                 raise ValueError(f"unknown backend {b!r}")
             if b == "dense" and not self.dense_eligible(li):
                 raise ValueError(f"conv {li} cannot run dense (16b/16b networks with channels % 16 == 0 only)")
+            if b == "tc" and not self.tc_eligible(li):
+                raise ValueError(f"conv {li} cannot run on the tensor-core backend")
 
     def _dense_fn(self, li, x_held, out_held, pool):
         """cuDNN (torch conv2d: binary16 tensor cores, channels_last) + ReLU (+ 2x2 max-pool)
@@ -322,8 +331,16 @@ class SparseVGG16:
             if st[0] == "dense" and st[2].__name__ == "fn" and st[2].__qualname__.startswith("SparseVGG16._dense_fn"):
                 dense_ms[st[1]] = time_median_cuda(lambda: self._run_step(st), repeats, warmup)
         argmin = ["dense" if elig[li] and dense_ms.get(li, 1e9) <= sparse_ms[li] else "sparse" for li in range(nl)]
+        tce = [self.tc_eligible(li) for li in range(nl)]
+        build(["tc" if e else "sparse" for e in tce])
+        tc_ms = {}
+        for st in self.steps:  # the tensor-core conv (+ its pool) on the BI64 buffers
+            if st[0] in ("tc", "pool") and tce[st[1]]:
+                tc_ms[st[1]] = tc_ms.get(st[1], 0.0) + time_median_cuda(lambda: self._run_step(st), repeats, warmup)
+        tc_argmin = ["tc" if tce[li] and tc_ms[li] <= sparse_ms[li] else "sparse" for li in range(nl)]
         cands = {"all-sparse": ["sparse"] * nl, "all-dense": ["dense" if e else "sparse" for e in elig],
-                 "argmin": argmin}
+                 "argmin": argmin, "tc-argmin": tc_argmin, "all-tc": ["tc" if e else "sparse" for e in tce],
+                 "tc-argmin+dense": ["tc" if tc_argmin[li] == "tc" else argmin[li] for li in range(nl)]}
         for k in range(1, nl):
             cands[f"dense-from-{k}"] = ["dense" if elig[li] and li >= k else "sparse" for li in range(nl)]
         times, seen = {}, set()
@@ -334,7 +351,8 @@ class SparseVGG16:
             build(bk)
             times[name] = self.network_ms()
         best = min(times, key=times.get)
-        self.backend_times = {li: {"sparse_ms": sparse_ms.get(li), "dense_ms": dense_ms.get(li)} for li in range(nl)}
+        self.backend_times = {li: {"sparse_ms": sparse_ms.get(li), "dense_ms": dense_ms.get(li), "tc_ms": tc_ms.get(li)}
+                              for li in range(nl)}
         self.backend_search = {k: round(v, 4) for k, v in times.items()}
         self.backend_pick = best
         build(cands[best])
@@ -396,10 +414,34 @@ class SparseVGG16:
                 cur_buf, cur_lay, cur_held = None, out_lay, out_held
                 li += 1
                 continue
-            if cur_buf is None:  # NHWC -> the BI64 layout this sparse conv reads
+            if cur_buf is None:  # NHWC -> the BI64 layout this sparse / tensor-core conv reads
                 cur_buf = self._buf(cur_lay)
                 self.steps.append(("dense", li, self._to_bi(cur_held, cur_buf, cur_lay)))
             cur_held = None
+            if self.backends[li] == "tc":  # tensor cores straight on the BI64 buffers (+ the pool kernel)
+                from .dense import dense_conv, pack_weights
+                if not hasattr(self, "_tc_w"):
+                    self._tc_w = {}
+                if li not in self._tc_w:
+                    self._tc_w[li] = pack_weights(self.weights[li], self.device)
+                last = i + 2 >= len(VGG16_CIFAR)
+                halo = 0 if nxt == "M" else 1
+                out_lay = _lib.act_layout(g.out_channels, g.out_h, g.out_w, halo, halo, self.eb, il)
+                out_buf = self._buf(out_lay)
+
+                def fn(stream=None, w=self._tc_w[li], g=g, x=cur_buf, xl=cur_lay, y=out_buf, yl=out_lay):
+                    dense_conv(w, g.in_channels, g.out_channels, 3, 1, n, x, xl, y, yl, None, None, True, stream)
+                self.steps.append(("tc", li, fn))
+                self.nonzero_macs += int(np.count_nonzero(self.filters[li].weights)) * g.out_h * g.out_w * n
+                cur_buf, cur_lay = out_buf, out_lay
+                if nxt == "M":
+                    ph = 0 if last else 1
+                    pool_lay = _lib.act_layout(g.out_channels, g.out_h // 2, g.out_w // 2, ph, ph, self.eb, il)
+                    pool_buf = self._buf(pool_lay)
+                    self.steps.append(("pool", li, cur_lay, pool_lay, cur_buf, pool_buf))
+                    cur_buf, cur_lay = pool_buf, pool_lay
+                li += 1
+                continue
             plan, blob = self._plan_for(li, plan_cfgs[li])
             epi = _lib.Epilogue()
             epi.relu = 1
@@ -463,7 +505,7 @@ class SparseVGG16:
     def _run_step(self, st, stream=None):
         L = _lib.lib()
         sp = _lib.stream_ptr(stream)
-        if st[0] == "dense":
+        if st[0] in ("dense", "tc"):
             st[2](stream)
         elif st[0] == "conv":
             _, _, plan, blob, xin, yout, epi = st
@@ -480,7 +522,7 @@ class SparseVGG16:
         L = _lib.lib()
         sp = _lib.stream_ptr(stream)
         for st in self.steps:
-            if st[0] == "dense":
+            if st[0] in ("dense", "tc"):
                 st[2](stream)
             elif st[0] == "conv":
                 _, _, plan, blob, xin, yout, epi = st

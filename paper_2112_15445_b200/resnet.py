@@ -101,15 +101,24 @@ class SparseResNet50:
         g = self.layers[li][1]
         return (self.dtype == _lib.USC_F16 and g.in_channels % 16 == 0 and g.out_channels % 16 == 0)
 
+    def tc_eligible(self, li: int) -> bool:
+        """The tensor-core backend (dense.py) may run conv li: binary16 network, channels
+        in % 64 and out % 128, 1x1 / 3x3, stride 1 / 2."""
+        from .dense import tc_eligible
+        _, g, role, s = self.layers[li]
+        return self.dtype == _lib.USC_F16 and tc_eligible(g.in_channels, g.out_channels, g.filter_h, s)
+
     def _check_backends(self):
         if len(self.backends) != len(self.layers):
             raise ValueError(f"{len(self.backends)} backends for {len(self.layers)} convs")
         for li, b in enumerate(self.backends):
-            if b not in ("sparse", "dense"):
+            if b not in ("sparse", "dense", "tc"):
                 raise ValueError(f"unknown backend {b!r}")
             if b == "dense" and not self.dense_eligible(li):
                 raise ValueError(f"conv {self.layers[li][0]} cannot run dense (binary16 networks with "
                                  f"channels % 16 == 0 only)")
+            if b == "tc" and not self.tc_eligible(li):
+                raise ValueError(f"conv {self.layers[li][0]} cannot run on the tensor-core backend")
 
     def _dense_weight(self, li):
         import torch
@@ -202,6 +211,22 @@ class SparseResNet50:
         def conv(li, xa, c_out, hw_out, halo, relu=True, residual=None):
             name, g, role, s = self.layers[li]
             ya = Act(c_out, hw_out, self._lay(c_out, hw_out, halo))
+            if self.backends[li] == "tc":  # tensor cores straight on the BI64 buffers
+                from .dense import dense_conv, pack_weights
+                if not hasattr(self, "_tc_w"):
+                    self._tc_w = {}
+                if li not in self._tc_w:
+                    self._tc_w[li] = pack_weights(self.weights[li], self.device)
+                w, x, x_lay = self._tc_w[li], xa.bi(), xa.lay
+                y = ya.buf = self._buf(ya.lay)
+                r, r_lay = (None, None) if residual is None else (residual.bi(), residual.lay)
+
+                def fn(stream=None, li=li, w=w, x=x, x_lay=x_lay, y=y, y_lay=ya.lay, r=r, r_lay=r_lay, relu=relu,
+                       g=g, s=s):
+                    dense_conv(w, g.in_channels, g.out_channels, g.filter_h, s, n, x, x_lay, y, y_lay, r, r_lay,
+                               relu, stream)
+                self.steps.append((li, None, None, None, None, None, fn))
+                return ya
             if self.backends[li] == "dense":
                 xa.nhwc()
                 if residual is not None:
@@ -409,9 +434,18 @@ class SparseResNet50:
         dense_ms = {st[0]: time_median_cuda(lambda: self._launch(st), repeats, warmup)
                     for st in self.steps if st[1] is None and st[0] >= 0}
         argmin = ["dense" if elig[li] and dense_ms[li] <= sparse_ms[li] else "sparse" for li in range(nl)]
+        tce = [self.tc_eligible(li) for li in range(nl)]
+        build(["tc" if e else "sparse" for e in tce])
+        tc_ms = {st[0]: time_median_cuda(lambda: self._launch(st), repeats, warmup)
+                 for st in self.steps if st[1] is None and st[0] >= 0}
+        # the tensor-core backend works on the BI64 buffers (no transposes): isolated costs add up
+        tc_argmin = ["tc" if tce[li] and tc_ms[li] <= sparse_ms[li] else "sparse" for li in range(nl)]
+        tc_argmin_dense = ["tc" if tce[li] and tc_ms[li] <= sparse_ms[li] else
+                           ("dense" if elig[li] and dense_ms[li] <= sparse_ms[li] else "sparse") for li in range(nl)]
         blocks = [li for li, (name, _, role, _) in enumerate(self.layers) if role == "c1"]
         cands = {"all-sparse": ["sparse"] * nl, "all-dense": ["dense" if e else "sparse" for e in elig],
-                 "argmin": argmin}
+                 "argmin": argmin, "tc-argmin": tc_argmin, "tc-argmin+dense": tc_argmin_dense,
+                 "all-tc": ["tc" if e else "sparse" for e in tce]}
         for k in blocks:
             cands[f"dense-from-{self.layers[k][0]}"] = ["dense" if elig[li] and li >= k else "sparse"
                                                         for li in range(nl)]
@@ -425,8 +459,8 @@ class SparseResNet50:
             build(bk)
             times[name] = self.network_ms()
         best = min(times, key=times.get)
-        self.backend_times = {self.layers[li][0]: {"sparse_ms": sparse_ms.get(li), "dense_ms": dense_ms.get(li)}
-                              for li in range(nl)}
+        self.backend_times = {self.layers[li][0]: {"sparse_ms": sparse_ms.get(li), "dense_ms": dense_ms.get(li),
+                                                   "tc_ms": tc_ms.get(li)} for li in range(nl)}
         self.backend_search = {k: round(v, 4) for k, v in times.items()}
         self.backend_pick = best
         build(cands[best])

