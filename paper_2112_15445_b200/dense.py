@@ -24,7 +24,8 @@ def tc_eligible(in_channels: int, out_channels: int, k: int, stride: int) -> boo
 def pack_weights(w, device=None):
     """Dense (D, C, K, K) weights -> the kernel's binary16 [D][K*K][C] (K-major) tensor."""
     import torch
-    t = w if type(w).__module__.startswith("torch") else torch.from_numpy(np.ascontiguousarray(w.data if hasattr(w, "data") else w))
+    t = w if type(w).__module__.startswith("torch") else torch.from_numpy(
+        np.array(w.data if hasattr(w, "data") else w, dtype=np.float32))
     t = t.to(device or "cuda", torch.float16)
     D, C, kh, kw = t.shape
     return t.permute(0, 2, 3, 1).reshape(D, kh * kw * C).contiguous()

@@ -72,15 +72,22 @@ def test_bi64_nhwc_transposes_exact():
     assert np.array_equal(plain.float().cpu().numpy(), ref)
 
 
-def test_resnet50_fp16_mixed_backends_within_tolerance():
-    """Every dense step kind (3x3 stride 1 and 2, projections, residual c3) on cuDNN,
-    the rest sparse, against the oracle composition."""
+@pytest.mark.parametrize("mix", ["cudnn", "tc"])
+def test_resnet50_fp16_mixed_backends_within_tolerance(mix):
+    """Every dense step kind (3x3 stride 1 and 2, projections, residual c3) on cuDNN (or on
+    the tensor-core backend where it applies, mixed with cuDNN), the rest sparse, against
+    the oracle composition."""
     import torch
     from paper_2112_15445_b200.resnet import STAGES, SparseResNet50, resnet50_layers, resnet50_weights
     ws = _tame(resnet50_weights(0.9, seed=4, precision=F16), 0.1)
     layers = resnet50_layers()
     backends = ["dense" if (role in ("c2", "proj") or (role == "c3" and li % 2 == 0)) else "sparse"
                 for li, (_, _, role, _) in enumerate(layers)]
+    if mix == "tc":
+        probe = SparseResNet50.__new__(SparseResNet50)
+        probe.layers, probe.dtype = layers, __import__("paper_2112_15445_b200")._lib.USC_F16
+        backends = ["tc" if probe.tc_eligible(li) and li % 3 != 1 else b for li, b in enumerate(backends)]
+        assert "tc" in backends
     x = oracle.round_to_binary16(np.random.default_rng(5).standard_normal((64, 3, 32, 32)).astype(np.float32))
     m = SparseResNet50(ws, 64, precision=F16, backends=backends)
     m.capture()
@@ -117,11 +124,18 @@ def test_resnet50_fp16_mixed_backends_within_tolerance():
         SparseResNet50(resnet50_weights(0.9, seed=4), 64, backends=backends)  # fp32: bitwise only
 
 
-def test_vgg16_fp16_mixed_backends_within_tolerance():
+@pytest.mark.parametrize("mix", ["cudnn", "tc"])
+def test_vgg16_fp16_mixed_backends_within_tolerance(mix):
+    """cudnn: every other conv on cuDNN (NHWC chains, transposes at the borders); tc: the
+    tensor-core backend on the BI64 buffers mixed with sparse and cuDNN convs."""
     import torch
     from paper_2112_15445_b200.models import VGG16_CIFAR, SparseVGG16, vgg16_rng, vgg16_weights
     ws = _tame(vgg16_weights(vgg16_rng(0.93, seed=8), 0.93, precision=F16), 0.07)
-    backends = ["dense" if li % 2 == 1 else "sparse" for li in range(13)]
+    if mix == "cudnn":
+        backends = ["dense" if li % 2 == 1 else "sparse" for li in range(13)]
+    else:
+        backends = ["sparse", "sparse", "tc", "dense", "tc", "tc", "sparse", "tc", "dense", "dense", "tc", "sparse",
+                    "tc"]
     x = oracle.round_to_binary16(np.random.default_rng(9).standard_normal((64, 3, 32, 32)).astype(np.float32))
     m = SparseVGG16(ws, 64, precision=F16, backends=backends)
     m.capture()
