@@ -13,9 +13,9 @@
 //   B = activations: per tile pixel one box [64 samples][1][1][64 channels] of the BI64
 //       tensor -> [64 c][64 s] (8 KB), i.e. MN-major (samples contiguous), one 128-B
 //       swizzle row per channel; the TWP boxes of a stage are the MN atoms of B.
-// Per stage: 4 MMAs of K = 16 (tcgen05.mma.cta_group::1.kind::f16, M128 x N, fp32 acc).
-// Warp roles: warps 0-3 epilogue (TMEM lane quarter = warp), warp 4 TMA producer and
-// TMEM owner, warp 5 MMA issuer.  Epilogue: tcgen05.ld 32 columns at a time, binary16
+// MMAs of K = 16 (tcgen05.mma.cta_group::1.kind::f16, M128 x N, fp32 acc), see k_dtc for
+// the stage shapes.  Warp roles: warps 0-3 epilogue (TMEM lane quarter = warp), warp 4
+// TMA producer and TMEM owner, warp 5 MMA issuer.  Epilogue: tcgen05.ld 32 columns at a time, binary16
 // rounding with saturation, optional residual add (binary16) + saturation, ReLU
 // (NaN -> 0), 64-byte stores into the output layout (halo untouched).
 #include <cudaTypedefs.h>
@@ -27,7 +27,6 @@ using namespace usc_dev;
 
 namespace {
 
-constexpr int kStages = 4;
 constexpr int kKC = 64;               // channels (K) per stage and tap
 constexpr int kABytes = 128 * kKC * 2;  // 16 KB
 constexpr int kBPix = kKC * 64 * 2;     // 8 KB per pixel box
@@ -53,6 +52,10 @@ __device__ __forceinline__ void mbar_wait_bounded(uint64_t *bar, uint32_t parity
             : "r"(smem_u32(bar)), "r"(parity)
             : "memory");
     if (!ok) __trap();
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
 __device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, int c0, int c1, uint64_t *bar) {
@@ -115,34 +118,41 @@ __device__ __forceinline__ uint32_t relu16x2(uint32_t w) {
     return out;
 }
 
-template <int TWP>
+// Persistent CTA (one per SM), tiles round-robin.  WIN (3x3, stride 1): a stage is one
+// (kh, 64-channel chunk): the TWP+2 input pixels of the row (one 8-KB box each) and the A
+// tiles of the 3 taps kw = 0..2 -- each pixel box is read once for 3 taps (tap kw's B
+// operand is the MN atoms kw .. kw+TWP-1 of the window); 12 MMAs per stage.  Otherwise a
+// stage is one (tap, chunk): TWP boxes + one A tile, 4 MMAs.  Two TMEM accumulators
+// (2 x N fp32 columns): the epilogue of tile i overlaps the main loop of tile i+1.
+template <int TWP, bool WIN>
 __global__ void __launch_bounds__(192, 1) k_dtc(const __grid_constant__ DtcArgs a) {
     constexpr int N = TWP * 64;
-    constexpr int kStage = kABytes + TWP * kBPix;
-    constexpr uint32_t kCols = N;  // fp32 accumulator columns (power of 2: 128 or 256)
+    constexpr int NA = WIN ? 3 : 1;                 // A tiles (taps) per stage
+    constexpr int NBX = WIN ? TWP + 2 : TWP;        // pixel boxes per stage
+    constexpr int kStage = NA * kABytes + NBX * kBPix;
+    constexpr int S = WIN ? 2 : (TWP == 4 ? 4 : 6);  // ring depth (<= ~200 KB)
+    constexpr uint32_t kCols = 2 * N;               // two accumulators
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char *smem = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint64_t *full = reinterpret_cast<uint64_t *>(smem + kStages * kStage);
-    uint64_t *empty = full + kStages;
-    uint64_t *tfull = empty + kStages;
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tfull + 1);
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + S * kStage);
+    uint64_t *empty = full + S;
+    uint64_t *tfull = empty + S;   // [2]
+    uint64_t *tempty = tfull + 2;  // [2]
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    // tile decode: (m block, x tile, y, sample block)
-    int t = blockIdx.x;
-    const int mb = t % a.m_blocks;
-    t /= a.m_blocks;
-    const int xt = t % a.x_tiles;
-    t /= a.x_tiles;
-    const int yo = t % a.Yh;
-    const int nb = t / a.Yh;
+    const int tiles = a.m_blocks * a.x_tiles * a.Yh * a.NB;
+    const int kiters = WIN ? a.Kh * a.cb : a.k_iters;
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < kStages; ++s) {
+        for (int s = 0; s < S; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
-        mbar_init(tfull, 1);
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&tfull[b], 1);
+            mbar_init(&tempty[b], 4);  // one arrive per epilogue warp
+        }
         fence_mbar_init();
     }
     if (warp == 4) {
@@ -155,97 +165,142 @@ __global__ void __launch_bounds__(192, 1) k_dtc(const __grid_constant__ DtcArgs 
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = *tmem_slot;
 
+    auto decode = [&](int t, int &mb, int &xt, int &yo, int &nb) {
+        mb = t % a.m_blocks;
+        t /= a.m_blocks;
+        xt = t % a.x_tiles;
+        t /= a.x_tiles;
+        yo = t % a.Yh;
+        nb = t / a.Yh;
+    };
+
     if (warp == 4) {
         // ---------------- TMA producer ----------------
         if (lane == 0) {
-            for (int i = 0; i < a.k_iters; ++i) {
-                const int s = i % kStages;
-                if (i >= kStages) mbar_wait_bounded(&empty[s], ((i / kStages) - 1) & 1);
-                unsigned char *st = smem + s * kStage;
-                const int tap = i / a.cb, cb = i - tap * a.cb;
-                const int kh = tap / a.Kw, kw = tap - kh * a.Kw;
-                mbar_expect_tx(&full[s], kStage);
-                tma_load_2d(st, &a.wmap, tap * a.C + cb * kKC, mb * 128, &full[s]);
-                const int yi = a.stride * yo + kh + a.offh;
+            int it = 0;  // running stage counter
+            for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+                int mb, xt, yo, nb;
+                decode(t, mb, xt, yo, nb);
+                for (int i = 0; i < kiters; ++i, ++it) {
+                    const int s = it % S;
+                    if (it >= S) mbar_wait_bounded(&empty[s], ((it / S) - 1) & 1);
+                    unsigned char *st = smem + s * kStage;
+                    mbar_expect_tx(&full[s], kStage);
+                    if constexpr (WIN) {
+                        const int kh = i / a.cb, cb = i - kh * a.cb;
 #pragma unroll
-                for (int j = 0; j < TWP; ++j) {
-                    const int xi = a.stride * (xt * TWP + j) + kw + a.offw;
-                    tma_load_5d(st + kABytes + j * kBPix, &a.xmap, 0, xi, yi, cb * kKC, nb, &full[s]);
+                        for (int kw = 0; kw < 3; ++kw)
+                            tma_load_2d(st + kw * kABytes, &a.wmap, (kh * 3 + kw) * a.C + cb * kKC, mb * 128, &full[s]);
+                        const int yi = yo + kh + a.offh;
+#pragma unroll
+                        for (int j = 0; j < NBX; ++j)
+                            tma_load_5d(st + NA * kABytes + j * kBPix, &a.xmap, 0, xt * TWP + j + a.offw, yi, cb * kKC,
+                                        nb, &full[s]);
+                    } else {
+                        const int tap = i / a.cb, cb = i - tap * a.cb;
+                        const int kh = tap / a.Kw, kw = tap - kh * a.Kw;
+                        tma_load_2d(st, &a.wmap, tap * a.C + cb * kKC, mb * 128, &full[s]);
+                        const int yi = a.stride * yo + kh + a.offh;
+#pragma unroll
+                        for (int j = 0; j < TWP; ++j)
+                            tma_load_5d(st + kABytes + j * kBPix, &a.xmap, 0, a.stride * (xt * TWP + j) + kw + a.offw, yi,
+                                        cb * kKC, nb, &full[s]);
+                    }
                 }
             }
         }
     } else if (warp == 5) {
         // ---------------- MMA issuer ----------------
-        // instruction descriptor: fp32 accumulate, f16 x f16, A K-major, B MN-major, N, M = 128
         const uint32_t idesc = (1u << 4) | (1u << 16) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
-        for (int i = 0; i < a.k_iters; ++i) {
-            const int s = i % kStages;
-            mbar_wait_bounded(&full[s], (i / kStages) & 1);
+        int it = 0, lt = 0;
+        for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++lt) {
+            const int ab = lt & 1;
+            if (lt >= 2) mbar_wait_bounded(&tempty[ab], ((lt >> 1) - 1) & 1);  // epilogue drained it
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            if (lane == 0) {
-                const uint32_t abase = smem_u32(smem + s * kStage), bbase = abase + kABytes;
+            const uint32_t acc = tmem + ab * N;
+            for (int i = 0; i < kiters; ++i, ++it) {
+                const int s = it % S;
+                mbar_wait_bounded(&full[s], (it / S) & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                if (lane == 0) {
+                    const uint32_t abase = smem_u32(smem + s * kStage), bbase = abase + NA * kABytes;
 #pragma unroll
-                for (int k = 0; k < kKC / 16; ++k) {
-                    const uint64_t ad = desc_sw128(abase + k * 32, 16, 1024);
-                    const uint64_t bd = desc_sw128(bbase + k * 16 * 128, kBPix, 1024);
-                    umma_f16(tmem, ad, bd, idesc, (i > 0 || k > 0) ? 1u : 0u);
+                    for (int q = 0; q < NA; ++q)
+#pragma unroll
+                        for (int k = 0; k < kKC / 16; ++k) {
+                            const uint64_t ad = desc_sw128(abase + q * kABytes + k * 32, 16, 1024);
+                            const uint64_t bd = desc_sw128(bbase + q * kBPix + k * 16 * 128, kBPix, 1024);
+                            umma_f16(acc, ad, bd, idesc, (i > 0 || q > 0 || k > 0) ? 1u : 0u);
+                        }
+                    umma_commit(&empty[s]);
+                    if (i == kiters - 1) umma_commit(&tfull[ab]);
                 }
-                umma_commit(&empty[s]);  // frees the stage once these MMAs have read it
-                if (i == a.k_iters - 1) umma_commit(tfull);
+                __syncwarp();
             }
-            __syncwarp();
         }
     } else {
         // ---------------- epilogue (warps 0-3: TMEM lanes 32w .. 32w+31) ----------------
-        mbar_wait_bounded(tfull, 0);
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const int d = mb * 128 + warp * 32 + lane;
-        const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16);
+        int lt = 0;
+        for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++lt) {
+            int mb, xt, yo, nb;
+            decode(t, mb, xt, yo, nb);
+            const int ab = lt & 1;
+            mbar_wait_bounded(&tfull[ab], (lt >> 1) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const int d = mb * 128 + warp * 32 + lane;
+            const uint32_t taddr = tmem + ab * N + ((uint32_t)(warp * 32) << 16);
 #pragma unroll 1
-        for (int ch = 0; ch < N / 32; ++ch) {  // 32 columns = 32 samples of one pixel
-            uint32_t v[32];
-            asm volatile(
-                "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
-                "%14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
-                : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-                  "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
-                  "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
-                  "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
-                  "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-                : "r"(taddr + ch * 32));
-            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-            const int px = ch >> 1, s0 = (ch & 1) * 32;
-            const int xo = xt * TWP + px;
-            if (d >= a.D || xo >= a.Yw) continue;
-            uint32_t h[16];
+            for (int ch = 0; ch < N / 32; ++ch) {  // 32 columns = 32 samples of one pixel
+                uint32_t v[32];
+                asm volatile(
+                    "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, "
+                    "%13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, "
+                    "[%32];"
+                    : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                      "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
+                      "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
+                      "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
+                      "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+                    : "r"(taddr + ch * 32));
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                if (ch == N / 32 - 1) {  // every column of this accumulator is in registers: release it
+                    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&tempty[ab]);
+                }
+                const int px = ch >> 1, s0 = (ch & 1) * 32;
+                const int xo = xt * TWP + px;
+                if (d >= a.D || xo >= a.Yw) continue;
+                uint32_t h[16];
 #pragma unroll
-            for (int k = 0; k < 16; ++k) {
-                const __half2 p = __floats2half2_rn(__uint_as_float(v[2 * k]), __uint_as_float(v[2 * k + 1]));
-                h[k] = sat16x2(*reinterpret_cast<const uint32_t *>(&p));
-            }
-            if (a.res) {
-                const uint4 *rp = reinterpret_cast<const uint4 *>(static_cast<const __half *>(a.res) +
-                                                                  lay_index(a.Lr, (long long)nb * 64, d, yo, xo) + s0);
+                for (int k = 0; k < 16; ++k) {
+                    const __half2 p = __floats2half2_rn(__uint_as_float(v[2 * k]), __uint_as_float(v[2 * k + 1]));
+                    h[k] = sat16x2(*reinterpret_cast<const uint32_t *>(&p));
+                }
+                if (a.res) {
+                    const uint4 *rp = reinterpret_cast<const uint4 *>(static_cast<const __half *>(a.res) +
+                                                                      lay_index(a.Lr, (long long)nb * 64, d, yo, xo) + s0);
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const uint4 r = __ldg(rp + q);
-                    const uint32_t rr[4] = {r.x, r.y, r.z, r.w};
+                    for (int q = 0; q < 4; ++q) {
+                        const uint4 r = __ldg(rp + q);
+                        const uint32_t rr[4] = {r.x, r.y, r.z, r.w};
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        __half2 sum = __hadd2(*reinterpret_cast<const __half2 *>(&h[4 * q + u]),
-                                              *reinterpret_cast<const __half2 *>(&rr[u]));
-                        h[4 * q + u] = sat16x2(*reinterpret_cast<uint32_t *>(&sum));
+                        for (int u = 0; u < 4; ++u) {
+                            __half2 sum = __hadd2(*reinterpret_cast<const __half2 *>(&h[4 * q + u]),
+                                                  *reinterpret_cast<const __half2 *>(&rr[u]));
+                            h[4 * q + u] = sat16x2(*reinterpret_cast<uint32_t *>(&sum));
+                        }
                     }
                 }
-            }
-            if (a.relu) {
+                if (a.relu) {
 #pragma unroll
-                for (int k = 0; k < 16; ++k) h[k] = relu16x2(h[k]);
-            }
-            uint4 *yp = reinterpret_cast<uint4 *>(static_cast<__half *>(a.y) +
-                                                  lay_index(a.Lo, (long long)nb * 64, d, yo, xo) + s0);
+                    for (int k = 0; k < 16; ++k) h[k] = relu16x2(h[k]);
+                }
+                uint4 *yp = reinterpret_cast<uint4 *>(static_cast<__half *>(a.y) +
+                                                      lay_index(a.Lo, (long long)nb * 64, d, yo, xo) + s0);
 #pragma unroll
-            for (int q = 0; q < 4; ++q) yp[q] = make_uint4(h[4 * q], h[4 * q + 1], h[4 * q + 2], h[4 * q + 3]);
+                for (int q = 0; q < 4; ++q) yp[q] = make_uint4(h[4 * q], h[4 * q + 1], h[4 * q + 2], h[4 * q + 3]);
+            }
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -254,6 +309,26 @@ __global__ void __launch_bounds__(192, 1) k_dtc(const __grid_constant__ DtcArgs 
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kCols));
     }
+}
+
+template <int TWP, bool WIN>
+constexpr int dtc_smem() {
+    constexpr int NA = WIN ? 3 : 1, NBX = WIN ? TWP + 2 : TWP, S = WIN ? 2 : (TWP == 4 ? 4 : 6);
+    return S * (NA * kABytes + NBX * kBPix) + 1024 + 256;
+}
+
+template <int TWP, bool WIN>
+cudaError_t launch_dtc(const DtcArgs &a, int tiles, cudaStream_t st) {
+    static std::atomic<uint64_t> attr{0};
+    constexpr int smem = dtc_smem<TWP, WIN>();
+    cudaError_t e = ensure_smem_attr(k_dtc<TWP, WIN>, attr, smem);
+    if (e != cudaSuccess) return e;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int sms = usc_device_sm_count(dev);
+    if (sms <= 0) sms = 148;
+    k_dtc<TWP, WIN><<<(unsigned)(tiles < sms ? tiles : sms), 192, smem, st>>>(a);
+    return cudaGetLastError();
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_tiled() {
@@ -338,17 +413,12 @@ int usc_dense_conv_f16(const usc_geometry *g, int32_t n, const void *w_dev, cons
     a.x_tiles = (Yw + twp - 1) / twp;
     const long long tiles = (long long)a.m_blocks * a.x_tiles * Yh * NB;
     if (tiles > 0x7fffffffLL) return usc::fail(USC_ERR_UNSUPPORTED, "dense conv: grid too large");
-    const int smem = kStages * (kABytes + twp * kBPix) + 1024 + 256;
+    const bool win = K == 3 && s == 1;  // the 3-tap row window (stride 1 only)
     cudaError_t e;
-    if (twp == 4) {
-        static std::atomic<uint64_t> attr{0};
-        e = ensure_smem_attr(k_dtc<4>, attr, smem);
-        if (e == cudaSuccess) k_dtc<4><<<(unsigned)tiles, 192, smem, st>>>(a);
-    } else {
-        static std::atomic<uint64_t> attr{0};
-        e = ensure_smem_attr(k_dtc<2>, attr, smem);
-        if (e == cudaSuccess) k_dtc<2><<<(unsigned)tiles, 192, smem, st>>>(a);
-    }
+    if (twp == 4)
+        e = win ? launch_dtc<4, true>(a, (int)tiles, st) : launch_dtc<4, false>(a, (int)tiles, st);
+    else
+        e = win ? launch_dtc<2, true>(a, (int)tiles, st) : launch_dtc<2, false>(a, (int)tiles, st);
     if (e == cudaSuccess) e = cudaGetLastError();
     return e == cudaSuccess ? USC_OK : usc::fail(USC_ERR_CUDA, "k_dtc: %s", cudaGetErrorString(e));
 }
