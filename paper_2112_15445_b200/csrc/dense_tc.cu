@@ -32,7 +32,7 @@ constexpr int kABytes = 128 * kKC * 2;  // 16 KB
 constexpr int kBPix = kKC * 64 * 2;     // 8 KB per pixel box
 
 struct DtcArgs {
-    CUtensorMap xmap, wmap;
+    CUtensorMap xmap, wmap, ymap, rmap;  // activations, weights, output, shortcut (TMA)
     void *y;
     const void *res;
     LayoutD Lo, Lr;
@@ -57,6 +57,19 @@ __device__ __forceinline__ void mbar_wait_bounded(uint64_t *bar, uint32_t parity
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+
+__device__ __forceinline__ void tma_store_5d(const CUtensorMap *map, const void *src, int c0, int c1, int c2, int c3,
+                                             int c4) {
+    asm volatile(
+        "cp.async.bulk.tensor.5d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5, %6}], [%1];" ::"l"(
+            reinterpret_cast<uint64_t>(map)),
+        "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
+        : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 
 __device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, int c0, int c1, uint64_t *bar) {
     asm volatile(
@@ -118,6 +131,13 @@ __device__ __forceinline__ uint32_t relu16x2(uint32_t w) {
     return out;
 }
 
+// ring depth: the staging tiles (2 x 16 KB output, + 2 x 16 KB shortcut without the
+// window) and the ring share the 227 KB of dynamic shared memory
+template <int TWP, bool WIN>
+constexpr int dtc_stages() {
+    return WIN ? 2 : (TWP == 4 ? 3 : 4);
+}
+
 // Persistent CTA (one per SM), tiles round-robin.  WIN (3x3, stride 1): a stage is one
 // (kh, 64-channel chunk): the TWP+2 input pixels of the row (one 8-KB box each) and the A
 // tiles of the 3 taps kw = 0..2 -- each pixel box is read once for 3 taps (tap kw's B
@@ -130,15 +150,19 @@ __global__ void __launch_bounds__(192, 1) k_dtc(const __grid_constant__ DtcArgs 
     constexpr int NA = WIN ? 3 : 1;                 // A tiles (taps) per stage
     constexpr int NBX = WIN ? TWP + 2 : TWP;        // pixel boxes per stage
     constexpr int kStage = NA * kABytes + NBX * kBPix;
-    constexpr int S = WIN ? 2 : (TWP == 4 ? 4 : 6);  // ring depth (<= ~200 KB)
+    constexpr int S = dtc_stages<TWP, WIN>();       // ring depth
     constexpr uint32_t kCols = 2 * N;               // two accumulators
+    constexpr int kPix = 128 * 128;                 // one output pixel tile: 128 rows (d) x 128 B
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char *smem = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint64_t *full = reinterpret_cast<uint64_t *>(smem + S * kStage);
+    unsigned char *ostage = smem + S * kStage;                  // 2 x 16 KB output staging (SW128)
+    unsigned char *rstage = ostage + 2 * kPix;                  // 2 x 16 KB shortcut staging (non-WIN)
+    uint64_t *full = reinterpret_cast<uint64_t *>(rstage + (WIN ? 0 : 2 * kPix));
     uint64_t *empty = full + S;
     uint64_t *tfull = empty + S;   // [2]
     uint64_t *tempty = tfull + 2;  // [2]
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
+    uint64_t *rfull = tempty + 2;  // [2] shortcut tile landed
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(rfull + 2);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int tiles = a.m_blocks * a.x_tiles * a.Yh * a.NB;
@@ -152,6 +176,7 @@ __global__ void __launch_bounds__(192, 1) k_dtc(const __grid_constant__ DtcArgs 
         for (int b = 0; b < 2; ++b) {
             mbar_init(&tfull[b], 1);
             mbar_init(&tempty[b], 4);  // one arrive per epilogue warp
+            mbar_init(&rfull[b], 1);
         }
         fence_mbar_init();
     }
@@ -240,68 +265,105 @@ __global__ void __launch_bounds__(192, 1) k_dtc(const __grid_constant__ DtcArgs 
         }
     } else {
         // ---------------- epilogue (warps 0-3: TMEM lanes 32w .. 32w+31) ----------------
-        int lt = 0;
+        // Per output pixel: TMEM -> registers (64 samples of row d), binary16 + epilogue,
+        // 128-B rows into a 128-byte-swizzled staging tile (16-B stores, conflict-free), then
+        // one TMA store of the [128 d][64 samples] box into the BI64 output.  The shortcut
+        // of the pixel arrives the same way (TMA load into a staging tile, one pixel ahead).
+        const bool leader = threadIdx.x == 0;
+        const int row = warp * 32 + lane;
+        const bool res = !WIN && a.res != nullptr;
+        const int npix_tile = TWP;
+        auto pixel_coords = [&](int q, int &mb, int &xo, int &yo, int &nb) {  // q-th pixel of this CTA
+            const int t = blockIdx.x + (q / npix_tile) * gridDim.x;
+            int xt;
+            decode(t, mb, xt, yo, nb);
+            xo = xt * TWP + q % npix_tile;
+        };
+        const int my_pixels = ((tiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x) * npix_tile;
+        if (res && leader && my_pixels > 0) {  // shortcut of the first pixel
+            int mb, xo, yo, nb;
+            pixel_coords(0, mb, xo, yo, nb);
+            mbar_expect_tx(&rfull[0], kPix);
+            tma_load_5d(rstage, &a.rmap, 0, xo + a.Lr.pw, yo + a.Lr.ph, mb * 128, nb, &rfull[0]);
+        }
+        int lt = 0, q = 0;
         for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++lt) {
             int mb, xt, yo, nb;
             decode(t, mb, xt, yo, nb);
             const int ab = lt & 1;
             mbar_wait_bounded(&tfull[ab], (lt >> 1) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            const int d = mb * 128 + warp * 32 + lane;
             const uint32_t taddr = tmem + ab * N + ((uint32_t)(warp * 32) << 16);
 #pragma unroll 1
-            for (int ch = 0; ch < N / 32; ++ch) {  // 32 columns = 32 samples of one pixel
-                uint32_t v[32];
-                asm volatile(
-                    "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, "
-                    "%13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, "
-                    "[%32];"
-                    : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-                      "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
-                      "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
-                      "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
-                      "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-                    : "r"(taddr + ch * 32));
-                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                if (ch == N / 32 - 1) {  // every column of this accumulator is in registers: release it
+            for (int px = 0; px < TWP; ++px, ++q) {
+                const int b = q & 1, xo = xt * TWP + px;
+                uint32_t h[32];
+#pragma unroll
+                for (int half = 0; half < 2; ++half) {
+                    uint32_t v[32];
+                    asm volatile(
+                        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, "
+                        "%13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, "
+                        "[%32];"
+                        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
+                          "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
+                          "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
+                          "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+                        : "r"(taddr + px * 64 + half * 32));
+                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+                    for (int k = 0; k < 16; ++k) {
+                        const __half2 p = __floats2half2_rn(__uint_as_float(v[2 * k]), __uint_as_float(v[2 * k + 1]));
+                        h[half * 16 + k] = sat16x2(*reinterpret_cast<const uint32_t *>(&p));
+                    }
+                }
+                if (px == TWP - 1) {  // every column of this accumulator is in registers: release it
                     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&tempty[ab]);
                 }
-                const int px = ch >> 1, s0 = (ch & 1) * 32;
-                const int xo = xt * TWP + px;
-                if (d >= a.D || xo >= a.Yw) continue;
-                uint32_t h[16];
+                // staging slot b is free once the store issued two pixels ago has read it
+                if (leader) bulk_wait_read1();
+                epi_bar();
+                if (res) {
+                    if (leader && q + 1 < my_pixels) {  // prefetch the next pixel's shortcut
+                        int mb2, xo2, yo2, nb2;
+                        pixel_coords(q + 1, mb2, xo2, yo2, nb2);
+                        mbar_expect_tx(&rfull[b ^ 1], kPix);
+                        tma_load_5d(rstage + (b ^ 1) * kPix, &a.rmap, 0, xo2 + a.Lr.pw, yo2 + a.Lr.ph, mb2 * 128, nb2,
+                                    &rfull[b ^ 1]);
+                    }
+                    mbar_wait_bounded(&rfull[b], (q >> 1) & 1);
+                    const unsigned char *rrow = rstage + b * kPix + row * 128;
 #pragma unroll
-                for (int k = 0; k < 16; ++k) {
-                    const __half2 p = __floats2half2_rn(__uint_as_float(v[2 * k]), __uint_as_float(v[2 * k + 1]));
-                    h[k] = sat16x2(*reinterpret_cast<const uint32_t *>(&p));
-                }
-                if (a.res) {
-                    const uint4 *rp = reinterpret_cast<const uint4 *>(static_cast<const __half *>(a.res) +
-                                                                      lay_index(a.Lr, (long long)nb * 64, d, yo, xo) + s0);
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        const uint4 r = __ldg(rp + q);
+                    for (int c = 0; c < 8; ++c) {
+                        const uint4 r = *reinterpret_cast<const uint4 *>(rrow + ((c ^ (row & 7)) << 4));
                         const uint32_t rr[4] = {r.x, r.y, r.z, r.w};
 #pragma unroll
                         for (int u = 0; u < 4; ++u) {
-                            __half2 sum = __hadd2(*reinterpret_cast<const __half2 *>(&h[4 * q + u]),
+                            __half2 sum = __hadd2(*reinterpret_cast<const __half2 *>(&h[4 * c + u]),
                                                   *reinterpret_cast<const __half2 *>(&rr[u]));
-                            h[4 * q + u] = sat16x2(*reinterpret_cast<uint32_t *>(&sum));
+                            h[4 * c + u] = sat16x2(*reinterpret_cast<uint32_t *>(&sum));
                         }
                     }
                 }
                 if (a.relu) {
 #pragma unroll
-                    for (int k = 0; k < 16; ++k) h[k] = relu16x2(h[k]);
+                    for (int k = 0; k < 32; ++k) h[k] = relu16x2(h[k]);
                 }
-                uint4 *yp = reinterpret_cast<uint4 *>(static_cast<__half *>(a.y) +
-                                                      lay_index(a.Lo, (long long)nb * 64, d, yo, xo) + s0);
+                unsigned char *orow = ostage + b * kPix + row * 128;
 #pragma unroll
-                for (int q = 0; q < 4; ++q) yp[q] = make_uint4(h[4 * q], h[4 * q + 1], h[4 * q + 2], h[4 * q + 3]);
+                for (int c = 0; c < 8; ++c)
+                    *reinterpret_cast<uint4 *>(orow + ((c ^ (row & 7)) << 4)) =
+                        make_uint4(h[4 * c], h[4 * c + 1], h[4 * c + 2], h[4 * c + 3]);
+                fence_proxy_async();  // the staged rows -> visible to the TMA engine
+                epi_bar();
+                if (leader && xo < a.Yw)
+                    tma_store_5d(&a.ymap, ostage + b * kPix, 0, xo + a.Lo.pw, yo + a.Lo.ph, mb * 128, nb);
             }
         }
+        if (leader) bulk_wait_all();
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
@@ -313,8 +375,8 @@ __global__ void __launch_bounds__(192, 1) k_dtc(const __grid_constant__ DtcArgs 
 
 template <int TWP, bool WIN>
 constexpr int dtc_smem() {
-    constexpr int NA = WIN ? 3 : 1, NBX = WIN ? TWP + 2 : TWP, S = WIN ? 2 : (TWP == 4 ? 4 : 6);
-    return S * (NA * kABytes + NBX * kBPix) + 1024 + 256;
+    constexpr int NA = WIN ? 3 : 1, NBX = WIN ? TWP + 2 : TWP, S = dtc_stages<TWP, WIN>();
+    return S * (NA * kABytes + NBX * kBPix) + (WIN ? 2 : 4) * 128 * 128 + 1024 + 256;
 }
 
 template <int TWP, bool WIN>
@@ -390,6 +452,20 @@ int usc_dense_conv_f16(const usc_geometry *g, int32_t n, const void *w_dev, cons
                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) return usc::fail(USC_ERR_CUDA, "dense conv: weight tensor map (%d)", (int)r);
     }
+    // output and shortcut: the same BI64 box shape, [128 channels][64 samples] of one pixel
+    auto bi_map = [&](CUtensorMap *m, const usc_act_layout *l, const void *p) -> CUresult {
+        const cuuint64_t dims[5] = {64, (cuuint64_t)l->ws, (cuuint64_t)l->hp, (cuuint64_t)l->channels, (cuuint64_t)NB};
+        const cuuint64_t strides[4] = {128, (cuuint64_t)l->ws * 128, (cuuint64_t)l->ws * l->hp * 128,
+                                       (cuuint64_t)l->sample_stride * 2};
+        const cuuint32_t box[5] = {64, 1, 1, 128, 1};
+        const cuuint32_t es[5] = {1, 1, 1, 1, 1};
+        return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 5, const_cast<void *>(p), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    };
+    if (bi_map(&a.ymap, yl, y) != CUDA_SUCCESS) return usc::fail(USC_ERR_CUDA, "dense conv: output tensor map");
+    if (res && bi_map(&a.rmap, rl, res) != CUDA_SUCCESS)
+        return usc::fail(USC_ERR_CUDA, "dense conv: shortcut tensor map");
     a.y = y;
     a.res = res;
     a.Lo = to_dev(*yl);
@@ -413,7 +489,7 @@ int usc_dense_conv_f16(const usc_geometry *g, int32_t n, const void *w_dev, cons
     a.x_tiles = (Yw + twp - 1) / twp;
     const long long tiles = (long long)a.m_blocks * a.x_tiles * Yh * NB;
     if (tiles > 0x7fffffffLL) return usc::fail(USC_ERR_UNSUPPORTED, "dense conv: grid too large");
-    const bool win = K == 3 && s == 1;  // the 3-tap row window (stride 1 only)
+    const bool win = K == 3 && s == 1 && !res;  // the 3-tap row window (stride 1; no shortcut staging room)
     cudaError_t e;
     if (twp == 4)
         e = win ? launch_dtc<4, true>(a, (int)tiles, st) : launch_dtc<4, false>(a, (int)tiles, st);
