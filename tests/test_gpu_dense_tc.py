@@ -9,7 +9,9 @@ pytestmark = pytest.mark.gpu
 
 @pytest.mark.parametrize("C,D,k,s,hw,n,res", [(64, 128, 3, 1, 8, 100, False), (256, 256, 1, 1, 8, 64, True),
                                               (128, 128, 3, 2, 16, 128, False), (64, 256, 1, 2, 16, 70, False),
-                                              (512, 512, 3, 1, 4, 64, True), (512, 512, 3, 1, 2, 64, False)])
+                                              (512, 512, 3, 1, 4, 64, True), (512, 512, 3, 1, 2, 64, False),
+                                              (512, 512, 3, 1, 4, 256, False), (512, 512, 3, 1, 2, 256, False),
+                                              (256, 512, 1, 1, 4, 256, True)])
 def test_dense_tc_matches_torch(C, D, k, s, hw, n, res):
     import torch
     from paper_2112_15445_b200 import _lib
