@@ -298,8 +298,9 @@ int usc_f16_epilogue(void *y, const void *res, int64_t count, int32_t relu, void
  * epilogue fused: round to binary16 with saturation, + shortcut `res` (binary16, sat16),
  * ReLU when relu != 0.  torch conv2d semantics: padding = filter/2 (read from the input
  * halo, which must be at least that wide), stride g->stride_h (= stride_w, 1 or 2),
- * filters 1x1 or 3x3; in_channels % 64 == 0, out_channels % 128 == 0.  `w_dev`: the dense
- * weights as [out_channels][filter_h*filter_w][in_channels] binary16 (K-major). */
+ * filters 1x1 or 3x3; in_channels % 64 == 0, out_channels % 64 == 0.  `w_dev`: the dense
+ * weights as [out_channels][filter_h*filter_w][in_channels] binary16 (K-major), padded with
+ * zero rows to a multiple of 128 output channels. */
 int usc_dense_conv_f16(const usc_geometry *g, int32_t n, const void *w_dev, const usc_act_layout *x_layout,
                        const void *x, const usc_act_layout *y_layout, void *y, const usc_act_layout *res_layout,
                        const void *res, int32_t relu, void *stream);

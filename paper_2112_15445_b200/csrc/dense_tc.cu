@@ -414,8 +414,8 @@ int usc_dense_conv_f16(const usc_geometry *g, int32_t n, const void *w_dev, cons
     if (g->filter_h != g->filter_w || (g->filter_h != 1 && g->filter_h != 3) || g->stride_h != g->stride_w ||
         (g->stride_h != 1 && g->stride_h != 2))
         return usc::fail(USC_ERR_UNSUPPORTED, "dense conv: 1x1 / 3x3 filters, stride 1 or 2");
-    if (g->in_channels % kKC || g->out_channels % 128)
-        return usc::fail(USC_ERR_UNSUPPORTED, "dense conv: channels in %% 64 and out %% 128 needed");
+    if (g->in_channels % kKC || g->out_channels % 64)
+        return usc::fail(USC_ERR_UNSUPPORTED, "dense conv: channels in %% 64 and out %% 64 needed");
     if (xl->interleave != 64 || yl->interleave != 64 || (res && (!rl || rl->interleave != 64)))
         return usc::fail(USC_ERR_UNSUPPORTED, "dense conv: BI64 layouts only");
     const int s = g->stride_h, K = g->filter_h, pad = K / 2;
@@ -442,8 +442,9 @@ int usc_dense_conv_f16(const usc_geometry *g, int32_t n, const void *w_dev, cons
         if (r != CUDA_SUCCESS) return usc::fail(USC_ERR_CUDA, "dense conv: activation tensor map (%d)", (int)r);
     }
     const int taps = K * K, Kd = taps * g->in_channels;
-    {   // weights: [D][taps*C] binary16 K-major, box [64 k][128 d]
-        const cuuint64_t dims[2] = {(cuuint64_t)Kd, (cuuint64_t)g->out_channels};
+    const int Dpad = (g->out_channels + 127) / 128 * 128;  // the packed weights carry zero rows up to 128k
+    {   // weights: [Dpad][taps*C] binary16 K-major, box [64 k][128 d]
+        const cuuint64_t dims[2] = {(cuuint64_t)Kd, (cuuint64_t)Dpad};
         const cuuint64_t strides[1] = {(cuuint64_t)Kd * 2};
         const cuuint32_t box[2] = {(cuuint32_t)kKC, 128};
         const cuuint32_t es[2] = {1, 1};
@@ -481,11 +482,15 @@ int usc_dense_conv_f16(const usc_geometry *g, int32_t n, const void *w_dev, cons
     a.Yw = Yw;
     a.NB = NB;
     a.relu = relu;
-    a.m_blocks = g->out_channels / 128;
+    a.m_blocks = Dpad / 128;  // a 64-channel layer runs M = 128 with zero rows; the TMA store clips them
     a.cb = g->in_channels / kKC;
     a.k_iters = taps * a.cb;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    const int twp = Yw % 4 == 0 ? 4 : 2;
+    int dev = 0, sms = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess && usc_device_sm_count(dev) > 0) sms = usc_device_sm_count(dev);
+    // N = 256 (4 pixels) unless that leaves SMs idle: then 2-pixel tiles (twice the tiles)
+    int twp = Yw % 4 == 0 ? 4 : 2;
+    if (twp == 4 && (long long)a.m_blocks * (Yw / 4) * Yh * NB < sms) twp = 2;
     a.x_tiles = (Yw + twp - 1) / twp;
     const long long tiles = (long long)a.m_blocks * a.x_tiles * Yh * NB;
     if (tiles > 0x7fffffffLL) return usc::fail(USC_ERR_UNSUPPORTED, "dense conv: grid too large");

@@ -18,17 +18,22 @@ from . import _lib
 
 def tc_eligible(in_channels: int, out_channels: int, k: int, stride: int) -> bool:
     """Shapes the tensor-core kernel takes."""
-    return in_channels % 64 == 0 and out_channels % 128 == 0 and k in (1, 3) and stride in (1, 2)
+    return in_channels % 64 == 0 and out_channels % 64 == 0 and k in (1, 3) and stride in (1, 2)
 
 
 def pack_weights(w, device=None):
-    """Dense (D, C, K, K) weights -> the kernel's binary16 [D][K*K][C] (K-major) tensor."""
+    """Dense (D, C, K, K) weights -> the kernel's binary16 [D][K*K][C] (K-major) tensor, zero
+    rows appended up to a multiple of 128 output channels (the MMA's M)."""
     import torch
     t = w if type(w).__module__.startswith("torch") else torch.from_numpy(
         np.array(w.data if hasattr(w, "data") else w, dtype=np.float32))
     t = t.to(device or "cuda", torch.float16)
     D, C, kh, kw = t.shape
-    return t.permute(0, 2, 3, 1).reshape(D, kh * kw * C).contiguous()
+    packed = t.permute(0, 2, 3, 1).reshape(D, kh * kw * C)
+    dpad = -(-D // 128) * 128
+    if dpad != D:
+        packed = torch.cat([packed, packed.new_zeros((dpad - D, kh * kw * C))])
+    return packed.contiguous()
 
 
 def dense_conv(w_packed, in_channels: int, out_channels: int, k: int, stride: int, n: int, x, x_lay, y, y_lay,

@@ -340,7 +340,10 @@ class SparseVGG16:
         tc_argmin = ["tc" if tce[li] and tc_ms[li] <= sparse_ms[li] else "sparse" for li in range(nl)]
         cands = {"all-sparse": ["sparse"] * nl, "all-dense": ["dense" if e else "sparse" for e in elig],
                  "argmin": argmin, "tc-argmin": tc_argmin, "all-tc": ["tc" if e else "sparse" for e in tce],
-                 "tc-argmin+dense": ["tc" if tc_argmin[li] == "tc" else argmin[li] for li in range(nl)]}
+                 "tc-argmin+dense": ["tc" if tc_argmin[li] == "tc" else argmin[li] for li in range(nl)],
+                 "min3": [min((("sparse", sparse_ms[li]),) + ((("tc", tc_ms[li]),) if tce[li] else ()) +
+                              ((("dense", dense_ms[li]),) if li in dense_ms else ()), key=lambda kv: kv[1])[0]
+                          for li in range(nl)]}
         for k in range(1, nl):
             cands[f"dense-from-{k}"] = ["dense" if elig[li] and li >= k else "sparse" for li in range(nl)]
         times, seen = {}, set()

@@ -445,6 +445,9 @@ class SparseResNet50:
         blocks = [li for li, (name, _, role, _) in enumerate(self.layers) if role == "c1"]
         cands = {"all-sparse": ["sparse"] * nl, "all-dense": ["dense" if e else "sparse" for e in elig],
                  "argmin": argmin, "tc-argmin": tc_argmin, "tc-argmin+dense": tc_argmin_dense,
+                 "min3": [min((("sparse", sparse_ms[li]),) + ((("tc", tc_ms[li]),) if tce[li] else ()) +
+                              ((("dense", dense_ms[li]),) if elig[li] else ()), key=lambda kv: kv[1])[0]
+                          for li in range(nl)],
                  "all-tc": ["tc" if e else "sparse" for e in tce]}
         for k in blocks:
             cands[f"dense-from-{self.layers[k][0]}"] = ["dense" if elig[li] and li >= k else "sparse"
