@@ -185,7 +185,7 @@ def test_benchmarked_dispatch_states_within_tolerance(net):
     import torch
     state = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles",
                                         f"r02_tuned_{net}_fp16_dispatch.json")))
-    assert "dense" in state["backends"] and "sparse" in state["backends"]
+    assert "sparse" in state["backends"] and set(state["backends"]) - {"sparse"}
     x = oracle.round_to_binary16(np.random.default_rng(31).standard_normal((256, 3, 32, 32)).astype(np.float32))
     th = oracle.max_threads()
     if net == "vgg16":
