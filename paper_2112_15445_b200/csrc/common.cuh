@@ -6,6 +6,7 @@
 
 #include <atomic>
 #include <cstdint>
+#include <utility>
 
 #include "usc_internal.h"
 
@@ -64,6 +65,34 @@ inline cudaError_t ensure_smem_attr(F fn, std::atomic<uint64_t> &done, int bytes
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
     if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_acq_rel);
     return e;
+}
+
+// --------------------------------------------------------------------------
+// Programmatic dependent launch (PDL): a kernel launched with launch_pdl may start its
+// prologue (barriers, TMEM, descriptor prefetch) while the previous kernel on the
+// stream drains; it must call pdl_wait() before its first global-memory access
+// (griddepcontrol.wait returns once the previous grid has completed and its writes
+// are visible -- a no-op for a plain launch).  pdl_release() lets the next PDL kernel
+// be scheduled onto SMs this grid frees.  USC_NO_PDL=1 turns the attribute off.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_release() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+bool pdl_enabled();  // host.cpp: false when USC_NO_PDL is set
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args &&...args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
 // --------------------------------------------------------------------------

@@ -22,6 +22,7 @@
 //     fp32 result is bit-identical to the reference.  Zero-weight entries are
 //     deduplicated by the packer (no-ops for finite inputs; one copy per offset
 //     preserves NaN propagation).
+#include <cstdlib>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
@@ -34,6 +35,16 @@
 #include "usc_internal.h"
 
 using usc::fail;
+
+namespace usc_dev {
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char *v = std::getenv("USC_NO_PDL");
+        return !(v && *v && *v != '0');
+    }();
+    return on;
+}
+}  // namespace usc_dev
 
 namespace {
 using namespace usc_dev;
@@ -344,7 +355,6 @@ __global__ void k_maxpool2(const T *__restrict__ src, T *__restrict__ dst, int n
     const long long total = (long long)n_total * C * OH * OW;
     for (long long i0 = blockIdx.x * (long long)blockDim.x + threadIdx.x; i0 < total;
          i0 += (long long)gridDim.x * blockDim.x) {
-        const long long i = i0;
         I t = static_cast<I>(i0);  // 32-bit index arithmetic when the count allows
         int lane = 0;
         if (Lo.il) {
@@ -377,6 +387,64 @@ __global__ void k_maxpool2(const T *__restrict__ src, T *__restrict__ dst, int n
                 }
             }
         dst[lay_index(Lo, b, c, y, x)] = w[m];
+    }
+}
+
+// The same pooling between two batch-interleaved layouts (BI32 / BI64): one 16-byte
+// vector of consecutive samples per thread, four vector loads (the 2x2 window), one
+// vector store -- every access a coalesced 16-B transaction.
+template <typename T, typename I>
+__global__ void k_maxpool2_bi(const T *__restrict__ src, T *__restrict__ dst, int NB, int C, int OH, int OW,
+                              const LayoutD Li, const LayoutD Lo) {
+    constexpr int V = 16 / sizeof(T);
+    pdl_release();
+    pdl_wait();
+    const int lanes = Lo.il / V;
+    const long long total = (long long)NB * C * OH * OW * lanes;
+    const long long rs = (long long)Li.Ws * Li.il;  // one input row
+    for (long long i0 = blockIdx.x * (long long)blockDim.x + threadIdx.x; i0 < total;
+         i0 += (long long)gridDim.x * blockDim.x) {
+        I t = static_cast<I>(i0);
+        const int l = static_cast<int>(t % lanes);
+        t /= lanes;
+        const int x = static_cast<int>(t % OW);
+        t /= OW;
+        const int y = static_cast<int>(t % OH);
+        t /= OH;
+        const int c = static_cast<int>(t % C);
+        const long long nb = static_cast<long long>(t / C);
+        const long long pi = nb * Li.ss + (((long long)c * Li.Hp + 2 * y + Li.ph) * Li.Ws + 2 * x + Li.pw) * Li.il + l * V;
+        const long long po = nb * Lo.ss + (((long long)c * Lo.Hp + y + Lo.ph) * Lo.Ws + x + Lo.pw) * Lo.il + l * V;
+        uint4 raw[4];
+        raw[0] = *reinterpret_cast<const uint4 *>(src + pi);
+        raw[1] = *reinterpret_cast<const uint4 *>(src + pi + Li.il);
+        raw[2] = *reinterpret_cast<const uint4 *>(src + pi + rs);
+        raw[3] = *reinterpret_cast<const uint4 *>(src + pi + rs + Li.il);
+        const T *w0 = reinterpret_cast<const T *>(&raw[0]);
+        uint4 out;
+        T *o = reinterpret_cast<T *>(&out);
+#pragma unroll
+        for (int e = 0; e < V; ++e) {
+            T best = w0[e];
+            float vm = static_cast<float>(best);
+            if (!isnan(vm)) {
+#pragma unroll
+                for (int k = 1; k < 4; ++k) {
+                    const T wk = reinterpret_cast<const T *>(&raw[k])[e];
+                    const float v = static_cast<float>(wk);
+                    if (isnan(v)) {
+                        best = wk;
+                        break;
+                    }
+                    if (v > vm) {
+                        vm = v;
+                        best = wk;
+                    }
+                }
+            }
+            o[e] = best;
+        }
+        *reinterpret_cast<uint4 *>(dst + po) = out;
     }
 }
 
@@ -828,6 +896,22 @@ int usc_maxpool2(const usc_act_layout *in_l, const usc_act_layout *out_l, int32_
     const int n_total = il ? (n + il - 1) / il * il : n;
     const long long total = (long long)n_total * in_l->channels * OH * OW;
     const LayoutD Li = to_dev(*in_l), Lo = to_dev(*out_l);
+    if (il && (dtype == USC_F32 || dtype == USC_F16 || dtype == USC_CB4)) {  // vectorised BI path
+        const int NB = n_total / il, V = dtype == USC_F32 ? 4 : 8;
+        const long long vecs = total / V;
+        const dim3 grid(grid_for(vecs)), block(256);
+        cudaError_t e;
+        if (dtype == USC_F32)
+            e = launch_pdl(vecs < 0x7fffffffLL ? k_maxpool2_bi<float, unsigned> : k_maxpool2_bi<float, long long>, grid,
+                           block, 0, st, static_cast<const float *>(src), static_cast<float *>(dst), NB,
+                           (int)in_l->channels, OH, OW, Li, Lo);
+        else
+            e = launch_pdl(vecs < 0x7fffffffLL ? k_maxpool2_bi<__half, unsigned> : k_maxpool2_bi<__half, long long>,
+                           grid, block, 0, st, static_cast<const __half *>(src), static_cast<__half *>(dst), NB,
+                           (int)in_l->channels, OH, OW, Li, Lo);
+        if (e != cudaSuccess) return fail(USC_ERR_CUDA, "k_maxpool2_bi launch: %s", cudaGetErrorString(e));
+        return cuda_check("k_maxpool2_bi launch");
+    }
     if (dtype == USC_F32) {
         (total < 0x7fffffffLL ? k_maxpool2<float, unsigned> : k_maxpool2<float, long long>)<<<grid_for(total), 256, 0, st>>>(static_cast<const float *>(src),
                                                            static_cast<float *>(dst), n_total,

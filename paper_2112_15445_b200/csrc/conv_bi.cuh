@@ -899,8 +899,11 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1) k_bi(const __grid_constant_
             mbar_init(&empty[s], NWC);
         }
         fence_mbar_init();
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&a.xmap)) : "memory");
     }
     __syncthreads();
+    pdl_release();
+    pdl_wait();  // every global access below: the previous kernel's output is complete
 
     if (warp == NWC) {
         // ---------------- producer warp ----------------
@@ -1020,8 +1023,8 @@ int launch_inst(const usc_plan *pl, const BiArgs &a, cudaStream_t st) {
     std::atomic<uint64_t> &attr = res ? attr_res : attr_plain;
     cudaError_t ae = ensure_smem_attr(fn, attr, 224 * 1024);
     if (ae != cudaSuccess) return usc::fail(USC_ERR_CUDA, "smem attribute: %s", cudaGetErrorString(ae));
-    fn<<<static_cast<unsigned>(pl->grid_x), (NWC + 1) * 32, pl->smem_bytes, st>>>(a);
-    cudaError_t e = cudaGetLastError();
+    cudaError_t e = launch_pdl(fn, dim3(static_cast<unsigned>(pl->grid_x)), dim3((NWC + 1) * 32), pl->smem_bytes, st, a);
+    if (e == cudaSuccess) e = cudaGetLastError();
     if (e != cudaSuccess) return usc::fail(USC_ERR_CUDA, "k_bi launch: %s", cudaGetErrorString(e));
     return USC_OK;
 }

@@ -14,10 +14,11 @@
 //       tensor -> [64 c][64 s] (8 KB), i.e. MN-major (samples contiguous), one 128-B
 //       swizzle row per channel; the TWP boxes of a stage are the MN atoms of B.
 // MMAs of K = 16 (tcgen05.mma.cta_group::1.kind::f16, M128 x N, fp32 acc), see k_dtc for
-// the stage shapes.  Warp roles: warps 0-3 epilogue (TMEM lane quarter = warp), warp 4
-// TMA producer and TMEM owner, warp 5 MMA issuer.  Epilogue: tcgen05.ld 32 columns at a time, binary16
-// rounding with saturation, optional residual add (binary16) + saturation, ReLU
-// (NaN -> 0), 64-byte stores into the output layout (halo untouched).
+// the stage shapes.  Warp roles: warps 0-7 epilogue (TMEM lane quarter = warp % 4), warp 8
+// TMA producer and TMEM owner, warp 9 MMA issuer.  Epilogue (each warp on its own 32
+// channels and every other pixel): tcgen05.ld, binary16 rounding with saturation (cvt.satfinite), optional
+// residual add (binary16) + saturation, ReLU (NaN -> 0), TMA stores of [32 c][64 s] boxes
+// into the output layout (halo untouched).
 #include <cudaTypedefs.h>
 
 #include "common.cuh"
@@ -26,6 +27,18 @@
 using namespace usc_dev;
 
 namespace {
+
+#ifdef DTC_TRACE  // timeline probe (tools/dtc_trace.cu): %globaltimer stamps per CTA, never in the product build
+__device__ unsigned long long g_dtc_trace[1024][8];
+__device__ __forceinline__ void dtc_stamp(int k) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_dtc_trace[blockIdx.x][k] = t;
+}
+#define DTC_STAMP(k) dtc_stamp(k)
+#else
+#define DTC_STAMP(k)
+#endif
 
 constexpr int kKC = 64;               // channels (K) per stage and tap
 constexpr int kABytes = 128 * kKC * 2;  // 16 KB
@@ -67,9 +80,9 @@ __device__ __forceinline__ void tma_store_5d(const CUtensorMap *map, const void 
         : "memory");
     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
-__device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory"); }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
-__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 
 __device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, int c0, int c1, uint64_t *bar) {
     asm volatile(
@@ -113,29 +126,36 @@ __device__ __forceinline__ void umma_commit(uint64_t *bar) {
                  : "memory");
 }
 
-__device__ __forceinline__ uint32_t sat16x2(uint32_t w) {  // +-inf -> +-65504 per half
-#pragma unroll
-    for (int k = 0; k < 2; ++k) {
-        const uint32_t h = (w >> (16 * k)) & 0xffffu;
-        if ((h & 0x7fffu) == 0x7c00u) w = (w & ~(0xffffu << (16 * k))) | (((h & 0x8000u) | 0x7bffu) << (16 * k));
-    }
-    return w;
-}
-__device__ __forceinline__ uint32_t relu16x2(uint32_t w) {
-    uint32_t out = 0;
-#pragma unroll
-    for (int k = 0; k < 2; ++k) {
-        const uint32_t h = (w >> (16 * k)) & 0xffffu, m = h & 0x7fffu;
-        if (!(h & 0x8000u) && m != 0 && m <= 0x7c00u) out |= h << (16 * k);
-    }
-    return out;
+// Epilogue: kEW warps, two per TMEM lane quarter (warp w: channels 32 (w % 4) .. +31 of
+// the tile, the tile's even (w < 4) or odd pixels).  Staging per warp: kOS output slots
+// and, with a shortcut, kRS shortcut slots of one pixel box [32 channels][64 samples]
+// binary16 = 4 KB each (128-byte swizzle, 1024-B aligned).
+constexpr int kWarpBox = 32 * 128;
+constexpr int kEW = 8, kOS = 1, kRS = 2;
+constexpr int kThreads = (kEW + 2) * 32;  // + TMA producer warp + MMA warp
+
+// ring depth: the ring and the staging slots share the 227 KB of dynamic shared memory
+template <int TWP, bool WIN, bool RES>
+constexpr int dtc_stages() {
+    return WIN ? 2 : (TWP == 4 ? (RES ? 2 : 3) : 4);
 }
 
-// ring depth: the staging tiles (2 x 16 KB output, + 2 x 16 KB shortcut without the
-// window) and the ring share the 227 KB of dynamic shared memory
-template <int TWP, bool WIN>
-constexpr int dtc_stages() {
-    return WIN ? 2 : (TWP == 4 ? 3 : 4);
+__device__ __forceinline__ uint32_t cvt_f16x2_sat(float lo, float hi) {  // +-inf/overflow -> +-65504, NaN kept
+    uint32_t r;
+    asm("cvt.rn.satfinite.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+    return r;
+}
+__device__ __forceinline__ uint32_t add_f16x2_sat(uint32_t x, uint32_t y) {  // binary16 sum, saturated, NaN kept
+    uint32_t r;
+    asm("{\n.reg .b32 t;\nadd.rn.f16x2 t, %1, %2;\nmin.NaN.f16x2 t, t, %3;\nmax.NaN.f16x2 %0, t, %4;\n}\n"
+        : "=r"(r)
+        : "r"(x), "r"(y), "r"(0x7bff7bffu), "r"(0xfbfffbffu));
+    return r;
+}
+__device__ __forceinline__ uint32_t relu_f16x2(uint32_t x) {  // max(x, 0): negatives and NaN -> 0
+    uint32_t r;
+    asm("max.f16x2 %0, %1, %2;" : "=r"(r) : "r"(x), "r"(0u));
+    return r;
 }
 
 // Persistent CTA (one per SM), tiles round-robin.  WIN (3x3, stride 1): a stage is one
@@ -144,43 +164,43 @@ constexpr int dtc_stages() {
 // operand is the MN atoms kw .. kw+TWP-1 of the window); 12 MMAs per stage.  Otherwise a
 // stage is one (tap, chunk): TWP boxes + one A tile, 4 MMAs.  Two TMEM accumulators
 // (2 x N fp32 columns): the epilogue of tile i overlaps the main loop of tile i+1.
-template <int TWP, bool WIN>
-__global__ void __launch_bounds__(192, 1) k_dtc(const __grid_constant__ DtcArgs a) {
+template <int TWP, bool WIN, bool RES>
+__global__ void __launch_bounds__(kThreads, 1) k_dtc(const __grid_constant__ DtcArgs a) {
     constexpr int N = TWP * 64;
     constexpr int NA = WIN ? 3 : 1;                 // A tiles (taps) per stage
     constexpr int NBX = WIN ? TWP + 2 : TWP;        // pixel boxes per stage
     constexpr int kStage = NA * kABytes + NBX * kBPix;
-    constexpr int S = dtc_stages<TWP, WIN>();       // ring depth
+    constexpr int S = dtc_stages<TWP, WIN, RES>();  // ring depth
     constexpr uint32_t kCols = 2 * N;               // two accumulators
-    constexpr int kPix = 128 * 128;                 // one output pixel tile: 128 rows (d) x 128 B
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char *smem = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    unsigned char *ostage = smem + S * kStage;                  // 2 x 16 KB output staging (SW128)
-    unsigned char *rstage = ostage + 2 * kPix;                  // 2 x 16 KB shortcut staging (non-WIN)
-    uint64_t *full = reinterpret_cast<uint64_t *>(rstage + (WIN ? 0 : 2 * kPix));
+    unsigned char *ostage = smem + S * kStage;           // [kEW warps][kOS] output boxes
+    unsigned char *rstage = ostage + kEW * kOS * kWarpBox;  // [kEW warps][kRS] shortcut boxes (RES)
+    uint64_t *full = reinterpret_cast<uint64_t *>(rstage + (RES ? kEW * kRS * kWarpBox : 0));
     uint64_t *empty = full + S;
     uint64_t *tfull = empty + S;   // [2]
     uint64_t *tempty = tfull + 2;  // [2]
-    uint64_t *rfull = tempty + 2;  // [2] shortcut tile landed
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(rfull + 2);
+    uint64_t *rfull = tempty + 2;  // [kEW warps][kRS] shortcut box landed
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(rfull + kEW * kRS);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int tiles = a.m_blocks * a.x_tiles * a.Yh * a.NB;
     const int kiters = WIN ? a.Kh * a.cb : a.k_iters;
 
     if (threadIdx.x == 0) {
+        DTC_STAMP(0);
         for (int s = 0; s < S; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&tfull[b], 1);
-            mbar_init(&tempty[b], 4);  // one arrive per epilogue warp
-            mbar_init(&rfull[b], 1);
+            mbar_init(&tempty[b], kEW);  // one arrive per epilogue warp
         }
+        for (int b = 0; b < kEW * kRS; ++b) mbar_init(&rfull[b], 1);
         fence_mbar_init();
     }
-    if (warp == 4) {
+    if (warp == kEW) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                      "n"(kCols));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -189,6 +209,15 @@ __global__ void __launch_bounds__(192, 1) k_dtc(const __grid_constant__ DtcArgs 
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = *tmem_slot;
+    if (threadIdx.x == 0) DTC_STAMP(1);
+    if (threadIdx.x == 0) {  // descriptors into the TMA unit while the previous kernel drains
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&a.xmap)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&a.wmap)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&a.ymap)) : "memory");
+        if (RES) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&a.rmap)) : "memory");
+    }
+    pdl_release();
+    pdl_wait();  // every global access below: the previous kernel's output is complete
 
     auto decode = [&](int t, int &mb, int &xt, int &yo, int &nb) {
         mb = t % a.m_blocks;
@@ -199,42 +228,40 @@ __global__ void __launch_bounds__(192, 1) k_dtc(const __grid_constant__ DtcArgs 
         nb = t / a.Yh;
     };
 
-    if (warp == 4) {
+    if (warp == kEW) {
         // ---------------- TMA producer ----------------
-        if (lane == 0) {
-            int it = 0;  // running stage counter
-            for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
-                int mb, xt, yo, nb;
-                decode(t, mb, xt, yo, nb);
-                for (int i = 0; i < kiters; ++i, ++it) {
-                    const int s = it % S;
-                    if (it >= S) mbar_wait_bounded(&empty[s], ((it / S) - 1) & 1);
-                    unsigned char *st = smem + s * kStage;
-                    mbar_expect_tx(&full[s], kStage);
-                    if constexpr (WIN) {
-                        const int kh = i / a.cb, cb = i - kh * a.cb;
-#pragma unroll
-                        for (int kw = 0; kw < 3; ++kw)
-                            tma_load_2d(st + kw * kABytes, &a.wmap, (kh * 3 + kw) * a.C + cb * kKC, mb * 128, &full[s]);
-                        const int yi = yo + kh + a.offh;
-#pragma unroll
-                        for (int j = 0; j < NBX; ++j)
-                            tma_load_5d(st + NA * kABytes + j * kBPix, &a.xmap, 0, xt * TWP + j + a.offw, yi, cb * kKC,
-                                        nb, &full[s]);
-                    } else {
-                        const int tap = i / a.cb, cb = i - tap * a.cb;
-                        const int kh = tap / a.Kw, kw = tap - kh * a.Kw;
+        // The stage's boxes are issued by parallel lanes, one box per lane: successive TMA
+        // instructions of one thread issue ~370 clocks apart (tools/tma_rate_bench.cu), so a
+        // single issuing lane caps the stream at ~20-35 B/clk per SM.
+        int it = 0;  // running stage counter
+        for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+            int mb, xt, yo, nb;
+            decode(t, mb, xt, yo, nb);
+            for (int i = 0; i < kiters; ++i, ++it) {
+                const int s = it % S;
+                if (it >= S) mbar_wait_bounded(&empty[s], ((it / S) - 1) & 1);
+                unsigned char *st = smem + s * kStage;
+                if (lane == 0) mbar_expect_tx(&full[s], kStage);
+                __syncwarp();
+                if constexpr (WIN) {
+                    const int kh = i / a.cb, cb = i - kh * a.cb;
+                    if (lane < 3)
+                        tma_load_2d(st + lane * kABytes, &a.wmap, (kh * 3 + lane) * a.C + cb * kKC, mb * 128, &full[s]);
+                    else if (lane < 3 + NBX)
+                        tma_load_5d(st + NA * kABytes + (lane - 3) * kBPix, &a.xmap, 0, xt * TWP + (lane - 3) + a.offw,
+                                    yo + kh + a.offh, cb * kKC, nb, &full[s]);
+                } else {
+                    const int tap = i / a.cb, cb = i - tap * a.cb;
+                    const int kh = tap / a.Kw, kw = tap - kh * a.Kw;
+                    if (lane == 0)
                         tma_load_2d(st, &a.wmap, tap * a.C + cb * kKC, mb * 128, &full[s]);
-                        const int yi = a.stride * yo + kh + a.offh;
-#pragma unroll
-                        for (int j = 0; j < TWP; ++j)
-                            tma_load_5d(st + kABytes + j * kBPix, &a.xmap, 0, a.stride * (xt * TWP + j) + kw + a.offw, yi,
-                                        cb * kKC, nb, &full[s]);
-                    }
+                    else if (lane <= TWP)
+                        tma_load_5d(st + kABytes + (lane - 1) * kBPix, &a.xmap, 0, a.stride * (xt * TWP + lane - 1) + kw + a.offw,
+                                    a.stride * yo + kh + a.offh, cb * kKC, nb, &full[s]);
                 }
             }
         }
-    } else if (warp == 5) {
+    } else if (warp == kEW + 1) {
         // ---------------- MMA issuer ----------------
         const uint32_t idesc = (1u << 4) | (1u << 16) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
         int it = 0, lt = 0;
@@ -247,6 +274,7 @@ __global__ void __launch_bounds__(192, 1) k_dtc(const __grid_constant__ DtcArgs 
                 const int s = it % S;
                 mbar_wait_bounded(&full[s], (it / S) & 1);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                if (lane == 0 && it == 0) DTC_STAMP(2);
                 if (lane == 0) {
                     const uint32_t abase = smem_u32(smem + s * kStage), bbase = abase + NA * kABytes;
 #pragma unroll
@@ -259,138 +287,149 @@ __global__ void __launch_bounds__(192, 1) k_dtc(const __grid_constant__ DtcArgs 
                         }
                     umma_commit(&empty[s]);
                     if (i == kiters - 1) umma_commit(&tfull[ab]);
+                    if (i == kiters - 1 && lt < 2) DTC_STAMP(3 + lt);
                 }
                 __syncwarp();
             }
         }
     } else {
-        // ---------------- epilogue (warps 0-3: TMEM lanes 32w .. 32w+31) ----------------
-        // Per output pixel: TMEM -> registers (64 samples of row d), binary16 + epilogue,
-        // 128-B rows into a 128-byte-swizzled staging tile (16-B stores, conflict-free), then
-        // one TMA store of the [128 d][64 samples] box into the BI64 output.  The shortcut
-        // of the pixel arrives the same way (TMA load into a staging tile, one pixel ahead).
-        const bool leader = threadIdx.x == 0;
-        const int row = warp * 32 + lane;
-        const bool res = !WIN && a.res != nullptr;
-        const int npix_tile = TWP;
+        // ---------------- epilogue (warp w: TMEM lanes 32 (w % 4) .. +31) ----------------
+        // Each warp owns output channels mb*128 + 32 (w % 4) .. +31 and every other pixel of
+        // every tile, and runs on its own: per output pixel, TMEM -> registers (64 samples
+        // of its channel row), binary16 with saturation, + shortcut, ReLU, 128-B rows into a
+        // swizzled 4-KB staging box, one TMA store of [32 channels][64 samples].  The
+        // shortcut boxes stream in through a kRS-deep per-warp ring issued ahead (HBM
+        // latency off the critical path).  j counts this warp's pixels (CTA pixel 2j + half).
+        const int ch0 = (warp & 3) * 32, half = warp >> 2;
+        unsigned char *ost = ostage + warp * kOS * kWarpBox;
+        unsigned char *rst = rstage + warp * kRS * kWarpBox;
+        uint64_t *rbar = rfull + warp * kRS;
         auto pixel_coords = [&](int q, int &mb, int &xo, int &yo, int &nb) {  // q-th pixel of this CTA
-            const int t = blockIdx.x + (q / npix_tile) * gridDim.x;
+            const int t = blockIdx.x + (q / TWP) * gridDim.x;
             int xt;
             decode(t, mb, xt, yo, nb);
-            xo = xt * TWP + q % npix_tile;
+            xo = xt * TWP + q % TWP;
         };
-        const int my_pixels = ((tiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x) * npix_tile;
-        if (res && leader && my_pixels > 0) {  // shortcut of the first pixel
+        const int my_pixels = ((tiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x) * (TWP / 2);
+        const bool res = RES && a.res != nullptr;
+        auto issue_res = [&](int jj) {  // lane 0: shortcut box of this warp's channels at its pixel jj
             int mb, xo, yo, nb;
-            pixel_coords(0, mb, xo, yo, nb);
-            mbar_expect_tx(&rfull[0], kPix);
-            tma_load_5d(rstage, &a.rmap, 0, xo + a.Lr.pw, yo + a.Lr.ph, mb * 128, nb, &rfull[0]);
-        }
+            pixel_coords(2 * jj + half, mb, xo, yo, nb);
+            const int slot = jj % kRS;
+            mbar_expect_tx(&rbar[slot], kWarpBox);
+            tma_load_5d(rst + slot * kWarpBox, &a.rmap, 0, xo + a.Lr.pw, yo + a.Lr.ph, mb * 128 + ch0, nb, &rbar[slot]);
+        };
+        if (res && lane == 0)
+            for (int jj = 0; jj < kRS && jj < my_pixels; ++jj) issue_res(jj);
         int lt = 0, q = 0;
         for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++lt) {
             int mb, xt, yo, nb;
             decode(t, mb, xt, yo, nb);
             const int ab = lt & 1;
+            const bool live = mb * 128 + ch0 < a.D;  // rows past D (64-channel layers) are not stored
             mbar_wait_bounded(&tfull[ab], (lt >> 1) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            const uint32_t taddr = tmem + ab * N + ((uint32_t)(warp * 32) << 16);
+            if (warp == 0 && lane == 0 && lt < 2) DTC_STAMP(5 + lt);
+            const uint32_t taddr = tmem + ab * N + ((uint32_t)(ch0) << 16);
 #pragma unroll 1
-            for (int px = 0; px < TWP; ++px, ++q) {
-                const int b = q & 1, xo = xt * TWP + px;
-                uint32_t h[32];
-#pragma unroll
-                for (int half = 0; half < 2; ++half) {
-                    uint32_t v[32];
-                    asm volatile(
-                        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, "
-                        "%13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, "
-                        "[%32];"
-                        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-                          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
-                          "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
-                          "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
-                          "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-                        : "r"(taddr + px * 64 + half * 32));
-                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-                    for (int k = 0; k < 16; ++k) {
-                        const __half2 p = __floats2half2_rn(__uint_as_float(v[2 * k]), __uint_as_float(v[2 * k + 1]));
-                        h[half * 16 + k] = sat16x2(*reinterpret_cast<const uint32_t *>(&p));
-                    }
-                }
-                if (px == TWP - 1) {  // every column of this accumulator is in registers: release it
+            for (int px = half; px < TWP; px += 2, ++q) {
+                const int xo = xt * TWP + px;
+                uint32_t v[64];
+                asm volatile(
+                    "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, "
+                    "%13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, "
+                    "[%32];"
+                    : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                      "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
+                      "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
+                      "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
+                      "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+                    : "r"(taddr + px * 64));
+                asm volatile(
+                    "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, "
+                    "%13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, "
+                    "[%32];"
+                    : "=r"(v[32]), "=r"(v[33]), "=r"(v[34]), "=r"(v[35]), "=r"(v[36]), "=r"(v[37]), "=r"(v[38]),
+                      "=r"(v[39]), "=r"(v[40]), "=r"(v[41]), "=r"(v[42]), "=r"(v[43]), "=r"(v[44]), "=r"(v[45]),
+                      "=r"(v[46]), "=r"(v[47]), "=r"(v[48]), "=r"(v[49]), "=r"(v[50]), "=r"(v[51]), "=r"(v[52]),
+                      "=r"(v[53]), "=r"(v[54]), "=r"(v[55]), "=r"(v[56]), "=r"(v[57]), "=r"(v[58]), "=r"(v[59]),
+                      "=r"(v[60]), "=r"(v[61]), "=r"(v[62]), "=r"(v[63])
+                    : "r"(taddr + px * 64 + 32));
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                if (px + 2 >= TWP) {  // this warp's columns of the accumulator are in registers: release
                     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&tempty[ab]);
                 }
-                // staging slot b is free once the store issued two pixels ago has read it
-                if (leader) bulk_wait_read1();
-                epi_bar();
+                uint32_t h[32];
+#pragma unroll
+                for (int k = 0; k < 32; ++k) h[k] = cvt_f16x2_sat(__uint_as_float(v[2 * k]), __uint_as_float(v[2 * k + 1]));
                 if (res) {
-                    if (leader && q + 1 < my_pixels) {  // prefetch the next pixel's shortcut
-                        int mb2, xo2, yo2, nb2;
-                        pixel_coords(q + 1, mb2, xo2, yo2, nb2);
-                        mbar_expect_tx(&rfull[b ^ 1], kPix);
-                        tma_load_5d(rstage + (b ^ 1) * kPix, &a.rmap, 0, xo2 + a.Lr.pw, yo2 + a.Lr.ph, mb2 * 128, nb2,
-                                    &rfull[b ^ 1]);
-                    }
-                    mbar_wait_bounded(&rfull[b], (q >> 1) & 1);
-                    const unsigned char *rrow = rstage + b * kPix + row * 128;
+                    const int slot = q % kRS;  // q counts this warp's pixels
+                    mbar_wait_bounded(&rbar[slot], (q / kRS) & 1);
+                    const unsigned char *rrow = rst + slot * kWarpBox + lane * 128;
 #pragma unroll
                     for (int c = 0; c < 8; ++c) {
-                        const uint4 r = *reinterpret_cast<const uint4 *>(rrow + ((c ^ (row & 7)) << 4));
-                        const uint32_t rr[4] = {r.x, r.y, r.z, r.w};
-#pragma unroll
-                        for (int u = 0; u < 4; ++u) {
-                            __half2 sum = __hadd2(*reinterpret_cast<const __half2 *>(&h[4 * c + u]),
-                                                  *reinterpret_cast<const __half2 *>(&rr[u]));
-                            h[4 * c + u] = sat16x2(*reinterpret_cast<uint32_t *>(&sum));
-                        }
+                        const uint4 r = *reinterpret_cast<const uint4 *>(rrow + ((c ^ (lane & 7)) << 4));
+                        h[4 * c] = add_f16x2_sat(h[4 * c], r.x);
+                        h[4 * c + 1] = add_f16x2_sat(h[4 * c + 1], r.y);
+                        h[4 * c + 2] = add_f16x2_sat(h[4 * c + 2], r.z);
+                        h[4 * c + 3] = add_f16x2_sat(h[4 * c + 3], r.w);
+                    }
+                    __syncwarp();  // every lane has read the slot: refill it kRS pixels ahead
+                    if (lane == 0 && q + kRS < my_pixels) {
+                        fence_proxy_async();
+                        issue_res(q + kRS);
                     }
                 }
                 if (a.relu) {
 #pragma unroll
-                    for (int k = 0; k < 32; ++k) h[k] = relu16x2(h[k]);
+                    for (int k = 0; k < 32; ++k) h[k] = relu_f16x2(h[k]);
                 }
-                unsigned char *orow = ostage + b * kPix + row * 128;
+                // staging slot q % kOS is free once the store issued kOS pixels ago has read it
+                unsigned char *obox = ost + (q % kOS) * kWarpBox;
+                if (lane == 0) bulk_wait_read<kOS - 1>();
+                __syncwarp();
+                unsigned char *orow = obox + lane * 128;
 #pragma unroll
                 for (int c = 0; c < 8; ++c)
-                    *reinterpret_cast<uint4 *>(orow + ((c ^ (row & 7)) << 4)) =
+                    *reinterpret_cast<uint4 *>(orow + ((c ^ (lane & 7)) << 4)) =
                         make_uint4(h[4 * c], h[4 * c + 1], h[4 * c + 2], h[4 * c + 3]);
                 fence_proxy_async();  // the staged rows -> visible to the TMA engine
-                epi_bar();
-                if (leader && xo < a.Yw)
-                    tma_store_5d(&a.ymap, ostage + b * kPix, 0, xo + a.Lo.pw, yo + a.Lo.ph, mb * 128, nb);
+                __syncwarp();
+                if (lane == 0 && live && xo < a.Yw)
+                    tma_store_5d(&a.ymap, obox, 0, xo + a.Lo.pw, yo + a.Lo.ph, mb * 128 + ch0, nb);
             }
         }
-        if (leader) bulk_wait_all();
+        if (lane == 0) bulk_wait_all();
+        if (warp == 0 && lane == 0) DTC_STAMP(7);
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
-    if (warp == 4) {
+    if (warp == kEW) {
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kCols));
     }
 }
 
-template <int TWP, bool WIN>
+template <int TWP, bool WIN, bool RES>
 constexpr int dtc_smem() {
-    constexpr int NA = WIN ? 3 : 1, NBX = WIN ? TWP + 2 : TWP, S = dtc_stages<TWP, WIN>();
-    return S * (NA * kABytes + NBX * kBPix) + (WIN ? 2 : 4) * 128 * 128 + 1024 + 256;
+    constexpr int NA = WIN ? 3 : 1, NBX = WIN ? TWP + 2 : TWP, S = dtc_stages<TWP, WIN, RES>();
+    return S * (NA * kABytes + NBX * kBPix) + kEW * (kOS + (RES ? kRS : 0)) * kWarpBox + 1024 + 256;
 }
 
-template <int TWP, bool WIN>
+template <int TWP, bool WIN, bool RES>
 cudaError_t launch_dtc(const DtcArgs &a, int tiles, cudaStream_t st) {
     static std::atomic<uint64_t> attr{0};
-    constexpr int smem = dtc_smem<TWP, WIN>();
-    cudaError_t e = ensure_smem_attr(k_dtc<TWP, WIN>, attr, smem);
+    constexpr int smem = dtc_smem<TWP, WIN, RES>();
+    static_assert(smem <= 227 * 1024, "k_dtc shared memory");
+    cudaError_t e = ensure_smem_attr(k_dtc<TWP, WIN, RES>, attr, smem);
     if (e != cudaSuccess) return e;
     int dev = 0;
     cudaGetDevice(&dev);
     int sms = usc_device_sm_count(dev);
     if (sms <= 0) sms = 148;
-    k_dtc<TWP, WIN><<<(unsigned)(tiles < sms ? tiles : sms), 192, smem, st>>>(a);
-    return cudaGetLastError();
+    return launch_pdl(k_dtc<TWP, WIN, RES>, dim3((unsigned)(tiles < sms ? tiles : sms)), dim3(kThreads), smem, st, a);
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_tiled() {
@@ -406,6 +445,12 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_tiled() {
 }
 
 }  // namespace
+
+#ifdef DTC_TRACE
+extern "C" int usc_dtc_trace_read(unsigned long long *out, int ctas) {
+    return cudaMemcpyFromSymbol(out, g_dtc_trace, (size_t)ctas * 8 * sizeof(unsigned long long)) == cudaSuccess ? 0 : -1;
+}
+#endif
 
 int usc_dense_conv_f16(const usc_geometry *g, int32_t n, const void *w_dev, const usc_act_layout *xl, const void *x,
                        const usc_act_layout *yl, void *y, const usc_act_layout *rl, const void *res, int32_t relu,
@@ -453,12 +498,12 @@ int usc_dense_conv_f16(const usc_geometry *g, int32_t n, const void *w_dev, cons
                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) return usc::fail(USC_ERR_CUDA, "dense conv: weight tensor map (%d)", (int)r);
     }
-    // output and shortcut: the same BI64 box shape, [128 channels][64 samples] of one pixel
+    // output and shortcut: the same BI64 box shape, [32 channels][64 samples] of one pixel
     auto bi_map = [&](CUtensorMap *m, const usc_act_layout *l, const void *p) -> CUresult {
         const cuuint64_t dims[5] = {64, (cuuint64_t)l->ws, (cuuint64_t)l->hp, (cuuint64_t)l->channels, (cuuint64_t)NB};
         const cuuint64_t strides[4] = {128, (cuuint64_t)l->ws * 128, (cuuint64_t)l->ws * l->hp * 128,
                                        (cuuint64_t)l->sample_stride * 2};
-        const cuuint32_t box[5] = {64, 1, 1, 128, 1};
+        const cuuint32_t box[5] = {64, 1, 1, 32, 1};  // one epilogue warp's 32 channels
         const cuuint32_t es[5] = {1, 1, 1, 1, 1};
         return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 5, const_cast<void *>(p), dims, strides, box, es,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -497,9 +542,11 @@ int usc_dense_conv_f16(const usc_geometry *g, int32_t n, const void *w_dev, cons
     const bool win = K == 3 && s == 1 && !res;  // the 3-tap row window (stride 1; no shortcut staging room)
     cudaError_t e;
     if (twp == 4)
-        e = win ? launch_dtc<4, true>(a, (int)tiles, st) : launch_dtc<4, false>(a, (int)tiles, st);
+        e = win ? launch_dtc<4, true, false>(a, (int)tiles, st)
+                : (res ? launch_dtc<4, false, true>(a, (int)tiles, st) : launch_dtc<4, false, false>(a, (int)tiles, st));
     else
-        e = win ? launch_dtc<2, true>(a, (int)tiles, st) : launch_dtc<2, false>(a, (int)tiles, st);
+        e = win ? launch_dtc<2, true, false>(a, (int)tiles, st)
+                : (res ? launch_dtc<2, false, true>(a, (int)tiles, st) : launch_dtc<2, false, false>(a, (int)tiles, st));
     if (e == cudaSuccess) e = cudaGetLastError();
     return e == cudaSuccess ? USC_OK : usc::fail(USC_ERR_CUDA, "k_dtc: %s", cudaGetErrorString(e));
 }

@@ -48,3 +48,42 @@ def test_dense_tc_matches_torch(C, D, k, s, hw, n, res):
     # the halo of the output buffer stays zero
     full = yb.view(-1)
     assert torch.isfinite(full.float()).all()
+
+
+@pytest.mark.parametrize("res,relu", [(False, False), (True, False), (True, True)])
+def test_dense_tc_saturates(res, relu):
+    """Outputs past the binary16 range saturate to +-65504 (conversion and shortcut add),
+    negatives survive without ReLU."""
+    import torch
+    from paper_2112_15445_b200 import _lib
+    from paper_2112_15445_b200.dense import dense_conv, pack_weights
+    C, D, hw, n = 64, 128, 4, 64
+    rng = np.random.default_rng([7, int(res), int(relu)])
+    x = torch.from_numpy(rng.standard_normal((n, C, hw, hw)).astype(np.float32) * 60).cuda().half()
+    w = torch.from_numpy(rng.standard_normal((D, C, 1, 1)).astype(np.float32) * 60).cuda().half()
+    xl = _lib.act_layout(C, hw, hw, 0, 0, 2, 64)
+    xb = torch.zeros(xl.elems(n), dtype=torch.float16, device="cuda")
+    L = _lib.lib()
+    _lib.check(L.usc_pad_input(_lib.ref(xl), _lib.USC_F16, n, _lib.t_ptr(x), _lib.t_ptr(xb), _lib.stream_ptr()))
+    yl = _lib.act_layout(D, hw, hw, 1, 1, 2, 64)
+    yb = torch.zeros(yl.elems(n), dtype=torch.float16, device="cuda")
+    ref = torch.nn.functional.conv2d(x.float(), w.float()).clamp(-65504, 65504)
+    rb, rl = None, None
+    if res:
+        r = torch.from_numpy(rng.standard_normal((n, D, hw, hw)).astype(np.float32) * 3e4).cuda().half()
+        rl = _lib.act_layout(D, hw, hw, 0, 0, 2, 64)
+        rb = torch.zeros(rl.elems(n), dtype=torch.float16, device="cuda")
+        _lib.check(L.usc_pad_input(_lib.ref(rl), _lib.USC_F16, n, _lib.t_ptr(r), _lib.t_ptr(rb), _lib.stream_ptr()))
+        ref = (ref.half().float() + r.float()).clamp(-65504, 65504)
+    if relu:
+        ref = torch.relu(ref)
+    dense_conv(pack_weights(w), C, D, 1, 1, n, xb, xl, yb, yl, rb, rl, relu=relu)
+    out = torch.empty((n, D, hw, hw), dtype=torch.float16, device="cuda")
+    _lib.check(L.usc_unpad_output(_lib.ref(yl), _lib.USC_F16, n, _lib.t_ptr(yb), _lib.t_ptr(out), _lib.stream_ptr()))
+    torch.cuda.synchronize()
+    assert torch.isfinite(out.float()).all()
+    assert float(out.float().abs().max()) == 65504.0
+    if not relu:
+        assert float(out.float().min()) < 0
+    err = float((out.float() - ref).abs().max())
+    assert err <= 1e-2 * 65504, err
