@@ -304,6 +304,17 @@ int usc_f16_epilogue(void *y, const void *res, int64_t count, int32_t relu, void
 int usc_dense_conv_f16(const usc_geometry *g, int32_t n, const void *w_dev, const usc_act_layout *x_layout,
                        const void *x, const usc_act_layout *y_layout, void *y, const usc_act_layout *res_layout,
                        const void *res, int32_t relu, void *stream);
+/* The same with a device workspace for split-K on small maps (tiles filling at most half
+ * the SMs, no shortcut): the CTA completing a tile's last K split sums the splits' fp32
+ * partials in split order and runs the epilogue.  `workspace` must hold
+ * usc_dense_conv_f16_ws_bytes() bytes and be zero-filled once before its first use (the
+ * kernel leaves its counters at zero); a null or short workspace runs without split. */
+int usc_dense_conv_f16_ws(const usc_geometry *g, int32_t n, const void *w_dev, const usc_act_layout *x_layout,
+                          const void *x, const usc_act_layout *y_layout, void *y, const usc_act_layout *res_layout,
+                          const void *res, int32_t relu, void *workspace, int64_t ws_bytes, void *stream);
+/* Workspace bytes usc_dense_conv_f16_ws needs for this shape on the current device (0: no split). */
+int64_t usc_dense_conv_f16_ws_bytes(const usc_geometry *g, int32_t n, const usc_act_layout *x_layout,
+                                    int32_t has_res);
 /* round_to_binary16 (tensor.py:48-63) on device: f32 in -> f32 on the binary16 grid
  * (to_half == 0) or binary16 storage (to_half == 1). */
 int usc_round_binary16(const float *src, void *dst, int64_t count, int32_t to_half, void *stream);

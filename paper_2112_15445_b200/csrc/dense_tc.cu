@@ -53,6 +53,9 @@ struct DtcArgs {
     int Yh, Yw, NB, relu;
     int m_blocks, x_tiles;
     int k_iters, cb;  // k_iters = taps * cb, cb = C / 64
+    int splits, kper;  // split-K: work item = (tile, split), split s runs k-iterations [s*kper, (s+1)*kper)
+    float *part;       // split-K partial sums [tile][split][N columns][128 rows] fp32
+    int *cnt;          // split-K arrival counter per tile (zero between launches)
 };
 
 __device__ __forceinline__ void mbar_wait_bounded(uint64_t *bar, uint32_t parity) {
@@ -80,6 +83,7 @@ __device__ __forceinline__ void tma_store_5d(const CUtensorMap *map, const void 
         : "memory");
     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
+__device__ __forceinline__ void epi_sync() { asm volatile("bar.sync 1, %0;" ::"n"(8 * 32) : "memory"); }
 template <int N>
 __device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory"); }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
@@ -172,6 +176,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_dtc(const __grid_constant__ Dtc
     constexpr int kStage = NA * kABytes + NBX * kBPix;
     constexpr int S = dtc_stages<TWP, WIN, RES>();  // ring depth
     constexpr uint32_t kCols = 2 * N;               // two accumulators
+    static_assert(kEW == 8, "epi_sync counts 8 epilogue warps");
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char *smem = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     unsigned char *ostage = smem + S * kStage;           // [kEW warps][kOS] output boxes
@@ -186,6 +191,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_dtc(const __grid_constant__ Dtc
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int tiles = a.m_blocks * a.x_tiles * a.Yh * a.NB;
     const int kiters = WIN ? a.Kh * a.cb : a.k_iters;
+    const int items = tiles * a.splits;
+    auto krange = [&](int t, int &tile, int &sp, int &k0, int &k1) {  // work item -> tile, k-iteration range
+        tile = t / a.splits;
+        sp = t - tile * a.splits;
+        k0 = sp * a.kper;
+        k1 = min(kiters, k0 + a.kper);
+    };
 
     if (threadIdx.x == 0) {
         DTC_STAMP(0);
@@ -234,10 +246,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_dtc(const __grid_constant__ Dtc
         // instructions of one thread issue ~370 clocks apart (tools/tma_rate_bench.cu), so a
         // single issuing lane caps the stream at ~20-35 B/clk per SM.
         int it = 0;  // running stage counter
-        for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
-            int mb, xt, yo, nb;
-            decode(t, mb, xt, yo, nb);
-            for (int i = 0; i < kiters; ++i, ++it) {
+        for (int t = blockIdx.x; t < items; t += gridDim.x) {
+            int tile, sp, k0, k1, mb, xt, yo, nb;
+            krange(t, tile, sp, k0, k1);
+            decode(tile, mb, xt, yo, nb);
+            for (int i = k0; i < k1; ++i, ++it) {
                 const int s = it % S;
                 if (it >= S) mbar_wait_bounded(&empty[s], ((it / S) - 1) & 1);
                 unsigned char *st = smem + s * kStage;
@@ -265,12 +278,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_dtc(const __grid_constant__ Dtc
         // ---------------- MMA issuer ----------------
         const uint32_t idesc = (1u << 4) | (1u << 16) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
         int it = 0, lt = 0;
-        for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++lt) {
+        for (int t = blockIdx.x; t < items; t += gridDim.x, ++lt) {
+            int tile, sp, k0, k1;
+            krange(t, tile, sp, k0, k1);
             const int ab = lt & 1;
             if (lt >= 2) mbar_wait_bounded(&tempty[ab], ((lt >> 1) - 1) & 1);  // epilogue drained it
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             const uint32_t acc = tmem + ab * N;
-            for (int i = 0; i < kiters; ++i, ++it) {
+            for (int i = k0; i < k1; ++i, ++it) {
                 const int s = it % S;
                 mbar_wait_bounded(&full[s], (it / S) & 1);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -283,11 +298,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_dtc(const __grid_constant__ Dtc
                         for (int k = 0; k < kKC / 16; ++k) {
                             const uint64_t ad = desc_sw128(abase + q * kABytes + k * 32, 16, 1024);
                             const uint64_t bd = desc_sw128(bbase + q * kBPix + k * 16 * 128, kBPix, 1024);
-                            umma_f16(acc, ad, bd, idesc, (i > 0 || q > 0 || k > 0) ? 1u : 0u);
+                            umma_f16(acc, ad, bd, idesc, (i > k0 || q > 0 || k > 0) ? 1u : 0u);
                         }
                     umma_commit(&empty[s]);
-                    if (i == kiters - 1) umma_commit(&tfull[ab]);
-                    if (i == kiters - 1 && lt < 2) DTC_STAMP(3 + lt);
+                    if (i == k1 - 1) umma_commit(&tfull[ab]);
+                    if (i == k1 - 1 && lt < 2) DTC_STAMP(3 + lt);
                 }
                 __syncwarp();
             }
@@ -321,85 +336,140 @@ __global__ void __launch_bounds__(kThreads, 1) k_dtc(const __grid_constant__ Dtc
         };
         if (res && lane == 0)
             for (int jj = 0; jj < kRS && jj < my_pixels; ++jj) issue_res(jj);
+        auto tmem_ld64 = [&](uint32_t addr, uint32_t(&v)[64]) {  // 64 fp32 columns of this warp's lanes
+            asm volatile(
+                "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, "
+                "%13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, "
+                "[%32];"
+                : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                  "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
+                  "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
+                  "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
+                  "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+                : "r"(addr));
+            asm volatile(
+                "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, "
+                "%13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, "
+                "[%32];"
+                : "=r"(v[32]), "=r"(v[33]), "=r"(v[34]), "=r"(v[35]), "=r"(v[36]), "=r"(v[37]), "=r"(v[38]),
+                  "=r"(v[39]), "=r"(v[40]), "=r"(v[41]), "=r"(v[42]), "=r"(v[43]), "=r"(v[44]), "=r"(v[45]),
+                  "=r"(v[46]), "=r"(v[47]), "=r"(v[48]), "=r"(v[49]), "=r"(v[50]), "=r"(v[51]), "=r"(v[52]),
+                  "=r"(v[53]), "=r"(v[54]), "=r"(v[55]), "=r"(v[56]), "=r"(v[57]), "=r"(v[58]), "=r"(v[59]),
+                  "=r"(v[60]), "=r"(v[61]), "=r"(v[62]), "=r"(v[63])
+                : "r"(addr + 32));
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        };
+        // one output pixel of this warp's 32 channels: fp32 sums -> binary16 (+ shortcut,
+        // ReLU) -> staging box -> TMA store; q counts this warp's pixels
+        auto emit = [&](const uint32_t(&v)[64], int q, int mb, int xo, int yo, int nb, bool live) {
+            uint32_t h[32];
+#pragma unroll
+            for (int k = 0; k < 32; ++k) h[k] = cvt_f16x2_sat(__uint_as_float(v[2 * k]), __uint_as_float(v[2 * k + 1]));
+            if (res) {
+                const int slot = q % kRS;
+                mbar_wait_bounded(&rbar[slot], (q / kRS) & 1);
+                const unsigned char *rrow = rst + slot * kWarpBox + lane * 128;
+#pragma unroll
+                for (int c = 0; c < 8; ++c) {
+                    const uint4 r = *reinterpret_cast<const uint4 *>(rrow + ((c ^ (lane & 7)) << 4));
+                    h[4 * c] = add_f16x2_sat(h[4 * c], r.x);
+                    h[4 * c + 1] = add_f16x2_sat(h[4 * c + 1], r.y);
+                    h[4 * c + 2] = add_f16x2_sat(h[4 * c + 2], r.z);
+                    h[4 * c + 3] = add_f16x2_sat(h[4 * c + 3], r.w);
+                }
+                __syncwarp();  // every lane has read the slot: refill it kRS pixels ahead
+                if (lane == 0 && q + kRS < my_pixels) {
+                    fence_proxy_async();
+                    issue_res(q + kRS);
+                }
+            }
+            if (a.relu) {
+#pragma unroll
+                for (int k = 0; k < 32; ++k) h[k] = relu_f16x2(h[k]);
+            }
+            // staging slot q % kOS is free once the store issued kOS pixels ago has read it
+            unsigned char *obox = ost + (q % kOS) * kWarpBox;
+            if (lane == 0) bulk_wait_read<kOS - 1>();
+            __syncwarp();
+            unsigned char *orow = obox + lane * 128;
+#pragma unroll
+            for (int c = 0; c < 8; ++c)
+                *reinterpret_cast<uint4 *>(orow + ((c ^ (lane & 7)) << 4)) =
+                    make_uint4(h[4 * c], h[4 * c + 1], h[4 * c + 2], h[4 * c + 3]);
+            fence_proxy_async();  // the staged rows -> visible to the TMA engine
+            __syncwarp();
+            if (lane == 0 && live && xo < a.Yw)
+                tma_store_5d(&a.ymap, obox, 0, xo + a.Lo.pw, yo + a.Lo.ph, mb * 128 + ch0, nb);
+        };
+        __shared__ int s_last;  // split-K: this CTA completed the tile's last split
         int lt = 0, q = 0;
-        for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++lt) {
-            int mb, xt, yo, nb;
-            decode(t, mb, xt, yo, nb);
+        for (int t = blockIdx.x; t < items; t += gridDim.x, ++lt) {
+            int tile, sp, k0, k1, mb, xt, yo, nb;
+            krange(t, tile, sp, k0, k1);
+            decode(tile, mb, xt, yo, nb);
             const int ab = lt & 1;
             const bool live = mb * 128 + ch0 < a.D;  // rows past D (64-channel layers) are not stored
             mbar_wait_bounded(&tfull[ab], (lt >> 1) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             if (warp == 0 && lane == 0 && lt < 2) DTC_STAMP(5 + lt);
             const uint32_t taddr = tmem + ab * N + ((uint32_t)(ch0) << 16);
+            if (a.splits == 1) {
 #pragma unroll 1
-            for (int px = half; px < TWP; px += 2, ++q) {
-                const int xo = xt * TWP + px;
+                for (int px = half; px < TWP; px += 2, ++q) {
+                    uint32_t v[64];
+                    tmem_ld64(taddr + px * 64, v);
+                    if (px + 2 >= TWP) {  // this warp's columns of the accumulator are in registers: release
+                        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(&tempty[ab]);
+                    }
+                    emit(v, q, mb, xt * TWP + px, yo, nb, live);
+                }
+                continue;
+            }
+            // split-K: the partial sums go to the workspace (column-major, 128 B per column
+            // and warp); the CTA that completes a tile's last split sums the splits in split
+            // order (deterministic) and runs the epilogue
+            float *mine = a.part + ((size_t)tile * a.splits + sp) * (N * 128) + ch0 + lane;
+#pragma unroll 1
+            for (int px = half; px < TWP; px += 2) {
                 uint32_t v[64];
-                asm volatile(
-                    "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, "
-                    "%13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, "
-                    "[%32];"
-                    : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-                      "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
-                      "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
-                      "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
-                      "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-                    : "r"(taddr + px * 64));
-                asm volatile(
-                    "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, "
-                    "%13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, "
-                    "[%32];"
-                    : "=r"(v[32]), "=r"(v[33]), "=r"(v[34]), "=r"(v[35]), "=r"(v[36]), "=r"(v[37]), "=r"(v[38]),
-                      "=r"(v[39]), "=r"(v[40]), "=r"(v[41]), "=r"(v[42]), "=r"(v[43]), "=r"(v[44]), "=r"(v[45]),
-                      "=r"(v[46]), "=r"(v[47]), "=r"(v[48]), "=r"(v[49]), "=r"(v[50]), "=r"(v[51]), "=r"(v[52]),
-                      "=r"(v[53]), "=r"(v[54]), "=r"(v[55]), "=r"(v[56]), "=r"(v[57]), "=r"(v[58]), "=r"(v[59]),
-                      "=r"(v[60]), "=r"(v[61]), "=r"(v[62]), "=r"(v[63])
-                    : "r"(taddr + px * 64 + 32));
-                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                if (px + 2 >= TWP) {  // this warp's columns of the accumulator are in registers: release
+                tmem_ld64(taddr + px * 64, v);
+                if (px + 2 >= TWP) {
                     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&tempty[ab]);
                 }
-                uint32_t h[32];
 #pragma unroll
-                for (int k = 0; k < 32; ++k) h[k] = cvt_f16x2_sat(__uint_as_float(v[2 * k]), __uint_as_float(v[2 * k + 1]));
-                if (res) {
-                    const int slot = q % kRS;  // q counts this warp's pixels
-                    mbar_wait_bounded(&rbar[slot], (q / kRS) & 1);
-                    const unsigned char *rrow = rst + slot * kWarpBox + lane * 128;
-#pragma unroll
-                    for (int c = 0; c < 8; ++c) {
-                        const uint4 r = *reinterpret_cast<const uint4 *>(rrow + ((c ^ (lane & 7)) << 4));
-                        h[4 * c] = add_f16x2_sat(h[4 * c], r.x);
-                        h[4 * c + 1] = add_f16x2_sat(h[4 * c + 1], r.y);
-                        h[4 * c + 2] = add_f16x2_sat(h[4 * c + 2], r.z);
-                        h[4 * c + 3] = add_f16x2_sat(h[4 * c + 3], r.w);
-                    }
-                    __syncwarp();  // every lane has read the slot: refill it kRS pixels ahead
-                    if (lane == 0 && q + kRS < my_pixels) {
-                        fence_proxy_async();
-                        issue_res(q + kRS);
-                    }
-                }
-                if (a.relu) {
-#pragma unroll
-                    for (int k = 0; k < 32; ++k) h[k] = relu_f16x2(h[k]);
-                }
-                // staging slot q % kOS is free once the store issued kOS pixels ago has read it
-                unsigned char *obox = ost + (q % kOS) * kWarpBox;
-                if (lane == 0) bulk_wait_read<kOS - 1>();
-                __syncwarp();
-                unsigned char *orow = obox + lane * 128;
-#pragma unroll
-                for (int c = 0; c < 8; ++c)
-                    *reinterpret_cast<uint4 *>(orow + ((c ^ (lane & 7)) << 4)) =
-                        make_uint4(h[4 * c], h[4 * c + 1], h[4 * c + 2], h[4 * c + 3]);
-                fence_proxy_async();  // the staged rows -> visible to the TMA engine
-                __syncwarp();
-                if (lane == 0 && live && xo < a.Yw)
-                    tma_store_5d(&a.ymap, obox, 0, xo + a.Lo.pw, yo + a.Lo.ph, mb * 128 + ch0, nb);
+                for (int c = 0; c < 64; ++c) mine[(px * 64 + c) * 128] = __uint_as_float(v[c]);
             }
+            __threadfence();
+            epi_sync();
+            if (threadIdx.x == 0) s_last = atomicAdd(&a.cnt[tile], 1) == a.splits - 1;
+            epi_sync();
+            if (!s_last) continue;
+            __threadfence();
+            const float *base = a.part + (size_t)tile * a.splits * (N * 128) + ch0 + lane;
+#pragma unroll 1
+            for (int px = half; px < TWP; px += 2, ++q) {
+                float acc[64];  // split 0, then + split 1, 2, ... (64 independent loads per split)
+#pragma unroll
+                for (int c = 0; c < 64; ++c) acc[c] = __ldcg(base + (px * 64 + c) * 128);
+#pragma unroll 1
+                for (int sp2 = 1; sp2 < a.splits; ++sp2) {
+                    const float *ps = base + (size_t)sp2 * (N * 128) + px * 64 * 128;
+                    float t[64];
+#pragma unroll
+                    for (int c = 0; c < 64; ++c) t[c] = __ldcg(ps + c * 128);
+#pragma unroll
+                    for (int c = 0; c < 64; ++c) acc[c] += t[c];
+                }
+                uint32_t v[64];
+#pragma unroll
+                for (int c = 0; c < 64; ++c) v[c] = __float_as_uint(acc[c]);
+                emit(v, q, mb, xt * TWP + px, yo, nb, live);
+            }
+            if (threadIdx.x == 0) a.cnt[tile] = 0;  // ready for the next launch
         }
         if (lane == 0) bulk_wait_all();
         if (warp == 0 && lane == 0) DTC_STAMP(7);
@@ -452,9 +522,47 @@ extern "C" int usc_dtc_trace_read(unsigned long long *out, int ctas) {
 }
 #endif
 
-int usc_dense_conv_f16(const usc_geometry *g, int32_t n, const void *w_dev, const usc_act_layout *xl, const void *x,
-                       const usc_act_layout *yl, void *y, const usc_act_layout *rl, const void *res, int32_t relu,
-                       void *stream) {
+namespace {
+
+// Tile shape and split-K factor of one launch (shared by the launch and the workspace query)
+struct DtcShape {
+    int twp, x_tiles, m_blocks, NB, Yh, Yw, kiters, splits, kper;
+    long long tiles;
+};
+
+DtcShape dtc_shape(const usc_geometry *g, int n, const usc_act_layout *xl, bool res, bool win, int sms) {
+    DtcShape d{};
+    const int s = g->stride_h, K = g->filter_h, pad = K / 2;
+    d.Yh = (xl->height + 2 * pad - K) / s + 1;
+    d.Yw = (xl->width + 2 * pad - K) / s + 1;
+    d.NB = (n + 63) / 64;
+    d.m_blocks = (g->out_channels + 127) / 128;
+    // N = 256 (4 pixels) unless that leaves SMs idle: then 2-pixel tiles (twice the tiles)
+    d.twp = d.Yw % 4 == 0 ? 4 : 2;
+    if (d.twp == 4 && (long long)d.m_blocks * (d.Yw / 4) * d.Yh * d.NB < sms) d.twp = 2;
+    d.x_tiles = (d.Yw + d.twp - 1) / d.twp;
+    d.tiles = (long long)d.m_blocks * d.x_tiles * d.Yh * d.NB;
+    d.kiters = (win ? K : K * K) * (g->in_channels / kKC);
+    // split-K when the tiles fill at most half the SMs (small maps): each split >= 4 k-iterations
+    d.splits = 1;
+    if (!res && d.tiles > 0 && d.tiles * 2 <= sms) {
+        const int want = (int)std::min<long long>(sms / d.tiles, d.kiters / 4);
+        if (want >= 2) d.splits = want;
+    }
+    d.kper = (d.kiters + d.splits - 1) / d.splits;
+    d.splits = (d.kiters + d.kper - 1) / d.kper;
+    return d;
+}
+
+size_t dtc_ws_bytes(const DtcShape &d) {
+    if (d.splits <= 1) return 0;
+    const size_t part = (size_t)d.tiles * d.splits * (d.twp * 64) * 128 * sizeof(float);
+    return part + (size_t)d.tiles * sizeof(int) + 256;
+}
+
+int dense_conv_impl(const usc_geometry *g, int32_t n, const void *w_dev, const usc_act_layout *xl, const void *x,
+                    const usc_act_layout *yl, void *y, const usc_act_layout *rl, const void *res, int32_t relu,
+                    void *workspace, size_t ws_bytes, void *stream) {
     if (!g || !w_dev || !xl || !x || !yl || !y || n < 1) return usc::fail(USC_ERR_VALUE, "dense conv: null argument");
     if (g->filter_h != g->filter_w || (g->filter_h != 1 && g->filter_h != 3) || g->stride_h != g->stride_w ||
         (g->stride_h != 1 && g->stride_h != 2))
@@ -533,13 +641,21 @@ int usc_dense_conv_f16(const usc_geometry *g, int32_t n, const void *w_dev, cons
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     int dev = 0, sms = 148;
     if (cudaGetDevice(&dev) == cudaSuccess && usc_device_sm_count(dev) > 0) sms = usc_device_sm_count(dev);
-    // N = 256 (4 pixels) unless that leaves SMs idle: then 2-pixel tiles (twice the tiles)
-    int twp = Yw % 4 == 0 ? 4 : 2;
-    if (twp == 4 && (long long)a.m_blocks * (Yw / 4) * Yh * NB < sms) twp = 2;
-    a.x_tiles = (Yw + twp - 1) / twp;
-    const long long tiles = (long long)a.m_blocks * a.x_tiles * Yh * NB;
-    if (tiles > 0x7fffffffLL) return usc::fail(USC_ERR_UNSUPPORTED, "dense conv: grid too large");
     const bool win = K == 3 && s == 1 && !res;  // the 3-tap row window (stride 1; no shortcut staging room)
+    DtcShape d = dtc_shape(g, n, xl, res != nullptr, win, sms);
+    const int twp = d.twp;
+    a.x_tiles = d.x_tiles;
+    if (d.tiles * d.splits > 0x7fffffffLL) return usc::fail(USC_ERR_UNSUPPORTED, "dense conv: grid too large");
+    const size_t need = dtc_ws_bytes(d);
+    if (need == 0 || !workspace || ws_bytes < need) d.splits = 1, d.kper = d.kiters;  // no workspace: no split
+    a.splits = d.splits;
+    a.kper = d.kper;
+    if (d.splits > 1) {
+        a.part = static_cast<float *>(workspace);
+        a.cnt = reinterpret_cast<int *>(static_cast<char *>(workspace) +
+                                        (size_t)d.tiles * d.splits * (twp * 64) * 128 * sizeof(float));
+    }
+    const long long tiles = d.tiles * d.splits;  // work items
     cudaError_t e;
     if (twp == 4)
         e = win ? launch_dtc<4, true, false>(a, (int)tiles, st)
@@ -549,4 +665,29 @@ int usc_dense_conv_f16(const usc_geometry *g, int32_t n, const void *w_dev, cons
                 : (res ? launch_dtc<2, false, true>(a, (int)tiles, st) : launch_dtc<2, false, false>(a, (int)tiles, st));
     if (e == cudaSuccess) e = cudaGetLastError();
     return e == cudaSuccess ? USC_OK : usc::fail(USC_ERR_CUDA, "k_dtc: %s", cudaGetErrorString(e));
+}
+
+}  // namespace
+
+int usc_dense_conv_f16(const usc_geometry *g, int32_t n, const void *w_dev, const usc_act_layout *xl, const void *x,
+                       const usc_act_layout *yl, void *y, const usc_act_layout *rl, const void *res, int32_t relu,
+                       void *stream) {
+    return dense_conv_impl(g, n, w_dev, xl, x, yl, y, rl, res, relu, nullptr, 0, stream);
+}
+
+int usc_dense_conv_f16_ws(const usc_geometry *g, int32_t n, const void *w_dev, const usc_act_layout *xl, const void *x,
+                          const usc_act_layout *yl, void *y, const usc_act_layout *rl, const void *res, int32_t relu,
+                          void *workspace, int64_t ws_bytes, void *stream) {
+    if (ws_bytes < 0) return usc::fail(USC_ERR_VALUE, "dense conv: negative workspace size");
+    return dense_conv_impl(g, n, w_dev, xl, x, yl, y, rl, res, relu, workspace, (size_t)ws_bytes, stream);
+}
+
+int64_t usc_dense_conv_f16_ws_bytes(const usc_geometry *g, int32_t n, const usc_act_layout *xl, int32_t has_res) {
+    if (!g || !xl || n < 1 || g->filter_h != g->filter_w || (g->filter_h != 1 && g->filter_h != 3) ||
+        g->in_channels % kKC)
+        return 0;
+    int dev = 0, sms = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess && usc_device_sm_count(dev) > 0) sms = usc_device_sm_count(dev);
+    const bool win = g->filter_h == 3 && g->stride_h == 1 && !has_res;
+    return (int64_t)dtc_ws_bytes(dtc_shape(g, n, xl, has_res != 0, win, sms));
 }

@@ -36,11 +36,29 @@ def pack_weights(w, device=None):
     return packed.contiguous()
 
 
-def dense_conv(w_packed, in_channels: int, out_channels: int, k: int, stride: int, n: int, x, x_lay, y, y_lay,
-               res=None, res_lay=None, relu: bool = True, stream=None):
-    """One tensor-core convolution on BI64 buffers (usc_dense_conv_f16)."""
+def dense_workspace(in_channels: int, out_channels: int, k: int, stride: int, n: int, x_lay, res: bool = False,
+                    device=None):
+    """Zero-filled split-K workspace for dense_conv on this shape (None when the shape does
+    not split: the tiles already fill the SMs, or a shortcut is fused).  Reusable across
+    launches of the same shape (the kernel leaves its counters at zero); not shareable
+    between launches that may run concurrently."""
+    import torch
     g = _lib.Geometry(in_channels, out_channels, k, k, x_lay.height, x_lay.width, stride, stride, k // 2, k // 2)
-    _lib.check(_lib.lib().usc_dense_conv_f16(
-        _lib.ref(g), n, _lib.t_ptr(w_packed), _lib.ref(x_lay), _lib.t_ptr(x), _lib.ref(y_lay), _lib.t_ptr(y),
-        None if res is None else _lib.ref(res_lay), None if res is None else _lib.t_ptr(res), int(relu),
-        _lib.stream_ptr(stream)), "dense_conv_f16")
+    nbytes = int(_lib.lib().usc_dense_conv_f16_ws_bytes(_lib.ref(g), n, _lib.ref(x_lay), int(res)))
+    if nbytes <= 0:
+        return None
+    return torch.zeros(nbytes, dtype=torch.uint8, device=device or "cuda")
+
+
+def dense_conv(w_packed, in_channels: int, out_channels: int, k: int, stride: int, n: int, x, x_lay, y, y_lay,
+               res=None, res_lay=None, relu: bool = True, stream=None, workspace=None):
+    """One tensor-core convolution on BI64 buffers (usc_dense_conv_f16[_ws]); `workspace`
+    from dense_workspace enables split-K on small maps."""
+    g = _lib.Geometry(in_channels, out_channels, k, k, x_lay.height, x_lay.width, stride, stride, k // 2, k // 2)
+    args = (_lib.ref(g), n, _lib.t_ptr(w_packed), _lib.ref(x_lay), _lib.t_ptr(x), _lib.ref(y_lay), _lib.t_ptr(y),
+            None if res is None else _lib.ref(res_lay), None if res is None else _lib.t_ptr(res), int(relu))
+    if workspace is None:
+        _lib.check(_lib.lib().usc_dense_conv_f16(*args, _lib.stream_ptr(stream)), "dense_conv_f16")
+    else:
+        _lib.check(_lib.lib().usc_dense_conv_f16_ws(*args, _lib.t_ptr(workspace), workspace.numel(),
+                                                    _lib.stream_ptr(stream)), "dense_conv_f16_ws")

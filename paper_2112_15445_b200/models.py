@@ -422,7 +422,7 @@ class SparseVGG16:
                 self.steps.append(("dense", li, self._to_bi(cur_held, cur_buf, cur_lay)))
             cur_held = None
             if self.backends[li] == "tc":  # tensor cores straight on the BI64 buffers (+ the pool kernel)
-                from .dense import dense_conv, pack_weights
+                from .dense import dense_conv, dense_workspace, pack_weights
                 if not hasattr(self, "_tc_w"):
                     self._tc_w = {}
                 if li not in self._tc_w:
@@ -432,8 +432,10 @@ class SparseVGG16:
                 out_lay = _lib.act_layout(g.out_channels, g.out_h, g.out_w, halo, halo, self.eb, il)
                 out_buf = self._buf(out_lay)
 
-                def fn(stream=None, w=self._tc_w[li], g=g, x=cur_buf, xl=cur_lay, y=out_buf, yl=out_lay):
-                    dense_conv(w, g.in_channels, g.out_channels, 3, 1, n, x, xl, y, yl, None, None, True, stream)
+                ws = dense_workspace(g.in_channels, g.out_channels, 3, 1, n, cur_lay, False, self.device)
+
+                def fn(stream=None, w=self._tc_w[li], g=g, x=cur_buf, xl=cur_lay, y=out_buf, yl=out_lay, ws=ws):
+                    dense_conv(w, g.in_channels, g.out_channels, 3, 1, n, x, xl, y, yl, None, None, True, stream, ws)
                 self.steps.append(("tc", li, fn))
                 self.nonzero_macs += int(np.count_nonzero(self.filters[li].weights)) * g.out_h * g.out_w * n
                 cur_buf, cur_lay = out_buf, out_lay

@@ -212,7 +212,7 @@ class SparseResNet50:
             name, g, role, s = self.layers[li]
             ya = Act(c_out, hw_out, self._lay(c_out, hw_out, halo))
             if self.backends[li] == "tc":  # tensor cores straight on the BI64 buffers
-                from .dense import dense_conv, pack_weights
+                from .dense import dense_conv, dense_workspace, pack_weights
                 if not hasattr(self, "_tc_w"):
                     self._tc_w = {}
                 if li not in self._tc_w:
@@ -220,11 +220,13 @@ class SparseResNet50:
                 w, x, x_lay = self._tc_w[li], xa.bi(), xa.lay
                 y = ya.buf = self._buf(ya.lay)
                 r, r_lay = (None, None) if residual is None else (residual.bi(), residual.lay)
+                ws = dense_workspace(g.in_channels, g.out_channels, g.filter_h, s, n, x_lay, residual is not None,
+                                     self.device)
 
                 def fn(stream=None, li=li, w=w, x=x, x_lay=x_lay, y=y, y_lay=ya.lay, r=r, r_lay=r_lay, relu=relu,
-                       g=g, s=s):
+                       g=g, s=s, ws=ws):
                     dense_conv(w, g.in_channels, g.out_channels, g.filter_h, s, n, x, x_lay, y, y_lay, r, r_lay,
-                               relu, stream)
+                               relu, stream, ws)
                 self.steps.append((li, None, None, None, None, None, fn))
                 return ya
             if self.backends[li] == "dense":

@@ -87,3 +87,44 @@ def test_dense_tc_saturates(res, relu):
         assert float(out.float().min()) < 0
     err = float((out.float() - ref).abs().max())
     assert err <= 1e-2 * 65504, err
+
+
+@pytest.mark.parametrize("C,D,hw,n", [(512, 512, 2, 256), (512, 512, 2, 64), (256, 512, 4, 64), (256, 128, 2, 128)])
+def test_dense_tc_split_k(C, D, hw, n):
+    """Small maps split K over CTAs (workspace path): the result matches torch within the
+    fp16 tolerance, and repeated launches are bitwise identical (splits summed in a fixed
+    order; the arrival counters are left at zero for the next launch)."""
+    import torch
+    from paper_2112_15445_b200 import _lib
+    from paper_2112_15445_b200.dense import dense_conv, dense_workspace, pack_weights
+    rng = np.random.default_rng([C, D, hw, n])
+    x = torch.from_numpy(rng.standard_normal((n, C, hw, hw)).astype(np.float32)).cuda().half()
+    w = torch.from_numpy((rng.standard_normal((D, C, 3, 3)) / np.sqrt(C * 9)).astype(np.float32)).cuda().half()
+    xl = _lib.act_layout(C, hw, hw, 1, 1, 2, 64)
+    xb = torch.zeros(xl.elems(n), dtype=torch.float16, device="cuda")
+    L = _lib.lib()
+    _lib.check(L.usc_pad_input(_lib.ref(xl), _lib.USC_F16, n, _lib.t_ptr(x), _lib.t_ptr(xb), _lib.stream_ptr()))
+    yl = _lib.act_layout(D, hw, hw, 1, 1, 2, 64)
+    ws = dense_workspace(C, D, 3, 1, n, xl)
+    assert ws is not None  # these shapes fill at most half the SMs
+    wp = pack_weights(w)
+    outs = []
+    for _ in range(3):
+        yb = torch.zeros(yl.elems(n), dtype=torch.float16, device="cuda")
+        dense_conv(wp, C, D, 3, 1, n, xb, xl, yb, yl, workspace=ws)
+        out = torch.empty((n, D, hw, hw), dtype=torch.float16, device="cuda")
+        _lib.check(L.usc_unpad_output(_lib.ref(yl), _lib.USC_F16, n, _lib.t_ptr(yb), _lib.t_ptr(out),
+                                      _lib.stream_ptr()))
+        outs.append(out)
+    torch.cuda.synchronize()
+    ref = torch.relu(torch.nn.functional.conv2d(x.float(), w.float(), padding=1))
+    err = float((outs[0].float() - ref).abs().max())
+    assert err <= 1e-2 * float(ref.abs().max()), err
+    assert all(torch.equal(outs[0], o) for o in outs[1:])
+    # the same conv without the workspace (one CTA per tile) agrees within the tolerance
+    yb = torch.zeros(yl.elems(n), dtype=torch.float16, device="cuda")
+    dense_conv(wp, C, D, 3, 1, n, xb, xl, yb, yl)
+    out = torch.empty((n, D, hw, hw), dtype=torch.float16, device="cuda")
+    _lib.check(L.usc_unpad_output(_lib.ref(yl), _lib.USC_F16, n, _lib.t_ptr(yb), _lib.t_ptr(out), _lib.stream_ptr()))
+    torch.cuda.synchronize()
+    assert float((out.float() - outs[0].float()).abs().max()) <= 1e-2 * float(ref.abs().max())

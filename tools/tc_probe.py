@@ -17,7 +17,7 @@ import torch  # noqa: E402
 
 def main():
     from paper_2112_15445_b200 import _lib
-    from paper_2112_15445_b200.dense import dense_conv, pack_weights, tc_eligible
+    from paper_2112_15445_b200.dense import dense_conv, dense_workspace, pack_weights, tc_eligible
     from paper_2112_15445_b200.engine import time_median_cuda
     torch.backends.cudnn.benchmark = True
     n = 256
@@ -51,7 +51,8 @@ def main():
             rl = _lib.act_layout(D, ho, ho, 0, 0, 2, 64)
             rb = torch.randn(rl.elems(n), device="cuda").half()
             rc = torch.randn(n, D, ho, ho, device="cuda").half().contiguous(memory_format=torch.channels_last)
-        tc = time_median_cuda(lambda: dense_conv(wp, C, D, k, s, n, xb, xl, yb, yl, rb, rl), 9, 3)
+        ws = dense_workspace(C, D, k, s, n, xl, use_res)
+        tc = time_median_cuda(lambda: dense_conv(wp, C, D, k, s, n, xb, xl, yb, yl, rb, rl, True, None, ws), 9, 3)
         xc = x.contiguous(memory_format=torch.channels_last)
         wc = w.contiguous(memory_format=torch.channels_last)
         if use_res:
@@ -63,7 +64,7 @@ def main():
         hbm = 2.0 * (n * C * hw * hw + n * D * ho * ho * (2 if use_res else 1) + D * C * k * k)
         print(json.dumps({"layer": name, "tc_us": round(tc * 1e3, 1), "cudnn_us": round(cd * 1e3, 1),
                           "speedup_vs_cudnn": round(cd / tc, 2), "tc_dense_tflops": round(flops / tc / 1e9, 1),
-                          "tc_algorithmic_gbs": round(hbm / tc / 1e6, 1)}),
+                          "tc_algorithmic_gbs": round(hbm / tc / 1e6, 1), "split_k": ws is not None}),
               flush=True)
 
 
