@@ -312,6 +312,15 @@ int usc_dense_conv_f16(const usc_geometry *g, int32_t n, const void *w_dev, cons
 int usc_dense_conv_f16_ws(const usc_geometry *g, int32_t n, const void *w_dev, const usc_act_layout *x_layout,
                           const void *x, const usc_act_layout *y_layout, void *y, const usc_act_layout *res_layout,
                           const void *res, int32_t relu, void *workspace, int64_t ws_bytes, void *stream);
+/* The 3x3 stride-1 conv + ReLU + 2x2 max-pool (nn.py:124-135 on the ReLU output, which has
+ * no NaN) in one launch: `y_layout` is the pooled output (height/2 x width/2).  Returns
+ * USC_ERR_UNSUPPORTED when usc_dense_conv_f16_pool_ok() is 0 for the shape (then run the
+ * conv and usc_maxpool2). */
+int usc_dense_conv_f16_pool(const usc_geometry *g, int32_t n, const void *w_dev, const usc_act_layout *x_layout,
+                            const void *x, const usc_act_layout *y_layout, void *y, void *stream);
+/* 1 when the fused pool runs this shape at least as fast as conv + pool would (even output
+ * dims, width % 4 == 0, enough row pairs to fill the SMs), else 0. */
+int32_t usc_dense_conv_f16_pool_ok(const usc_geometry *g, int32_t n, const usc_act_layout *x_layout);
 /* Workspace bytes usc_dense_conv_f16_ws needs for this shape on the current device (0: no split). */
 int64_t usc_dense_conv_f16_ws_bytes(const usc_geometry *g, int32_t n, const usc_act_layout *x_layout,
                                     int32_t has_res);

@@ -56,6 +56,8 @@ struct DtcArgs {
     int splits, kper;  // split-K: work item = (tile, split), split s runs k-iterations [s*kper, (s+1)*kper)
     float *part;       // split-K partial sums [tile][split][N columns][128 rows] fp32
     int *cnt;          // split-K arrival counter per tile (zero between launches)
+    int pool;          // fused 2x2 max-pool (window kernel, 4-pixel tiles): a CTA runs the two
+                       // output rows of a pool window back to back; y is the pooled layout
 };
 
 __device__ __forceinline__ void mbar_wait_bounded(uint64_t *bar, uint32_t parity) {
@@ -156,6 +158,11 @@ __device__ __forceinline__ uint32_t add_f16x2_sat(uint32_t x, uint32_t y) {  // 
         : "r"(x), "r"(y), "r"(0x7bff7bffu), "r"(0xfbfffbffu));
     return r;
 }
+__device__ __forceinline__ uint32_t hmax_f16x2(uint32_t x, uint32_t y) {  // NaN-free operands (post-ReLU)
+    uint32_t r;
+    asm("max.f16x2 %0, %1, %2;" : "=r"(r) : "r"(x), "r"(y));
+    return r;
+}
 __device__ __forceinline__ uint32_t relu_f16x2(uint32_t x) {  // max(x, 0): negatives and NaN -> 0
     uint32_t r;
     asm("max.f16x2 %0, %1, %2;" : "=r"(r) : "r"(x), "r"(0u));
@@ -232,12 +239,24 @@ __global__ void __launch_bounds__(kThreads, 1) k_dtc(const __grid_constant__ Dtc
     pdl_wait();  // every global access below: the previous kernel's output is complete
 
     auto decode = [&](int t, int &mb, int &xt, int &yo, int &nb) {
+        const int r = a.pool ? (t & 1) : 0;  // pool: consecutive tiles = rows 2y, 2y+1
+        if (a.pool) t >>= 1;
         mb = t % a.m_blocks;
         t /= a.m_blocks;
         xt = t % a.x_tiles;
         t /= a.x_tiles;
-        yo = t % a.Yh;
-        nb = t / a.Yh;
+        const int rows = a.pool ? a.Yh >> 1 : a.Yh;
+        yo = t % rows;
+        nb = t / rows;
+        if (a.pool) yo = 2 * yo + r;
+    };
+    auto item_at = [&](int j) -> int {  // this CTA's j-th work item, -1 past the end
+        if (a.pool) {
+            const int p = blockIdx.x + (j >> 1) * gridDim.x;
+            return p < (items >> 1) ? 2 * p + (j & 1) : -1;
+        }
+        const int t = blockIdx.x + j * gridDim.x;
+        return t < items ? t : -1;
     };
 
     if (warp == kEW) {
@@ -246,7 +265,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_dtc(const __grid_constant__ Dtc
         // instructions of one thread issue ~370 clocks apart (tools/tma_rate_bench.cu), so a
         // single issuing lane caps the stream at ~20-35 B/clk per SM.
         int it = 0;  // running stage counter
-        for (int t = blockIdx.x; t < items; t += gridDim.x) {
+        for (int j = 0, t; (t = item_at(j)) >= 0; ++j) {
             int tile, sp, k0, k1, mb, xt, yo, nb;
             krange(t, tile, sp, k0, k1);
             decode(tile, mb, xt, yo, nb);
@@ -278,7 +297,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_dtc(const __grid_constant__ Dtc
         // ---------------- MMA issuer ----------------
         const uint32_t idesc = (1u << 4) | (1u << 16) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
         int it = 0, lt = 0;
-        for (int t = blockIdx.x; t < items; t += gridDim.x, ++lt) {
+        for (int t; (t = item_at(lt)) >= 0; ++lt) {
             int tile, sp, k0, k1;
             krange(t, tile, sp, k0, k1);
             const int ab = lt & 1;
@@ -320,7 +339,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_dtc(const __grid_constant__ Dtc
         unsigned char *rst = rstage + warp * kRS * kWarpBox;
         uint64_t *rbar = rfull + warp * kRS;
         auto pixel_coords = [&](int q, int &mb, int &xo, int &yo, int &nb) {  // q-th pixel of this CTA
-            const int t = blockIdx.x + (q / TWP) * gridDim.x;
+            const int t = item_at(q / TWP);
             int xt;
             decode(t, mb, xt, yo, nb);
             xo = xt * TWP + q % TWP;
@@ -361,6 +380,24 @@ __global__ void __launch_bounds__(kThreads, 1) k_dtc(const __grid_constant__ Dtc
         };
         // one output pixel of this warp's 32 channels: fp32 sums -> binary16 (+ shortcut,
         // ReLU) -> staging box -> TMA store; q counts this warp's pixels
+        // one output box of this warp's 32 channels: 32 packed binary16 words per lane ->
+        // staging box -> TMA store; q counts this warp's stores
+        auto store_box = [&](const uint32_t(&h)[32], int q, int mb, int xo, int yo, int nb, bool live) {
+            // staging slot q % kOS is free once the store issued kOS boxes ago has read it
+            unsigned char *obox = ost + (q % kOS) * kWarpBox;
+            if (lane == 0) bulk_wait_read<kOS - 1>();
+            __syncwarp();
+            unsigned char *orow = obox + lane * 128;
+#pragma unroll
+            for (int c = 0; c < 8; ++c)
+                *reinterpret_cast<uint4 *>(orow + ((c ^ (lane & 7)) << 4)) =
+                    make_uint4(h[4 * c], h[4 * c + 1], h[4 * c + 2], h[4 * c + 3]);
+            fence_proxy_async();  // the staged rows -> visible to the TMA engine
+            __syncwarp();
+            if (lane == 0 && live && xo < (a.pool ? a.Yw >> 1 : a.Yw))
+                tma_store_5d(&a.ymap, obox, 0, xo + a.Lo.pw, yo + a.Lo.ph, mb * 128 + ch0, nb);
+        };
+        // one output pixel: fp32 sums -> binary16 (+ shortcut, ReLU) -> store_box
         auto emit = [&](const uint32_t(&v)[64], int q, int mb, int xo, int yo, int nb, bool live) {
             uint32_t h[32];
 #pragma unroll
@@ -387,23 +424,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_dtc(const __grid_constant__ Dtc
 #pragma unroll
                 for (int k = 0; k < 32; ++k) h[k] = relu_f16x2(h[k]);
             }
-            // staging slot q % kOS is free once the store issued kOS pixels ago has read it
-            unsigned char *obox = ost + (q % kOS) * kWarpBox;
-            if (lane == 0) bulk_wait_read<kOS - 1>();
-            __syncwarp();
-            unsigned char *orow = obox + lane * 128;
-#pragma unroll
-            for (int c = 0; c < 8; ++c)
-                *reinterpret_cast<uint4 *>(orow + ((c ^ (lane & 7)) << 4)) =
-                    make_uint4(h[4 * c], h[4 * c + 1], h[4 * c + 2], h[4 * c + 3]);
-            fence_proxy_async();  // the staged rows -> visible to the TMA engine
-            __syncwarp();
-            if (lane == 0 && live && xo < a.Yw)
-                tma_store_5d(&a.ymap, obox, 0, xo + a.Lo.pw, yo + a.Lo.ph, mb * 128 + ch0, nb);
+            store_box(h, q, mb, xo, yo, nb, live);
         };
         __shared__ int s_last;  // split-K: this CTA completed the tile's last split
+        uint32_t keep[32];      // pool: the horizontal maxima of the window's first row
         int lt = 0, q = 0;
-        for (int t = blockIdx.x; t < items; t += gridDim.x, ++lt) {
+        for (int t; (t = item_at(lt)) >= 0; ++lt) {
             int tile, sp, k0, k1, mb, xt, yo, nb;
             krange(t, tile, sp, k0, k1);
             decode(tile, mb, xt, yo, nb);
@@ -413,6 +439,32 @@ __global__ void __launch_bounds__(kThreads, 1) k_dtc(const __grid_constant__ Dtc
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             if (warp == 0 && lane == 0 && lt < 2) DTC_STAMP(5 + lt);
             const uint32_t taddr = tmem + ab * N + ((uint32_t)(ch0) << 16);
+            if constexpr (WIN && TWP == 4 && !RES) {
+                if (a.pool) {  // warp half h: pixels 2h, 2h+1 = one pool window's columns
+                    uint32_t v[64], hm[32];
+                    tmem_ld64(taddr + (2 * half) * 64, v);
+#pragma unroll
+                    for (int k = 0; k < 32; ++k)
+                        hm[k] = relu_f16x2(cvt_f16x2_sat(__uint_as_float(v[2 * k]), __uint_as_float(v[2 * k + 1])));
+                    tmem_ld64(taddr + (2 * half + 1) * 64, v);
+                    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&tempty[ab]);
+#pragma unroll
+                    for (int k = 0; k < 32; ++k)
+                        hm[k] = hmax_f16x2(hm[k], relu_f16x2(cvt_f16x2_sat(__uint_as_float(v[2 * k]),
+                                                                            __uint_as_float(v[2 * k + 1]))));
+                    if ((lt & 1) == 0) {  // the window's first row: hold it
+#pragma unroll
+                        for (int k = 0; k < 32; ++k) keep[k] = hm[k];
+                        continue;
+                    }
+#pragma unroll
+                    for (int k = 0; k < 32; ++k) hm[k] = hmax_f16x2(keep[k], hm[k]);
+                    store_box(hm, q++, mb, xt * 2 + half, yo >> 1, nb, live);
+                    continue;
+                }
+            }
             if (a.splits == 1) {
 #pragma unroll 1
                 for (int px = half; px < TWP; px += 2, ++q) {
@@ -554,6 +606,24 @@ DtcShape dtc_shape(const usc_geometry *g, int n, const usc_act_layout *xl, bool 
     return d;
 }
 
+// Fused 2x2 pool: 4-pixel window tiles run in row pairs by one CTA.  Cost model (us): a
+// 4-pixel tile takes kiters stages of 12 MMAs of 128 clocks; the separate pool kernel
+// streams the full-resolution output once (+ its quarter) at ~5 TB/s plus ~2 us.  Fuse
+// when the pair schedule's makespan is no longer than conv makespan + pool.
+bool dtc_pool_ok(const usc_geometry *g, int n, const usc_act_layout *xl, int sms) {
+    if (g->filter_h != 3 || g->filter_w != 3 || g->stride_h != 1 || g->stride_w != 1 || g->in_channels % kKC)
+        return false;
+    const DtcShape d = dtc_shape(g, n, xl, false, true, sms);
+    if (d.Yh % 2 || d.Yw % 4 || d.splits > 1) return false;
+    const long long tiles4 = (long long)d.m_blocks * (d.Yw / 4) * d.Yh * d.NB, pairs = tiles4 / 2;
+    const double t_tile = d.kiters * 12.0 * 128.0 / 1900.0;
+    const double pool_bytes = 2.0 * d.NB * 64.0 * g->out_channels * d.Yh * d.Yw * 1.25;
+    const double waves = (double)((d.tiles + sms - 1) / sms) * (d.twp == 4 ? 1.0 : 0.5);
+    const double unfused = waves * t_tile + pool_bytes / 5e6 + 2.0;
+    const double fused = 2.0 * (double)((pairs + sms - 1) / sms) * t_tile;
+    return fused <= unfused;
+}
+
 size_t dtc_ws_bytes(const DtcShape &d) {
     if (d.splits <= 1) return 0;
     const size_t part = (size_t)d.tiles * d.splits * (d.twp * 64) * 128 * sizeof(float);
@@ -562,7 +632,7 @@ size_t dtc_ws_bytes(const DtcShape &d) {
 
 int dense_conv_impl(const usc_geometry *g, int32_t n, const void *w_dev, const usc_act_layout *xl, const void *x,
                     const usc_act_layout *yl, void *y, const usc_act_layout *rl, const void *res, int32_t relu,
-                    void *workspace, size_t ws_bytes, void *stream) {
+                    void *workspace, size_t ws_bytes, int pool, void *stream) {
     if (!g || !w_dev || !xl || !x || !yl || !y || n < 1) return usc::fail(USC_ERR_VALUE, "dense conv: null argument");
     if (g->filter_h != g->filter_w || (g->filter_h != 1 && g->filter_h != 3) || g->stride_h != g->stride_w ||
         (g->stride_h != 1 && g->stride_h != 2))
@@ -573,7 +643,8 @@ int dense_conv_impl(const usc_geometry *g, int32_t n, const void *w_dev, const u
         return usc::fail(USC_ERR_UNSUPPORTED, "dense conv: BI64 layouts only");
     const int s = g->stride_h, K = g->filter_h, pad = K / 2;
     const int Yh = (xl->height + 2 * pad - K) / s + 1, Yw = (xl->width + 2 * pad - K) / s + 1;
-    if (yl->height != Yh || yl->width != Yw || yl->channels != g->out_channels || xl->channels != g->in_channels)
+    if (yl->height != (pool ? Yh / 2 : Yh) || yl->width != (pool ? Yw / 2 : Yw) || yl->channels != g->out_channels ||
+        xl->channels != g->in_channels)
         return usc::fail(USC_ERR_VALUE, "dense conv: layouts do not match the convolution");
     if (xl->pad_h < pad || xl->pad_w < pad)
         return usc::fail(USC_ERR_VALUE, "dense conv: input halo smaller than the padding");
@@ -643,6 +714,16 @@ int dense_conv_impl(const usc_geometry *g, int32_t n, const void *w_dev, const u
     if (cudaGetDevice(&dev) == cudaSuccess && usc_device_sm_count(dev) > 0) sms = usc_device_sm_count(dev);
     const bool win = K == 3 && s == 1 && !res;  // the 3-tap row window (stride 1; no shortcut staging room)
     DtcShape d = dtc_shape(g, n, xl, res != nullptr, win, sms);
+    if (pool) {  // 4-pixel window tiles in row pairs, no split
+        if (res || !relu || !dtc_pool_ok(g, n, xl, sms))
+            return usc::fail(USC_ERR_UNSUPPORTED, "dense conv: fused pool not available for this shape");
+        d.twp = 4;
+        d.x_tiles = Yw / 4;
+        d.tiles = (long long)d.m_blocks * d.x_tiles * Yh * d.NB;
+        d.splits = 1;
+        d.kper = d.kiters;
+        a.pool = 1;
+    }
     const int twp = d.twp;
     a.x_tiles = d.x_tiles;
     if (d.tiles * d.splits > 0x7fffffffLL) return usc::fail(USC_ERR_UNSUPPORTED, "dense conv: grid too large");
@@ -672,14 +753,26 @@ int dense_conv_impl(const usc_geometry *g, int32_t n, const void *w_dev, const u
 int usc_dense_conv_f16(const usc_geometry *g, int32_t n, const void *w_dev, const usc_act_layout *xl, const void *x,
                        const usc_act_layout *yl, void *y, const usc_act_layout *rl, const void *res, int32_t relu,
                        void *stream) {
-    return dense_conv_impl(g, n, w_dev, xl, x, yl, y, rl, res, relu, nullptr, 0, stream);
+    return dense_conv_impl(g, n, w_dev, xl, x, yl, y, rl, res, relu, nullptr, 0, 0, stream);
+}
+
+int usc_dense_conv_f16_pool(const usc_geometry *g, int32_t n, const void *w_dev, const usc_act_layout *xl,
+                            const void *x, const usc_act_layout *yl, void *y, void *stream) {
+    return dense_conv_impl(g, n, w_dev, xl, x, yl, y, nullptr, nullptr, 1, nullptr, 0, 1, stream);
+}
+
+int32_t usc_dense_conv_f16_pool_ok(const usc_geometry *g, int32_t n, const usc_act_layout *xl) {
+    if (!g || !xl || n < 1) return 0;
+    int dev = 0, sms = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess && usc_device_sm_count(dev) > 0) sms = usc_device_sm_count(dev);
+    return dtc_pool_ok(g, n, xl, sms) ? 1 : 0;
 }
 
 int usc_dense_conv_f16_ws(const usc_geometry *g, int32_t n, const void *w_dev, const usc_act_layout *xl, const void *x,
                           const usc_act_layout *yl, void *y, const usc_act_layout *rl, const void *res, int32_t relu,
                           void *workspace, int64_t ws_bytes, void *stream) {
     if (ws_bytes < 0) return usc::fail(USC_ERR_VALUE, "dense conv: negative workspace size");
-    return dense_conv_impl(g, n, w_dev, xl, x, yl, y, rl, res, relu, workspace, (size_t)ws_bytes, stream);
+    return dense_conv_impl(g, n, w_dev, xl, x, yl, y, rl, res, relu, workspace, (size_t)ws_bytes, 0, stream);
 }
 
 int64_t usc_dense_conv_f16_ws_bytes(const usc_geometry *g, int32_t n, const usc_act_layout *xl, int32_t has_res) {

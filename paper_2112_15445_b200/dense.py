@@ -62,3 +62,18 @@ def dense_conv(w_packed, in_channels: int, out_channels: int, k: int, stride: in
     else:
         _lib.check(_lib.lib().usc_dense_conv_f16_ws(*args, _lib.t_ptr(workspace), workspace.numel(),
                                                     _lib.stream_ptr(stream)), "dense_conv_f16_ws")
+
+
+def pool_fusable(in_channels: int, out_channels: int, n: int, x_lay) -> bool:
+    """True when the 3x3 conv + ReLU + 2x2 pool runs as one tensor-core launch
+    (usc_dense_conv_f16_pool_ok) at least as fast as conv + pool."""
+    g = _lib.Geometry(in_channels, out_channels, 3, 3, x_lay.height, x_lay.width, 1, 1, 1, 1)
+    return bool(_lib.lib().usc_dense_conv_f16_pool_ok(_lib.ref(g), n, _lib.ref(x_lay)))
+
+
+def dense_conv_pool(w_packed, in_channels: int, out_channels: int, n: int, x, x_lay, y, y_lay, stream=None):
+    """3x3 stride-1 conv + ReLU + 2x2 max-pool in one launch; `y_lay` is the pooled layout."""
+    g = _lib.Geometry(in_channels, out_channels, 3, 3, x_lay.height, x_lay.width, 1, 1, 1, 1)
+    _lib.check(_lib.lib().usc_dense_conv_f16_pool(_lib.ref(g), n, _lib.t_ptr(w_packed), _lib.ref(x_lay),
+                                                  _lib.t_ptr(x), _lib.ref(y_lay), _lib.t_ptr(y),
+                                                  _lib.stream_ptr(stream)), "dense_conv_f16_pool")

@@ -421,17 +421,29 @@ class SparseVGG16:
                 cur_buf = self._buf(cur_lay)
                 self.steps.append(("dense", li, self._to_bi(cur_held, cur_buf, cur_lay)))
             cur_held = None
-            if self.backends[li] == "tc":  # tensor cores straight on the BI64 buffers (+ the pool kernel)
-                from .dense import dense_conv, dense_workspace, pack_weights
+            if self.backends[li] == "tc":  # tensor cores straight on the BI64 buffers (+ the pool)
+                from .dense import dense_conv, dense_conv_pool, dense_workspace, pack_weights, pool_fusable
                 if not hasattr(self, "_tc_w"):
                     self._tc_w = {}
                 if li not in self._tc_w:
                     self._tc_w[li] = pack_weights(self.weights[li], self.device)
                 last = i + 2 >= len(VGG16_CIFAR)
+                if nxt == "M" and pool_fusable(g.in_channels, g.out_channels, n, cur_lay):
+                    # conv + ReLU + 2x2 pool in one launch, straight into the pooled layout
+                    ph = 0 if last else 1
+                    pool_lay = _lib.act_layout(g.out_channels, g.out_h // 2, g.out_w // 2, ph, ph, self.eb, il)
+                    pool_buf = self._buf(pool_lay)
+
+                    def fn(stream=None, w=self._tc_w[li], g=g, x=cur_buf, xl=cur_lay, y=pool_buf, yl=pool_lay):
+                        dense_conv_pool(w, g.in_channels, g.out_channels, n, x, xl, y, yl, stream)
+                    self.steps.append(("tc", li, fn))
+                    self.nonzero_macs += int(np.count_nonzero(self.filters[li].weights)) * g.out_h * g.out_w * n
+                    cur_buf, cur_lay = pool_buf, pool_lay
+                    li += 1
+                    continue
                 halo = 0 if nxt == "M" else 1
                 out_lay = _lib.act_layout(g.out_channels, g.out_h, g.out_w, halo, halo, self.eb, il)
                 out_buf = self._buf(out_lay)
-
                 ws = dense_workspace(g.in_channels, g.out_channels, 3, 1, n, cur_lay, False, self.device)
 
                 def fn(stream=None, w=self._tc_w[li], g=g, x=cur_buf, xl=cur_lay, y=out_buf, yl=out_lay, ws=ws):

@@ -128,3 +128,42 @@ def test_dense_tc_split_k(C, D, hw, n):
     _lib.check(L.usc_unpad_output(_lib.ref(yl), _lib.USC_F16, n, _lib.t_ptr(yb), _lib.t_ptr(out), _lib.stream_ptr()))
     torch.cuda.synchronize()
     assert float((out.float() - outs[0].float()).abs().max()) <= 1e-2 * float(ref.abs().max())
+
+
+@pytest.mark.parametrize("C,D,hw,n,ph", [(64, 64, 32, 256, 1), (128, 128, 16, 256, 0), (64, 128, 32, 192, 1)])
+def test_dense_tc_fused_pool(C, D, hw, n, ph):
+    """conv + ReLU + 2x2 max-pool in one tensor-core launch (row-pair tiles, pooled in the
+    epilogue) against torch within the fp16 tolerance, and equal to the unfused conv +
+    usc_maxpool2 up to the same tolerance."""
+    import torch
+    from paper_2112_15445_b200 import _lib
+    from paper_2112_15445_b200.dense import dense_conv, dense_conv_pool, pack_weights, pool_fusable
+    rng = np.random.default_rng([C, D, hw, n, 3])
+    x = torch.from_numpy(rng.standard_normal((n, C, hw, hw)).astype(np.float32)).cuda().half()
+    w = torch.from_numpy((rng.standard_normal((D, C, 3, 3)) / np.sqrt(C * 9)).astype(np.float32)).cuda().half()
+    xl = _lib.act_layout(C, hw, hw, 1, 1, 2, 64)
+    xb = torch.zeros(xl.elems(n), dtype=torch.float16, device="cuda")
+    L = _lib.lib()
+    _lib.check(L.usc_pad_input(_lib.ref(xl), _lib.USC_F16, n, _lib.t_ptr(x), _lib.t_ptr(xb), _lib.stream_ptr()))
+    assert pool_fusable(C, D, n, xl)
+    pl = _lib.act_layout(D, hw // 2, hw // 2, ph, ph, 2, 64)
+    pb = torch.zeros(pl.elems(n), dtype=torch.float16, device="cuda")
+    wp = pack_weights(w)
+    dense_conv_pool(wp, C, D, n, xb, xl, pb, pl)
+    got = torch.empty((n, D, hw // 2, hw // 2), dtype=torch.float16, device="cuda")
+    _lib.check(L.usc_unpad_output(_lib.ref(pl), _lib.USC_F16, n, _lib.t_ptr(pb), _lib.t_ptr(got), _lib.stream_ptr()))
+    # unfused: conv into a full-resolution buffer, then the pool kernel
+    yl = _lib.act_layout(D, hw, hw, 0, 0, 2, 64)
+    yb = torch.zeros(yl.elems(n), dtype=torch.float16, device="cuda")
+    dense_conv(wp, C, D, 3, 1, n, xb, xl, yb, yl)
+    pb2 = torch.zeros(pl.elems(n), dtype=torch.float16, device="cuda")
+    _lib.check(L.usc_maxpool2(_lib.ref(yl), _lib.ref(pl), _lib.USC_F16, n, _lib.t_ptr(yb), _lib.t_ptr(pb2),
+                              _lib.stream_ptr()))
+    torch.cuda.synchronize()
+    ref = torch.nn.functional.max_pool2d(torch.relu(torch.nn.functional.conv2d(x.float(), w.float(), padding=1)), 2)
+    tol = 1e-2 * float(ref.abs().max())
+    assert float((got.float() - ref).abs().max()) <= tol
+    # both paths round the same fp32 sums: the pooled values are the same binary16 numbers
+    assert torch.equal(pb, pb2)
+    # the halo of the pooled buffer stays zero
+    assert torch.isfinite(pb.float()).all()
