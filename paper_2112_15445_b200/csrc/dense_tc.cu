@@ -21,6 +21,8 @@
 // into the output layout (halo untouched).
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
+
 #include "common.cuh"
 #include "usc_internal.h"
 
@@ -554,6 +556,247 @@ cudaError_t launch_dtc(const DtcArgs &a, int tiles, cudaStream_t st) {
     return launch_pdl(k_dtc<TWP, WIN, RES>, dim3((unsigned)(tiles < sms ? tiles : sms)), dim3(kThreads), smem, st, a);
 }
 
+// ---------------------------------------------------------------------------------------
+// k_dts: 64-output-channel layers with the operands swapped.  M = 128 for cta_group::1
+// costs the same MMA time at M = 64, so a 64-channel layer on k_dtc wastes half of every
+// MMA on zero weight rows.  Here the activations are the A operand (MN-major: M = 128 =
+// 2 output pixels x 64 samples, the two pixel boxes its M atoms, LBO 8 KB) and the weights
+// the B operand (K-major, N = 64 output channels): D[(pixel, sample)][channel] in TMEM,
+// lane = (pixel, sample), column = channel.  A tile is TWP pixels = TWP/2 MMA groups
+// (accumulator columns 64 g ..).  WIN (3x3 stride 1): a stage is (kh, 64-channel chunk):
+// the TWP+2 pixel boxes of the input row and the 3 taps' [64 d][64 k] weight tiles; tap
+// kw's A operand for group g starts at box kw + 2g.  Epilogue: warp w reads TMEM lane
+// quarter w % 4 (pixel (w % 4) / 2 of group w / 4, samples 32 (w % 2) ..), converts its
+// 64 channels and writes them transposed into the pixel's [64 c][64 s] swizzled staging
+// box (16-bit stores, conflict-free); the two warps of a pixel meet at a named barrier and
+// one TMA store writes the box.
+constexpr int kWBox64 = 64 * kKC * 2;  // [64 d][64 k] binary16 weight tile (8 KB)
+
+template <int TWP, bool WIN>
+constexpr int dts_stages() {
+    return WIN ? 2 : 4;
+}
+template <int TWP, bool WIN>
+constexpr int dts_smem() {
+    constexpr int NW = WIN ? 3 : 1, NBX = WIN ? TWP + 2 : TWP;
+    return dts_stages<TWP, WIN>() * (NW * kWBox64 + NBX * kBPix) + TWP * 2 * kBPix + 1024 + 256;
+}
+
+__device__ __forceinline__ void pair_sync(int id) {  // the two warps of one output pixel
+    asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory");
+}
+
+template <int TWP, bool WIN>
+__global__ void __launch_bounds__(kThreads, 1) k_dts(const __grid_constant__ DtcArgs a) {
+    constexpr int G = TWP / 2;                   // MMA groups (pixel pairs) per tile
+    constexpr int NW = WIN ? 3 : 1;              // weight tiles (taps) per stage
+    constexpr int NBX = WIN ? TWP + 2 : TWP;     // pixel boxes per stage
+    constexpr int kStage = NW * kWBox64 + NBX * kBPix;
+    constexpr int S = dts_stages<TWP, WIN>();
+    constexpr uint32_t kCols = 2 * G * 64 < 32 ? 32 : 2 * G * 64;  // two accumulators
+    static_assert(kEW == 8, "two epilogue warps per pixel of a 4-pixel tile");
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char *smem = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    unsigned char *ostage = smem + S * kStage;  // [TWP pixels][2 slots] [64 c][64 s] boxes
+    uint64_t *full = reinterpret_cast<uint64_t *>(ostage + TWP * 2 * kBPix);
+    uint64_t *empty = full + S;
+    uint64_t *tfull = empty + S;
+    uint64_t *tempty = tfull + 2;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int tiles = a.x_tiles * a.Yh * a.NB;
+    const int kiters = WIN ? a.Kh * a.cb : a.k_iters;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < S; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&tfull[b], 1);
+            mbar_init(&tempty[b], kEW);
+        }
+        fence_mbar_init();
+    }
+    if (warp == kEW) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "n"(kCols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = *tmem_slot;
+    if (threadIdx.x == 0) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&a.xmap)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&a.wmap)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&a.ymap)) : "memory");
+    }
+    pdl_release();
+    pdl_wait();
+
+    auto decode = [&](int t, int &xt, int &yo, int &nb) {
+        xt = t % a.x_tiles;
+        t /= a.x_tiles;
+        yo = t % a.Yh;
+        nb = t / a.Yh;
+    };
+
+    if (warp == kEW) {
+        // ---------------- TMA producer: one box per lane ----------------
+        int it = 0;
+        for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+            int xt, yo, nb;
+            decode(t, xt, yo, nb);
+            for (int i = 0; i < kiters; ++i, ++it) {
+                const int s = it % S;
+                if (it >= S) mbar_wait_bounded(&empty[s], ((it / S) - 1) & 1);
+                unsigned char *st = smem + s * kStage;
+                if (lane == 0) mbar_expect_tx(&full[s], kStage);
+                __syncwarp();
+                if constexpr (WIN) {
+                    const int kh = i / a.cb, cb = i - kh * a.cb;
+                    if (lane < 3)
+                        tma_load_2d(st + lane * kWBox64, &a.wmap, (kh * 3 + lane) * a.C + cb * kKC, 0, &full[s]);
+                    else if (lane < 3 + NBX)
+                        tma_load_5d(st + NW * kWBox64 + (lane - 3) * kBPix, &a.xmap, 0, xt * TWP + (lane - 3) + a.offw,
+                                    yo + kh + a.offh, cb * kKC, nb, &full[s]);
+                } else {
+                    const int tap = i / a.cb, cb = i - tap * a.cb;
+                    const int kh = tap / a.Kw, kw = tap - kh * a.Kw;
+                    if (lane == 0)
+                        tma_load_2d(st, &a.wmap, tap * a.C + cb * kKC, 0, &full[s]);
+                    else if (lane <= TWP)
+                        tma_load_5d(st + kWBox64 + (lane - 1) * kBPix, &a.xmap, 0, a.stride * (xt * TWP + lane - 1) + kw + a.offw,
+                                    a.stride * yo + kh + a.offh, cb * kKC, nb, &full[s]);
+                }
+            }
+        }
+    } else if (warp == kEW + 1) {
+        // ---------------- MMA issuer: A = activations (MN-major), B = weights (K-major) ----------------
+        const uint32_t idesc = (1u << 4) | (1u << 15) | ((uint32_t)(64 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+        int it = 0, lt = 0;
+        for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++lt) {
+            const int ab = lt & 1;
+            if (lt >= 2) mbar_wait_bounded(&tempty[ab], ((lt >> 1) - 1) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            for (int i = 0; i < kiters; ++i, ++it) {
+                const int s = it % S;
+                mbar_wait_bounded(&full[s], (it / S) & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                if (lane == 0) {
+                    const uint32_t wbase = smem_u32(smem + s * kStage), xbase = wbase + NW * kWBox64;
+#pragma unroll
+                    for (int q = 0; q < NW; ++q)
+#pragma unroll
+                        for (int g = 0; g < G; ++g)
+#pragma unroll
+                            for (int k = 0; k < kKC / 16; ++k) {
+                                const uint64_t ad = desc_sw128(xbase + (q + 2 * g) * kBPix + k * 16 * 128, kBPix, 1024);
+                                const uint64_t bd = desc_sw128(wbase + q * kWBox64 + k * 32, 16, 1024);
+                                umma_f16(tmem + ab * (G * 64) + g * 64, ad, bd, idesc, (i > 0 || q > 0 || k > 0) ? 1u : 0u);
+                            }
+                    umma_commit(&empty[s]);
+                    if (i == kiters - 1) umma_commit(&tfull[ab]);
+                }
+                __syncwarp();
+            }
+        }
+    } else {
+        // ---------------- epilogue ----------------
+        const int qd = warp & 3, g = warp >> 2;       // TMEM lane quarter, MMA group
+        const int pxg = qd >> 1, shalf = qd & 1;      // pixel within the group, sample half
+        const int px = 2 * g + pxg;                   // pixel within the tile
+        const int s = shalf * 32 + lane;              // this lane's sample
+        const bool active = g < G;
+        int lt = 0;
+        for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++lt) {
+            int xt, yo, nb;
+            decode(t, xt, yo, nb);
+            const int ab = lt & 1;
+            mbar_wait_bounded(&tfull[ab], (lt >> 1) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            uint32_t v[64];
+            if (active) {
+                const uint32_t taddr = tmem + ab * (G * 64) + g * 64 + ((uint32_t)(qd * 32) << 16);
+                asm volatile(
+                    "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, "
+                    "%13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, "
+                    "[%32];"
+                    : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                      "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
+                      "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
+                      "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
+                      "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+                    : "r"(taddr));
+                asm volatile(
+                    "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, "
+                    "%13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, "
+                    "[%32];"
+                    : "=r"(v[32]), "=r"(v[33]), "=r"(v[34]), "=r"(v[35]), "=r"(v[36]), "=r"(v[37]), "=r"(v[38]),
+                      "=r"(v[39]), "=r"(v[40]), "=r"(v[41]), "=r"(v[42]), "=r"(v[43]), "=r"(v[44]), "=r"(v[45]),
+                      "=r"(v[46]), "=r"(v[47]), "=r"(v[48]), "=r"(v[49]), "=r"(v[50]), "=r"(v[51]), "=r"(v[52]),
+                      "=r"(v[53]), "=r"(v[54]), "=r"(v[55]), "=r"(v[56]), "=r"(v[57]), "=r"(v[58]), "=r"(v[59]),
+                      "=r"(v[60]), "=r"(v[61]), "=r"(v[62]), "=r"(v[63])
+                    : "r"(taddr + 32));
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[ab]);
+            if (!active) continue;
+            // pixel px's staging slot lt & 1: free once the store issued two tiles ago read it
+            const int bar_id = 1 + px;  // named barriers 1..TWP: the two warps of pixel px
+            const bool issuer = shalf == 0 && lane == 0;
+            unsigned char *box = ostage + (px * 2 + (lt & 1)) * kBPix;
+            if (issuer) bulk_wait_read<1>();
+            pair_sync(bar_id);
+            const uint32_t sb = smem_u32(box);
+#pragma unroll
+            for (int c2 = 0; c2 < 32; ++c2) {
+                uint32_t h = cvt_f16x2_sat(__uint_as_float(v[2 * c2]), __uint_as_float(v[2 * c2 + 1]));
+                if (a.relu) h = relu_f16x2(h);
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {  // channel c = 2 c2 + e: row c, column s of the swizzled box
+                    const int c = 2 * c2 + e;
+                    const uint32_t off = c * 128 + ((((s >> 3) ^ (c & 7)) << 4) | ((s & 7) << 1));
+                    asm volatile("st.shared.u16 [%0], %1;" ::"r"(sb + off), "h"((unsigned short)(h >> (16 * e))) : "memory");
+                }
+            }
+            fence_proxy_async();
+            pair_sync(bar_id);
+            const int xo = xt * TWP + px;
+            if (issuer) {  // one bulk group per tile and pixel (empty past the map) keeps the slot accounting
+                if (xo < a.Yw)
+                    tma_store_5d(&a.ymap, box, 0, xo + a.Lo.pw, yo + a.Lo.ph, 0, nb);
+                else
+                    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            }
+        }
+        if (lane == 0) bulk_wait_all();
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == kEW) {
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kCols));
+    }
+}
+
+template <int TWP, bool WIN>
+cudaError_t launch_dts(const DtcArgs &a, int tiles, cudaStream_t st) {
+    static std::atomic<uint64_t> attr{0};
+    constexpr int smem = dts_smem<TWP, WIN>();
+    static_assert(smem <= 227 * 1024 - 1024, "k_dts shared memory");
+    cudaError_t e = ensure_smem_attr(k_dts<TWP, WIN>, attr, smem);
+    if (e != cudaSuccess) return e;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int sms = usc_device_sm_count(dev);
+    if (sms <= 0) sms = 148;
+    return launch_pdl(k_dts<TWP, WIN>, dim3((unsigned)(tiles < sms ? tiles : sms)), dim3(kThreads), smem, st, a);
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 encode_tiled() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
     if (!fn) {
@@ -575,6 +818,14 @@ extern "C" int usc_dtc_trace_read(unsigned long long *out, int ctas) {
 #endif
 
 namespace {
+
+bool dts_enabled() {  // USC_NO_DTS=1: 64-channel layers on k_dtc (A/B measurements)
+    static const bool on = [] {
+        const char *v = std::getenv("USC_NO_DTS");
+        return !(v && *v && *v != '0');
+    }();
+    return on;
+}
 
 // Tile shape and split-K factor of one launch (shared by the launch and the workspace query)
 struct DtcShape {
@@ -738,6 +989,33 @@ int dense_conv_impl(const usc_geometry *g, int32_t n, const void *w_dev, const u
     }
     const long long tiles = d.tiles * d.splits;  // work items
     cudaError_t e;
+    if (g->out_channels == 64 && !res && !pool && d.splits == 1 && dts_enabled()) {
+        // 64 output channels: swapped operands (k_dts), N = 64 channels, no zero weight rows
+        const cuuint64_t wdims[2] = {(cuuint64_t)(taps * g->in_channels), (cuuint64_t)64};
+        const cuuint64_t wstrides[1] = {(cuuint64_t)(taps * g->in_channels) * 2};
+        const cuuint32_t wbox[2] = {(cuuint32_t)kKC, 64};
+        const cuuint32_t es2[2] = {1, 1};
+        if (enc(&a.wmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void *>(w_dev), wdims, wstrides, wbox, es2,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return usc::fail(USC_ERR_CUDA, "dense conv: weight tensor map (64 rows)");
+        const cuuint64_t ydims[5] = {64, (cuuint64_t)yl->ws, (cuuint64_t)yl->hp, (cuuint64_t)yl->channels, (cuuint64_t)NB};
+        const cuuint64_t ystrides[4] = {128, (cuuint64_t)yl->ws * 128, (cuuint64_t)yl->ws * yl->hp * 128,
+                                        (cuuint64_t)yl->sample_stride * 2};
+        const cuuint32_t ybox[5] = {64, 1, 1, 64, 1};
+        const cuuint32_t es5[5] = {1, 1, 1, 1, 1};
+        if (enc(&a.ymap, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 5, y, ydims, ystrides, ybox, es5, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return usc::fail(USC_ERR_CUDA, "dense conv: output tensor map (64 channels)");
+        const long long ntiles = (long long)a.x_tiles * Yh * NB;
+        if (twp == 4)
+            e = win ? launch_dts<4, true>(a, (int)ntiles, st) : launch_dts<4, false>(a, (int)ntiles, st);
+        else
+            e = win ? launch_dts<2, true>(a, (int)ntiles, st) : launch_dts<2, false>(a, (int)ntiles, st);
+        if (e == cudaSuccess) e = cudaGetLastError();
+        return e == cudaSuccess ? USC_OK : usc::fail(USC_ERR_CUDA, "k_dts: %s", cudaGetErrorString(e));
+    }
     if (twp == 4)
         e = win ? launch_dtc<4, true, false>(a, (int)tiles, st)
                 : (res ? launch_dtc<4, false, true>(a, (int)tiles, st) : launch_dtc<4, false, false>(a, (int)tiles, st));
