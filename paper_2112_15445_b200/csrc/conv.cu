@@ -289,7 +289,8 @@ __global__ void k_pad_bi(const T *__restrict__ src, TD *__restrict__ dst, int n,
     TD *drow = dst + nb * L.ss + ((long long)c * L.Hp + yp) * L.Ws * IL;
     const int iy = yp - L.ph;
     const bool rowin = iy >= 0 && iy < H;
-    for (int x0 = 0; x0 < L.Ws; x0 += 32) {
+    {  // one 32-column chunk of the row per block (blockIdx.y): many short blocks keep HBM busy
+        const int x0 = blockIdx.y * 32;
         for (int i = threadIdx.x; i < IL * 32; i += blockDim.x) {
             const int sm = i >> 5, xx = i & 31, ix = x0 + xx - L.pw;
             const long long b = nb * IL + sm;
@@ -307,7 +308,6 @@ __global__ void k_pad_bi(const T *__restrict__ src, TD *__restrict__ dst, int n,
                     drow[(long long)xp * IL + sm] = __short2half_rn(static_cast<short>(tile[sm][xx]));
             }
         }
-        __syncthreads();
     }
 }
 
@@ -791,20 +791,21 @@ int usc_pad_input(const usc_act_layout *l, int32_t dtype, int32_t n, const void 
     const int grid = grid_for(total);
     const LayoutD L = to_dev(*l);
     if (l->interleave) {  // batch-interleaved: the tiled transpose
-        const long long blocks = (long long)((n + l->interleave - 1) / l->interleave) * l->channels * l->hp;
-        if (blocks > 0x7fffffffLL) return fail(USC_ERR_UNSUPPORTED, "pad: too many rows");
+        const long long rows = (long long)((n + l->interleave - 1) / l->interleave) * l->channels * l->hp;
+        if (rows > 0x7fffffffLL) return fail(USC_ERR_UNSUPPORTED, "pad: too many rows");
+        const dim3 blocks((unsigned)rows, (unsigned)((l->ws + 31) / 32));
         switch (usc::elem_bytes(dtype)) {
             case 4:
-                k_pad_bi<float><<<(unsigned)blocks, 256, 0, st>>>(static_cast<const float *>(src),
+                k_pad_bi<float><<<blocks, 256, 0, st>>>(static_cast<const float *>(src),
                                                                    static_cast<float *>(dst), n, l->height, l->width, L);
                 break;
             case 2:
-                k_pad_bi<uint16_t><<<(unsigned)blocks, 256, 0, st>>>(static_cast<const uint16_t *>(src),
+                k_pad_bi<uint16_t><<<blocks, 256, 0, st>>>(static_cast<const uint16_t *>(src),
                                                                       static_cast<uint16_t *>(dst), n, l->height,
                                                                       l->width, L);
                 break;
             case 1:  // the BI kernel stages int8 codes as binary16
-                k_pad_bi<int8_t, __half><<<(unsigned)blocks, 256, 0, st>>>(static_cast<const int8_t *>(src),
+                k_pad_bi<int8_t, __half><<<blocks, 256, 0, st>>>(static_cast<const int8_t *>(src),
                                                                             static_cast<__half *>(dst), n, l->height,
                                                                             l->width, L);
                 break;
