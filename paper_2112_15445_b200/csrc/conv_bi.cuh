@@ -903,7 +903,9 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1) k_bi(const __grid_constant_
     }
     __syncthreads();
     pdl_release();
-    pdl_wait();  // every global access below: the previous kernel's output is complete
+    // every global access below waits for the previous kernel's output, except the producer's
+    // entry blocks for the first S stages (the packed filter: constant data)
+    if (warp != NWC) pdl_wait();
 
     if (warp == NWC) {
         // ---------------- producer warp ----------------
@@ -911,6 +913,20 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1) k_bi(const __grid_constant_
             int s = 0;
             uint32_t ph = 1;
             const uint32_t xbytes = static_cast<uint32_t>(a.CC) * a.HS * a.TWs * PXB;  // full box
+            int pre = 0;  // stages whose entry block went out before the wait
+            for (int it = blockIdx.x; it < a.items && pre < a.S; it += gridDim.x) {
+                int part;
+                const int g = item_tile(a, it, part) % a.G;
+                const int *blk_g = a.blk + g * a.n_chunks;
+                for (int k = 0; k < a.n_chunks && pre < a.S; ++k, ++pre) {
+                    const int lo = __ldg(blk_g + k), hi = __ldg(blk_g + k + 1);
+                    const uint32_t eb = static_cast<uint32_t>(hi - lo);
+                    mbar_expect_tx(&full[pre], xbytes + eb);
+                    bulk_g2s(ring + pre * a.stage_bytes + a.x_stage_bytes, a.blocks + lo, eb, &full[pre]);
+                }
+            }
+            pdl_wait();
+            int n_st = 0;
             for (int it = blockIdx.x; it < a.items; it += gridDim.x) {
                 int part;
                 int q = item_tile(a, it, part);
@@ -923,14 +939,16 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1) k_bi(const __grid_constant_
                 const int y0 = rt * a.TH * a.s_h;
                 const int x0 = ct * a.SPRt * PC * SW;
                 const int *blk_g = a.blk + g * a.n_chunks;
-                for (int k = 0; k < a.n_chunks; ++k) {
+                for (int k = 0; k < a.n_chunks; ++k, ++n_st) {
                     mbar_wait(&empty[s], ph);
                     unsigned char *st = ring + s * a.stage_bytes;
-                    const int lo = __ldg(blk_g + k), hi = __ldg(blk_g + k + 1);
-                    const uint32_t eb = static_cast<uint32_t>(hi - lo);
-                    mbar_expect_tx(&full[s], xbytes + eb);
+                    if (n_st >= pre) {  // (the first `pre` stages' entries are already in flight)
+                        const int lo = __ldg(blk_g + k), hi = __ldg(blk_g + k + 1);
+                        const uint32_t eb = static_cast<uint32_t>(hi - lo);
+                        mbar_expect_tx(&full[s], xbytes + eb);
+                        bulk_g2s(st + a.x_stage_bytes, a.blocks + lo, eb, &full[s]);
+                    }
                     tma_load_5d(st, &a.xmap, 0, x0, y0, k * a.CC, sb, &full[s]);
-                    bulk_g2s(st + a.x_stage_bytes, a.blocks + lo, eb, &full[s]);
                     if (++s == a.S) {
                         s = 0;
                         ph ^= 1;

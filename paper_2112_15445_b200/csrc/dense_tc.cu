@@ -238,7 +238,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_dtc(const __grid_constant__ Dtc
         if (RES) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&a.rmap)) : "memory");
     }
     pdl_release();
-    pdl_wait();  // every global access below: the previous kernel's output is complete
+    // every global access below waits for the previous kernel's output, except the producer's
+    // weight tiles for the first S stages (constant data, loaded while the previous kernel drains)
+    if (warp != kEW) pdl_wait();
 
     auto decode = [&](int t, int &mb, int &xt, int &yo, int &nb) {
         const int r = a.pool ? (t & 1) : 0;  // pool: consecutive tiles = rows 2y, 2y+1
@@ -266,6 +268,43 @@ __global__ void __launch_bounds__(kThreads, 1) k_dtc(const __grid_constant__ Dtc
         // The stage's boxes are issued by parallel lanes, one box per lane: successive TMA
         // instructions of one thread issue ~370 clocks apart (tools/tma_rate_bench.cu), so a
         // single issuing lane caps the stream at ~20-35 B/clk per SM.
+        auto load_a = [&](unsigned char *st, uint64_t *bar, int i, int mb) {  // weight tiles of k-iteration i
+            if constexpr (WIN) {
+                const int kh = i / a.cb, cb = i - kh * a.cb;
+                if (lane < 3) tma_load_2d(st + lane * kABytes, &a.wmap, (kh * 3 + lane) * a.C + cb * kKC, mb * 128, bar);
+            } else {
+                const int tap = i / a.cb, cb = i - tap * a.cb;
+                if (lane == 0) tma_load_2d(st, &a.wmap, tap * a.C + cb * kKC, mb * 128, bar);
+            }
+        };
+        auto load_b = [&](unsigned char *st, uint64_t *bar, int i, int xt, int yo, int nb) {  // activation boxes
+            if constexpr (WIN) {
+                const int kh = i / a.cb, cb = i - kh * a.cb;
+                if (lane >= 3 && lane < 3 + NBX)
+                    tma_load_5d(st + NA * kABytes + (lane - 3) * kBPix, &a.xmap, 0, xt * TWP + (lane - 3) + a.offw,
+                                yo + kh + a.offh, cb * kKC, nb, bar);
+            } else {
+                const int tap = i / a.cb, cb = i - tap * a.cb;
+                const int kh = tap / a.Kw, kw = tap - kh * a.Kw;
+                if (lane >= 1 && lane <= TWP)
+                    tma_load_5d(st + kABytes + (lane - 1) * kBPix, &a.xmap, 0, a.stride * (xt * TWP + lane - 1) + kw + a.offw,
+                                a.stride * yo + kh + a.offh, cb * kKC, nb, bar);
+            }
+        };
+        {  // the first S stages' weight tiles go out before the wait on the previous kernel
+            int it = 0;
+            for (int j = 0, t; it < S && (t = item_at(j)) >= 0; ++j) {
+                int tile, sp, k0, k1, mb, xt, yo, nb;
+                krange(t, tile, sp, k0, k1);
+                decode(tile, mb, xt, yo, nb);
+                for (int i = k0; i < k1 && it < S; ++i, ++it) {
+                    if (lane == 0) mbar_expect_tx(&full[it], kStage);
+                    __syncwarp();
+                    load_a(smem + it * kStage, &full[it], i, mb);
+                }
+            }
+        }
+        pdl_wait();
         int it = 0;  // running stage counter
         for (int j = 0, t; (t = item_at(j)) >= 0; ++j) {
             int tile, sp, k0, k1, mb, xt, yo, nb;
@@ -273,26 +312,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_dtc(const __grid_constant__ Dtc
             decode(tile, mb, xt, yo, nb);
             for (int i = k0; i < k1; ++i, ++it) {
                 const int s = it % S;
-                if (it >= S) mbar_wait_bounded(&empty[s], ((it / S) - 1) & 1);
                 unsigned char *st = smem + s * kStage;
-                if (lane == 0) mbar_expect_tx(&full[s], kStage);
-                __syncwarp();
-                if constexpr (WIN) {
-                    const int kh = i / a.cb, cb = i - kh * a.cb;
-                    if (lane < 3)
-                        tma_load_2d(st + lane * kABytes, &a.wmap, (kh * 3 + lane) * a.C + cb * kKC, mb * 128, &full[s]);
-                    else if (lane < 3 + NBX)
-                        tma_load_5d(st + NA * kABytes + (lane - 3) * kBPix, &a.xmap, 0, xt * TWP + (lane - 3) + a.offw,
-                                    yo + kh + a.offh, cb * kKC, nb, &full[s]);
-                } else {
-                    const int tap = i / a.cb, cb = i - tap * a.cb;
-                    const int kh = tap / a.Kw, kw = tap - kh * a.Kw;
-                    if (lane == 0)
-                        tma_load_2d(st, &a.wmap, tap * a.C + cb * kKC, mb * 128, &full[s]);
-                    else if (lane <= TWP)
-                        tma_load_5d(st + kABytes + (lane - 1) * kBPix, &a.xmap, 0, a.stride * (xt * TWP + lane - 1) + kw + a.offw,
-                                    a.stride * yo + kh + a.offh, cb * kKC, nb, &full[s]);
+                if (it >= S) {
+                    mbar_wait_bounded(&empty[s], ((it / S) - 1) & 1);
+                    if (lane == 0) mbar_expect_tx(&full[s], kStage);
+                    __syncwarp();
+                    load_a(st, &full[s], i, mb);
                 }
+                load_b(st, &full[s], i, xt, yo, nb);
             }
         }
     } else if (warp == kEW + 1) {
@@ -633,7 +660,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_dts(const __grid_constant__ Dtc
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&a.ymap)) : "memory");
     }
     pdl_release();
-    pdl_wait();
+    if (warp != kEW) pdl_wait();  // the producer waits after issuing the first stages' weight tiles
 
     auto decode = [&](int t, int &xt, int &yo, int &nb) {
         xt = t % a.x_tiles;
@@ -644,32 +671,53 @@ __global__ void __launch_bounds__(kThreads, 1) k_dts(const __grid_constant__ Dtc
 
     if (warp == kEW) {
         // ---------------- TMA producer: one box per lane ----------------
+        auto load_w = [&](unsigned char *st, uint64_t *bar, int i) {  // weight tiles of k-iteration i
+            if constexpr (WIN) {
+                const int kh = i / a.cb, cb = i - kh * a.cb;
+                if (lane < 3) tma_load_2d(st + lane * kWBox64, &a.wmap, (kh * 3 + lane) * a.C + cb * kKC, 0, bar);
+            } else {
+                const int tap = i / a.cb, cb = i - tap * a.cb;
+                if (lane == 0) tma_load_2d(st, &a.wmap, tap * a.C + cb * kKC, 0, bar);
+            }
+        };
+        auto load_x = [&](unsigned char *st, uint64_t *bar, int i, int xt, int yo, int nb) {
+            if constexpr (WIN) {
+                const int kh = i / a.cb, cb = i - kh * a.cb;
+                if (lane >= 3 && lane < 3 + NBX)
+                    tma_load_5d(st + NW * kWBox64 + (lane - 3) * kBPix, &a.xmap, 0, xt * TWP + (lane - 3) + a.offw,
+                                yo + kh + a.offh, cb * kKC, nb, bar);
+            } else {
+                const int tap = i / a.cb, cb = i - tap * a.cb;
+                const int kh = tap / a.Kw, kw = tap - kh * a.Kw;
+                if (lane >= 1 && lane <= TWP)
+                    tma_load_5d(st + kWBox64 + (lane - 1) * kBPix, &a.xmap, 0, a.stride * (xt * TWP + lane - 1) + kw + a.offw,
+                                a.stride * yo + kh + a.offh, cb * kKC, nb, bar);
+            }
+        };
+        {  // weights of the first S stages before the wait on the previous kernel
+            int it = 0;
+            for (int t = blockIdx.x; it < S && t < tiles; t += gridDim.x)
+                for (int i = 0; i < kiters && it < S; ++i, ++it) {
+                    if (lane == 0) mbar_expect_tx(&full[it], kStage);
+                    __syncwarp();
+                    load_w(smem + it * kStage, &full[it], i);
+                }
+        }
+        pdl_wait();
         int it = 0;
         for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
             int xt, yo, nb;
             decode(t, xt, yo, nb);
             for (int i = 0; i < kiters; ++i, ++it) {
                 const int s = it % S;
-                if (it >= S) mbar_wait_bounded(&empty[s], ((it / S) - 1) & 1);
                 unsigned char *st = smem + s * kStage;
-                if (lane == 0) mbar_expect_tx(&full[s], kStage);
-                __syncwarp();
-                if constexpr (WIN) {
-                    const int kh = i / a.cb, cb = i - kh * a.cb;
-                    if (lane < 3)
-                        tma_load_2d(st + lane * kWBox64, &a.wmap, (kh * 3 + lane) * a.C + cb * kKC, 0, &full[s]);
-                    else if (lane < 3 + NBX)
-                        tma_load_5d(st + NW * kWBox64 + (lane - 3) * kBPix, &a.xmap, 0, xt * TWP + (lane - 3) + a.offw,
-                                    yo + kh + a.offh, cb * kKC, nb, &full[s]);
-                } else {
-                    const int tap = i / a.cb, cb = i - tap * a.cb;
-                    const int kh = tap / a.Kw, kw = tap - kh * a.Kw;
-                    if (lane == 0)
-                        tma_load_2d(st, &a.wmap, tap * a.C + cb * kKC, 0, &full[s]);
-                    else if (lane <= TWP)
-                        tma_load_5d(st + kWBox64 + (lane - 1) * kBPix, &a.xmap, 0, a.stride * (xt * TWP + lane - 1) + kw + a.offw,
-                                    a.stride * yo + kh + a.offh, cb * kKC, nb, &full[s]);
+                if (it >= S) {
+                    mbar_wait_bounded(&empty[s], ((it / S) - 1) & 1);
+                    if (lane == 0) mbar_expect_tx(&full[s], kStage);
+                    __syncwarp();
+                    load_w(st, &full[s], i);
                 }
+                load_x(st, &full[s], i, xt, yo, nb);
             }
         }
     } else if (warp == kEW + 1) {
