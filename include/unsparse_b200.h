@@ -304,14 +304,17 @@ int usc_f16_epilogue(void *y, const void *res, int64_t count, int32_t relu, void
 int usc_dense_conv_f16(const usc_geometry *g, int32_t n, const void *w_dev, const usc_act_layout *x_layout,
                        const void *x, const usc_act_layout *y_layout, void *y, const usc_act_layout *res_layout,
                        const void *res, int32_t relu, void *stream);
-/* The same with a device workspace for split-K on small maps (tiles filling at most half
- * the SMs, no shortcut): the CTA completing a tile's last K split sums the splits' fp32
- * partials in split order and runs the epilogue.  `workspace` must hold
- * usc_dense_conv_f16_ws_bytes() bytes and be zero-filled once before its first use (the
- * kernel leaves its counters at zero); a null or short workspace runs without split. */
+/* The same with a tile configuration and a device workspace for split-K: `twp` output
+ * pixels per tile (2 or 4; 0 = automatic), `splits` K splits (>= 1; 0 = automatic: split
+ * only small maps whose tiles fill at most half the SMs; never with a shortcut).  The CTA
+ * completing a tile's last K split sums the splits' fp32 partials in split order and runs
+ * the epilogue.  `workspace` must hold usc_dense_conv_f16_ws_bytes() bytes for the same
+ * (twp, splits) and be zero-filled once before its first use (the kernel leaves its
+ * counters at zero); a null or short workspace runs without split. */
 int usc_dense_conv_f16_ws(const usc_geometry *g, int32_t n, const void *w_dev, const usc_act_layout *x_layout,
                           const void *x, const usc_act_layout *y_layout, void *y, const usc_act_layout *res_layout,
-                          const void *res, int32_t relu, void *workspace, int64_t ws_bytes, void *stream);
+                          const void *res, int32_t relu, void *workspace, int64_t ws_bytes, int32_t twp,
+                          int32_t splits, void *stream);
 /* The 3x3 stride-1 conv + ReLU + 2x2 max-pool (nn.py:124-135 on the ReLU output, which has
  * no NaN) in one launch: `y_layout` is the pooled output (height/2 x width/2).  Returns
  * USC_ERR_UNSUPPORTED when usc_dense_conv_f16_pool_ok() is 0 for the shape (then run the
@@ -321,9 +324,10 @@ int usc_dense_conv_f16_pool(const usc_geometry *g, int32_t n, const void *w_dev,
 /* 1 when the fused pool runs this shape at least as fast as conv + pool would (even output
  * dims, width % 4 == 0, enough row pairs to fill the SMs), else 0. */
 int32_t usc_dense_conv_f16_pool_ok(const usc_geometry *g, int32_t n, const usc_act_layout *x_layout);
-/* Workspace bytes usc_dense_conv_f16_ws needs for this shape on the current device (0: no split). */
+/* Workspace bytes usc_dense_conv_f16_ws needs for this shape and configuration on the current
+ * device (0: no split). */
 int64_t usc_dense_conv_f16_ws_bytes(const usc_geometry *g, int32_t n, const usc_act_layout *x_layout,
-                                    int32_t has_res);
+                                    int32_t has_res, int32_t twp, int32_t splits);
 /* round_to_binary16 (tensor.py:48-63) on device: f32 in -> f32 on the binary16 grid
  * (to_half == 0) or binary16 storage (to_half == 1). */
 int usc_round_binary16(const float *src, void *dst, int64_t count, int32_t to_half, void *stream);

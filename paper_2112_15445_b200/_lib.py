@@ -111,8 +111,8 @@ _SIGS = {
     "usc_f16_epilogue": (c_i32, [c_ptr, c_ptr, c_i64, c_i32, c_ptr]),
     "usc_dense_conv_f16": (c_i32, [c_ptr, c_i32, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_i32, c_ptr]),
     "usc_dense_conv_f16_ws": (c_i32, [c_ptr, c_i32, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_i32, c_ptr,
-                                      c_i64, c_ptr]),
-    "usc_dense_conv_f16_ws_bytes": (c_i64, [c_ptr, c_i32, c_ptr, c_i32]),
+                                      c_i64, c_i32, c_i32, c_ptr]),
+    "usc_dense_conv_f16_ws_bytes": (c_i64, [c_ptr, c_i32, c_ptr, c_i32, c_i32, c_i32]),
     "usc_dense_conv_f16_pool": (c_i32, [c_ptr, c_i32, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr]),
     "usc_dense_conv_f16_pool_ok": (c_i32, [c_ptr, c_i32, c_ptr]),
     "usc_conv_forward": (c_i32, [c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr]),

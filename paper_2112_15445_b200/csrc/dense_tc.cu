@@ -881,7 +881,9 @@ struct DtcShape {
     long long tiles;
 };
 
-DtcShape dtc_shape(const usc_geometry *g, int n, const usc_act_layout *xl, bool res, bool win, int sms) {
+// req_twp (2 or 4) / req_splits (>= 1) override the automatic choice (0 = automatic)
+DtcShape dtc_shape(const usc_geometry *g, int n, const usc_act_layout *xl, bool res, bool win, int sms,
+                   int req_twp = 0, int req_splits = 0) {
     DtcShape d{};
     const int s = g->stride_h, K = g->filter_h, pad = K / 2;
     d.Yh = (xl->height + 2 * pad - K) / s + 1;
@@ -891,6 +893,7 @@ DtcShape dtc_shape(const usc_geometry *g, int n, const usc_act_layout *xl, bool 
     // N = 256 (4 pixels) unless that leaves SMs idle: then 2-pixel tiles (twice the tiles)
     d.twp = d.Yw % 4 == 0 ? 4 : 2;
     if (d.twp == 4 && (long long)d.m_blocks * (d.Yw / 4) * d.Yh * d.NB < sms) d.twp = 2;
+    if (req_twp == 2 || req_twp == 4) d.twp = req_twp;
     d.x_tiles = (d.Yw + d.twp - 1) / d.twp;
     d.tiles = (long long)d.m_blocks * d.x_tiles * d.Yh * d.NB;
     d.kiters = (win ? K : K * K) * (g->in_channels / kKC);
@@ -900,6 +903,7 @@ DtcShape dtc_shape(const usc_geometry *g, int n, const usc_act_layout *xl, bool 
         const int want = (int)std::min<long long>(sms / d.tiles, d.kiters / 4);
         if (want >= 2) d.splits = want;
     }
+    if (req_splits >= 1) d.splits = res ? 1 : std::min(req_splits, d.kiters);
     d.kper = (d.kiters + d.splits - 1) / d.splits;
     d.splits = (d.kiters + d.kper - 1) / d.kper;
     return d;
@@ -931,7 +935,7 @@ size_t dtc_ws_bytes(const DtcShape &d) {
 
 int dense_conv_impl(const usc_geometry *g, int32_t n, const void *w_dev, const usc_act_layout *xl, const void *x,
                     const usc_act_layout *yl, void *y, const usc_act_layout *rl, const void *res, int32_t relu,
-                    void *workspace, size_t ws_bytes, int pool, void *stream) {
+                    void *workspace, size_t ws_bytes, int pool, int req_twp, int req_splits, void *stream) {
     if (!g || !w_dev || !xl || !x || !yl || !y || n < 1) return usc::fail(USC_ERR_VALUE, "dense conv: null argument");
     if (g->filter_h != g->filter_w || (g->filter_h != 1 && g->filter_h != 3) || g->stride_h != g->stride_w ||
         (g->stride_h != 1 && g->stride_h != 2))
@@ -1012,7 +1016,10 @@ int dense_conv_impl(const usc_geometry *g, int32_t n, const void *w_dev, const u
     int dev = 0, sms = 148;
     if (cudaGetDevice(&dev) == cudaSuccess && usc_device_sm_count(dev) > 0) sms = usc_device_sm_count(dev);
     const bool win = K == 3 && s == 1 && !res;  // the 3-tap row window (stride 1; no shortcut staging room)
-    DtcShape d = dtc_shape(g, n, xl, res != nullptr, win, sms);
+    if (req_twp != 0 && req_twp != 2 && req_twp != 4)
+        return usc::fail(USC_ERR_VALUE, "dense conv: pixels per tile must be 0 (auto), 2 or 4");
+    if (req_splits < 0) return usc::fail(USC_ERR_VALUE, "dense conv: negative split count");
+    DtcShape d = dtc_shape(g, n, xl, res != nullptr, win, sms, req_twp, req_splits);
     if (pool) {  // 4-pixel window tiles in row pairs, no split
         if (res || !relu || !dtc_pool_ok(g, n, xl, sms))
             return usc::fail(USC_ERR_UNSUPPORTED, "dense conv: fused pool not available for this shape");
@@ -1079,12 +1086,12 @@ int dense_conv_impl(const usc_geometry *g, int32_t n, const void *w_dev, const u
 int usc_dense_conv_f16(const usc_geometry *g, int32_t n, const void *w_dev, const usc_act_layout *xl, const void *x,
                        const usc_act_layout *yl, void *y, const usc_act_layout *rl, const void *res, int32_t relu,
                        void *stream) {
-    return dense_conv_impl(g, n, w_dev, xl, x, yl, y, rl, res, relu, nullptr, 0, 0, stream);
+    return dense_conv_impl(g, n, w_dev, xl, x, yl, y, rl, res, relu, nullptr, 0, 0, 0, 0, stream);
 }
 
 int usc_dense_conv_f16_pool(const usc_geometry *g, int32_t n, const void *w_dev, const usc_act_layout *xl,
                             const void *x, const usc_act_layout *yl, void *y, void *stream) {
-    return dense_conv_impl(g, n, w_dev, xl, x, yl, y, nullptr, nullptr, 1, nullptr, 0, 1, stream);
+    return dense_conv_impl(g, n, w_dev, xl, x, yl, y, nullptr, nullptr, 1, nullptr, 0, 1, 0, 0, stream);
 }
 
 int32_t usc_dense_conv_f16_pool_ok(const usc_geometry *g, int32_t n, const usc_act_layout *xl) {
@@ -1096,17 +1103,19 @@ int32_t usc_dense_conv_f16_pool_ok(const usc_geometry *g, int32_t n, const usc_a
 
 int usc_dense_conv_f16_ws(const usc_geometry *g, int32_t n, const void *w_dev, const usc_act_layout *xl, const void *x,
                           const usc_act_layout *yl, void *y, const usc_act_layout *rl, const void *res, int32_t relu,
-                          void *workspace, int64_t ws_bytes, void *stream) {
+                          void *workspace, int64_t ws_bytes, int32_t twp, int32_t splits, void *stream) {
     if (ws_bytes < 0) return usc::fail(USC_ERR_VALUE, "dense conv: negative workspace size");
-    return dense_conv_impl(g, n, w_dev, xl, x, yl, y, rl, res, relu, workspace, (size_t)ws_bytes, 0, stream);
+    return dense_conv_impl(g, n, w_dev, xl, x, yl, y, rl, res, relu, workspace, (size_t)ws_bytes, 0, twp, splits,
+                           stream);
 }
 
-int64_t usc_dense_conv_f16_ws_bytes(const usc_geometry *g, int32_t n, const usc_act_layout *xl, int32_t has_res) {
+int64_t usc_dense_conv_f16_ws_bytes(const usc_geometry *g, int32_t n, const usc_act_layout *xl, int32_t has_res,
+                                    int32_t twp, int32_t splits) {
     if (!g || !xl || n < 1 || g->filter_h != g->filter_w || (g->filter_h != 1 && g->filter_h != 3) ||
         g->in_channels % kKC)
         return 0;
     int dev = 0, sms = 148;
     if (cudaGetDevice(&dev) == cudaSuccess && usc_device_sm_count(dev) > 0) sms = usc_device_sm_count(dev);
     const bool win = g->filter_h == 3 && g->stride_h == 1 && !has_res;
-    return (int64_t)dtc_ws_bytes(dtc_shape(g, n, xl, has_res != 0, win, sms));
+    return (int64_t)dtc_ws_bytes(dtc_shape(g, n, xl, has_res != 0, win, sms, twp, splits));
 }

@@ -37,31 +37,35 @@ def pack_weights(w, device=None):
 
 
 def dense_workspace(in_channels: int, out_channels: int, k: int, stride: int, n: int, x_lay, res: bool = False,
-                    device=None):
-    """Zero-filled split-K workspace for dense_conv on this shape (None when the shape does
-    not split: the tiles already fill the SMs, or a shortcut is fused).  Reusable across
-    launches of the same shape (the kernel leaves its counters at zero); not shareable
-    between launches that may run concurrently."""
+                    device=None, twp: int = 0, splits: int = 0):
+    """Zero-filled split-K workspace for dense_conv on this shape and tile configuration
+    (None when it does not split: automatic configurations split only small maps; a fused
+    shortcut never splits).  Reusable across launches of the same shape (the kernel leaves
+    its counters at zero); not shareable between launches that may run concurrently."""
     import torch
     g = _lib.Geometry(in_channels, out_channels, k, k, x_lay.height, x_lay.width, stride, stride, k // 2, k // 2)
-    nbytes = int(_lib.lib().usc_dense_conv_f16_ws_bytes(_lib.ref(g), n, _lib.ref(x_lay), int(res)))
+    nbytes = int(_lib.lib().usc_dense_conv_f16_ws_bytes(_lib.ref(g), n, _lib.ref(x_lay), int(res), int(twp),
+                                                        int(splits)))
     if nbytes <= 0:
         return None
     return torch.zeros(nbytes, dtype=torch.uint8, device=device or "cuda")
 
 
 def dense_conv(w_packed, in_channels: int, out_channels: int, k: int, stride: int, n: int, x, x_lay, y, y_lay,
-               res=None, res_lay=None, relu: bool = True, stream=None, workspace=None):
-    """One tensor-core convolution on BI64 buffers (usc_dense_conv_f16[_ws]); `workspace`
-    from dense_workspace enables split-K on small maps."""
+               res=None, res_lay=None, relu: bool = True, stream=None, workspace=None, twp: int = 0,
+               splits: int = 0):
+    """One tensor-core convolution on BI64 buffers (usc_dense_conv_f16[_ws]).  `twp` /
+    `splits` pick the tile (pixels per tile 2 or 4, K splits; 0 = automatic); `workspace`
+    from dense_workspace(..., twp, splits) enables split-K."""
     g = _lib.Geometry(in_channels, out_channels, k, k, x_lay.height, x_lay.width, stride, stride, k // 2, k // 2)
     args = (_lib.ref(g), n, _lib.t_ptr(w_packed), _lib.ref(x_lay), _lib.t_ptr(x), _lib.ref(y_lay), _lib.t_ptr(y),
             None if res is None else _lib.ref(res_lay), None if res is None else _lib.t_ptr(res), int(relu))
-    if workspace is None:
+    if workspace is None and not twp and not splits:
         _lib.check(_lib.lib().usc_dense_conv_f16(*args, _lib.stream_ptr(stream)), "dense_conv_f16")
     else:
-        _lib.check(_lib.lib().usc_dense_conv_f16_ws(*args, _lib.t_ptr(workspace), workspace.numel(),
-                                                    _lib.stream_ptr(stream)), "dense_conv_f16_ws")
+        _lib.check(_lib.lib().usc_dense_conv_f16_ws(
+            *args, None if workspace is None else _lib.t_ptr(workspace), 0 if workspace is None else workspace.numel(),
+            int(twp), int(splits), _lib.stream_ptr(stream)), "dense_conv_f16_ws")
 
 
 def pool_fusable(in_channels: int, out_channels: int, n: int, x_lay) -> bool:
@@ -77,3 +81,25 @@ def dense_conv_pool(w_packed, in_channels: int, out_channels: int, n: int, x, x_
     _lib.check(_lib.lib().usc_dense_conv_f16_pool(_lib.ref(g), n, _lib.t_ptr(w_packed), _lib.ref(x_lay),
                                                   _lib.t_ptr(x), _lib.ref(y_lay), _lib.t_ptr(y),
                                                   _lib.stream_ptr(stream)), "dense_conv_f16_pool")
+
+
+# (pixels per tile, K splits) candidates of the per-layer tile search; 0 = automatic
+TILE_CANDIDATES = ((0, 0), (2, 1), (4, 1), (2, 2), (4, 2), (2, 4), (4, 4))
+
+
+def tune_tile(launch, in_channels: int, out_channels: int, k: int, stride: int, n: int, x_lay, res: bool = False,
+              device=None, repeats: int = 5) -> tuple:
+    """Per-layer tile search of the tensor-core backend (the dense-side analogue of the
+    sparse autotune_sb, ref/engine.py:139-170): `launch(twp, splits, workspace)` runs the
+    layer on its real buffers; every candidate is timed with CUDA events (host cost hidden)
+    and the fastest (twp, splits) returned.  Splits never combine with a fused shortcut."""
+    from .engine import time_median_cuda
+    best, best_ms = (0, 0), None
+    for twp, sp in TILE_CANDIDATES:
+        if res and sp > 1:
+            continue
+        ws = dense_workspace(in_channels, out_channels, k, stride, n, x_lay, res, device, twp, sp)
+        ms = time_median_cuda(lambda: launch(twp, sp, ws), repeats, 2, 4)
+        if best_ms is None or ms < best_ms:
+            best, best_ms = (twp, sp), ms
+    return best

@@ -136,6 +136,7 @@ class SparseVGG16:
         self._check_backends()
         self.pre_pool = self._pre_pool_layers()
         self.fuse_pool = {}  # per pool-feeding conv: fuse the pool into its epilogue (autotuned)
+        self.tc_cfg = {}     # per tensor-core conv: (pixels per tile, K splits), 0 = automatic (autotune_tc)
         self.saturation = saturation
         self.layer_params = [dict() for _ in self.geoms]
         if mode == "cb4" and maxima is not None:  # calibrate_activation_maxima output
@@ -360,7 +361,29 @@ class SparseVGG16:
         self.backend_pick = best
         build(cands[best])
         torch.cuda.synchronize()
+        self.autotune_tc()
         return self.backends
+
+    def autotune_tc(self) -> dict:
+        """Tile search of every tensor-core conv (dense.tune_tile on the layer's own
+        buffers); kept only if the captured network gets faster."""
+        from .dense import tune_tile
+        if not self._tc_launch:
+            return self.tc_cfg
+        before, old = self.network_ms(), dict(self.tc_cfg)
+        for li, (launch, x_lay, res) in sorted(self._tc_launch.items()):
+            g = self.geoms[li]
+            self.tc_cfg[li] = tune_tile(launch, g.in_channels, g.out_channels, 3, 1, self.batch, x_lay, res,
+                                        self.device)
+        self.graph = None
+        self._build()
+        after = self.network_ms()
+        if after > before:
+            self.tc_cfg = old
+            self.graph = None
+            self._build()
+        self.tc_search = {"auto_ms": round(before, 4), "tuned_ms": round(after, 4)}
+        return self.tc_cfg
 
     # -- buffers and plans ---------------------------------------------------
     def _buf(self, lay, dtype=None):
@@ -375,6 +398,7 @@ class SparseVGG16:
         import torch
         n = self.batch
         self.plans, self.blobs, self.steps = [], [], []
+        self._tc_launch = {}  # tensor-core conv -> (launch(twp, splits, ws), input layout, shortcut) for autotune_tc
         # input buffer of the first conv
         plans = [make_plan(g, n, self.dtype, c) for g, c in zip(self.geoms, self.configs)]
         # every layer reads the layout its plan wants: one interleave for the network
@@ -444,10 +468,17 @@ class SparseVGG16:
                 halo = 0 if nxt == "M" else 1
                 out_lay = _lib.act_layout(g.out_channels, g.out_h, g.out_w, halo, halo, self.eb, il)
                 out_buf = self._buf(out_lay)
-                ws = dense_workspace(g.in_channels, g.out_channels, 3, 1, n, cur_lay, False, self.device)
+                twp, sp = self.tc_cfg.get(li, (0, 0))
+                ws = dense_workspace(g.in_channels, g.out_channels, 3, 1, n, cur_lay, False, self.device, twp, sp)
 
-                def fn(stream=None, w=self._tc_w[li], g=g, x=cur_buf, xl=cur_lay, y=out_buf, yl=out_lay, ws=ws):
-                    dense_conv(w, g.in_channels, g.out_channels, 3, 1, n, x, xl, y, yl, None, None, True, stream, ws)
+                def launch(twp, sp, ws, stream=None, w=self._tc_w[li], g=g, x=cur_buf, xl=cur_lay, y=out_buf,
+                           yl=out_lay):
+                    dense_conv(w, g.in_channels, g.out_channels, 3, 1, n, x, xl, y, yl, None, None, True, stream, ws,
+                               twp, sp)
+                self._tc_launch[li] = (launch, cur_lay, False)
+
+                def fn(stream=None, launch=launch, twp=twp, sp=sp, ws=ws):
+                    launch(twp, sp, ws, stream)
                 self.steps.append(("tc", li, fn))
                 self.nonzero_macs += int(np.count_nonzero(self.filters[li].weights)) * g.out_h * g.out_w * n
                 cur_buf, cur_lay = out_buf, out_lay
@@ -677,7 +708,8 @@ class SparseVGG16:
         import dataclasses
         return {"configs": [dataclasses.asdict(c) for c in self.configs],
                 "fuse_pool": {str(k): bool(v) for k, v in self.fuse_pool.items()},
-                "backends": list(self.backends)}
+                "backends": list(self.backends),
+                "tc_cfg": {str(k): list(v) for k, v in self.tc_cfg.items()}}
 
     def load_tuned_state(self, state) -> None:
         """Accepts tuned_state() output (or a bare list of ExecConfig dicts)."""
@@ -685,6 +717,7 @@ class SparseVGG16:
             state = {"configs": state, "fuse_pool": {}}
         self.configs = [ExecConfig(**c) for c in state["configs"]]
         self.fuse_pool = {int(k): bool(v) for k, v in state.get("fuse_pool", {}).items()}
+        self.tc_cfg = {int(k): tuple(v) for k, v in state.get("tc_cfg", {}).items()}
         if "backends" in state:
             self.backends = list(state["backends"])
             self._check_backends()

@@ -90,6 +90,7 @@ class SparseResNet50:
         self.weights = weights
         self.configs = [ExecConfig(samples_per_cta=64) for _ in self.layers]
         self.backends = list(backends) if backends is not None else ["sparse"] * len(self.layers)
+        self.tc_cfg = {}  # per tensor-core conv: (pixels per tile, K splits), 0 = automatic (autotune_tc)
         self._check_backends()
         self.graph = None
         self._build()
@@ -168,6 +169,7 @@ class SparseResNet50:
         n = self.batch
         net = self
         self.steps = []  # (li, plan, blob, x, x_view_layout | None, y, epilogue) | (li, None, .., fn)
+        self._tc_launch = {}  # tensor-core conv -> (launch(twp, splits, ws), input layout, shortcut)
         self.in_layout = self._lay(3, 32, 1)
         self.x_buf = self._buf(self.in_layout)
         L = _lib.lib()
@@ -220,13 +222,18 @@ class SparseResNet50:
                 w, x, x_lay = self._tc_w[li], xa.bi(), xa.lay
                 y = ya.buf = self._buf(ya.lay)
                 r, r_lay = (None, None) if residual is None else (residual.bi(), residual.lay)
+                twp, sp = self.tc_cfg.get(li, (0, 0))
                 ws = dense_workspace(g.in_channels, g.out_channels, g.filter_h, s, n, x_lay, residual is not None,
-                                     self.device)
+                                     self.device, twp, sp)
 
-                def fn(stream=None, li=li, w=w, x=x, x_lay=x_lay, y=y, y_lay=ya.lay, r=r, r_lay=r_lay, relu=relu,
-                       g=g, s=s, ws=ws):
+                def launch(twp, sp, ws, stream=None, w=w, x=x, x_lay=x_lay, y=y, y_lay=ya.lay, r=r, r_lay=r_lay,
+                           relu=relu, g=g, s=s):
                     dense_conv(w, g.in_channels, g.out_channels, g.filter_h, s, n, x, x_lay, y, y_lay, r, r_lay,
-                               relu, stream, ws)
+                               relu, stream, ws, twp, sp)
+                self._tc_launch[li] = (launch, x_lay, residual is not None)
+
+                def fn(stream=None, launch=launch, twp=twp, sp=sp, ws=ws):
+                    launch(twp, sp, ws, stream)
                 self.steps.append((li, None, None, None, None, None, fn))
                 return ya
             if self.backends[li] == "dense":
@@ -343,7 +350,8 @@ class SparseResNet50:
     # -- tuned state (per-conv tiles) -------------------------------------------------
     def tuned_state(self) -> dict:
         import dataclasses
-        return {"configs": [dataclasses.asdict(c) for c in self.configs], "backends": list(self.backends)}
+        return {"configs": [dataclasses.asdict(c) for c in self.configs], "backends": list(self.backends),
+                "tc_cfg": {str(k): list(v) for k, v in self.tc_cfg.items()}}
 
     def load_tuned_state(self, state) -> None:
         """Accepts tuned_state() output (or a bare list of ExecConfig dicts)."""
@@ -351,6 +359,7 @@ class SparseResNet50:
             if "backends" in state:
                 self.backends = list(state["backends"])
                 self._check_backends()
+            self.tc_cfg = {int(k): tuple(v) for k, v in state.get("tc_cfg", {}).items()}
             state = state["configs"]
         if len(state) != len(self.layers):
             raise ValueError(f"tuned state has {len(state)} configs for {len(self.layers)} convs")
@@ -470,4 +479,26 @@ class SparseResNet50:
         self.backend_pick = best
         build(cands[best])
         torch.cuda.synchronize()
+        self.autotune_tc()
         return self.backends
+
+    def autotune_tc(self) -> dict:
+        """Tile search of every tensor-core conv (dense.tune_tile on the layer's own
+        buffers and epilogue); kept only if the captured network gets faster."""
+        from .dense import tune_tile
+        if not self._tc_launch:
+            return self.tc_cfg
+        before, old = self.network_ms(), dict(self.tc_cfg)
+        for li, (launch, x_lay, res) in sorted(self._tc_launch.items()):
+            _, g, _, s = self.layers[li]
+            self.tc_cfg[li] = tune_tile(launch, g.in_channels, g.out_channels, g.filter_h, s, self.batch, x_lay, res,
+                                        self.device)
+        self.graph = None
+        self._build()
+        after = self.network_ms()
+        if after > before:
+            self.tc_cfg = old
+            self.graph = None
+            self._build()
+        self.tc_search = {"auto_ms": round(before, 4), "tuned_ms": round(after, 4)}
+        return self.tc_cfg

@@ -134,12 +134,17 @@ def dispatched(m, name, steps, flush, cudnn_ms):
     out = {"images_per_s": round(m.batch / (ms / 1e3), 1), "ms_per_step": round(ms, 4),
            "speedup_vs_cudnn": round(cudnn_ms / ms, 3), "sparse_layers": backends.count("sparse"),
            "dense_layers": backends.count("dense"), "backends": backends,
-           "rule": "per-conv argmin of the sparse step vs transpose + cuDNN + fused epilogue, ties to dense"}
+           "tc_layers": backends.count("tc"),
+           "rule": "network-level search over per-conv argmins of sparse / tensor-core / cuDNN and block splits; "
+                   "then the tensor-core tile search (pixels per tile, K splits) per conv"}
     if hasattr(m, "backend_search"):
         out["pick"], out["search"] = m.backend_pick, m.backend_search
     if hasattr(m, "backend_times"):
         out["per_conv_ms"] = {str(k): {a: (round(b, 4) if b is not None else None) for a, b in v.items()}
                               for k, v in m.backend_times.items()}
+    out["tc_tiles"] = {str(k): list(v) for k, v in getattr(m, "tc_cfg", {}).items() if tuple(v) != (0, 0)}
+    if hasattr(m, "tc_search"):
+        out["tc_search"] = m.tc_search
     return out
 
 
