@@ -937,6 +937,9 @@ int dense_conv_impl(const usc_geometry *g, int32_t n, const void *w_dev, const u
                     const usc_act_layout *yl, void *y, const usc_act_layout *rl, const void *res, int32_t relu,
                     void *workspace, size_t ws_bytes, int pool, int req_twp, int req_splits, void *stream) {
     if (!g || !w_dev || !xl || !x || !yl || !y || n < 1) return usc::fail(USC_ERR_VALUE, "dense conv: null argument");
+    if (req_twp != 0 && req_twp != 2 && req_twp != 4)
+        return usc::fail(USC_ERR_VALUE, "dense conv: pixels per tile must be 0 (auto), 2 or 4");
+    if (req_splits < 0) return usc::fail(USC_ERR_VALUE, "dense conv: negative split count");
     if (g->filter_h != g->filter_w || (g->filter_h != 1 && g->filter_h != 3) || g->stride_h != g->stride_w ||
         (g->stride_h != 1 && g->stride_h != 2))
         return usc::fail(USC_ERR_UNSUPPORTED, "dense conv: 1x1 / 3x3 filters, stride 1 or 2");
@@ -1016,9 +1019,6 @@ int dense_conv_impl(const usc_geometry *g, int32_t n, const void *w_dev, const u
     int dev = 0, sms = 148;
     if (cudaGetDevice(&dev) == cudaSuccess && usc_device_sm_count(dev) > 0) sms = usc_device_sm_count(dev);
     const bool win = K == 3 && s == 1 && !res;  // the 3-tap row window (stride 1; no shortcut staging room)
-    if (req_twp != 0 && req_twp != 2 && req_twp != 4)
-        return usc::fail(USC_ERR_VALUE, "dense conv: pixels per tile must be 0 (auto), 2 or 4");
-    if (req_splits < 0) return usc::fail(USC_ERR_VALUE, "dense conv: negative split count");
     DtcShape d = dtc_shape(g, n, xl, res != nullptr, win, sms, req_twp, req_splits);
     if (pool) {  // 4-pixel window tiles in row pairs, no split
         if (res || !relu || !dtc_pool_ok(g, n, xl, sms))

@@ -304,3 +304,37 @@ def test_empty_batch_like_reference():
     assert U.autotune_sb(x, f).sub_batch == 2
     with pytest.raises(ValueError):
         U.sparse_conv_forward(U.DenseTensor4.from_array(np.zeros((3, 4, 5, 5), np.float32)), f, U.ExecConfig(2))
+
+
+def test_dense_tc_schedule_queries():
+    """Host-side schedule decisions of the tensor-core backend (no GPU needed: 148 SMs
+    assumed when no device is visible): split-K workspace sizes, the fused-pool gate, and
+    argument validation before any driver call."""
+    from paper_2112_15445_b200.dense import pool_fusable
+
+    def ws_bytes(C, D, k, s, hw, n, res=False, twp=0, splits=0):
+        g = _lib.Geometry(C, D, k, k, hw, hw, s, s, k // 2, k // 2)
+        xl = _lib.act_layout(C, hw, hw, k // 2, k // 2, 2, 64)
+        return int(_lib.lib().usc_dense_conv_f16_ws_bytes(_lib.ref(g), n, _lib.ref(xl), int(res), twp, splits))
+
+    # VGG conv5 (2x2 maps, 32 two-pixel tiles): automatic split-K, 4 splits of 6 k-iterations
+    tiles, splits = 4 * 1 * 2 * 4, 4
+    assert ws_bytes(512, 512, 3, 1, 2, 256) == tiles * splits * 128 * 128 * 4 + tiles * 4 + 256
+    assert ws_bytes(64, 64, 3, 1, 32, 256) == 0          # 32x32 maps fill the SMs: no split
+    assert ws_bytes(512, 512, 3, 1, 2, 256, res=True) == 0  # never with a fused shortcut
+    assert ws_bytes(256, 256, 3, 1, 8, 256, twp=4, splits=2) == (2 * 2 * 8 * 4) * 2 * 256 * 128 * 4 + 128 * 4 + 256
+    assert ws_bytes(256, 256, 3, 1, 8, 256, twp=4, splits=1) == 0
+    # the fused-pool cost model: VGG conv1_2 / conv2_2 fuse, the 8x8 and 4x4 maps do not
+    lay = lambda C, hw: _lib.act_layout(C, hw, hw, 1, 1, 2, 64)  # noqa: E731
+    assert pool_fusable(64, 64, 256, lay(64, 32)) and pool_fusable(128, 128, 256, lay(128, 16))
+    assert not pool_fusable(256, 256, 256, lay(256, 8)) and not pool_fusable(512, 512, 256, lay(512, 4))
+    # bad tile arguments fail before any device work
+    g = _lib.Geometry(64, 64, 3, 3, 8, 8, 1, 1, 1, 1)
+    xl, yl = lay(64, 8), lay(64, 8)
+    dummy = ctypes.c_void_p(16)
+    rc = _lib.lib().usc_dense_conv_f16_ws(_lib.ref(g), 64, dummy, _lib.ref(xl), dummy, _lib.ref(yl), dummy, None, None,
+                                         1, None, 0, 3, 0, None)
+    assert rc == _lib.USC_ERR_VALUE
+    rc = _lib.lib().usc_dense_conv_f16_ws(_lib.ref(g), 64, dummy, _lib.ref(xl), dummy, _lib.ref(yl), dummy, None, None,
+                                         1, None, 0, 0, -1, None)
+    assert rc == _lib.USC_ERR_VALUE
