@@ -887,6 +887,10 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1) k_bi(const __grid_constant_
     constexpr int RVR = (KIND == USC_F32) ? SPL : 1;  // registers per shortcut value
     constexpr bool RPRE = RES && (KIND == USC_F32 || KIND == USC_F16) &&
                           SPL * DW * P + (PIPE ? 4 : 2) * P * VR + DW * P * RVR + 40 <= REGCAP;
+    // otherwise the shortcut loads go out at the start of the last chunk, whose pair loop then
+    // runs without software pipelining so the shortcut registers fit the cap
+    constexpr bool LPRE = RES && !RPRE && (KIND == USC_F32 || KIND == USC_F16) &&
+                          SPL * DW * P + 2 * P * VR + DW * P * RVR + 40 <= REGCAP;
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t *full = reinterpret_cast<uint64_t *>(smem);
     uint64_t *empty = full + 8;
@@ -999,6 +1003,11 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1) k_bi(const __grid_constant_
 
         for (int k = 0; k < a.n_chunks; ++k) {
             const uint32_t st = smem_u32(ring + s * a.stage_bytes);
+            const bool late = LPRE && k == a.n_chunks - 1;
+            if constexpr (LPRE) {
+                if (late && a.fast && active && r < a.Yh)
+                    fast_loads<KIND, PC, PR, DW, SPL, RES>(a, g, wc, sb, r, col0, part, lane, dch, rv);
+            }
             mbar_wait(&full[s], ph);
             if (active) {
                 const uint32_t xs = st + base;  // this thread's first pixel, tap (0,0,0)
@@ -1008,7 +1017,10 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1) k_bi(const __grid_constant_
                 for (int dw = 0; dw < DW; ++dw) {
                     const int2 h = lds_v2(hdr + dw * 8);  // run [h.x, h.y), h.x even
                     if (part >= 0 && dw % a.split != part) continue;
-                    run_pairs<KIND, PC, PR, SW, SPL, PIPE>(acc[dw], xs, rs, E + h.x * 8, E + h.y * 8);
+                    if (LPRE && late)
+                        run_pairs<KIND, PC, PR, SW, SPL, false>(acc[dw], xs, rs, E + h.x * 8, E + h.y * 8);
+                    else
+                        run_pairs<KIND, PC, PR, SW, SPL, PIPE>(acc[dw], xs, rs, E + h.x * 8, E + h.y * 8);
                 }
             }
             __syncwarp();
@@ -1022,7 +1034,8 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1) k_bi(const __grid_constant_
         if (active && r < a.Yh) {
             if constexpr (KIND == USC_F32 || KIND == USC_F16 || KIND == USC_I8 || KIND == USC_CB4) {
                 if (a.fast) {
-                    if constexpr (!RPRE) fast_loads<KIND, PC, PR, DW, SPL, RES>(a, g, wc, sb, r, col0, part, lane, dch, rv);
+                    if constexpr (!RPRE && !LPRE)
+                        fast_loads<KIND, PC, PR, DW, SPL, RES>(a, g, wc, sb, r, col0, part, lane, dch, rv);
                     store_tile_fast<KIND, PC, PR, DW, SPL, RES>(a, acc, sb, r, col0, lane, dch, rv);
                     continue;
                 }
