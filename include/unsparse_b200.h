@@ -300,7 +300,9 @@ int usc_f16_epilogue(void *y, const void *res, int64_t count, int32_t relu, void
  * halo, which must be at least that wide), stride g->stride_h (= stride_w, 1 or 2),
  * filters 1x1 or 3x3; in_channels % 64 == 0, out_channels % 64 == 0.  `w_dev`: the dense
  * weights as [out_channels][filter_h*filter_w][in_channels] binary16 (K-major), padded with
- * zero rows to a multiple of 128 output channels. */
+ * zero rows to a multiple of 128 output channels.  First-layer form: in_channels <= 16,
+ * 3x3 stride 1, out_channels == 64, no shortcut, `w_dev` = [9][16][64] binary16 (input
+ * channels zero-padded to 16, output channel fastest). */
 int usc_dense_conv_f16(const usc_geometry *g, int32_t n, const void *w_dev, const usc_act_layout *x_layout,
                        const void *x, const usc_act_layout *y_layout, void *y, const usc_act_layout *res_layout,
                        const void *res, int32_t relu, void *stream);

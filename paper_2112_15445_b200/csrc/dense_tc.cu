@@ -597,29 +597,40 @@ cudaError_t launch_dtc(const DtcArgs &a, int tiles, cudaStream_t st) {
 // 64 channels and writes them transposed into the pixel's [64 c][64 s] swizzled staging
 // box (16-bit stores, conflict-free); the two warps of a pixel meet at a named barrier and
 // one TMA store writes the box.
-constexpr int kWBox64 = 64 * kKC * 2;  // [64 d][64 k] binary16 weight tile (8 KB)
-
-template <int TWP, bool WIN>
-constexpr int dts_stages() {
-    return WIN ? 2 : 4;
+// KC = 16: the first-layer form (a few input channels, zero-filled to 16 by the TMA): pixel
+// boxes [16 c][64 s] (2 KB), the weights MN-major [16 k][64 d] per tap (packed
+// [taps][16][64], one 2-KB tile per tap), one K = 16 MMA per tap.
+template <int KC>
+constexpr int dts_wbox() {
+    return 64 * KC * 2;  // [64 d][KC k] binary16 weight tile
 }
-template <int TWP, bool WIN>
+template <int KC>
+constexpr int dts_xbox() {
+    return KC * 64 * 2;  // [KC c][64 s] binary16 pixel box
+}
+template <int TWP, bool WIN, int KC>
+constexpr int dts_stages() {
+    return KC == 16 ? 6 : (WIN ? 2 : 4);
+}
+template <int TWP, bool WIN, int KC>
 constexpr int dts_smem() {
     constexpr int NW = WIN ? 3 : 1, NBX = WIN ? TWP + 2 : TWP;
-    return dts_stages<TWP, WIN>() * (NW * kWBox64 + NBX * kBPix) + TWP * 2 * kBPix + 1024 + 256;
+    return dts_stages<TWP, WIN, KC>() * (NW * dts_wbox<KC>() + NBX * dts_xbox<KC>()) + TWP * 2 * kBPix + 1024 + 256;
 }
 
 __device__ __forceinline__ void pair_sync(int id) {  // the two warps of one output pixel
     asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory");
 }
 
-template <int TWP, bool WIN>
+template <int TWP, bool WIN, int KC>
 __global__ void __launch_bounds__(kThreads, 1) k_dts(const __grid_constant__ DtcArgs a) {
     constexpr int G = TWP / 2;                   // MMA groups (pixel pairs) per tile
     constexpr int NW = WIN ? 3 : 1;              // weight tiles (taps) per stage
     constexpr int NBX = WIN ? TWP + 2 : TWP;     // pixel boxes per stage
-    constexpr int kStage = NW * kWBox64 + NBX * kBPix;
-    constexpr int S = dts_stages<TWP, WIN>();
+    constexpr int kW = dts_wbox<KC>(), kX = dts_xbox<KC>();
+    constexpr int kStage = NW * kW + NBX * kX;
+    constexpr int S = dts_stages<TWP, WIN, KC>();
+    static_assert(KC == 64 || (KC == 16 && WIN), "the 16-channel form is the 3x3 stride-1 window");
     constexpr uint32_t kCols = 2 * G * 64 < 32 ? 32 : 2 * G * 64;  // two accumulators
     static_assert(kEW == 8, "two epilogue warps per pixel of a 4-pixel tile");
     extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -672,9 +683,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_dts(const __grid_constant__ Dtc
     if (warp == kEW) {
         // ---------------- TMA producer: one box per lane ----------------
         auto load_w = [&](unsigned char *st, uint64_t *bar, int i) {  // weight tiles of k-iteration i
-            if constexpr (WIN) {
+            if constexpr (KC == 16) {  // [taps][16 k][64 d]: rows (tap * 16 ..), 64 channels
+                if (lane < 3) tma_load_2d(st + lane * kW, &a.wmap, 0, (i * 3 + lane) * 16, bar);
+            } else if constexpr (WIN) {
                 const int kh = i / a.cb, cb = i - kh * a.cb;
-                if (lane < 3) tma_load_2d(st + lane * kWBox64, &a.wmap, (kh * 3 + lane) * a.C + cb * kKC, 0, bar);
+                if (lane < 3) tma_load_2d(st + lane * kW, &a.wmap, (kh * 3 + lane) * a.C + cb * kKC, 0, bar);
             } else {
                 const int tap = i / a.cb, cb = i - tap * a.cb;
                 if (lane == 0) tma_load_2d(st, &a.wmap, tap * a.C + cb * kKC, 0, bar);
@@ -684,14 +697,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_dts(const __grid_constant__ Dtc
             if constexpr (WIN) {
                 const int kh = i / a.cb, cb = i - kh * a.cb;
                 if (lane >= 3 && lane < 3 + NBX)
-                    tma_load_5d(st + NW * kWBox64 + (lane - 3) * kBPix, &a.xmap, 0, xt * TWP + (lane - 3) + a.offw,
-                                yo + kh + a.offh, cb * kKC, nb, bar);
+                    tma_load_5d(st + NW * kW + (lane - 3) * kX, &a.xmap, 0, xt * TWP + (lane - 3) + a.offw,
+                                yo + kh + a.offh, cb * KC, nb, bar);
             } else {
                 const int tap = i / a.cb, cb = i - tap * a.cb;
                 const int kh = tap / a.Kw, kw = tap - kh * a.Kw;
                 if (lane >= 1 && lane <= TWP)
-                    tma_load_5d(st + kWBox64 + (lane - 1) * kBPix, &a.xmap, 0, a.stride * (xt * TWP + lane - 1) + kw + a.offw,
-                                a.stride * yo + kh + a.offh, cb * kKC, nb, bar);
+                    tma_load_5d(st + kW + (lane - 1) * kX, &a.xmap, 0, a.stride * (xt * TWP + lane - 1) + kw + a.offw,
+                                a.stride * yo + kh + a.offh, cb * KC, nb, bar);
             }
         };
         {  // weights of the first S stages before the wait on the previous kernel
@@ -722,7 +735,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_dts(const __grid_constant__ Dtc
         }
     } else if (warp == kEW + 1) {
         // ---------------- MMA issuer: A = activations (MN-major), B = weights (K-major) ----------------
-        const uint32_t idesc = (1u << 4) | (1u << 15) | ((uint32_t)(64 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+        // A MN-major (bit 15); B K-major, or MN-major (bit 16) in the 16-channel form
+        const uint32_t idesc = (1u << 4) | (1u << 15) | (KC == 16 ? (1u << 16) : 0u) | ((uint32_t)(64 >> 3) << 17) |
+                               ((uint32_t)(128 >> 4) << 24);
         int it = 0, lt = 0;
         for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++lt) {
             const int ab = lt & 1;
@@ -733,15 +748,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_dts(const __grid_constant__ Dtc
                 mbar_wait_bounded(&full[s], (it / S) & 1);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 if (lane == 0) {
-                    const uint32_t wbase = smem_u32(smem + s * kStage), xbase = wbase + NW * kWBox64;
+                    const uint32_t wbase = smem_u32(smem + s * kStage), xbase = wbase + NW * kW;
 #pragma unroll
                     for (int q = 0; q < NW; ++q)
 #pragma unroll
                         for (int g = 0; g < G; ++g)
 #pragma unroll
-                            for (int k = 0; k < kKC / 16; ++k) {
-                                const uint64_t ad = desc_sw128(xbase + (q + 2 * g) * kBPix + k * 16 * 128, kBPix, 1024);
-                                const uint64_t bd = desc_sw128(wbase + q * kWBox64 + k * 32, 16, 1024);
+                            for (int k = 0; k < KC / 16; ++k) {
+                                const uint64_t ad = desc_sw128(xbase + (q + 2 * g) * kX + k * 16 * 128, kX, 1024);
+                                const uint64_t bd = KC == 16 ? desc_sw128(wbase + q * kW, kW, 1024)
+                                                             : desc_sw128(wbase + q * kW + k * 32, 16, 1024);
                                 umma_f16(tmem + ab * (G * 64) + g * 64, ad, bd, idesc, (i > 0 || q > 0 || k > 0) ? 1u : 0u);
                             }
                     umma_commit(&empty[s]);
@@ -831,18 +847,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_dts(const __grid_constant__ Dtc
     }
 }
 
-template <int TWP, bool WIN>
+template <int TWP, bool WIN, int KC = 64>
 cudaError_t launch_dts(const DtcArgs &a, int tiles, cudaStream_t st) {
     static std::atomic<uint64_t> attr{0};
-    constexpr int smem = dts_smem<TWP, WIN>();
+    constexpr int smem = dts_smem<TWP, WIN, KC>();
     static_assert(smem <= 227 * 1024 - 1024, "k_dts shared memory");
-    cudaError_t e = ensure_smem_attr(k_dts<TWP, WIN>, attr, smem);
+    cudaError_t e = ensure_smem_attr(k_dts<TWP, WIN, KC>, attr, smem);
     if (e != cudaSuccess) return e;
     int dev = 0;
     cudaGetDevice(&dev);
     int sms = usc_device_sm_count(dev);
     if (sms <= 0) sms = 148;
-    return launch_pdl(k_dts<TWP, WIN>, dim3((unsigned)(tiles < sms ? tiles : sms)), dim3(kThreads), smem, st, a);
+    return launch_pdl(k_dts<TWP, WIN, KC>, dim3((unsigned)(tiles < sms ? tiles : sms)), dim3(kThreads), smem, st, a);
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_tiled() {
@@ -896,7 +912,8 @@ DtcShape dtc_shape(const usc_geometry *g, int n, const usc_act_layout *xl, bool 
     if (req_twp == 2 || req_twp == 4) d.twp = req_twp;
     d.x_tiles = (d.Yw + d.twp - 1) / d.twp;
     d.tiles = (long long)d.m_blocks * d.x_tiles * d.Yh * d.NB;
-    d.kiters = (win ? K : K * K) * (g->in_channels / kKC);
+    // (a first layer with < 64 input channels runs one 16-channel chunk)
+    d.kiters = (win ? K : K * K) * std::max(1, g->in_channels / kKC);
     // split-K when the tiles fill at most half the SMs (small maps): each split >= 4 k-iterations
     d.splits = 1;
     if (!res && d.tiles > 0 && d.tiles * 2 <= sms) {
@@ -943,8 +960,12 @@ int dense_conv_impl(const usc_geometry *g, int32_t n, const void *w_dev, const u
     if (g->filter_h != g->filter_w || (g->filter_h != 1 && g->filter_h != 3) || g->stride_h != g->stride_w ||
         (g->stride_h != 1 && g->stride_h != 2))
         return usc::fail(USC_ERR_UNSUPPORTED, "dense conv: 1x1 / 3x3 filters, stride 1 or 2");
-    if (g->in_channels % kKC || g->out_channels % 64)
-        return usc::fail(USC_ERR_UNSUPPORTED, "dense conv: channels in %% 64 and out %% 64 needed");
+    // first-layer form: <= 16 input channels (zero-filled to 16), 3x3 stride 1, 64 outputs
+    const bool first = g->in_channels < kKC && g->in_channels <= 16 && g->filter_h == 3 && g->stride_h == 1 &&
+                       g->out_channels == 64 && !res && !pool;
+    if ((g->in_channels % kKC && !first) || g->out_channels % 64)
+        return usc::fail(USC_ERR_UNSUPPORTED,
+                         "dense conv: channels in %% 64 (or <= 16 for a 3x3 stride-1 64-channel first layer) and out %% 64");
     if (xl->interleave != 64 || yl->interleave != 64 || (res && (!rl || rl->interleave != 64)))
         return usc::fail(USC_ERR_UNSUPPORTED, "dense conv: BI64 layouts only");
     const int s = g->stride_h, K = g->filter_h, pad = K / 2;
@@ -964,7 +985,7 @@ int dense_conv_impl(const usc_geometry *g, int32_t n, const void *w_dev, const u
         const cuuint64_t dims[5] = {64, (cuuint64_t)xl->ws, (cuuint64_t)xl->hp, (cuuint64_t)xl->channels, (cuuint64_t)NB};
         const cuuint64_t strides[4] = {128, (cuuint64_t)xl->ws * 128, (cuuint64_t)xl->ws * xl->hp * 128,
                                        (cuuint64_t)xl->sample_stride * 2};
-        const cuuint32_t box[5] = {64, 1, 1, (cuuint32_t)kKC, 1};
+        const cuuint32_t box[5] = {64, 1, 1, (cuuint32_t)(first ? 16 : kKC), 1};  // first layer: OOB channels read 0
         const cuuint32_t es[5] = {1, 1, 1, 1, 1};
         CUresult r = enc(&a.xmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 5, const_cast<void *>(x), dims, strides, box, es,
                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -973,7 +994,7 @@ int dense_conv_impl(const usc_geometry *g, int32_t n, const void *w_dev, const u
     }
     const int taps = K * K, Kd = taps * g->in_channels;
     const int Dpad = (g->out_channels + 127) / 128 * 128;  // the packed weights carry zero rows up to 128k
-    {   // weights: [Dpad][taps*C] binary16 K-major, box [64 k][128 d]
+    if (!first) {  // weights: [Dpad][taps*C] binary16 K-major, box [64 k][128 d]
         const cuuint64_t dims[2] = {(cuuint64_t)Kd, (cuuint64_t)Dpad};
         const cuuint64_t strides[1] = {(cuuint64_t)Kd * 2};
         const cuuint32_t box[2] = {(cuuint32_t)kKC, 128};
@@ -1020,6 +1041,7 @@ int dense_conv_impl(const usc_geometry *g, int32_t n, const void *w_dev, const u
     if (cudaGetDevice(&dev) == cudaSuccess && usc_device_sm_count(dev) > 0) sms = usc_device_sm_count(dev);
     const bool win = K == 3 && s == 1 && !res;  // the 3-tap row window (stride 1; no shortcut staging room)
     DtcShape d = dtc_shape(g, n, xl, res != nullptr, win, sms, req_twp, req_splits);
+    if (first) d.splits = 1, d.kper = d.kiters;  // the first-layer form has no split-K
     if (pool) {  // 4-pixel window tiles in row pairs, no split
         if (res || !relu || !dtc_pool_ok(g, n, xl, sms))
             return usc::fail(USC_ERR_UNSUPPORTED, "dense conv: fused pool not available for this shape");
@@ -1044,13 +1066,24 @@ int dense_conv_impl(const usc_geometry *g, int32_t n, const void *w_dev, const u
     }
     const long long tiles = d.tiles * d.splits;  // work items
     cudaError_t e;
-    if (g->out_channels == 64 && !res && !pool && d.splits == 1 && dts_enabled()) {
+    if (first) {  // [taps][16 k][64 d] MN-major weights, one 2-KB tile per tap; one 16-channel chunk
+        a.cb = 1;
+        const cuuint64_t wdims[2] = {64, (cuuint64_t)(taps * 16)};
+        const cuuint64_t wstrides[1] = {128};
+        const cuuint32_t wbox[2] = {64, 16};
+        const cuuint32_t es2[2] = {1, 1};
+        if (enc(&a.wmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void *>(w_dev), wdims, wstrides, wbox, es2,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return usc::fail(USC_ERR_CUDA, "dense conv: first-layer weight tensor map");
+    }
+    if (g->out_channels == 64 && !res && !pool && d.splits == 1 && (dts_enabled() || first)) {
         // 64 output channels: swapped operands (k_dts), N = 64 channels, no zero weight rows
         const cuuint64_t wdims[2] = {(cuuint64_t)(taps * g->in_channels), (cuuint64_t)64};
         const cuuint64_t wstrides[1] = {(cuuint64_t)(taps * g->in_channels) * 2};
         const cuuint32_t wbox[2] = {(cuuint32_t)kKC, 64};
         const cuuint32_t es2[2] = {1, 1};
-        if (enc(&a.wmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void *>(w_dev), wdims, wstrides, wbox, es2,
+        if (!first && enc(&a.wmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void *>(w_dev), wdims, wstrides, wbox, es2,
                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
             return usc::fail(USC_ERR_CUDA, "dense conv: weight tensor map (64 rows)");
@@ -1064,7 +1097,9 @@ int dense_conv_impl(const usc_geometry *g, int32_t n, const void *w_dev, const u
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
             return usc::fail(USC_ERR_CUDA, "dense conv: output tensor map (64 channels)");
         const long long ntiles = (long long)a.x_tiles * Yh * NB;
-        if (twp == 4)
+        if (first)
+            e = twp == 4 ? launch_dts<4, true, 16>(a, (int)ntiles, st) : launch_dts<2, true, 16>(a, (int)ntiles, st);
+        else if (twp == 4)
             e = win ? launch_dts<4, true>(a, (int)ntiles, st) : launch_dts<4, false>(a, (int)ntiles, st);
         else
             e = win ? launch_dts<2, true>(a, (int)ntiles, st) : launch_dts<2, false>(a, (int)ntiles, st);

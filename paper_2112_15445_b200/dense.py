@@ -17,18 +17,26 @@ from . import _lib
 
 
 def tc_eligible(in_channels: int, out_channels: int, k: int, stride: int) -> bool:
-    """Shapes the tensor-core kernel takes."""
+    """Shapes the tensor-core kernel takes: channels in % 64 (1x1 / 3x3, stride 1 / 2), or the
+    first-layer form (<= 16 input channels, 3x3 stride 1, 64 outputs)."""
+    if in_channels <= 16 and in_channels % 64:
+        return out_channels == 64 and k == 3 and stride == 1
     return in_channels % 64 == 0 and out_channels % 64 == 0 and k in (1, 3) and stride in (1, 2)
 
 
 def pack_weights(w, device=None):
     """Dense (D, C, K, K) weights -> the kernel's binary16 [D][K*K][C] (K-major) tensor, zero
-    rows appended up to a multiple of 128 output channels (the MMA's M)."""
+    rows appended up to a multiple of 128 output channels (the MMA's M); a first layer with
+    <= 16 input channels packs as [K*K][16][D] (channels zero-padded, D contiguous)."""
     import torch
     t = w if type(w).__module__.startswith("torch") else torch.from_numpy(
         np.array(w.data if hasattr(w, "data") else w, dtype=np.float32))
     t = t.to(device or "cuda", torch.float16)
     D, C, kh, kw = t.shape
+    if C <= 16 and C % 64:  # first-layer form: [taps][16 channels (zero-padded)][D], D contiguous
+        packed = t.new_zeros((kh * kw, 16, D))
+        packed[:, :C, :] = t.permute(2, 3, 1, 0).reshape(kh * kw, C, D)
+        return packed.reshape(kh * kw * 16, D).contiguous()
     packed = t.permute(0, 2, 3, 1).reshape(D, kh * kw * C)
     dpad = -(-D // 128) * 128
     if dpad != D:

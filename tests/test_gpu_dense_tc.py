@@ -14,7 +14,9 @@ pytestmark = pytest.mark.gpu
                                               (256, 512, 1, 1, 4, 256, True), (64, 64, 3, 1, 32, 96, False),
                                               (64, 64, 1, 1, 32, 64, True), (256, 64, 1, 1, 8, 64, False),
                                               (128, 64, 3, 2, 16, 64, False), (64, 64, 3, 1, 7, 64, False),
-                                              (64, 64, 3, 1, 32, 256, False), (256, 64, 1, 1, 32, 128, False)])
+                                              (64, 64, 3, 1, 32, 256, False), (256, 64, 1, 1, 32, 128, False),
+                                              (3, 64, 3, 1, 32, 256, False), (3, 64, 3, 1, 6, 70, False),
+                                              (16, 64, 3, 1, 8, 64, False), (5, 64, 3, 1, 7, 64, False)])
 def test_dense_tc_matches_torch(C, D, k, s, hw, n, res):
     import torch
     from paper_2112_15445_b200 import _lib

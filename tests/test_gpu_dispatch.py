@@ -165,7 +165,7 @@ def test_autotune_backends_picks_and_runs():
     m = SparseResNet50(ws, 64, precision=F16)
     ref = m.forward(x).float().cpu().numpy()
     picks = m.autotune_backends(repeats=3, warmup=1)
-    assert set(picks) <= {"sparse", "dense", "tc"} and picks[0] == "sparse"
+    assert set(picks) <= {"sparse", "dense", "tc"} and picks[0] in ("sparse", "tc")  # the 3-channel stem: no cuDNN form
     assert set(m.backend_times) and m.tuned_state()["backends"] == picks
     ok, err = _close(m.forward(x).float().cpu().numpy(), ref)
     assert ok, err

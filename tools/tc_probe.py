@@ -29,7 +29,7 @@ def main():
               ("r50-3x3-128x128-16", 128, 128, 3, 1, 16), ("r50-1x1-512x256-16", 512, 256, 1, 1, 16),
               ("r50-3x3-256x256-8", 256, 256, 3, 1, 8), ("r50-1x1-1024x256-8", 1024, 256, 1, 1, 8),
               ("r50-3x3-128x128-32-s2", 128, 128, 3, 2, 32), ("r50-1x1-256x512-32-s2", 256, 512, 1, 2, 32),
-              ("vgg-64x64-32", 64, 64, 3, 1, 32), ("r50-1x1-256x64-32", 256, 64, 1, 1, 32),
+              ("vgg-3x64-32-first", 3, 64, 3, 1, 32), ("vgg-64x64-32", 64, 64, 3, 1, 32), ("r50-1x1-256x64-32", 256, 64, 1, 1, 32),
               ("r50-1x1-64x64-32", 64, 64, 1, 1, 32),
               ("r50-1x1-64x256-32-res", 64, 256, 1, 1, 32), ("r50-1x1-128x512-16-res", 128, 512, 1, 1, 16),
               ("r50-1x1-256x1024-8-res", 256, 1024, 1, 1, 8), ("r50-1x1-512x2048-4-res", 512, 2048, 1, 1, 4)]
