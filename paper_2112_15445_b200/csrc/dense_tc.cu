@@ -58,6 +58,7 @@ struct DtcArgs {
     int splits, kper;  // split-K: work item = (tile, split), split s runs k-iterations [s*kper, (s+1)*kper)
     float *part;       // split-K partial sums [tile][split][N columns][128 rows] fp32
     int *cnt;          // split-K arrival counter per tile (zero between launches)
+    int xrow;          // window kernels: xmap is (s, c, x, y, nb) and one box covers the row window
     int pool;          // fused 2x2 max-pool (window kernel, 4-pixel tiles): a CTA runs the two
                        // output rows of a pool window back to back; y is the pooled layout
 };
@@ -280,9 +281,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_dtc(const __grid_constant__ Dtc
         auto load_b = [&](unsigned char *st, uint64_t *bar, int i, int xt, int yo, int nb) {  // activation boxes
             if constexpr (WIN) {
                 const int kh = i / a.cb, cb = i - kh * a.cb;
-                if (lane >= 3 && lane < 3 + NBX)
+                if (a.xrow) {
+                    if (lane == 3)
+                        tma_load_5d(st + NA * kABytes, &a.xmap, 0, cb * kKC, xt * TWP + a.offw, yo + kh + a.offh, nb, bar);
+                } else if (lane >= 3 && lane < 3 + NBX) {
                     tma_load_5d(st + NA * kABytes + (lane - 3) * kBPix, &a.xmap, 0, xt * TWP + (lane - 3) + a.offw,
                                 yo + kh + a.offh, cb * kKC, nb, bar);
+                }
             } else {
                 const int tap = i / a.cb, cb = i - tap * a.cb;
                 const int kh = tap / a.Kw, kw = tap - kh * a.Kw;
@@ -696,9 +701,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_dts(const __grid_constant__ Dtc
         auto load_x = [&](unsigned char *st, uint64_t *bar, int i, int xt, int yo, int nb) {
             if constexpr (WIN) {
                 const int kh = i / a.cb, cb = i - kh * a.cb;
-                if (lane >= 3 && lane < 3 + NBX)
+                if (a.xrow) {
+                    if (lane == 3)
+                        tma_load_5d(st + NW * kW, &a.xmap, 0, cb * KC, xt * TWP + a.offw, yo + kh + a.offh, nb, bar);
+                } else if (lane >= 3 && lane < 3 + NBX) {
                     tma_load_5d(st + NW * kW + (lane - 3) * kX, &a.xmap, 0, xt * TWP + (lane - 3) + a.offw,
                                 yo + kh + a.offh, cb * KC, nb, bar);
+                }
             } else {
                 const int tap = i / a.cb, cb = i - tap * a.cb;
                 const int kh = tap / a.Kw, kw = tap - kh * a.Kw;
@@ -883,6 +892,14 @@ extern "C" int usc_dtc_trace_read(unsigned long long *out, int ctas) {
 
 namespace {
 
+bool xrow_enabled() {  // USC_NO_XROW=1: one TMA box per pixel in the window kernels (A/B measurements)
+    static const bool on = [] {
+        const char *v = std::getenv("USC_NO_XROW");
+        return !(v && *v && *v != '0');
+    }();
+    return on;
+}
+
 bool dts_enabled() {  // USC_NO_DTS=1: 64-channel layers on k_dtc (A/B measurements)
     static const bool on = [] {
         const char *v = std::getenv("USC_NO_DTS");
@@ -1054,6 +1071,18 @@ int dense_conv_impl(const usc_geometry *g, int32_t n, const void *w_dev, const u
     }
     const int twp = d.twp;
     a.x_tiles = d.x_tiles;
+    if (win && xrow_enabled()) {  // one TMA box per row window: the map re-ordered as (s, c, x, y, nb)
+        const cuuint64_t dims[5] = {64, (cuuint64_t)xl->channels, (cuuint64_t)xl->ws, (cuuint64_t)xl->hp, (cuuint64_t)NB};
+        const cuuint64_t strides[4] = {(cuuint64_t)xl->ws * xl->hp * 128, 128, (cuuint64_t)xl->ws * 128,
+                                       (cuuint64_t)xl->sample_stride * 2};
+        const cuuint32_t box[5] = {64, (cuuint32_t)(first ? 16 : kKC), (cuuint32_t)(twp + 2), 1, 1};
+        const cuuint32_t es[5] = {1, 1, 1, 1, 1};
+        if (enc(&a.xmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 5, const_cast<void *>(x), dims, strides, box, es,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return usc::fail(USC_ERR_CUDA, "dense conv: row-window activation tensor map");
+        a.xrow = 1;
+    }
     if (d.tiles * d.splits > 0x7fffffffLL) return usc::fail(USC_ERR_UNSUPPORTED, "dense conv: grid too large");
     const size_t need = dtc_ws_bytes(d);
     if (need == 0 || !workspace || ws_bytes < need) d.splits = 1, d.kper = d.kiters;  // no workspace: no split
