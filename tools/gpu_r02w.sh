@@ -17,4 +17,4 @@ rm -f gpurun_out/$tag.ncu-rep
 timeout 2400 python tools/bench_variants.py --steps 30 > gpurun_out/variants.jsonl 2> gpurun_out/variants.err
 cat gpurun_out/pytest_gpu.txt gpurun_out/smoke.txt; cut -c1-300 gpurun_out/bench.json; echo; cut -c1-300 gpurun_out/bench_ref.json; echo
 head -12 gpurun_out/r02_launches.md; head -12 gpurun_out/r02_ncu_$tag.md
-cut -c1-250 gpurun_out/variants.jsonl | head -8; tail -3 gpurun_out/variants.err gpurun_out/bench.err
+cut -c1-250 gpurun_out/variants.jsonl | head -8; tail -n 3 gpurun_out/variants.err; tail -n 3 gpurun_out/bench.err
