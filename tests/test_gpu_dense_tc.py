@@ -93,7 +93,8 @@ def test_dense_tc_saturates(res, relu):
     assert err <= 1e-2 * 65504, err
 
 
-@pytest.mark.parametrize("C,D,hw,n", [(512, 512, 2, 256), (512, 512, 2, 64), (256, 512, 4, 64), (256, 128, 2, 128)])
+@pytest.mark.parametrize("C,D,hw,n", [(512, 512, 2, 256), (512, 512, 2, 64), (256, 512, 4, 64), (256, 128, 2, 128),
+                                     (512, 512, 2, 70)])
 def test_dense_tc_split_k(C, D, hw, n):
     """Small maps split K over CTAs (workspace path): the result matches torch within the
     fp16 tolerance, and repeated launches are bitwise identical (splits summed in a fixed
@@ -134,7 +135,8 @@ def test_dense_tc_split_k(C, D, hw, n):
     assert float((out.float() - outs[0].float()).abs().max()) <= 1e-2 * float(ref.abs().max())
 
 
-@pytest.mark.parametrize("C,D,hw,n,ph", [(64, 64, 32, 256, 1), (128, 128, 16, 256, 0), (64, 128, 32, 192, 1)])
+@pytest.mark.parametrize("C,D,hw,n,ph", [(64, 64, 32, 256, 1), (128, 128, 16, 256, 0), (64, 128, 32, 192, 1),
+                                        (64, 64, 32, 70, 1)])
 def test_dense_tc_fused_pool(C, D, hw, n, ph):
     """conv + ReLU + 2x2 max-pool in one tensor-core launch (row-pair tiles, pooled in the
     epilogue) against torch within the fp16 tolerance, and equal to the unfused conv +
