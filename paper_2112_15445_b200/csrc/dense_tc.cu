@@ -651,6 +651,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_dts(const __grid_constant__ Dtc
     const int tiles = a.x_tiles * a.Yh * a.NB;
     const int kiters = WIN ? a.Kh * a.cb : a.k_iters;
     if (threadIdx.x == 0) {
+        DTC_STAMP(0);
         for (int s = 0; s < S; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
@@ -670,6 +671,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_dts(const __grid_constant__ Dtc
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = *tmem_slot;
+    if (threadIdx.x == 0) DTC_STAMP(1);
     if (threadIdx.x == 0) {
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&a.xmap)) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&a.wmap)) : "memory");
@@ -756,6 +758,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_dts(const __grid_constant__ Dtc
                 const int s = it % S;
                 mbar_wait_bounded(&full[s], (it / S) & 1);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                if (lane == 0 && it == 0) DTC_STAMP(2);
                 if (lane == 0) {
                     const uint32_t wbase = smem_u32(smem + s * kStage), xbase = wbase + NW * kW;
 #pragma unroll
@@ -771,6 +774,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_dts(const __grid_constant__ Dtc
                             }
                     umma_commit(&empty[s]);
                     if (i == kiters - 1) umma_commit(&tfull[ab]);
+                    if (i == kiters - 1 && (lt == 0 || lt == 6)) DTC_STAMP(3 + (lt != 0));
                 }
                 __syncwarp();
             }
@@ -789,6 +793,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_dts(const __grid_constant__ Dtc
             const int ab = lt & 1;
             mbar_wait_bounded(&tfull[ab], (lt >> 1) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            if (warp == 0 && lane == 0 && (lt == 0 || lt == 6)) DTC_STAMP(5 + (lt != 0));
             uint32_t v[64];
             if (active) {
                 const uint32_t taddr = tmem + ab * (G * 64) + g * 64 + ((uint32_t)(qd * 32) << 16);
@@ -847,6 +852,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_dts(const __grid_constant__ Dtc
             }
         }
         if (lane == 0) bulk_wait_all();
+        if (warp == 0 && lane == 0) DTC_STAMP(7);
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();

@@ -27,9 +27,10 @@ int main(int argc, char **argv) {
     cudaMalloc(&x, xe * 2);
     cudaMalloc(&y, ye * 2);
     const int Dp = (D + 127) / 128 * 128;
-    cudaMalloc(&w, (size_t)Dp * K * K * C * 2);
+    const size_t wbytes = std::max((size_t)Dp * K * K * C * 2, (size_t)9 * 16 * 64 * 2);  // (first-layer packing)
+    cudaMalloc(&w, wbytes);
     cudaMemset(x, 0, xe * 2);
-    cudaMemset(w, 0, (size_t)Dp * K * K * C * 2);
+    cudaMemset(w, 0, wbytes);
     cudaEvent_t a, b;
     cudaEventCreate(&a);
     cudaEventCreate(&b);
@@ -45,7 +46,7 @@ int main(int argc, char **argv) {
     unsigned long long t0 = ~0ull;
     for (int c = 0; c < 148; ++c) t0 = std::min(t0, t[c * 8]);
     printf("C %d D %d K %d s %d hw %d rc %d event_us %.1f\n", C, D, K, s, hw, rc, ms * 1e3);
-    printf("cta   entry  setup  land0  mma0  mma1  acc0  acc1  drained (us from first entry)\n");
+    printf("cta   entry  setup  land0  mma0  mma1  acc0  acc1  drained (us from first entry; k_dtc: tiles 0/1, k_dts: tiles 0/6)\n");
     double sum[8] = {0};
     int cnt[8] = {0};
     for (int c = 0; c < 148; ++c) {
