@@ -876,6 +876,274 @@ cudaError_t launch_dts(const DtcArgs &a, int tiles, cudaStream_t st) {
     return launch_pdl(k_dts<TWP, WIN, KC>, dim3((unsigned)(tiles < sms ? tiles : sms)), dim3(kThreads), smem, st, a);
 }
 
+// ---------------------------------------------------------------------------------------
+// k_dtc2: the 3x3 stride-1 window tile on a CTA pair (cta_group::2, cluster of 2 on one TPC).
+// The pair computes M = 256 output channels x N = 4 pixels x 64 samples: each CTA stages
+// its 128 weight rows (A) and the row window of ITS two pixels (+ the 2-pixel halo, 4 boxes:
+// half of B); the leader's single thread issues tcgen05.mma.cta_group::2, which reads A and
+// B from both CTAs' shared memory at the same offsets.  Each SM thus reads half of B per MMA
+// (the shared-memory port bound of k_dtc's window tiles).  Every TMA of
+// both CTAs completes on the LEADER's full barrier (.cta_group::2, peer bit cleared); the
+// leader's commits multicast to both CTAs' empty / tfull barriers; both CTAs' epilogue warps
+// release the accumulator on the leader's tempty barrier.  Each CTA's TMEM holds its 128
+// channels for all 4 pixels; the epilogue is k_dtc's.
+constexpr uint32_t kPeerMask = 0xFEFFFFFFu;  // shared::cluster address of the leader's copy
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tma2_load_2d(void *dst, const CUtensorMap *map, int c0, int c1, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+        "[%4];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar) & kPeerMask)
+        : "memory");
+}
+__device__ __forceinline__ void tma2_load_5d(void *dst, const CUtensorMap *map, int c0, int c1, int c2, int c3, int c4,
+                                             uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.5d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(smem_u32(bar) & kPeerMask)
+        : "memory");
+}
+__device__ __forceinline__ void umma2_f16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                          uint32_t accumulate) {
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void umma2_commit_both(uint64_t *bar) {  // arrive on the barrier in both CTAs
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_u32(bar)),
+        "h"((uint16_t)3)
+        : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_leader(uint64_t *bar) {  // arrive on the leader CTA's copy
+    uint32_t remote;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(remote) : "r"(smem_u32(bar)));
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+}
+
+constexpr int kCg2Stage = 3 * kABytes + 4 * kBPix;  // 3 taps of own A rows + own half window (80 KB)
+constexpr int kCg2S = 2;
+constexpr int cg2_smem() { return kCg2S * kCg2Stage + kEW * kOS * kWarpBox + 1024 + 256; }
+
+__global__ void __launch_bounds__(kThreads, 1) k_dtc2(const __grid_constant__ DtcArgs a) {
+    constexpr int TWP = 4, N = 256, S = kCg2S, kStage = kCg2Stage;
+    constexpr uint32_t kCols = 2 * N;
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char *smem = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    unsigned char *ostage = smem + S * kStage;
+    uint64_t *full = reinterpret_cast<uint64_t *>(ostage + kEW * kOS * kWarpBox);
+    uint64_t *empty = full + S;
+    uint64_t *tfull = empty + S;
+    uint64_t *tempty = tfull + 2;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_rank();
+    const bool leader = rank == 0;
+    const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+    const int tiles = a.m_blocks * a.x_tiles * a.Yh * a.NB;  // m_blocks: 256-channel blocks
+    const int kiters = a.Kh * a.cb;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < S; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&tfull[b], 1);
+            mbar_init(&tempty[b], 2 * kEW);  // both CTAs' epilogue warps (the leader's copy counts)
+        }
+        fence_mbar_init();
+    }
+    if (warp == kEW) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "n"(kCols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    cluster_sync_all();  // barriers of both CTAs initialised before any cross-CTA signal
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = *tmem_slot;
+    if (threadIdx.x == 0) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&a.xmap)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&a.wmap)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&a.ymap)) : "memory");
+    }
+    pdl_release();
+    pdl_wait();
+
+    auto decode = [&](int t, int &mb, int &xt, int &yo, int &nb) {
+        mb = t % a.m_blocks;
+        t /= a.m_blocks;
+        xt = t % a.x_tiles;
+        t /= a.x_tiles;
+        yo = t % a.Yh;
+        nb = t / a.Yh;
+    };
+
+    if (warp == kEW) {
+        // ---------------- TMA producer (both CTAs): own A rows + own half window ----------------
+        int it = 0;
+        for (int t = pair; t < tiles; t += npairs) {
+            int mb, xt, yo, nb;
+            decode(t, mb, xt, yo, nb);
+            for (int i = 0; i < kiters; ++i, ++it) {
+                const int s = it % S;
+                if (it >= S) mbar_wait_bounded(&empty[s], ((it / S) - 1) & 1);
+                unsigned char *st = smem + s * kStage;
+                if (leader && lane == 0) mbar_expect_tx(&full[s], 2 * kStage);  // both CTAs' bytes
+                __syncwarp();
+                const int kh = i / a.cb, cb = i - kh * a.cb;
+                if (lane < 3)
+                    tma2_load_2d(st + lane * kABytes, &a.wmap, (kh * 3 + lane) * a.C + cb * kKC, mb * 256 + rank * 128,
+                                 &full[s]);
+                else if (lane == 3)  // own half window: pixels 2 rank .. 2 rank + 3 of the tile's 6 (map (s, c, x, y, nb))
+                    tma2_load_5d(st + 3 * kABytes, &a.xmap, 0, cb * kKC, xt * TWP + rank * 2 + a.offw, yo + kh + a.offh,
+                                 nb, &full[s]);
+            }
+        }
+    } else if (warp == kEW + 1) {
+        // ---------------- MMA issuer (leader only) ----------------
+        if (leader) {
+            const uint32_t idesc = (1u << 4) | (1u << 16) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
+            int it = 0, lt = 0;
+            for (int t = pair; t < tiles; t += npairs, ++lt) {
+                const int ab = lt & 1;
+                if (lt >= 2) mbar_wait_bounded(&tempty[ab], ((lt >> 1) - 1) & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const uint32_t acc = tmem + ab * N;
+                for (int i = 0; i < kiters; ++i, ++it) {
+                    const int s = it % S;
+                    mbar_wait_bounded(&full[s], (it / S) & 1);
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    if (lane == 0) {
+                        const uint32_t abase = smem_u32(smem + s * kStage), bbase = abase + 3 * kABytes;
+#pragma unroll
+                        for (int q = 0; q < 3; ++q)
+#pragma unroll
+                            for (int k = 0; k < kKC / 16; ++k) {
+                                const uint64_t ad = desc_sw128(abase + q * kABytes + k * 32, 16, 1024);
+                                const uint64_t bd = desc_sw128(bbase + q * kBPix + k * 16 * 128, kBPix, 1024);
+                                umma2_f16(acc, ad, bd, idesc, (i > 0 || q > 0 || k > 0) ? 1u : 0u);
+                            }
+                        umma2_commit_both(&empty[s]);
+                        if (i == kiters - 1) umma2_commit_both(&tfull[ab]);
+                    }
+                    __syncwarp();
+                }
+            }
+        }
+    } else {
+        // ---------------- epilogue (both CTAs): own 128 channels, 4 pixels ----------------
+        const int ch0 = (warp & 3) * 32, half = warp >> 2;
+        unsigned char *ost = ostage + warp * kOS * kWarpBox;
+        int lt = 0, q = 0;
+        for (int t = pair; t < tiles; t += npairs, ++lt) {
+            int mb, xt, yo, nb;
+            decode(t, mb, xt, yo, nb);
+            const int ab = lt & 1;
+            mbar_wait_bounded(&tfull[ab], (lt >> 1) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint32_t taddr = tmem + ab * N + ((uint32_t)(ch0) << 16);
+            const int cbase = mb * 256 + (int)rank * 128 + ch0;
+#pragma unroll 1
+            for (int px = half; px < TWP; px += 2, ++q) {
+                uint32_t v[64];
+                asm volatile(
+                    "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, "
+                    "%13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, "
+                    "[%32];"
+                    : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                      "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
+                      "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
+                      "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
+                      "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+                    : "r"(taddr + px * 64));
+                asm volatile(
+                    "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, "
+                    "%13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, "
+                    "[%32];"
+                    : "=r"(v[32]), "=r"(v[33]), "=r"(v[34]), "=r"(v[35]), "=r"(v[36]), "=r"(v[37]), "=r"(v[38]),
+                      "=r"(v[39]), "=r"(v[40]), "=r"(v[41]), "=r"(v[42]), "=r"(v[43]), "=r"(v[44]), "=r"(v[45]),
+                      "=r"(v[46]), "=r"(v[47]), "=r"(v[48]), "=r"(v[49]), "=r"(v[50]), "=r"(v[51]), "=r"(v[52]),
+                      "=r"(v[53]), "=r"(v[54]), "=r"(v[55]), "=r"(v[56]), "=r"(v[57]), "=r"(v[58]), "=r"(v[59]),
+                      "=r"(v[60]), "=r"(v[61]), "=r"(v[62]), "=r"(v[63])
+                    : "r"(taddr + px * 64 + 32));
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                if (px + 2 >= TWP) {
+                    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive_leader(&tempty[ab]);
+                }
+                uint32_t h[32];
+#pragma unroll
+                for (int k = 0; k < 32; ++k) {
+                    h[k] = cvt_f16x2_sat(__uint_as_float(v[2 * k]), __uint_as_float(v[2 * k + 1]));
+                    if (a.relu) h[k] = relu_f16x2(h[k]);
+                }
+                unsigned char *obox = ost + (q % kOS) * kWarpBox;
+                if (lane == 0) bulk_wait_read<kOS - 1>();
+                __syncwarp();
+                unsigned char *orow = obox + lane * 128;
+#pragma unroll
+                for (int c = 0; c < 8; ++c)
+                    *reinterpret_cast<uint4 *>(orow + ((c ^ (lane & 7)) << 4)) =
+                        make_uint4(h[4 * c], h[4 * c + 1], h[4 * c + 2], h[4 * c + 3]);
+                fence_proxy_async();
+                __syncwarp();
+                const int xo = xt * TWP + px;
+                if (lane == 0 && cbase < a.D && xo < a.Yw)
+                    tma_store_5d(&a.ymap, obox, 0, xo + a.Lo.pw, yo + a.Lo.ph, cbase, nb);
+            }
+        }
+        if (lane == 0) bulk_wait_all();
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    cluster_sync_all();  // both CTAs done with the pair's tensor memory and barriers
+    if (warp == kEW) {
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kCols));
+    }
+}
+
+cudaError_t launch_dtc2(const DtcArgs &a, int pair_tiles, cudaStream_t st) {
+    static std::atomic<uint64_t> attr{0};
+    constexpr int smem = cg2_smem();
+    static_assert(smem <= 227 * 1024 - 1024, "k_dtc2 shared memory");
+    cudaError_t e = ensure_smem_attr(k_dtc2, attr, smem);
+    if (e != cudaSuccess) return e;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int sms = usc_device_sm_count(dev);
+    if (sms <= 0) sms = 148;
+    const int pairs = pair_tiles < sms / 2 ? pair_tiles : sms / 2;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(2 * pairs));
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_enabled() ? 2 : 1;
+    return cudaLaunchKernelEx(&cfg, k_dtc2, a);
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 encode_tiled() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
     if (!fn) {
@@ -902,6 +1170,14 @@ bool xrow_enabled() {  // USC_NO_XROW=1: one TMA box per pixel in the window ker
     static const bool on = [] {
         const char *v = std::getenv("USC_NO_XROW");
         return !(v && *v && *v != '0');
+    }();
+    return on;
+}
+
+bool cg2_enabled() {  // USC_CG2=1: 3x3 window tiles of >= 256-channel layers on CTA pairs (opt-in while measured)
+    static const bool on = [] {
+        const char *v = std::getenv("USC_CG2");
+        return v && *v && *v != '0';
     }();
     return on;
 }
@@ -1101,6 +1377,27 @@ int dense_conv_impl(const usc_geometry *g, int32_t n, const void *w_dev, const u
     }
     const long long tiles = d.tiles * d.splits;  // work items
     cudaError_t e;
+    if (win && !first && !pool && d.splits == 1 && twp == 4 && g->out_channels % 256 == 0 && cg2_enabled()) {
+        // CTA pairs: M = 256 (weights packed to 128 rows suffice: D % 256 == 0), 4-pixel tiles
+        a.m_blocks = g->out_channels / 256;
+        a.x_tiles = Yw / 4 + (Yw % 4 != 0);
+        {  // activations as (s, c, x, y, nb), one box = a CTA's 4-pixel half window
+            const cuuint64_t dims[5] = {64, (cuuint64_t)xl->channels, (cuuint64_t)xl->ws, (cuuint64_t)xl->hp,
+                                        (cuuint64_t)NB};
+            const cuuint64_t strides[4] = {(cuuint64_t)xl->ws * xl->hp * 128, 128, (cuuint64_t)xl->ws * 128,
+                                           (cuuint64_t)xl->sample_stride * 2};
+            const cuuint32_t box[5] = {64, (cuuint32_t)kKC, 4, 1, 1};
+            const cuuint32_t es[5] = {1, 1, 1, 1, 1};
+            if (enc(&a.xmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 5, const_cast<void *>(x), dims, strides, box, es,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+                return usc::fail(USC_ERR_CUDA, "dense conv: pair-window activation tensor map");
+        }
+        const long long pair_tiles = (long long)a.m_blocks * a.x_tiles * Yh * NB;
+        e = launch_dtc2(a, (int)pair_tiles, st);
+        if (e == cudaSuccess) e = cudaGetLastError();
+        return e == cudaSuccess ? USC_OK : usc::fail(USC_ERR_CUDA, "k_dtc2: %s", cudaGetErrorString(e));
+    }
     if (first) {  // [taps][16 k][64 d] MN-major weights, one 2-KB tile per tap; one 16-channel chunk
         a.cb = 1;
         const cuuint64_t wdims[2] = {64, (cuuint64_t)(taps * 16)};
