@@ -324,6 +324,29 @@ def self_check(model, x_np, ws, samples=8):
             "checker": "oracle/oracle.c (C restatement of kernels.py:57-100, pinned to the reference's golden vectors)"}
 
 
+def binary16_leg(steps=20):
+    """BASELINE configs[2] (and the binary16 VGG-16) in the same run: the networks with the
+    committed per-layer dispatch states (profiles/r02_tuned_*_fp16_dispatch.json: sparse /
+    tcgen05 backend per conv, tile configurations) next to all-sparse and cuDNN fp16, batch
+    256, L2 flushed between steps (tools/bench_variants.py, the fp16 tolerance path)."""
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    import bench_variants as bv
+    out = {"note": "binary16 storage, fp32 accumulate; committed dispatch states; timed in this run"}
+    v = bv.vgg16_fp16(steps)
+    out["vgg16"] = {"all_sparse_images_per_s": v["images_per_s"],
+                    "dispatch_images_per_s": v["dispatch"]["images_per_s"],
+                    "cudnn_fp16_images_per_s": v["cudnn_fp16_tensor_core"]["images_per_s"],
+                    "dispatch_vs_cudnn": v["dispatch"]["speedup_vs_cudnn"],
+                    "backends": sorted(set(v["dispatch"]["backends"]))}
+    r = bv.resnet50_network("fp16", steps)
+    out["resnet50"] = {"all_sparse_images_per_s": r["images_per_s"],
+                       "dispatch_images_per_s": r["dispatch"]["images_per_s"],
+                       "cudnn_fp16_images_per_s": r["cudnn"]["images_per_s"],
+                       "dispatch_vs_cudnn": r["dispatch"]["speedup_vs_cudnn"],
+                       "backends": sorted(set(r["dispatch"]["backends"]))}
+    return out
+
+
 def cfg1_leg(device, steps=50, cpu=True):
     """BASELINE configs[0]: one pruned VGG-16 256->256 3x3 layer, 8x8 map, batch 32,
     90% sparsity, fp32 -- the reference's bench_layer comparison (bench.py:98-130):
@@ -439,6 +462,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-cudnn", action="store_true")
     ap.add_argument("--no-cfg1", action="store_true")
+    ap.add_argument("--no-binary16", action="store_true",
+                    help="skip the binary16 VGG-16 / ResNet-50 dispatcher leg (configs[2])")
     ap.add_argument("--dump-configs", default=None, help="write the autotuned per-layer tiles (JSON)")
     ap.add_argument("--configs", default=None, help="per-layer tiles (JSON from --dump-configs); no autotune")
     ap.add_argument("--retune", action="store_true",
@@ -640,6 +665,7 @@ def main():
             cudnn = {"fp32_tf32_off": cudnn_reference(ws, batch, device),
                      "tf32": cudnn_reference(ws, batch, device, tf32=True)}
         cfg1 = None if args.no_cfg1 else cfg1_leg(device, cpu=not args.no_cpu_baseline and world == 1)
+        b16 = None if args.no_binary16 or world > 1 else binary16_leg()
         cpu = None
         if not args.no_cpu_baseline and world == 1:
             import oracle
@@ -674,7 +700,7 @@ def main():
                 "e2e": e2e, "gpu_launches": args.steps * (model.launches_per_forward + 2),
                 "parity": parity,
                 "roofline": roofline, "layers": layers, "cudnn": cudnn, "cpu_baseline": cpu,
-                "cfg1": cfg1, "clocks": clk.summary()}
+                "cfg1": cfg1, "binary16": b16, "clocks": clk.summary()}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
