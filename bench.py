@@ -347,6 +347,21 @@ def binary16_leg(steps=20):
     return out
 
 
+def exact_variants_leg(steps=20):
+    """BASELINE configs[3] (int8 and 4b/16b codebook VGG-16, bit-exact) and the fp32 ResNet-50
+    network vs cuDNN fp32 (TF32 off), committed tiles, in the same run."""
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    import bench_variants as bv
+    out = {"note": "bit-exact sparse kernels; committed tiles; timed in this run"}
+    for mode in ("int8", "cb4"):
+        q = bv.vgg16_quantised(mode, steps)
+        out[f"vgg16_{mode}_images_per_s"] = q["images_per_s"]
+    r = bv.resnet50_network("fp32", steps)
+    out["resnet50_fp32"] = {"images_per_s": r["images_per_s"], "cudnn_fp32_images_per_s": r["cudnn"]["images_per_s"],
+                            "speedup_vs_cudnn": r["speedup_vs_cudnn"]}
+    return out
+
+
 def cfg1_leg(device, steps=50, cpu=True):
     """BASELINE configs[0]: one pruned VGG-16 256->256 3x3 layer, 8x8 map, batch 32,
     90% sparsity, fp32 -- the reference's bench_layer comparison (bench.py:98-130):
@@ -463,7 +478,7 @@ def main():
     ap.add_argument("--no-cudnn", action="store_true")
     ap.add_argument("--no-cfg1", action="store_true")
     ap.add_argument("--no-binary16", action="store_true",
-                    help="skip the binary16 VGG-16 / ResNet-50 dispatcher leg (configs[2])")
+                    help="skip the variant legs (binary16 dispatcher networks, int8 / cb4 VGG-16, fp32 ResNet-50)")
     ap.add_argument("--dump-configs", default=None, help="write the autotuned per-layer tiles (JSON)")
     ap.add_argument("--configs", default=None, help="per-layer tiles (JSON from --dump-configs); no autotune")
     ap.add_argument("--retune", action="store_true",
@@ -666,6 +681,7 @@ def main():
                      "tf32": cudnn_reference(ws, batch, device, tf32=True)}
         cfg1 = None if args.no_cfg1 else cfg1_leg(device, cpu=not args.no_cpu_baseline and world == 1)
         b16 = None if args.no_binary16 or world > 1 else binary16_leg()
+        exact = None if args.no_binary16 or world > 1 else exact_variants_leg()
         cpu = None
         if not args.no_cpu_baseline and world == 1:
             import oracle
@@ -700,7 +716,7 @@ def main():
                 "e2e": e2e, "gpu_launches": args.steps * (model.launches_per_forward + 2),
                 "parity": parity,
                 "roofline": roofline, "layers": layers, "cudnn": cudnn, "cpu_baseline": cpu,
-                "cfg1": cfg1, "binary16": b16, "clocks": clk.summary()}
+                "cfg1": cfg1, "binary16": b16, "exact_variants": exact, "clocks": clk.summary()}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
