@@ -362,6 +362,45 @@ def exact_variants_leg(steps=20):
     return out
 
 
+def sweep_leg(sparsities=(0.9, 0.95, 0.98)):
+    """BASELINE configs[4] at its >= 90% points in the same run: the ResNet-50 layer shapes at
+    batch 1024, fp32, each point's committed tile (profiles/r02_tuned_sweep.json), the launch
+    that writes the resident BI layout, vs cuDNN fp32 (TF32 off); algorithmic HBM GB/s."""
+    import numpy as np
+    import torch
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    import bench_variants as bv
+    from paper_2112_15445_b200 import build_csr
+    from paper_2112_15445_b200.engine import ExecConfig, padded_input, plan_for, time_median_cuda
+    from paper_2112_15445_b200.pruning import synthesize_masked_weights
+    from paper_2112_15445_b200.tensor import ConvGeometry
+    tiles = json.load(open(os.path.join(ROOT, "profiles", "r02_tuned_sweep.json")))
+    batch, out = 1024, []
+    torch.backends.cudnn.benchmark = True
+    torch.backends.cudnn.allow_tf32 = False
+    for name, (c, d, k, hw) in bv.SWEEP_SHAPES.items():
+        g = ConvGeometry(c, d, k, k, hw, hw, padding=(k // 2, k // 2))
+        x = torch.randn(batch, c, hw, hw, device="cuda")
+        for sp in sparsities:
+            key = f"{name}@{sp}"
+            if key not in tiles:
+                continue
+            w = synthesize_masked_weights(g, sp, np.random.default_rng([0, int(sp * 1000)]))
+            f = build_csr(w, g)
+            plan, blob = plan_for(f, batch, 0, ExecConfig(**tiles[key]), f.weights)
+            ms = time_median_cuda(bv._resident_launch(plan, blob, padded_input(x, plan), d, g, batch, torch.float32), 9, 2)
+            wd = torch.from_numpy(np.array(w.data)).cuda()
+            cd = time_median_cuda(lambda: torch.nn.functional.conv2d(x, wd, padding=k // 2), 9, 2)
+            nnz = int(np.count_nonzero(f.weights))
+            nbytes = 4.0 * batch * (c + d) * hw * hw + 8.0 * nnz
+            out.append({"point": key, "us": round(ms * 1e3, 1), "cudnn_fp32_us": round(cd * 1e3, 1),
+                        "speedup_vs_cudnn": round(cd / ms, 3),
+                        "nonzero_tflops": round(2.0 * nnz * hw * hw * batch / (ms / 1e3) / 1e12, 2),
+                        "hbm_frac": round(nbytes / (ms / 1e3) / 1e9 / bv.measured_hbm_peak(), 3)})
+            f._packs.clear()
+    return out
+
+
 def cfg1_leg(device, steps=50, cpu=True):
     """BASELINE configs[0]: one pruned VGG-16 256->256 3x3 layer, 8x8 map, batch 32,
     90% sparsity, fp32 -- the reference's bench_layer comparison (bench.py:98-130):
@@ -478,7 +517,8 @@ def main():
     ap.add_argument("--no-cudnn", action="store_true")
     ap.add_argument("--no-cfg1", action="store_true")
     ap.add_argument("--no-binary16", action="store_true",
-                    help="skip the variant legs (binary16 dispatcher networks, int8 / cb4 VGG-16, fp32 ResNet-50)")
+                    help="skip the variant legs (binary16 dispatcher networks, int8 / cb4 VGG-16, fp32 ResNet-50, "
+                         "the >= 90%% sweep points)")
     ap.add_argument("--dump-configs", default=None, help="write the autotuned per-layer tiles (JSON)")
     ap.add_argument("--configs", default=None, help="per-layer tiles (JSON from --dump-configs); no autotune")
     ap.add_argument("--retune", action="store_true",
@@ -680,8 +720,14 @@ def main():
             cudnn = {"fp32_tf32_off": cudnn_reference(ws, batch, device),
                      "tf32": cudnn_reference(ws, batch, device, tf32=True)}
         cfg1 = None if args.no_cfg1 else cfg1_leg(device, cpu=not args.no_cpu_baseline and world == 1)
-        b16 = None if args.no_binary16 or world > 1 else binary16_leg()
-        exact = None if args.no_binary16 or world > 1 else exact_variants_leg()
+        def aux(leg):  # an auxiliary leg never costs the headline line
+            if args.no_binary16 or world > 1:
+                return None
+            try:
+                return leg()
+            except Exception as exc:  # noqa: BLE001 -- reported in the line, not raised
+                return {"error": f"{type(exc).__name__}: {exc}"[:300]}
+        b16, exact, sweep = aux(binary16_leg), aux(exact_variants_leg), aux(sweep_leg)
         cpu = None
         if not args.no_cpu_baseline and world == 1:
             import oracle
@@ -716,7 +762,7 @@ def main():
                 "e2e": e2e, "gpu_launches": args.steps * (model.launches_per_forward + 2),
                 "parity": parity,
                 "roofline": roofline, "layers": layers, "cudnn": cudnn, "cpu_baseline": cpu,
-                "cfg1": cfg1, "binary16": b16, "exact_variants": exact, "clocks": clk.summary()}
+                "cfg1": cfg1, "binary16": b16, "exact_variants": exact, "sweep": sweep, "clocks": clk.summary()}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
